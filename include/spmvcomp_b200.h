@@ -1,0 +1,208 @@
+/*
+ * spmvcomp_b200.h -- C-ABI of the B200-native SpMV path of `spmvcomp`
+ * (arxiv 1612.00530).  This is the drop-in boundary: plain pointers and sizes,
+ * no C++ or torch types.  Every entry point returns an int status (0 = ok);
+ * no exception crosses the boundary; spmvb_last_error() gives the message of
+ * the calling thread's last failure.
+ *
+ * Each entry point names the reference interface it stands in for, as
+ * file:line under /root/reference/proj/include/spmvcomp (abbreviated inc/).
+ * The C++ header set in include/spmvcomp/ implements the reference's C++ API
+ * on top of these calls; INTEGRATION.md shows the binding a maintainer adds.
+ *
+ * Threading: one host thread drives a handle; calls on one handle are not
+ * re-entrant; distinct handles are independent.  All device work is issued on
+ * the caller's stream (a cudaStream_t passed as void*; NULL = default stream).
+ * There is NO CPU fallback: without a CUDA device every compute entry point
+ * fails with SPMVB_ERR_CUDA.
+ */
+#ifndef SPMVCOMP_B200_H
+#define SPMVCOMP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes: 1:1 with the reference's exception taxonomy (inc/errors.hpp:9-42,
+ * std::invalid_argument from inc/grid.hpp:35-47) plus CUDA / NCCL / memory. */
+enum spmvb_status {
+    SPMVB_OK = 0,
+    SPMVB_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+    SPMVB_ERR_TABLE_OVERFLOW = 2,   /* TableOverflowError  inc/errors.hpp:9  */
+    SPMVB_ERR_INTEGRITY = 3,        /* IntegrityError      inc/errors.hpp:16 */
+    SPMVB_ERR_VERIFICATION = 4,     /* VerificationError   inc/errors.hpp:33 */
+    SPMVB_ERR_IO = 5,               /* IoError             inc/errors.hpp:39 */
+    SPMVB_ERR_DIVERGENCE = 6,       /* DivergenceError     inc/errors.hpp:22 */
+    SPMVB_ERR_CUDA = 7,
+    SPMVB_ERR_NCCL = 8,
+    SPMVB_ERR_NOMEM = 9
+};
+
+/* inc/perf_model.hpp:14 MatrixFormat (pattern_with_values is the same device
+ * structure as pattern with values_in_pattern set, inc/compress.hpp:60-64). */
+enum spmvb_format { SPMVB_FMT_ELL = 0, SPMVB_FMT_VT = 1, SPMVB_FMT_PATTERN = 2, SPMVB_FMT_CSR = 3 };
+
+/* Device arrays of a matrix handle; names follow the reference structs
+ * (inc/ell.hpp:14-24, inc/compress.hpp:35-44,65-76, inc/stencil.hpp:19-36). */
+enum spmvb_stream_id {
+    SPMVB_S_VALUES = 0,          /* EllMatrix::values            f64  n*width      */
+    SPMVB_S_COLUMNS = 1,         /* EllMatrix::columns           i32  n*width      */
+    SPMVB_S_TABLE = 2,           /* ValueTable::entries          f64  m            */
+    SPMVB_S_SORTED_COLUMNS = 3,  /* VtCompressedMatrix::sorted_columns i32 n*width */
+    SPMVB_S_ENDS = 4,            /* VtCompressedMatrix::ends     i32  n*m          */
+    SPMVB_S_ROW_PATTERN = 5,     /* PatternCompressedMatrix::row_pattern i32 n     */
+    SPMVB_S_DISP_OFFSETS = 6,    /* offsets of patterns[p].displacements i64 P+1   */
+    SPMVB_S_DISP_FLAT = 7,       /* patterns[p].displacements concatenated i32     */
+    SPMVB_S_ENDS_FLAT = 8,       /* patterns[p].ends concatenated  i32 P*m         */
+    SPMVB_S_EXC_ROWS = 9,        /* exception rows (extension)   i32  n_exc        */
+    SPMVB_S_EXC_VALUES = 10,     /* exception ELL values         f64  n_exc*w_exc  */
+    SPMVB_S_EXC_COLUMNS = 11,    /* exception ELL columns        i32  n_exc*w_exc  */
+    SPMVB_S_CSR_ROW_START = 12,  /* StencilMatrix::row_start     i64  n+1          */
+    SPMVB_S_CSR_COLS = 13,       /* StencilMatrix::cols          i32  nnz          */
+    SPMVB_S_CSR_VALS = 14,       /* StencilMatrix::vals          f64  nnz          */
+    SPMVB_S_COUNT_ = 15
+};
+
+typedef struct spmvb_matrix spmvb_matrix; /* opaque, device-resident, caller-destroyed */
+
+typedef struct spmvb_matrix_info {
+    int32_t format;            /* spmvb_format */
+    int32_t n;                 /* local rows */
+    int32_t width;             /* ELL / vt slot width */
+    int32_t m;                 /* value-table size */
+    int32_t n_patterns;
+    int32_t n_exc, w_exc;      /* exception block */
+    int32_t values_in_pattern;
+    int64_t nnz;               /* real entries */
+    int64_t row_offset;        /* global id of local row 0 (z-slab support) */
+    int64_t disp_total;        /* total displacement count over all patterns */
+    int32_t device;
+    int32_t kernel_plan;       /* 0 generic, 1 sliding-window box plan (pattern format) */
+    int32_t box_stride_y, box_stride_z; /* strides found in the dictionary (plan 1) */
+    int32_t reserved_;
+} spmvb_matrix_info;
+
+/* Stencil grid + optional config-4 perturbation. */
+typedef struct spmvb_grid {
+    int32_t nx, ny, nz;        /* inc/grid.hpp:15-19 (GLOBAL grid) */
+    double diagonal;           /* inc/stencil.hpp:44 default 26.0 */
+    double off_diagonal;       /* inc/stencil.hpp:45 default -1.0 */
+    int32_t perturb;           /* 0 = pure stencil */
+    uint64_t perturb_seed;
+    double perturb_fraction;   /* 0.1 */
+    double perturb_noise;      /* 0.1 */
+} spmvb_grid;
+
+/* inc/compress.hpp:22-26 CompressOptions + the hybrid (exception-row) rule. */
+typedef struct spmvb_compress_options {
+    uint64_t value_table_limit; /* default 256 */
+    int32_t values_in_pattern;  /* inc/compress.hpp:84 */
+    int32_t min_pattern_rows;   /* 1 = reference scheme; >=2 = exception rows enabled */
+    int32_t dict_cap;           /* 0 = unlimited */
+} spmvb_compress_options;
+
+/* ---- library / device ------------------------------------------------------ */
+const char *spmvb_last_error(void);
+int spmvb_version(void);
+int spmvb_device_count(int *count);
+int spmvb_set_device(int device);
+/* Tuning knobs for A/B measurement ("pattern_kernel": 0 auto, 1 generic, 2 box;
+ * "ell_kernel": 0 auto ...).  Unknown keys -> SPMVB_ERR_INVALID_ARGUMENT. */
+int spmvb_set_option(const char *key, int value);
+int spmvb_get_option(const char *key, int *value);
+
+/* ---- upload: the reference structs' arrays, byte for byte ------------------- */
+/* EllMatrix (inc/ell.hpp:14-24).  row_offset = global id of row 0 (0 for a whole matrix). */
+int spmvb_ell_upload(int32_t n, int32_t width, int64_t nnz, int64_t row_offset, const double *values,
+                     const int32_t *columns, spmvb_matrix **out);
+/* VtCompressedMatrix (inc/compress.hpp:35-44). */
+int spmvb_vt_upload(int32_t n, int32_t width, int32_t m, int64_t row_offset, const double *table,
+                    const int32_t *sorted_columns, const int32_t *ends, spmvb_matrix **out);
+/* PatternCompressedMatrix (inc/compress.hpp:52-76): patterns flattened as
+ * disp_offsets[P+1] / disp_flat / ends_flat[P*m]; exception block may be empty
+ * (n_exc = 0, pointers NULL).  Validates like validate() (inc/compress.hpp:95)
+ * when check != 0 and n_cols > 0. */
+int spmvb_pattern_upload(int32_t n, int32_t m, int64_t row_offset, const double *table,
+                         int32_t n_patterns, const int64_t *disp_offsets, const int32_t *disp_flat,
+                         const int32_t *ends_flat, const int32_t *row_pattern, int32_t values_in_pattern,
+                         int32_t n_exc, int32_t w_exc, const int32_t *exc_rows, const double *exc_values,
+                         const int32_t *exc_columns, spmvb_matrix **out);
+/* StencilMatrix (inc/stencil.hpp:19-36, stencil_from_rows :47-50): validates
+ * strictly ascending in-range columns. n_cols = global column count. */
+int spmvb_csr_upload(int32_t n, int64_t n_cols, int64_t row_offset, const int64_t *row_start,
+                     const int32_t *cols, const double *vals, spmvb_matrix **out);
+
+/* ---- device-side build ------------------------------------------------------ */
+/* generate_matrix (inc/stencil.hpp:40-45) for global rows [row_begin,row_end)
+ * of the grid, as a device CSR handle (columns are global). */
+int spmvb_generate_csr(const spmvb_grid *grid, int64_t row_begin, int64_t row_end, void *stream,
+                       spmvb_matrix **out);
+/* to_ell (inc/ell.hpp:28-29); min_width lets a slab use the global width. */
+int spmvb_csr_to_ell(const spmvb_matrix *csr, int32_t min_width, void *stream, spmvb_matrix **out);
+/* compress_values (inc/compress.hpp:82). */
+int spmvb_csr_compress_values(const spmvb_matrix *csr, const spmvb_compress_options *opts,
+                              int32_t min_width, void *stream, spmvb_matrix **out);
+/* compress_patterns (inc/compress.hpp:84-85) + exception rows. */
+int spmvb_csr_compress_patterns(const spmvb_matrix *csr, const spmvb_compress_options *opts,
+                                void *stream, spmvb_matrix **out);
+/* decompress / to_stencil (inc/compress.hpp:87-90, inc/ell.hpp:31-32): any
+ * format back to a device CSR handle, columns re-sorted ascending. */
+int spmvb_to_csr(const spmvb_matrix *a, void *stream, spmvb_matrix **out);
+/* validate (inc/compress.hpp:92-95) on the device arrays; n_cols = global
+ * column count.  SPMVB_ERR_INTEGRITY on any violation. */
+int spmvb_validate(const spmvb_matrix *a, int64_t n_cols, void *stream);
+/* Multi-slab dictionary merge: replace this handle's dictionary by `merged`
+ * (same flattened layout as spmvb_pattern_upload) and remap row_pattern through
+ * old_to_new[n_patterns_old]. */
+int spmvb_pattern_remap(spmvb_matrix *a, int32_t n_patterns, const int64_t *disp_offsets,
+                        const int32_t *disp_flat, const int32_t *ends_flat, const int32_t *old_to_new,
+                        void *stream);
+
+/* ---- introspection / download (bit-exact stream comparison) ------------------ */
+int spmvb_matrix_get_info(const spmvb_matrix *a, spmvb_matrix_info *info);
+int spmvb_matrix_stream_bytes(const spmvb_matrix *a, int32_t stream_id, uint64_t *bytes);
+int spmvb_matrix_download(const spmvb_matrix *a, int32_t stream_id, uint64_t offset, uint64_t bytes,
+                          void *dst);
+/* raw device pointer of a stream (for torch / NCCL callers); NULL when absent */
+int spmvb_matrix_stream_ptr(const spmvb_matrix *a, int32_t stream_id, void **dev_ptr);
+int spmvb_matrix_destroy(spmvb_matrix *a);
+
+/* ---- vectors (inc/stencil.hpp:14,54-59) ------------------------------------- */
+int spmvb_vec_alloc(int64_t n, double **dev);
+int spmvb_vec_free(double *dev);
+int spmvb_vec_upload(double *dev, const double *host, int64_t n, void *stream);
+int spmvb_vec_download(double *host, const double *dev, int64_t n, void *stream);
+/* make_test_vector on the device: kind 0 ones, 1 linear, 2 random in [lo,hi);
+ * element i is a pure function of (seed, first_index + i). */
+int spmvb_vec_fill(double *dev, int64_t n, int32_t kind, uint64_t seed, double lo, double hi,
+                   int64_t first_index, void *stream);
+
+/* ---- SpMV (inc/kernels.hpp:19-36) -------------------------------------------- */
+/* unchecked::spmv_rows: y[i] = (A x)[i] for local rows [row_begin,row_end),
+ * overwrite, other rows untouched.  x_dev[j] holds the entry of global column
+ * x_col0 + j, j in [0,x_len); a whole matrix uses x_col0 = 0, x_len = n; a
+ * z-slab passes its ghosted local vector.  Asynchronous on `stream`. */
+int spmvb_spmv(const spmvb_matrix *a, const double *x_dev, int64_t x_col0, int64_t x_len, double *y_dev,
+               int32_t row_begin, int32_t row_end, void *stream);
+/* spmv(fmt, Vector) -> Vector with HOST buffers (inc/kernels.hpp:23-25): checks
+ * x_len == n (length mismatch -> SPMVB_ERR_INVALID_ARGUMENT), copies x to the
+ * device, runs, copies y back, synchronises. */
+int spmvb_spmv_host(const spmvb_matrix *a, const double *x_host, int64_t x_len, double *y_host);
+
+/* ---- verification helpers ----------------------------------------------------- */
+/* max_i |y[i]-ref[i]| / (|ref[i]| or scale[i] when ref[i]==0) and the number of
+ * entries whose bit patterns differ; all pointers are device pointers
+ * (scale may be NULL). */
+int spmvb_compare(const double *y, const double *ref, const double *scale, int64_t n, double *max_rel,
+                  int64_t *n_bit_mismatch, void *stream);
+/* sum_k |a_ik x_k| per local row (CSR handle), the scale above. */
+int spmvb_row_abs_scale(const spmvb_matrix *csr, const double *x_dev, int64_t x_col0, double *scale_dev,
+                        void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,310 @@
+"""Host-side mirror of the reference's C++ interface for the SpMV path, as thin
+wrappers over the C-ABI (include/spmvcomp_b200.h).  Names, argument meaning and
+error behaviour follow /root/reference/proj/include/spmvcomp (cited per symbol);
+all computation happens on the GPU -- there is no CPU path in this package.
+
+Matrices are device-resident handles (`DeviceMatrix`); vectors are device arrays
+(`DeviceVector`, or anything with a `.data_ptr()` such as a CUDA torch tensor).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _cabi as cabi
+from ._cabi import (FMT_CSR, FMT_ELL, FMT_PATTERN, FMT_VT, CudaError, IntegrityError, InvalidArgument,  # noqa: F401
+                    SpmvcompError, TableOverflowError, VerificationError, check, lib)
+
+K_MAX_ROWS = (1 << 31) - 1  # grid.hpp:11 kMaxRows
+ONES, LINEAR, RANDOM = 0, 1, 2  # stencil.hpp:54 VectorKind
+
+_DTYPES = {
+    cabi.S_VALUES: np.float64, cabi.S_COLUMNS: np.int32, cabi.S_TABLE: np.float64,
+    cabi.S_SORTED_COLUMNS: np.int32, cabi.S_ENDS: np.int32, cabi.S_ROW_PATTERN: np.int32,
+    cabi.S_DISP_OFFSETS: np.int64, cabi.S_DISP_FLAT: np.int32, cabi.S_ENDS_FLAT: np.int32,
+    cabi.S_EXC_ROWS: np.int32, cabi.S_EXC_VALUES: np.float64, cabi.S_EXC_COLUMNS: np.int32,
+    cabi.S_CSR_ROW_START: np.int64, cabi.S_CSR_COLS: np.int32, cabi.S_CSR_VALS: np.float64,
+}
+_NAMES = {
+    "values": cabi.S_VALUES, "columns": cabi.S_COLUMNS, "table": cabi.S_TABLE,
+    "sorted_columns": cabi.S_SORTED_COLUMNS, "ends": cabi.S_ENDS, "row_pattern": cabi.S_ROW_PATTERN,
+    "disp_offsets": cabi.S_DISP_OFFSETS, "disp_flat": cabi.S_DISP_FLAT, "ends_flat": cabi.S_ENDS_FLAT,
+    "exc_rows": cabi.S_EXC_ROWS, "exc_values": cabi.S_EXC_VALUES, "exc_columns": cabi.S_EXC_COLUMNS,
+    "row_start": cabi.S_CSR_ROW_START, "cols": cabi.S_CSR_COLS, "vals": cabi.S_CSR_VALS,
+}
+
+
+@dataclass(frozen=True)
+class GridSpec:
+    """grid.hpp:15-33."""
+    nx: int = 1
+    ny: int = 1
+    nz: int = 1
+
+    def rows(self) -> int:
+        return self.nx * self.ny * self.nz
+
+    def node(self, ix, iy, iz) -> int:
+        return ix + self.nx * (iy + self.ny * iz)
+
+
+def validate_grid(g: GridSpec):
+    """grid.hpp:35-47."""
+    if g.nx < 1 or g.ny < 1 or g.nz < 1:
+        raise InvalidArgument(f"grid dimensions must be >= 1, got {g.nx}x{g.ny}x{g.nz}")
+    if g.rows() > K_MAX_ROWS:
+        raise InvalidArgument(f"grid {g.nx}x{g.ny}x{g.nz} has {g.rows()} rows; column indices must fit a "
+                              "4-byte signed integer")
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        return C.c_void_p(a.data_ptr())
+    if isinstance(a, DeviceVector):
+        return C.c_void_p(a.ptr)
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _stream(stream):
+    if stream is None:
+        return None
+    return C.c_void_p(getattr(stream, "cuda_stream", stream))
+
+
+def _np(a, dtype):
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+class DeviceVector:
+    """A length-n fp64 device array (Vector, stencil.hpp:14)."""
+
+    def __init__(self, n: int):
+        p = C.c_void_p()
+        check(lib.spmvb_vec_alloc(n, C.byref(p)))
+        self.ptr, self.n = p.value, n
+
+    def __del__(self):
+        if getattr(self, "ptr", None):
+            lib.spmvb_vec_free(C.c_void_p(self.ptr))
+            self.ptr = None
+
+    def data_ptr(self):
+        return self.ptr
+
+    @classmethod
+    def from_host(cls, host, stream=None):
+        host = _np(host, np.float64)
+        v = cls(host.shape[0])
+        check(lib.spmvb_vec_upload(C.c_void_p(v.ptr), _ptr(host), host.shape[0], _stream(stream)))
+        return v
+
+    def to_host(self, stream=None):
+        out = np.empty(self.n, dtype=np.float64)
+        check(lib.spmvb_vec_download(_ptr(out), C.c_void_p(self.ptr), self.n, _stream(stream)))
+        return out
+
+    def fill(self, kind, seed=None, lo=0.0, hi=1.0, first_index=0, stream=None):
+        if kind == RANDOM and seed is None:
+            raise InvalidArgument("seed is required for the random kind")  # stencil.hpp:56-57
+        check(lib.spmvb_vec_fill(C.c_void_p(self.ptr), self.n, kind, seed or 0, lo, hi, first_index, _stream(stream)))
+        return self
+
+
+def make_test_vector(n, kind, seed=None, lo=0.0, hi=1.0, first_index=0, stream=None) -> DeviceVector:
+    """make_test_vector (stencil.hpp:54-59) on the device; [lo,hi) defaults to the header's [0,1)."""
+    if n < 1:
+        raise InvalidArgument("vector length must be >= 1")
+    return DeviceVector(n).fill(kind, seed, lo, hi, first_index, stream)
+
+
+class DeviceMatrix:
+    """Opaque device-resident matrix in one of the reference's formats."""
+
+    def __init__(self, handle):
+        self.h = handle
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib.spmvb_matrix_destroy(self.h)
+            self.h = None
+
+    @property
+    def info(self) -> cabi.MatrixInfo:
+        i = cabi.MatrixInfo()
+        check(lib.spmvb_matrix_get_info(self.h, C.byref(i)))
+        return i
+
+    n = property(lambda self: self.info.n)
+    nnz = property(lambda self: self.info.nnz)
+    format = property(lambda self: self.info.format)
+
+    def stream_bytes(self, name) -> int:
+        b = C.c_uint64()
+        check(lib.spmvb_matrix_stream_bytes(self.h, _NAMES[name], C.byref(b)))
+        return b.value
+
+    def download(self, name, offset_elems=0, count=None) -> np.ndarray:
+        """Copy one device stream back (bit-exact comparison against the oracle)."""
+        sid = _NAMES[name]
+        dt = np.dtype(_DTYPES[sid])
+        total = self.stream_bytes(name) // dt.itemsize
+        count = total - offset_elems if count is None else count
+        out = np.empty(count, dtype=dt)
+        check(lib.spmvb_matrix_download(self.h, sid, offset_elems * dt.itemsize, count * dt.itemsize, _ptr(out)))
+        return out
+
+    def stream_ptr(self, name) -> int:
+        p = C.c_void_p()
+        check(lib.spmvb_matrix_stream_ptr(self.h, _NAMES[name], C.byref(p)))
+        return p.value or 0
+
+
+def _wrap(call, *args):
+    out = C.c_void_p()
+    check(call(*args, C.byref(out)))
+    return DeviceMatrix(out)
+
+
+# ---- upload of the reference structs' arrays --------------------------------------
+def upload_ell(n, width, nnz, values, columns, row_offset=0) -> DeviceMatrix:
+    """EllMatrix (ell.hpp:14-24)."""
+    values, columns = _np(values, np.float64), _np(columns, np.int32)
+    if values.size != n * width or columns.size != n * width:
+        raise InvalidArgument("EllMatrix arrays must hold n*width entries")
+    return _wrap(lib.spmvb_ell_upload, n, width, nnz, row_offset, _ptr(values), _ptr(columns))
+
+
+def upload_vt(n, width, table, sorted_columns, ends, row_offset=0) -> DeviceMatrix:
+    """VtCompressedMatrix (compress.hpp:35-44)."""
+    table, sc, ends = _np(table, np.float64), _np(sorted_columns, np.int32), _np(ends, np.int32)
+    m = table.size
+    if sc.size != n * width or ends.size != n * m:
+        raise InvalidArgument("VtCompressedMatrix arrays have the wrong size")
+    return _wrap(lib.spmvb_vt_upload, n, width, m, row_offset, _ptr(table), _ptr(sc), _ptr(ends))
+
+
+def upload_pattern(n, table, disp_offsets, disp_flat, ends_flat, row_pattern, values_in_pattern=False,
+                   exc_rows=None, exc_values=None, exc_columns=None, w_exc=0, row_offset=0) -> DeviceMatrix:
+    """PatternCompressedMatrix (compress.hpp:52-76) with the optional exception block."""
+    table = _np(table, np.float64)
+    do, df, ef = _np(disp_offsets, np.int64), _np(disp_flat, np.int32), _np(ends_flat, np.int32)
+    rp = _np(row_pattern, np.int32)
+    n_pat = do.size - 1
+    if rp.size != n or ef.size != n_pat * table.size or df.size != (do[-1] if do.size else 0):
+        raise InvalidArgument("PatternCompressedMatrix arrays have the wrong size")
+    er = _np(exc_rows if exc_rows is not None else [], np.int32)
+    ev = _np(exc_values if exc_values is not None else [], np.float64)
+    ec = _np(exc_columns if exc_columns is not None else [], np.int32)
+    return _wrap(lib.spmvb_pattern_upload, n, table.size, row_offset, _ptr(table), n_pat, _ptr(do), _ptr(df),
+                 _ptr(ef), _ptr(rp), int(values_in_pattern), er.size, w_exc, _ptr(er), _ptr(ev), _ptr(ec))
+
+
+def upload_csr(n, row_start, cols, vals, n_cols=None, row_offset=0) -> DeviceMatrix:
+    """StencilMatrix / stencil_from_rows (stencil.hpp:19-36,47-50)."""
+    rs, cols, vals = _np(row_start, np.int64), _np(cols, np.int32), _np(vals, np.float64)
+    return _wrap(lib.spmvb_csr_upload, n, n if n_cols is None else n_cols, row_offset, _ptr(rs), _ptr(cols),
+                 _ptr(vals))
+
+
+def stencil_from_rows(n, rows) -> DeviceMatrix:
+    """stencil_from_rows (stencil.hpp:47-50): rows = per-row lists of (column, value)."""
+    rs = np.zeros(n + 1, dtype=np.int64)
+    cols, vals = [], []
+    for i, r in enumerate(rows):
+        rs[i + 1] = rs[i] + len(r)
+        cols += [c for c, _ in r]
+        vals += [v for _, v in r]
+    return upload_csr(n, rs, cols, vals)
+
+
+# ---- device-side build --------------------------------------------------------------
+def generate_matrix(spec: GridSpec, diagonal=26.0, off_diagonal=-1.0, perturb=None, row_begin=0, row_end=None,
+                    stream=None) -> DeviceMatrix:
+    """generate_matrix (stencil.hpp:40-45) on the device, as a CSR handle.  `perturb`
+    = (seed, fraction, noise) enables BASELINE.json's config-4 recipe; [row_begin,row_end)
+    selects a slab of global rows."""
+    validate_grid(spec)
+    g = cabi.Grid(spec.nx, spec.ny, spec.nz, diagonal, off_diagonal, 0, 0, 0.0, 0.0)
+    if perturb is not None:
+        g.perturb, g.perturb_seed, g.perturb_fraction, g.perturb_noise = 1, perturb[0], perturb[1], perturb[2]
+    row_end = spec.rows() if row_end is None else row_end
+    return _wrap(lib.spmvb_generate_csr, C.byref(g), row_begin, row_end, _stream(stream))
+
+
+def to_ell(m: DeviceMatrix, min_width=0, stream=None) -> DeviceMatrix:
+    """to_ell (ell.hpp:28-29)."""
+    return _wrap(lib.spmvb_csr_to_ell, m.h, min_width, _stream(stream))
+
+
+def _opts(limit, values_in_pattern=False, min_pattern_rows=1, dict_cap=0):
+    return cabi.CompressOptions(limit, int(values_in_pattern), min_pattern_rows, dict_cap)
+
+
+def compress_values(m: DeviceMatrix, value_table_limit=256, min_width=0, stream=None) -> DeviceMatrix:
+    """compress_values (compress.hpp:82)."""
+    return _wrap(lib.spmvb_csr_compress_values, m.h, C.byref(_opts(value_table_limit)), min_width, _stream(stream))
+
+
+def compress_patterns(m: DeviceMatrix, values_in_pattern=False, value_table_limit=256, min_pattern_rows=1,
+                      dict_cap=0, stream=None) -> DeviceMatrix:
+    """compress_patterns (compress.hpp:84-85); min_pattern_rows >= 2 enables exception rows."""
+    o = _opts(value_table_limit, values_in_pattern, min_pattern_rows, dict_cap)
+    return _wrap(lib.spmvb_csr_compress_patterns, m.h, C.byref(o), _stream(stream))
+
+
+def decompress(c: DeviceMatrix, stream=None) -> DeviceMatrix:
+    """decompress / to_stencil (compress.hpp:87-90, ell.hpp:31-32) -> CSR handle."""
+    return _wrap(lib.spmvb_to_csr, c.h, _stream(stream))
+
+
+to_stencil = decompress
+
+
+def validate(c: DeviceMatrix, n_cols=None, stream=None):
+    """validate (compress.hpp:92-95)."""
+    check(lib.spmvb_validate(c.h, c.n if n_cols is None else n_cols, _stream(stream)))
+
+
+# ---- SpMV (kernels.hpp:19-36) -----------------------------------------------------------
+def spmv_flops(nnz):
+    return 2 * nnz  # kernels.hpp:14
+
+
+def spmv_rows(a: DeviceMatrix, x, y, begin, end, x_col0=0, x_len=None, stream=None):
+    """unchecked::spmv_rows (kernels.hpp:27-36): device x and y, rows [begin,end), asynchronous."""
+    if x_len is None:
+        x_len = x.n if isinstance(x, DeviceVector) else x.numel()
+    check(lib.spmvb_spmv(a.h, _ptr(x), x_col0, x_len, _ptr(y), begin, end, _stream(stream)))
+
+
+def spmv(a: DeviceMatrix, x) -> np.ndarray:
+    """spmv (kernels.hpp:23-25) with host vectors: validated, returns a fresh vector."""
+    x = _np(x, np.float64)
+    y = np.empty(a.n, dtype=np.float64)
+    check(lib.spmvb_spmv_host(a.h, _ptr(x), x.shape[0], _ptr(y)))
+    return y
+
+
+def compare(y, ref, n, scale=None, stream=None):
+    """Device-side (max relative deviation, number of bit-different entries)."""
+    worst, bad = C.c_double(), C.c_int64()
+    check(lib.spmvb_compare(_ptr(y), _ptr(ref), _ptr(scale), n, C.byref(worst), C.byref(bad), _stream(stream)))
+    return worst.value, bad.value
+
+
+def row_abs_scale(csr: DeviceMatrix, x, out, x_col0=0, stream=None):
+    check(lib.spmvb_row_abs_scale(csr.h, _ptr(x), x_col0, _ptr(out), _stream(stream)))
+
+
+def set_option(key: str, value: int):
+    check(lib.spmvb_set_option(key.encode(), value))
+
+
+def device_count() -> int:
+    c = C.c_int()
+    check(lib.spmvb_device_count(C.byref(c)))
+    return c.value

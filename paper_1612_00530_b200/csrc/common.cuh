@@ -1,0 +1,89 @@
+// Internal declarations shared by the translation units of libspmvcomp_b200.so.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "spmvcomp_b200.h"
+
+namespace spmvb {
+
+// ---- error plumbing ---------------------------------------------------------
+std::string &last_error_ref();
+int fail(int code, const char *fmt, ...);
+
+#define SPMVB_CUDA(expr)                                                                   \
+    do {                                                                                   \
+        cudaError_t e__ = (expr);                                                          \
+        if (e__ != cudaSuccess)                                                            \
+            return ::spmvb::fail(SPMVB_ERR_CUDA, "%s failed: %s (%s:%d)", #expr,           \
+                                 cudaGetErrorString(e__), __FILE__, __LINE__);             \
+    } while (0)
+
+#define SPMVB_TRY(expr)              \
+    do {                             \
+        int rc__ = (expr);           \
+        if (rc__ != SPMVB_OK) return rc__; \
+    } while (0)
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Rows per CTA tile of the row-major ELL-like streams.  Device allocations of
+// those streams are padded to a whole number of tiles so a tile can always be
+// fetched with full 16-byte vector loads.
+constexpr int kTileRows = 128;
+
+// Sliding-window ("box") plan for a pattern dictionary whose dominant pattern is a
+// 3x3x3 box of displacements dx + sy*dy + sz*dz (the 27-point stencil in x-fastest
+// numbering), all 26 off-centre entries sharing one table value.
+struct BoxPlan {
+    bool valid = false;
+    int32_t sy = 0, sz = 0;     // strides found in the dictionary
+    int32_t center_pos = 0;     // 0 centre first, 1 centre last, 2 centre in place (m == 1)
+    int32_t k_off = 0, k_center = 0;  // value-table indices
+    std::vector<uint32_t> masks;      // per pattern: 27-bit sub-box mask, or kGenericMask
+};
+constexpr uint32_t kGenericMask = 0xFFFFFFFFu;
+
+}  // namespace spmvb
+
+struct spmvb_matrix {
+    int32_t format = 0;
+    int32_t device = 0;
+    int32_t n = 0, width = 0, m = 0, n_patterns = 0, n_exc = 0, w_exc = 0, values_in_pattern = 0;
+    int64_t nnz = 0, row_offset = 0, disp_total = 0, n_cols = 0;
+    void *s[SPMVB_S_COUNT_] = {};
+    uint64_t bytes[SPMVB_S_COUNT_] = {};
+    // host mirrors of the small pattern-side tables
+    std::vector<double> h_table;
+    std::vector<int64_t> h_disp_offsets;
+    std::vector<int32_t> h_disp_flat, h_ends_flat, h_exc_rows;
+    spmvb::BoxPlan box;
+    uint32_t *d_masks = nullptr;      // device copy of box.masks
+    int32_t *d_disp_off32 = nullptr;  // 32-bit copy of disp_offsets for the kernels
+};
+
+namespace spmvb {
+
+// Allocates `bytes` (+ zeroed slack so vector loads of a partial tile stay in bounds).
+int dev_alloc(spmvb_matrix *a, int sid, uint64_t bytes, uint64_t slack = 0);
+int upload_stream(spmvb_matrix *a, int sid, const void *host, uint64_t bytes, uint64_t slack = 0);
+int finish_pattern_handle(spmvb_matrix *a);  // builds host mirrors' device copies and the box plan
+void analyse_box_plan(spmvb_matrix *a);
+void destroy(spmvb_matrix *a);
+
+struct Options {
+    int pattern_kernel = 0;  // 0 auto, 1 generic, 2 box
+    int ell_kernel = 0;      // 0 auto (staged), 1 naive thread-per-row
+    int box_march = 0;       // 0 default
+    int box_prefetch = -1;   // L2 prefetch distance in lines (-1 = default)
+};
+Options &options();
+
+}  // namespace spmvb

@@ -1,0 +1,85 @@
+"""Exploratory kernel timing on the GPU box (not a test, not the bench):
+python tests/perf_probe.py [n] [reps].  Formats are built by the oracle here
+only because this probe predates the device builders; bench.py does not do that."""
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+import paper_1612_00530_b200 as sp  # noqa: E402
+from oracle import oracle as orc  # noqa: E402
+
+n1 = int(sys.argv[1]) if len(sys.argv) > 1 else 128
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 50
+fmts = sys.argv[3].split(",") if len(sys.argv) > 3 else ["pattern", "generic", "vt", "ell"]
+g = (n1, n1, n1)
+n = n1 ** 3
+nnz = (3 * n1 - 2) ** 3
+t0 = time.time()
+pc = orc.compress_patterns_grid(*g, values_in_pattern=True)
+print(f"oracle pattern build {time.time()-t0:.1f}s", flush=True)
+x = torch.empty(n, dtype=torch.float64, device="cuda")
+y = torch.empty(n, dtype=torch.float64, device="cuda")
+sp.lib.spmvb_vec_fill(x.data_ptr(), n, 2, 7, -1.0, 1.0, 0, None)
+torch.cuda.synchronize()
+flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+
+
+def timeit(a, label, bytes_per_row, **opts):
+    for k, v in opts.items():
+        sp.set_option(k, v)
+    st = torch.cuda.current_stream()
+    for _ in range(3):
+        sp.spmv_rows(a, x, y, 0, n, stream=st)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    for s, e in ev:
+        flush.zero_()
+        s.record()
+        sp.spmv_rows(a, x, y, 0, n, stream=st)
+        e.record()
+    torch.cuda.synchronize()
+    ts = sorted(s.elapsed_time(e) * 1e3 for s, e in ev)
+    med = ts[len(ts) // 2]
+    # back-to-back (no flush) average
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(reps):
+        sp.spmv_rows(a, x, y, 0, n, stream=st)
+    e.record()
+    torch.cuda.synchronize()
+    b2b = s.elapsed_time(e) * 1e3 / reps
+    print(f"{label:34s} flushed med {med:9.1f} us  min {ts[0]:9.1f} | b2b {b2b:9.1f} us  "
+          f"{2*nnz/b2b/1e3:9.1f} GF/s  {bytes_per_row*n/b2b/1e3:8.1f} GB/s ({bytes_per_row} B/row)", flush=True)
+    for k in opts:
+        sp.set_option(k, 0 if k != "box_prefetch" else -1)
+
+
+if "pattern" in fmts or "generic" in fmts:
+    d = sp.upload_pattern(pc.n, pc.table, pc.disp_offsets, pc.disp_flat, pc.ends_flat, pc.row_pattern, True)
+    ref = None
+    if "pattern" in fmts:
+        for march in (0, 1, 2, 3, 4):
+            for pf in (0, 4, 8, 16):
+                timeit(d, f"pattern box march={march} pf={pf}", 20, pattern_kernel=2, box_march=march, box_prefetch=pf)
+    if "generic" in fmts:
+        timeit(d, "pattern generic", 20, pattern_kernel=1)
+    del d
+if "vt" in fmts or "ell" in fmts:
+    t0 = time.time()
+    m = orc.generate_matrix(*g)
+    print(f"oracle csr build {time.time()-t0:.1f}s", flush=True)
+    if "vt" in fmts:
+        vt = orc.compress_values(m)
+        d = sp.upload_vt(vt.n, vt.width, vt.table, vt.sorted_columns, vt.ends)
+        del vt
+        timeit(d, "vt staged", 132)
+        del d
+    if "ell" in fmts:
+        e = orc.to_ell(m)
+        d = sp.upload_ell(e.n, e.width, e.nnz, e.values, e.columns)
+        del e
+        timeit(d, "ell staged", 340)
+        timeit(d, "ell naive", 340, ell_kernel=1)
