@@ -161,6 +161,11 @@ int spmvb_pattern_remap(spmvb_matrix *a, int32_t n_patterns, const int64_t *disp
                         const int32_t *disp_flat, const int32_t *ends_flat, const int32_t *old_to_new,
                         void *stream);
 
+/* First local row of every pattern (n_patterns entries; -1 when unknown, e.g.
+ * after upload).  With row_offset it gives the global first occurrence used to
+ * merge per-slab dictionaries into the single-matrix numbering. */
+int spmvb_pattern_first_rows(const spmvb_matrix *a, int32_t *out);
+
 /* ---- introspection / download (bit-exact stream comparison) ------------------ */
 int spmvb_matrix_get_info(const spmvb_matrix *a, spmvb_matrix_info *info);
 int spmvb_matrix_stream_bytes(const spmvb_matrix *a, int32_t stream_id, uint64_t *bytes);
@@ -193,9 +198,10 @@ int spmvb_spmv(const spmvb_matrix *a, const double *x_dev, int64_t x_col0, int64
 int spmvb_spmv_host(const spmvb_matrix *a, const double *x_host, int64_t x_len, double *y_host);
 
 /* ---- verification helpers ----------------------------------------------------- */
-/* max_i |y[i]-ref[i]| / (|ref[i]| or scale[i] when ref[i]==0) and the number of
- * entries whose bit patterns differ; all pointers are device pointers
- * (scale may be NULL). */
+/* max_i |y[i]-ref[i]| / den[i] and the number of entries whose bit patterns
+ * differ.  den = scale[i] (= sum_k |a_ik x_k|, from spmvb_row_abs_scale) when a
+ * scale is given -- the per-row measure used between formats whose summation
+ * orders differ -- else |ref[i]| (1 where that is 0).  Device pointers. */
 int spmvb_compare(const double *y, const double *ref, const double *scale, int64_t n, double *max_rel,
                   int64_t *n_bit_mismatch, void *stream);
 /* sum_k |a_ik x_k| per local row (CSR handle), the scale above. */

@@ -103,7 +103,7 @@ def lib():
         _lib.orc_compress_values.argtypes = [C.POINTER(_Csr), C.c_size_t, C.c_int32, C.c_int64,
                                              C.POINTER(C.POINTER(_Vt))]
         _lib.orc_compress_patterns.argtypes = [C.POINTER(_Csr), C.c_int, C.c_size_t, C.c_int32, C.c_int32,
-                                               C.POINTER(C.POINTER(_Pattern))]
+                                               C.c_int64, C.POINTER(C.POINTER(_Pattern))]
         _lib.orc_scan_value_table.argtypes = [C.POINTER(_Csr), C.c_size_t, C.c_void_p, C.POINTER(C.c_int32)]
         _lib.orc_validate_vt.argtypes = [C.POINTER(_Vt), C.c_int64]
         _lib.orc_validate_pattern.argtypes = [C.POINTER(_Pattern), C.c_int64]
@@ -307,9 +307,9 @@ def compress_values(m, limit=256, min_width=0, row_offset=0):
     return Vt(out)
 
 
-def compress_patterns(m, values_in_pattern=False, limit=256, min_pattern_rows=1, dict_cap=0):
+def compress_patterns(m, values_in_pattern=False, limit=256, min_pattern_rows=1, dict_cap=0, row_offset=0):
     out = C.POINTER(_Pattern)()
-    _check(lib().orc_compress_patterns(m.p, int(values_in_pattern), limit, min_pattern_rows, dict_cap,
+    _check(lib().orc_compress_patterns(m.p, int(values_in_pattern), limit, min_pattern_rows, dict_cap, row_offset,
                                        C.byref(out)))
     return Pattern(out)
 

@@ -627,8 +627,8 @@ static int cmp_kept_first(const void *a, const void *b) {
     return x->first_row < y->first_row ? -1 : x->first_row > y->first_row;
 }
 
-static int compress_patterns_gen(const rowgen *g, int64_t n, int values_in_pattern, size_t limit,
-                                 int32_t min_rows, int32_t dict_cap, orc_pattern **out) {
+static int compress_patterns_gen(const rowgen *g, int64_t n, int64_t row_offset, int values_in_pattern,
+                                 size_t limit, int32_t min_rows, int32_t dict_cap, orc_pattern **out) {
     if (min_rows < 1) min_rows = 1;
     shape_map mp;
     shape_map_init(&mp);
@@ -639,7 +639,7 @@ static int compress_patterns_gen(const rowgen *g, int64_t n, int values_in_patte
     for (int64_t i = 0; i < n; i++) {
         int k = rowgen_row(g, i, cols, vals);
         if (k > ORC_MAX_ROW) { shape_map_free(&mp); FAIL(ORC_INVALID_ARGUMENT, "row %lld longer than %d", (long long)i, ORC_MAX_ROW); }
-        row_shape(i, k, cols, vals, &s);
+        row_shape(row_offset + i, k, cols, vals, &s);
         shape_map_add(&mp, &s, i);
     }
     /* choose the dictionary: shapes used by >= min_rows rows; if more than
@@ -682,6 +682,7 @@ static int compress_patterns_gen(const rowgen *g, int64_t n, int values_in_patte
     }
     orc_pattern *c = calloc(1, sizeof *c);
     c->n = (int32_t)n;
+    c->row_offset = row_offset;
     c->m = vs.m;
     c->table = vs.v;
     c->n_patterns = (int32_t)nk;
@@ -708,7 +709,7 @@ static int compress_patterns_gen(const rowgen *g, int64_t n, int values_in_patte
     int32_t n_exc = 0, w_exc = 0;
     for (int64_t i = 0; i < n; i++) {
         int k = rowgen_row(g, i, cols, vals);
-        row_shape(i, k, cols, vals, &s);
+        row_shape(row_offset + i, k, cols, vals, &s);
         shape_slot *sl = shape_map_probe(&mp, &s, shape_hash(&s));
         int32_t id = slot_id[sl - mp.slots];
         c->row_pattern[i] = id;
@@ -727,7 +728,7 @@ static int compress_patterns_gen(const rowgen *g, int64_t n, int values_in_patte
         c->exc_rows[q] = (int32_t)i;
         for (int32_t t = 0; t < w_exc; t++) {
             c->exc_values[(int64_t)q * w_exc + t] = t < k ? vals[t] : 0.0;
-            c->exc_columns[(int64_t)q * w_exc + t] = t < k ? cols[t] : (int32_t)i;
+            c->exc_columns[(int64_t)q * w_exc + t] = t < k ? cols[t] : (int32_t)(row_offset + i);
         }
         q++;
     }
@@ -737,12 +738,12 @@ static int compress_patterns_gen(const rowgen *g, int64_t n, int values_in_patte
 }
 
 int orc_compress_patterns(const orc_csr *m, int values_in_pattern, size_t limit,
-                          int32_t min_pattern_rows, int32_t dict_cap, orc_pattern **out) {
+                          int32_t min_pattern_rows, int32_t dict_cap, int64_t row_offset, orc_pattern **out) {
     rowgen g;
     memset(&g, 0, sizeof g);
     g.csr = m;
     g.n = m->n;
-    return compress_patterns_gen(&g, m->n, values_in_pattern, limit, min_pattern_rows, dict_cap, out);
+    return compress_patterns_gen(&g, m->n, row_offset, values_in_pattern, limit, min_pattern_rows, dict_cap, out);
 }
 
 int orc_compress_patterns_grid(int nx, int ny, int nz, double diagonal, double off_diagonal,
@@ -752,7 +753,7 @@ int orc_compress_patterns_grid(int nx, int ny, int nz, double diagonal, double o
     if (rc) return rc;
     rowgen g = {nx, ny, nz, diagonal, off_diagonal, {0, 0, 0, 0}, (int64_t)nx * ny * nz, NULL};
     if (p && p->enabled) g.pert = *p;
-    return compress_patterns_gen(&g, g.n, values_in_pattern, limit, min_pattern_rows, dict_cap, out);
+    return compress_patterns_gen(&g, g.n, 0, values_in_pattern, limit, min_pattern_rows, dict_cap, out);
 }
 
 int orc_validate_pattern(const orc_pattern *c, int64_t n_cols) {

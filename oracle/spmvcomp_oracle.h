@@ -134,9 +134,11 @@ typedef struct orc_pattern {
  * reproduces the reference scheme (every row gets an id, no exceptions).
  * min_pattern_rows>=2 activates the hybrid rule of DESIGN.md: a full
  * (displacement,value) row shape enters the dictionary iff at least that many
- * rows use it; all other rows become exception rows. */
+ * rows use it; all other rows become exception rows.  row_offset = global id of
+ * the CSR's row 0 when it is a slab of a larger matrix (displacements are taken
+ * against the GLOBAL row index). */
 int orc_compress_patterns(const orc_csr *m, int values_in_pattern, size_t limit,
-                          int32_t min_pattern_rows, int32_t dict_cap, orc_pattern **out);
+                          int32_t min_pattern_rows, int32_t dict_cap, int64_t row_offset, orc_pattern **out);
 /* Same result as orc_generate_rows(whole grid) + orc_compress_patterns, but
  * streams the rows through the deduplicator without materialising the CSR
  * (for 256^3 and above). */

@@ -84,7 +84,7 @@ SYMBOLS = [
     "spmvb_last_error", "spmvb_version", "spmvb_device_count", "spmvb_set_device", "spmvb_set_option",
     "spmvb_get_option", "spmvb_ell_upload", "spmvb_vt_upload", "spmvb_pattern_upload", "spmvb_csr_upload",
     "spmvb_generate_csr", "spmvb_csr_to_ell", "spmvb_csr_compress_values", "spmvb_csr_compress_patterns",
-    "spmvb_to_csr", "spmvb_validate", "spmvb_pattern_remap", "spmvb_matrix_get_info",
+    "spmvb_to_csr", "spmvb_validate", "spmvb_pattern_remap", "spmvb_pattern_first_rows", "spmvb_matrix_get_info",
     "spmvb_matrix_stream_bytes", "spmvb_matrix_download", "spmvb_matrix_stream_ptr", "spmvb_matrix_destroy",
     "spmvb_vec_alloc", "spmvb_vec_free", "spmvb_vec_upload", "spmvb_vec_download", "spmvb_vec_fill",
     "spmvb_spmv", "spmvb_spmv_host", "spmvb_compare", "spmvb_row_abs_scale",
@@ -111,6 +111,7 @@ lib.spmvb_csr_compress_patterns.argtypes = [_vp, C.POINTER(CompressOptions), _vp
 lib.spmvb_to_csr.argtypes = [_vp, _vp, _pp]
 lib.spmvb_validate.argtypes = [_vp, _i64, _vp]
 lib.spmvb_pattern_remap.argtypes = [_vp, _i32, _vp, _vp, _vp, _vp, _vp]
+lib.spmvb_pattern_first_rows.argtypes = [_vp, _vp]
 lib.spmvb_matrix_get_info.argtypes = [_vp, C.POINTER(MatrixInfo)]
 lib.spmvb_matrix_stream_bytes.argtypes = [_vp, _i32, C.POINTER(_u64)]
 lib.spmvb_matrix_download.argtypes = [_vp, _i32, _u64, _u64, _vp]

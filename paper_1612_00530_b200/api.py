@@ -264,6 +264,20 @@ def decompress(c: DeviceMatrix, stream=None) -> DeviceMatrix:
 to_stencil = decompress
 
 
+def pattern_first_rows(c: DeviceMatrix) -> np.ndarray:
+    """First local row of each pattern of a device-built pattern handle (-1 = unknown)."""
+    out = np.empty(c.info.n_patterns, dtype=np.int32)
+    check(lib.spmvb_pattern_first_rows(c.h, _ptr(out)))
+    return out
+
+
+def pattern_remap(c: DeviceMatrix, disp_offsets, disp_flat, ends_flat, old_to_new, stream=None):
+    """Install a merged dictionary and renumber row_pattern (multi-slab build)."""
+    do, df = _np(disp_offsets, np.int64), _np(disp_flat, np.int32)
+    ef, o2n = _np(ends_flat, np.int32), _np(old_to_new, np.int32)
+    check(lib.spmvb_pattern_remap(c.h, do.size - 1, _ptr(do), _ptr(df), _ptr(ef), _ptr(o2n), _stream(stream)))
+
+
 def validate(c: DeviceMatrix, n_cols=None, stream=None):
     """validate (compress.hpp:92-95)."""
     check(lib.spmvb_validate(c.h, c.n if n_cols is None else n_cols, _stream(stream)))

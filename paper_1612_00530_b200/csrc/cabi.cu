@@ -54,6 +54,8 @@ void destroy(spmvb_matrix *a) {
     if (!a) return;
     for (int i = 0; i < SPMVB_S_COUNT_; i++)
         if (a->s[i]) cudaFree(a->s[i]);
+    if (a->scratch_x) cudaFree(a->scratch_x);
+    if (a->scratch_y) cudaFree(a->scratch_y);
     if (a->d_masks) cudaFree(a->d_masks);
     if (a->d_disp_off32) cudaFree(a->d_disp_off32);
     delete a;
@@ -367,6 +369,12 @@ int spmvb_matrix_download(const spmvb_matrix *a, int32_t sid, uint64_t offset, u
 int spmvb_matrix_stream_ptr(const spmvb_matrix *a, int32_t sid, void **dev_ptr) {
     if (!a || !dev_ptr || sid < 0 || sid >= SPMVB_S_COUNT_) return fail(SPMVB_ERR_INVALID_ARGUMENT, "bad stream id %d", sid);
     *dev_ptr = a->s[sid];
+    return SPMVB_OK;
+}
+
+int spmvb_pattern_first_rows(const spmvb_matrix *a, int32_t *out) {
+    if (!a || !out || a->format != SPMVB_FMT_PATTERN) return fail(SPMVB_ERR_INVALID_ARGUMENT, "first_rows: needs a pattern handle");
+    for (int p = 0; p < a->n_patterns; p++) out[p] = p < (int)a->h_first_rows.size() ? a->h_first_rows[p] : -1;
     return SPMVB_OK;
 }
 

@@ -64,6 +64,10 @@ struct spmvb_matrix {
     std::vector<double> h_table;
     std::vector<int64_t> h_disp_offsets;
     std::vector<int32_t> h_disp_flat, h_ends_flat, h_exc_rows;
+    std::vector<int32_t> h_first_rows;  // first local row of each pattern (device-built handles)
+    // persistent scratch of spmvb_spmv_host (x and y on the device)
+    mutable double *scratch_x = nullptr, *scratch_y = nullptr;
+    mutable int64_t scratch_x_len = 0;
     spmvb::BoxPlan box;
     uint32_t *d_masks = nullptr;      // device copy of box.masks
     int32_t *d_disp_off32 = nullptr;  // 32-bit copy of disp_offsets for the kernels

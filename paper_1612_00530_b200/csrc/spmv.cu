@@ -216,70 +216,130 @@ __device__ __forceinline__ double box_load(const double *__restrict__ x, int64_t
     return __ldg(x + idx);
 }
 
-template <int R, int WC, bool OFF_NEG1, int CENTER_POS, bool GUARD>
+constexpr uint32_t kFullBox = 0x07FFFFFFu;
+
+// One warp: 32 consecutive a, Q consecutive planes c0..c0+Q-1 per thread (Q
+// independent accumulation chains), marching nb lines.  Window w[slot][plane][dx]
+// holds lines j-1, j, j+1 (+LA lines of look-ahead) of planes c0-1..c0+Q.
+template <int Q, int LA, bool OFF_NEG1, int CENTER_POS, bool GUARD>
 __device__ __forceinline__ void box_march(const PatternArgs &p, const uint32_t *s_masks, int64_t r, int nb,
-                                          int64_t n_rows, int c_dz_lo, int c_dz_hi) {
+                                          int64_t n_rows, int nq, bool lane_ok, bool pf_lo, bool pf_hi) {
+    constexpr int S = 3 + LA;
+    constexpr int P = Q + 2;
     const int64_t sy = p.sy;
     const int64_t sz = sy * p.plane_lines;
     const double *__restrict__ x = p.x;
-    int64_t xi = p.g0 + p.row_begin + r;  // x index of the diagonal of the current row
-    double w[4][9];
+    const int32_t *__restrict__ ids = p.ids + p.row_begin;
+    double *__restrict__ y = p.y + p.row_begin;
+    int64_t xi = p.g0 + p.row_begin + r;  // x index of the diagonal of (current line, plane c0)
+    double w[S][P][3];
     auto load_line = [&](int slot, int64_t centre) {
 #pragma unroll
-        for (int dz = 0; dz < 3; dz++)
+        for (int pz = 0; pz < P; pz++)
 #pragma unroll
             for (int dx = 0; dx < 3; dx++)
-                w[slot][dz * 3 + dx] = box_load<GUARD>(x, centre + (dz - 1) * sz + (dx - 1), p.x_len);
+                w[slot][pz][dx] = box_load<GUARD>(x, centre + (pz - 1) * sz + (dx - 1), p.x_len);
     };
-    load_line(3, xi - sy);
+    load_line(S - 1, xi - sy);
     load_line(0, xi);
-    load_line(1, xi + sy);
-    int id_next = (r < n_rows) ? ld_stream(p.ids + p.row_begin + r) : -1;
-    const int pf = p.prefetch;
-#pragma unroll 1
-    for (int j0 = 0; j0 < nb; j0 += 4) {
+    if (LA) load_line(1, xi + sy);
+    int id_next[Q];
 #pragma unroll
-        for (int k = 0; k < 4; k++) {
+    for (int q = 0; q < Q; q++)
+        id_next[q] = (lane_ok && q < nq && r + q * sz < n_rows) ? ld_stream(ids + r + q * sz) : -1;
+    const int pf = p.prefetch;
+    const double vc = p.v_center, vo = p.v_off;
+#pragma unroll 1
+    for (int j0 = 0; j0 < nb; j0 += S) {
+#pragma unroll
+        for (int k = 0; k < S; k++) {
             const int j = j0 + k;
-            if (j < nb && r < n_rows) {
-                // look-ahead: line j+2 into the free slot, next row's id
-                load_line((k + 2) & 3, xi + 2 * sy);
-                const int id = id_next;
-                id_next = (j + 1 < nb && r + sy < n_rows) ? ld_stream(p.ids + p.row_begin + r + sy) : -1;
+            if (j < nb) {
+                load_line((k + 1 + LA) % S, xi + (1 + LA) * sy);
+                int id[Q];
+                uint32_t mk[Q];
+                bool full = true;
+#pragma unroll
+                for (int q = 0; q < Q; q++) {
+                    id[q] = id_next[q];
+                    id_next[q] = (lane_ok && q < nq && j + 1 < nb && r + sy + q * sz < n_rows)
+                                     ? ld_stream(ids + r + sy + q * sz) : -1;
+                    mk[q] = id[q] >= 0 ? (s_masks ? s_masks[id[q]] : __ldg(p.masks + id[q])) : 0u;
+                    full = full && (mk[q] == kFullBox);
+                }
                 if (pf > 0) {  // pull the lines `pf` steps ahead from HBM into L2
                     const int64_t t = xi + (int64_t)pf * sy;
-                    if ((uint64_t)t < (uint64_t)p.x_len) prefetch_l2(x + t);
-                    if (c_dz_lo && (uint64_t)(t - sz) < (uint64_t)p.x_len) prefetch_l2(x + t - sz);
-                    if (c_dz_hi && (uint64_t)(t + sz) < (uint64_t)p.x_len) prefetch_l2(x + t + sz);
-                    if (r + (int64_t)pf * sy < n_rows) prefetch_l2(p.ids + p.row_begin + r + (int64_t)pf * sy);
-                }
-                if (id >= 0) {
-                    const uint32_t mask = s_masks ? s_masks[id] : __ldg(p.masks + id);
-                    double acc = 0.0;
-                    if (mask == kGenericMask) {
-                        acc = pattern_row(p, p.disp, p.ends, p.table, id, xi);
-                    } else {
-                        const double vc = p.v_center, vo = p.v_off;
-                        const double e13 = w[k & 3][4];
-                        if (CENTER_POS == 0) {
-                            if (mask >> 13 & 1u) acc = __dadd_rn(acc, __dmul_rn(vc, e13));
-                        }
 #pragma unroll
-                        for (int t = 0; t < 27; t++) {
-                            if (t == 13 && CENTER_POS != 2) continue;
-                            const int dz = t / 9, dy = (t / 3) % 3, dx = t % 3;
-                            const double e = w[(k + dy + 3) & 3][dz * 3 + dx];
-                            if (mask >> t & 1u) {
-                                if (OFF_NEG1) acc = __dsub_rn(acc, e);
-                                else acc = __dadd_rn(acc, __dmul_rn(vo, e));
-                            }
-                        }
-                        if (CENTER_POS == 1) {
-                            if (mask >> 13 & 1u) acc = __dadd_rn(acc, __dmul_rn(vc, e13));
+                    for (int q = 0; q < Q; q++) {
+                        const int64_t tq = t + q * sz;
+                        if ((uint64_t)tq < (uint64_t)p.x_len) prefetch_l2(x + tq);
+                        const int64_t rq = r + (int64_t)pf * sy + q * sz;
+                        if (q < nq && rq < n_rows) prefetch_l2(ids + rq);
+                    }
+                    if (pf_lo && (uint64_t)(t - sz) < (uint64_t)p.x_len) prefetch_l2(x + t - sz);
+                    if (pf_hi && (uint64_t)(t + Q * sz) < (uint64_t)p.x_len) prefetch_l2(x + t + Q * sz);
+                }
+                double acc[Q];
+#pragma unroll
+                for (int q = 0; q < Q; q++) acc[q] = 0.0;
+                const int sl[3] = {(k + S - 1) % S, k, (k + 1) % S};
+                if (__all_sync(0xffffffffu, full)) {
+                    // every row of this step has the full box: no selects on the chain
+                    if (CENTER_POS == 0) {
+#pragma unroll
+                        for (int q = 0; q < Q; q++) acc[q] = __dadd_rn(acc[q], __dmul_rn(vc, w[sl[1]][q + 1][1]));
+                    }
+#pragma unroll
+                    for (int t = 0; t < 27; t++) {
+                        if (t == 13 && CENTER_POS != 2) continue;
+                        const int dz = t / 9, dy = (t / 3) % 3, dx = t % 3;
+#pragma unroll
+                        for (int q = 0; q < Q; q++) {
+                            const double e = w[sl[dy]][q + dz][dx];
+                            acc[q] = OFF_NEG1 ? __dsub_rn(acc[q], e) : __dadd_rn(acc[q], __dmul_rn(vo, e));
                         }
                     }
-                    p.y[p.row_begin + r] = acc;
+                    if (CENTER_POS == 1) {
+#pragma unroll
+                        for (int q = 0; q < Q; q++) acc[q] = __dadd_rn(acc[q], __dmul_rn(vc, w[sl[1]][q + 1][1]));
+                    }
+                } else {
+                    // Masked rows: an absent entry contributes +0.0.  acc starts at +0.0 and can
+                    // never become -0.0 (round to nearest), so adding +-0.0 leaves it unchanged
+                    // bit for bit: identical to skipping the term as the reference does.
+                    if (CENTER_POS == 0) {
+#pragma unroll
+                        for (int q = 0; q < Q; q++) {
+                            const double pr = __dmul_rn(vc, w[sl[1]][q + 1][1]);
+                            acc[q] = __dadd_rn(acc[q], (mk[q] >> 13 & 1u) ? pr : 0.0);
+                        }
+                    }
+#pragma unroll
+                    for (int t = 0; t < 27; t++) {
+                        if (t == 13 && CENTER_POS != 2) continue;
+                        const int dz = t / 9, dy = (t / 3) % 3, dx = t % 3;
+#pragma unroll
+                        for (int q = 0; q < Q; q++) {
+                            const double e = w[sl[dy]][q + dz][dx];
+                            const bool on = mk[q] >> t & 1u;
+                            if (OFF_NEG1) acc[q] = __dsub_rn(acc[q], on ? e : 0.0);
+                            else acc[q] = __dadd_rn(acc[q], on ? __dmul_rn(vo, e) : 0.0);
+                        }
+                    }
+                    if (CENTER_POS == 1) {
+#pragma unroll
+                        for (int q = 0; q < Q; q++) {
+                            const double pr = __dmul_rn(vc, w[sl[1]][q + 1][1]);
+                            acc[q] = __dadd_rn(acc[q], (mk[q] >> 13 & 1u) ? pr : 0.0);
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < Q; q++)  // patterns outside the box: List 1 per lane
+                        if (mk[q] == kGenericMask) acc[q] = pattern_row(p, p.disp, p.ends, p.table, id[q], xi + q * sz);
                 }
+#pragma unroll
+                for (int q = 0; q < Q; q++)
+                    if (id[q] >= 0) y[r + q * sz] = acc[q];
                 r += sy;
                 xi += sy;
             }
@@ -287,7 +347,7 @@ __device__ __forceinline__ void box_march(const PatternArgs &p, const uint32_t *
     }
 }
 
-template <int R, int WC, bool OFF_NEG1, int CENTER_POS>
+template <int R, int WC, int Q, int LA, bool OFF_NEG1, int CENTER_POS>
 __global__ void __launch_bounds__(WC * 32) spmv_pattern_box_kernel(PatternArgs p, int n_planes) {
     __shared__ uint32_t s_masks_buf[kDictSmemPat];
     const uint32_t *s_masks = nullptr;
@@ -298,22 +358,25 @@ __global__ void __launch_bounds__(WC * 32) spmv_pattern_box_kernel(PatternArgs p
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int a = blockIdx.x * 32 + lane;
-    const int c = blockIdx.z * WC + warp;
+    const int c0 = (blockIdx.z * WC + warp) * Q;
     const int b0 = blockIdx.y * R;
-    if (a >= p.sy || c >= n_planes) return;
+    if (c0 >= n_planes) return;  // warp-uniform
     const int nb = min(R, p.plane_lines - b0);
+    const int nq = min(Q, n_planes - c0);
     const int64_t n_rows = (int64_t)p.row_end - p.row_begin;
-    const int64_t r = a + (int64_t)p.sy * (b0 + (int64_t)p.plane_lines * c);
-    if (r >= n_rows) return;
-    // Guard-free marching when every speculative window load of this warp is in range.
     const int64_t sy = p.sy, sz = sy * p.plane_lines;
-    const int64_t xi0 = p.g0 + p.row_begin + (r - lane);
+    const int64_t r = a + sy * (b0 + (int64_t)p.plane_lines * c0);
+    const int64_t r_warp = r - lane;
+    if (r_warp >= n_rows) return;  // warp-uniform
+    const bool lane_ok = a < p.sy;
+    // Guard-free marching when every speculative window load of this warp is in range.
+    const int64_t xi0 = p.g0 + p.row_begin + r_warp;
     const int64_t lo = xi0 - sy - sz - 1;
-    const int64_t hi = xi0 + 31 + (int64_t)(nb + 1) * sy + sz + 1;
+    const int64_t hi = xi0 + 31 + (int64_t)(nb + 1 + LA) * sy + (int64_t)Q * sz + 1;
     const bool safe = lo >= 0 && hi < p.x_len;
-    const int dz_lo = warp == 0, dz_hi = (warp == WC - 1) || (c == n_planes - 1);
-    if (safe) box_march<R, WC, OFF_NEG1, CENTER_POS, false>(p, s_masks, r, nb, n_rows, dz_lo, dz_hi);
-    else box_march<R, WC, OFF_NEG1, CENTER_POS, true>(p, s_masks, r, nb, n_rows, dz_lo, dz_hi);
+    const bool pf_lo = warp == 0, pf_hi = (warp == WC - 1) || (c0 + Q >= n_planes);
+    if (safe) box_march<Q, LA, OFF_NEG1, CENTER_POS, false>(p, s_masks, r, nb, n_rows, nq, lane_ok, pf_lo, pf_hi);
+    else box_march<Q, LA, OFF_NEG1, CENTER_POS, true>(p, s_masks, r, nb, n_rows, nq, lane_ok, pf_lo, pf_hi);
 }
 
 // ---- host-side launchers -----------------------------------------------------------
@@ -368,16 +431,16 @@ static int launch_vt(const spmvb_matrix *a, const double *x, int64_t x_col0, dou
     return check_launch("spmv_vt");
 }
 
-template <int R, int WC>
+template <int R, int WC, int Q, int LA>
 static int launch_box_rw(const spmvb_matrix *a, PatternArgs &p, cudaStream_t st) {
     const int64_t n_rows = (int64_t)p.row_end - p.row_begin;
     const int64_t sz = (int64_t)p.sy * p.plane_lines;
     const int n_planes = (int)((n_rows + sz - 1) / sz);
-    dim3 grid((p.sy + 31) / 32, (p.plane_lines + R - 1) / R, (n_planes + WC - 1) / WC);
+    dim3 grid((p.sy + 31) / 32, (p.plane_lines + R - 1) / R, (n_planes + WC * Q - 1) / (WC * Q));
     dim3 block(WC * 32);
     const bool neg1 = p.v_off == -1.0;
     const int cp = a->box.center_pos;
-#define LAUNCH(NEG, CP) spmv_pattern_box_kernel<R, WC, NEG, CP><<<grid, block, 0, st>>>(p, n_planes)
+#define LAUNCH(NEG, CP) spmv_pattern_box_kernel<R, WC, Q, LA, NEG, CP><<<grid, block, 0, st>>>(p, n_planes)
     if (neg1) {
         if (cp == 0) LAUNCH(true, 0); else if (cp == 1) LAUNCH(true, 1); else LAUNCH(true, 2);
     } else {
@@ -411,12 +474,17 @@ static int launch_pattern(const spmvb_matrix *a, const double *x, int64_t x_col0
         if (o.pattern_kernel == 2 && !a->box.valid)
             return fail(SPMVB_ERR_INVALID_ARGUMENT, "box kernel requested but the dictionary has no box plan");
         if (use_box) {
-            switch (o.box_march) {
-                case 1: SPMVB_TRY((launch_box_rw<16, 8>(a, p, st))); break;
-                case 2: SPMVB_TRY((launch_box_rw<64, 8>(a, p, st))); break;
-                case 3: SPMVB_TRY((launch_box_rw<32, 4>(a, p, st))); break;
-                case 4: SPMVB_TRY((launch_box_rw<32, 16>(a, p, st))); break;
-                default: SPMVB_TRY((launch_box_rw<32, 8>(a, p, st))); break;
+            switch (o.box_march) {  // <R lines, WC warps, Q planes/thread, look-ahead>
+                case 1: SPMVB_TRY((launch_box_rw<32, 8, 1, 1>(a, p, st))); break;
+                case 2: SPMVB_TRY((launch_box_rw<32, 4, 2, 1>(a, p, st))); break;
+                case 3: SPMVB_TRY((launch_box_rw<16, 4, 2, 1>(a, p, st))); break;
+                case 4: SPMVB_TRY((launch_box_rw<32, 4, 2, 0>(a, p, st))); break;
+                case 5: SPMVB_TRY((launch_box_rw<16, 4, 3, 0>(a, p, st))); break;
+                case 6: SPMVB_TRY((launch_box_rw<32, 4, 4, 0>(a, p, st))); break;
+                case 7: SPMVB_TRY((launch_box_rw<16, 4, 4, 0>(a, p, st))); break;
+                case 8: SPMVB_TRY((launch_box_rw<16, 2, 4, 0>(a, p, st))); break;
+                case 9: SPMVB_TRY((launch_box_rw<16, 8, 2, 0>(a, p, st))); break;
+                default: SPMVB_TRY((launch_box_rw<32, 4, 2, 1>(a, p, st))); break;
             }
         } else {
             const int threads = 256;
@@ -470,15 +538,21 @@ int spmvb_spmv_host(const spmvb_matrix *a, const double *x_host, int64_t x_len, 
     if (a->row_offset != 0) return fail(SPMVB_ERR_INVALID_ARGUMENT, "spmv_host: handle is a slab (row_offset != 0)");
     if (x_len != a->n)  // SPEC.md:212,222,232 "length mismatch"
         return fail(SPMVB_ERR_INVALID_ARGUMENT, "spmv: x has %lld entries, matrix has %d rows", (long long)x_len, a->n);
-    double *dx = nullptr, *dy = nullptr;
-    SPMVB_TRY(spmvb_vec_alloc(x_len, &dx));
-    int rc = spmvb_vec_alloc(a->n, &dy);
-    if (rc == SPMVB_OK) rc = spmvb_vec_upload(dx, x_host, x_len, nullptr);
-    if (rc == SPMVB_OK) rc = spmvb_spmv(a, dx, 0, x_len, dy, 0, a->n, nullptr);
-    if (rc == SPMVB_OK) rc = spmvb_vec_download(y_host, dy, a->n, nullptr);
-    cudaFree(dx);
-    if (dy) cudaFree(dy);
-    return rc;
+    // persistent device scratch: the matrix stays resident, only x and y cross the bus
+    if (a->scratch_x_len < x_len || !a->scratch_x) {
+        if (a->scratch_x) cudaFree(a->scratch_x);
+        if (a->scratch_y) cudaFree(a->scratch_y);
+        a->scratch_x = a->scratch_y = nullptr;
+        a->scratch_x_len = 0;
+        SPMVB_TRY(spmvb_vec_alloc(x_len, &a->scratch_x));
+        SPMVB_TRY(spmvb_vec_alloc(a->n, &a->scratch_y));
+        a->scratch_x_len = x_len;
+    }
+    SPMVB_CUDA(cudaMemcpyAsync(a->scratch_x, x_host, (size_t)x_len * 8, cudaMemcpyHostToDevice, nullptr));
+    SPMVB_TRY(spmvb_spmv(a, a->scratch_x, 0, x_len, a->scratch_y, 0, a->n, nullptr));
+    SPMVB_CUDA(cudaMemcpyAsync(y_host, a->scratch_y, (size_t)a->n * 8, cudaMemcpyDeviceToHost, nullptr));
+    SPMVB_CUDA(cudaStreamSynchronize(nullptr));
+    return SPMVB_OK;
 }
 
 }  // extern "C"

@@ -31,8 +31,9 @@ __global__ void compare_kernel(const double *__restrict__ y, const double *__res
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
         const double a = y[i], b = ref[i];
         if (__double_as_longlong(a) != __double_as_longlong(b)) bad++;
-        double den = fabs(b);
-        if (den == 0.0) den = scale ? scale[i] : 1.0;
+        // with a scale (sum_k |a_ik x_k|, >= |ref|) the deviation is relative to it, which does
+        // not blow up on rows whose terms cancel; without one it is relative to |ref|
+        double den = scale ? scale[i] : fabs(b);
         if (den == 0.0) den = 1.0;
         double rel = fabs(a - b) / den;
         if (!(rel == rel)) rel = INFINITY;  // NaN anywhere is a failure

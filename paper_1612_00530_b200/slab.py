@@ -1,0 +1,182 @@
+"""z-slab multi-GPU SpMV: one process per GPU, one-plane halo of x exchanged with
+the z-neighbours each SpMV (torch.distributed send/recv: NCCL over NVLink on
+GPUs, gloo in the CPU tests), overlapped with the rows that need no halo.
+
+Partitioning: with x-fastest numbering a z-slab is a
+contiguous row range [z0*plane, z1*plane) -- exactly the [begin,end) that
+unchecked::spmv_rows (kernels.hpp:27-36) already takes.  Rank r keeps
+x_local = [ghost plane below | owned planes | ghost plane above]; a global column
+c lives at x_local[c - x_col0] with x_col0 = (z0-1)*plane.  Displacements are
+translation invariant, so the global dictionary and the slice of the global
+row_pattern are used unchanged: per-slab streams are bit-identical to the slice
+of a single-device compression (ids after the dictionary merge below).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+
+@dataclass(frozen=True)
+class SlabLayout:
+    """Rows and ghost planes of one rank."""
+    nx: int
+    ny: int
+    nz_global: int
+    rank: int
+    world: int
+
+    @property
+    def plane(self):
+        return self.nx * self.ny
+
+    @property
+    def z_range(self):
+        """Planes [z0,z1): nz_global split as evenly as possible, low ranks get the remainder."""
+        base, rem = divmod(self.nz_global, self.world)
+        z0 = self.rank * base + min(self.rank, rem)
+        return z0, z0 + base + (1 if self.rank < rem else 0)
+
+    @property
+    def row_range(self):
+        z0, z1 = self.z_range
+        return z0 * self.plane, z1 * self.plane
+
+    @property
+    def n_local(self):
+        r0, r1 = self.row_range
+        return r1 - r0
+
+    @property
+    def has_lower(self):
+        return self.rank > 0
+
+    @property
+    def has_upper(self):
+        return self.rank < self.world - 1
+
+    @property
+    def x_col0(self):
+        """Global column of x_local[0]; the ghost slot below is allocated even on rank 0."""
+        return self.row_range[0] - self.plane
+
+    @property
+    def x_len(self):
+        return self.n_local + 2 * self.plane
+
+    def owned(self, x_local):
+        return x_local[self.plane:self.plane + self.n_local]
+
+
+def merge_dictionaries(local_dicts):
+    """Merge per-slab dictionaries into the numbering a single-matrix compression issues:
+    ids by first occurrence in ascending GLOBAL row order.
+
+    local_dicts: per rank, a list of (first_global_row, displacements tuple, ends tuple).
+    Returns (merged list of (displacements, ends), per-rank old->new id maps)."""
+    best = {}
+    for d in local_dicts:
+        for first, disp, ends in d:
+            key = (tuple(disp), tuple(ends))
+            if key not in best or first < best[key]:
+                best[key] = first
+    order = sorted(best, key=lambda k: best[k])
+    new_id = {k: i for i, k in enumerate(order)}
+    maps = [[new_id[(tuple(disp), tuple(ends))] for _, disp, ends in d] for d in local_dicts]
+    return order, maps
+
+
+class SlabSpmv:
+    """y_local = (A x)[slab rows] with the halo exchange overlapped with interior rows.
+
+    kernel(x_local, y_local, begin, end) computes local rows [begin,end); the product
+    passes the CUDA spmv_rows, the CPU tests inject the oracle's.  `dist` is
+    torch.distributed (or None for a single slab)."""
+
+    def __init__(self, layout: SlabLayout, kernel, dist=None, comm_stream=None, main_stream=None, torch=None):
+        self.L, self.kernel, self.dist = layout, kernel, dist
+        self.comm_stream, self.main_stream, self.torch = comm_stream, main_stream, torch
+
+    def _exchange_ops(self, x_local):
+        L, d = self.L, self.dist
+        p, n = L.plane, L.n_local
+        ops = []
+        if L.has_lower:  # my first owned plane -> lower neighbour's upper ghost; its last plane -> my lower ghost
+            ops.append(d.P2POp(d.isend, x_local[p:2 * p], L.rank - 1))
+            ops.append(d.P2POp(d.irecv, x_local[0:p], L.rank - 1))
+        if L.has_upper:
+            ops.append(d.P2POp(d.isend, x_local[n:n + p], L.rank + 1))
+            ops.append(d.P2POp(d.irecv, x_local[n + p:n + 2 * p], L.rank + 1))
+        return ops
+
+    def exchange(self, x_local):
+        """Blocking halo exchange (used by tests and as the non-overlapped baseline)."""
+        if self.dist is None or self.L.world == 1:
+            return
+        for r in self.dist.batch_isend_irecv(self._exchange_ops(x_local)):
+            r.wait()
+
+    def spmv(self, x_local, y_local):
+        """One SpMV: exchange || interior rows, then the first and last owned planes."""
+        L = self.L
+        p, n = L.plane, L.n_local
+        if self.dist is None or L.world == 1:
+            self.kernel(x_local, y_local, 0, n)
+            return
+        lo = min(p, n) if L.has_lower else 0        # rows [0,lo) need the lower ghost
+        hi = max(n - p, lo) if L.has_upper else n   # rows [hi,n) need the upper ghost
+        if self.comm_stream is not None:
+            t = self.torch
+            self.comm_stream.wait_stream(self.main_stream)  # x_local is ready
+            with t.cuda.stream(self.comm_stream):
+                reqs = self.dist.batch_isend_irecv(self._exchange_ops(x_local))
+            if hi > lo:
+                self.kernel(x_local, y_local, lo, hi)       # interior rows overlap the exchange
+            with t.cuda.stream(self.comm_stream):
+                for r in reqs:
+                    r.wait()
+            self.main_stream.wait_stream(self.comm_stream)
+        else:
+            reqs = self.dist.batch_isend_irecv(self._exchange_ops(x_local))
+            if hi > lo:
+                self.kernel(x_local, y_local, lo, hi)
+            for r in reqs:
+                r.wait()
+        if lo > 0:
+            self.kernel(x_local, y_local, 0, lo)
+        if hi < n:
+            self.kernel(x_local, y_local, hi, n)
+
+
+def build_slab_pattern(sp, layout: SlabLayout, dist=None, diagonal=26.0, off_diagonal=-1.0, perturb=None,
+                       values_in_pattern=True, min_pattern_rows=1, stream=None, keep_csr=False):
+    """Device-side build of one rank's compressed slab: generate the slab's rows, compress
+    them, then merge the per-slab dictionaries over `dist` so every rank holds the GLOBAL
+    dictionary and ids numbered as a single-device compression would (first occurrence in
+    ascending global row order).  No matrix data crosses ranks -- only the tiny dictionaries.
+    `sp` is the paper_1612_00530_b200 package."""
+    import numpy as np
+
+    spec = sp.GridSpec(layout.nx, layout.ny, layout.nz_global)
+    r0, r1 = layout.row_range
+    csr = sp.generate_matrix(spec, diagonal, off_diagonal, perturb=perturb, row_begin=r0, row_end=r1, stream=stream)
+    pc = sp.compress_patterns(csr, values_in_pattern, min_pattern_rows=min_pattern_rows, stream=stream)
+    if dist is not None and layout.world > 1:
+        info = pc.info
+        off = pc.download("disp_offsets")
+        disp, ends = pc.download("disp_flat"), pc.download("ends_flat")
+        first = sp.pattern_first_rows(pc)
+        mine = [(int(first[q]) + r0, tuple(disp[off[q]:off[q + 1]].tolist()),
+                 tuple(ends[q * info.m:(q + 1) * info.m].tolist())) for q in range(info.n_patterns)]
+        table = pc.download("table").tolist()
+        gathered = [None] * layout.world
+        dist.all_gather_object(gathered, (table, mine))
+        if any(t != table for t, _ in gathered):
+            raise sp.IntegrityError("slabs disagree on the value table")
+        merged, maps = merge_dictionaries([d for _, d in gathered])
+        offsets = np.zeros(len(merged) + 1, dtype=np.int64)
+        for q, (dd, _) in enumerate(merged):
+            offsets[q + 1] = offsets[q] + len(dd)
+        flat = np.array([v for dd, _ in merged for v in dd], dtype=np.int32)
+        ends_flat = np.array([v for _, ee in merged for v in ee], dtype=np.int32)
+        sp.pattern_remap(pc, offsets, flat, ends_flat, np.array(maps[layout.rank], dtype=np.int32), stream=stream)
+    return (pc, csr) if keep_csr else pc

@@ -61,8 +61,8 @@ if "pattern" in fmts or "generic" in fmts:
     d = sp.upload_pattern(pc.n, pc.table, pc.disp_offsets, pc.disp_flat, pc.ends_flat, pc.row_pattern, True)
     ref = None
     if "pattern" in fmts:
-        for march in (0, 1, 2, 3, 4):
-            for pf in (0, 4, 8, 16):
+        for march in (1, 2, 3, 4, 5, 6, 7, 8, 9):
+            for pf in (0, 4, 8):
                 timeit(d, f"pattern box march={march} pf={pf}", 20, pattern_kernel=2, box_march=march, box_prefetch=pf)
     if "generic" in fmts:
         timeit(d, "pattern generic", 20, pattern_kernel=1)
