@@ -176,6 +176,7 @@ static int *option_slot(const char *key) {
     if (!strcmp(key, "ell_kernel")) return &o.ell_kernel;
     if (!strcmp(key, "box_march")) return &o.box_march;
     if (!strcmp(key, "box_prefetch")) return &o.box_prefetch;
+    if (!strcmp(key, "box_prefetch_l1")) return &o.box_prefetch_l1;
     return nullptr;
 }
 

@@ -27,6 +27,14 @@ __device__ __forceinline__ int ld_stream(const int *p) {
 __device__ __forceinline__ void prefetch_l2(const void *p) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void prefetch_l1(const void *p) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
 
 // =============================================================================
 // ELL (inc/ell.hpp:10-24; spmv: inc/kernels.hpp:23,31-32)
@@ -148,6 +156,7 @@ struct PatternArgs {
     int sy, plane_lines;       // sy = stride of dy; plane_lines = sz / sy
     double v_off, v_center;
     int prefetch;              // L2 prefetch distance in lines
+    int prefetch_l1;           // L1 prefetch distance in lines (v3), 0 = off
 };
 
 // List 1, one row: groups in table order, per element value * x.
@@ -379,6 +388,493 @@ __global__ void __launch_bounds__(WC * 32) spmv_pattern_box_kernel(PatternArgs p
     else box_march<Q, LA, OFF_NEG1, CENTER_POS, true>(p, s_masks, r, nb, n_rows, nq, lane_ok, pf_lo, pf_hi);
 }
 
+// -----------------------------------------------------------------------------
+// Sliding-window kernel, version 3 ("box3"): the same plan as above with two
+// adjacent columns, Q planes and LPS lines per thread and step.
+//   * x-tiling: a thread owns columns a0, a0+1, so one 128-bit load brings both of
+//     its own elements of a line and two 64-bit loads bring the halo columns
+//     a0-1 / a0+2: 3 loads per (line, plane) serve 2 rows (v2: 3 loads per row).
+//   * 2*Q*LPS independent accumulation chains per thread: the reference's fixed
+//     summation order makes every row a 27-deep dependent DADD chain, so the FP64
+//     pipe is only kept busy by many chains in flight per scheduler.
+//   * All addresses are a warp-uniform base pointer (bumped once per step) plus a
+//     per-thread 32-bit offset.
+//   * Row masks: rows whose only missing entries are the nine dx=-1 (or dx=+1)
+//     ones -- the x-boundary rows, which sit in the thread's edge column -- are
+//     served by zeroing those nine halo operands; any other partial mask takes the
+//     fully masked chain.  Absent operands are +0.0, which leaves the accumulator
+//     unchanged bit for bit (it can never be -0.0), i.e. the reference's order.
+// Interior tiles (every window load and prefetch in range) march guard-free; edge
+// tiles use the guarded v2 march.  Needs even strides/offsets and 16-byte aligned
+// x, y, ids; otherwise the v2 kernel above is used.
+// -----------------------------------------------------------------------------
+constexpr uint32_t kLBits = 0x1249249u;  // box entries with dx = -1
+constexpr uint32_t kRBits = 0x4924924u;  // box entries with dx = +1
+
+template <int Q, int S, int LPS, bool OFF_NEG1, int CENTER_POS, int MODE, bool SELL, bool SELR>
+__device__ __forceinline__ void box3_chain(const double (&w)[S][Q + 2][4], int kb, const uint32_t (&mk)[LPS][Q][2],
+                                           const bool (&zl)[LPS][Q], const bool (&zr)[LPS][Q], double vc, double vo,
+                                           double (&acc)[LPS][Q][2]) {
+    // MODE 0: operands straight from the window (with SELL/SELR: halo operands zeroed per lane)
+    // MODE 1: every operand selected by its mask bit
+    // line l of the step reads slots (kb+l-1, kb+l, kb+l+1) mod S for dy = -1, 0, +1
+    double hl[LPS][Q][3][3], hr[LPS][Q][3][3];
+    if (MODE == 0 && (SELL || SELR)) {
+#pragma unroll
+        for (int l = 0; l < LPS; l++)
+#pragma unroll
+            for (int q = 0; q < Q; q++)
+#pragma unroll
+                for (int dz = 0; dz < 3; dz++)
+#pragma unroll
+                    for (int dy = 0; dy < 3; dy++) {
+                        const int s = (kb + l + dy + S - 1) % S;
+                        if (SELL) hl[l][q][dz][dy] = zl[l][q] ? 0.0 : w[s][q + dz][0];
+                        if (SELR) hr[l][q][dz][dy] = zr[l][q] ? 0.0 : w[s][q + dz][3];
+                    }
+    }
+#pragma unroll
+    for (int l = 0; l < LPS; l++)
+#pragma unroll
+        for (int q = 0; q < Q; q++) acc[l][q][0] = acc[l][q][1] = 0.0;
+    auto centre = [&]() {
+#pragma unroll
+        for (int l = 0; l < LPS; l++)
+#pragma unroll
+            for (int q = 0; q < Q; q++)
+#pragma unroll
+                for (int i = 0; i < 2; i++) {
+                    const double pr = __dmul_rn(vc, w[(kb + l) % S][q + 1][i + 1]);
+                    acc[l][q][i] = __dadd_rn(acc[l][q][i], (MODE == 1 && !(mk[l][q][i] >> 13 & 1u)) ? 0.0 : pr);
+                }
+    };
+    if (CENTER_POS == 0) centre();
+#pragma unroll
+    for (int t = 0; t < 27; t++) {
+        if (t == 13 && CENTER_POS != 2) continue;
+        const int dz = t / 9, dy = (t / 3) % 3, dx = t % 3;
+#pragma unroll
+        for (int l = 0; l < LPS; l++)
+#pragma unroll
+            for (int q = 0; q < Q; q++)
+#pragma unroll
+                for (int i = 0; i < 2; i++) {
+                    double e = w[(kb + l + dy + S - 1) % S][q + dz][i + dx];
+                    if (MODE == 0 && SELL && i + dx == 0) e = hl[l][q][dz][dy];
+                    if (MODE == 0 && SELR && i + dx == 3) e = hr[l][q][dz][dy];
+                    if (OFF_NEG1) {
+                        if (MODE == 1) e = (mk[l][q][i] >> t & 1u) ? e : 0.0;
+                        acc[l][q][i] = __dsub_rn(acc[l][q][i], e);
+                    } else {
+                        double pr = __dmul_rn(vo, e);
+                        if (MODE == 1) pr = (mk[l][q][i] >> t & 1u) ? pr : 0.0;
+                        acc[l][q][i] = __dadd_rn(acc[l][q][i], pr);
+                    }
+                }
+    }
+    if (CENTER_POS == 1) centre();
+}
+
+// Row classes (shared-memory tables indexed by pattern id + 1; entry 0 serves exception
+// rows, id = -1, which are computed as full rows and never stored).  cls0 is for rows in
+// the thread's left column, cls1 for its right column:
+//   0 full box; 1 (cls0) only the nine dx=-1 entries missing; 2 (cls1) only the nine
+//   dx=+1 entries missing; 4 any other mask (fully masked chain / List 1).
+struct Box3Smem {
+    uint32_t cls0, cls1, masks;  // 32-bit shared addresses of the three tables
+};
+
+template <int Q, int LPS, bool OFF_NEG1, int CENTER_POS>
+__device__ __forceinline__ void box3_march(const PatternArgs &p, const Box3Smem sm, const double *__restrict__ xw,
+                                           const int32_t *__restrict__ idw, double *__restrict__ yw, int64_t xi_w, int lane,
+                                           int nb, bool lane_ok, int nq) {
+    constexpr int S = LPS + 2, P = Q + 2;
+    constexpr int U = (S % LPS == 0) ? S / LPS : S;  // steps until the slot pattern repeats
+    const int sy = p.sy;
+    const int sz = sy * p.plane_lines;
+    const int lo = lane * 2;
+    double w[S][P][4];
+    auto load_line = [&](int slot, int line_off) {
+#pragma unroll
+        for (int pz = 0; pz < P; pz++) {
+            const double *pl = xw + (lo + (pz - 1) * sz + line_off);
+            const double2 v = __ldg(reinterpret_cast<const double2 *>(pl));
+            w[slot][pz][0] = __ldg(pl - 1);
+            w[slot][pz][1] = v.x;
+            w[slot][pz][2] = v.y;
+            w[slot][pz][3] = __ldg(pl + 2);
+        }
+    };
+    bool vq[Q];  // rows of plane q exist for this lane
+#pragma unroll
+    for (int q = 0; q < Q; q++) vq[q] = lane_ok && q < nq;
+    auto load_ids = [&](int q, bool line_ok, int line_off) {
+        int2 r = make_int2(-1, -1);  // rows outside the tile's valid columns / planes / lines: computed, never stored
+        if (vq[q] && line_ok) {
+            const int2 *ptr = reinterpret_cast<const int2 *>(idw + (lo + q * sz + line_off));
+            asm volatile("ld.global.nc.L1::no_allocate.v2.s32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(ptr));
+        }
+        return r;
+    };
+    load_line(S - 1, -sy);
+    load_line(0, 0);
+    int2 idn[LPS][Q];
+#pragma unroll
+    for (int l = 0; l < LPS; l++)
+#pragma unroll
+        for (int q = 0; q < Q; q++) idn[l][q] = load_ids(q, l < nb, l * sy);
+    const int pf = p.prefetch * LPS * sy;  // L2 prefetch distance in elements
+    const double vc = p.v_center, vo = p.v_off;
+#pragma unroll 1
+    for (int j0 = 0; j0 < nb; j0 += U * LPS) {
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int jb = j0 + u * LPS;   // first line of this step
+            const int kb = (u * LPS) % S;  // its slot
+            if (jb < nb) {
+#pragma unroll
+                for (int l = 0; l < LPS; l++) load_line((kb + 1 + l) % S, (1 + l) * sy);
+                int id[LPS][Q][2];
+                uint32_t c0[LPS][Q], c1[LPS][Q], wv = 0;
+#pragma unroll
+                for (int l = 0; l < LPS; l++)
+#pragma unroll
+                    for (int q = 0; q < Q; q++) {
+                        id[l][q][0] = idn[l][q].x;
+                        id[l][q][1] = idn[l][q].y;
+                        idn[l][q] = load_ids(q, jb + LPS + l < nb, (LPS + l) * sy);
+                        c0[l][q] = lds_u32(sm.cls0 + 4 + 4 * id[l][q][0]);
+                        c1[l][q] = lds_u32(sm.cls1 + 4 + 4 * id[l][q][1]);
+                        wv |= c0[l][q] | c1[l][q];
+                    }
+                if (pf > 0) {  // pull the lines `prefetch` steps ahead from HBM into L2
+#pragma unroll
+                    for (int l = 0; l < LPS; l++)
+#pragma unroll
+                        for (int q = 0; q < Q; q++) {
+                            prefetch_l2(xw + (lo + q * sz + l * sy + pf));
+                            prefetch_l2(idw + (lo + q * sz + l * sy + pf));
+                        }
+                }
+                double acc[LPS][Q][2];
+                uint32_t mk[LPS][Q][2];
+                bool zl[LPS][Q], zr[LPS][Q];
+                const unsigned vote = __reduce_or_sync(0xffffffffu, wv);  // 1 some L-partial, 2 some R-partial, 4 other
+                if (vote == 0) {
+                    box3_chain<Q, S, LPS, OFF_NEG1, CENTER_POS, 0, false, false>(w, kb, mk, zl, zr, vc, vo, acc);
+                } else if (vote == 1 || vote == 2) {
+#pragma unroll
+                    for (int l = 0; l < LPS; l++)
+#pragma unroll
+                        for (int q = 0; q < Q; q++) {
+                            zl[l][q] = c0[l][q] != 0;
+                            zr[l][q] = c1[l][q] != 0;
+                        }
+                    if (vote == 1) box3_chain<Q, S, LPS, OFF_NEG1, CENTER_POS, 0, true, false>(w, kb, mk, zl, zr, vc, vo, acc);
+                    else box3_chain<Q, S, LPS, OFF_NEG1, CENTER_POS, 0, false, true>(w, kb, mk, zl, zr, vc, vo, acc);
+                } else {
+#pragma unroll
+                    for (int l = 0; l < LPS; l++)
+#pragma unroll
+                        for (int q = 0; q < Q; q++)
+#pragma unroll
+                            for (int i = 0; i < 2; i++) mk[l][q][i] = lds_u32(sm.masks + 4 + 4 * id[l][q][i]);
+                    box3_chain<Q, S, LPS, OFF_NEG1, CENTER_POS, 1, false, false>(w, kb, mk, zl, zr, vc, vo, acc);
+#pragma unroll
+                    for (int l = 0; l < LPS; l++)
+#pragma unroll
+                        for (int q = 0; q < Q; q++)
+#pragma unroll
+                            for (int i = 0; i < 2; i++)  // patterns outside the box: List 1 per lane
+                                if (mk[l][q][i] == kGenericMask)
+                                    acc[l][q][i] = pattern_row(p, p.disp, p.ends, p.table, id[l][q][i],
+                                                               xi_w + lo + (int64_t)l * sy + q * (int64_t)sz + i);
+                }
+#pragma unroll
+                for (int l = 0; l < LPS; l++)
+#pragma unroll
+                    for (int q = 0; q < Q; q++) {
+                        double *dst = yw + (lo + q * sz + l * sy);
+                        if ((id[l][q][0] | id[l][q][1]) >= 0)
+                            *reinterpret_cast<double2 *>(dst) = make_double2(acc[l][q][0], acc[l][q][1]);
+                        else {
+                            if (id[l][q][0] >= 0) dst[0] = acc[l][q][0];
+                            if (id[l][q][1] >= 0) dst[1] = acc[l][q][1];
+                        }
+                    }
+                xw += LPS * sy;
+                idw += LPS * sy;
+                yw += LPS * sy;
+                xi_w += (int64_t)LPS * sy;
+            }
+        }
+    }
+}
+
+// Fills the class / mask tables of Box3Smem (entry 0 = exception rows -> full box).
+__device__ __forceinline__ void box3_fill_tables(const PatternArgs &p, uint32_t *cls0, uint32_t *cls1, uint32_t *masks,
+                                                 int tid, int nthreads) {
+    for (int i = tid; i <= p.n_patterns; i += nthreads) {
+        const uint32_t m = i == 0 ? kFullBox : p.masks[i - 1];
+        masks[i] = m;
+        cls0[i] = m == kFullBox ? 0u : (m == (kFullBox & ~kLBits) ? 1u : 4u);
+        cls1[i] = m == kFullBox ? 0u : (m == (kFullBox & ~kRBits) ? 2u : 4u);
+    }
+}
+
+// grid edges / slab ends / ragged ranges: the guarded one-column march of the v2 kernel, per half warp-tile
+template <int Q, bool OFF_NEG1, int CENTER_POS>
+__device__ __noinline__ void box3_edge_tile(const PatternArgs &p, const uint32_t *s_masks, int64_t r_w, int lane, int nb,
+                                            int64_t n_rows, int nq, int cols_ok) {
+#pragma unroll 1
+    for (int half = 0; half < 2; half++)
+        box_march<Q, 0, OFF_NEG1, CENTER_POS, true>(p, s_masks, r_w + half * 32 + lane, nb, n_rows, nq,
+                                                    half * 32 + lane < cols_ok, false, false);
+}
+
+template <int R, int WC, int Q, int LPS, int MINB, bool OFF_NEG1, int CENTER_POS>
+__global__ void __launch_bounds__(WC * 32, MINB) spmv_pattern_box3_kernel(PatternArgs p, int n_planes) {
+    __shared__ uint32_t s_cls0[kDictSmemPat + 1], s_cls1[kDictSmemPat + 1], s_masks1[kDictSmemPat + 1];
+    box3_fill_tables(p, s_cls0, s_cls1, s_masks1, threadIdx.x, WC * 32);
+    const uint32_t *s_masks = s_masks1 + 1;
+    __syncthreads();
+    Box3Smem sm;
+    sm.cls0 = (uint32_t)__cvta_generic_to_shared(s_cls0);
+    sm.cls1 = (uint32_t)__cvta_generic_to_shared(s_cls1);
+    sm.masks = (uint32_t)__cvta_generic_to_shared(s_masks1);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int a_w = blockIdx.x * 64;  // first column of the warp
+    const int c0 = (blockIdx.z * WC + warp) * Q;
+    const int b0 = blockIdx.y * R;
+    if (c0 >= n_planes) return;
+    const int nb = min(R, p.plane_lines - b0);
+    const int nq = min(Q, n_planes - c0);
+    const int64_t n_rows = (int64_t)p.row_end - p.row_begin;
+    const int64_t sy = p.sy, sz = sy * p.plane_lines;
+    const int64_t r_w = a_w + sy * (b0 + (int64_t)p.plane_lines * c0);  // relative row of (lane 0, first line, plane c0)
+    if (r_w >= n_rows) return;
+    const int cols_ok = min(64, p.sy - a_w);
+    const int64_t xi_w = p.g0 + p.row_begin + r_w;
+    const int pf = (p.prefetch > 0 ? p.prefetch : 0) * LPS;
+    // Guard-free march when every row of the tile's valid columns/planes/lines is in the row range
+    // and every window load and prefetch of the warp is in range; rows of missing columns / planes
+    // / lines are computed on in-range data and dropped.
+    const int nb_up = (nb + LPS - 1) / LPS * LPS;
+    const int64_t last_row = r_w + (cols_ok - 1) + (int64_t)(nb - 1) * sy + (int64_t)(nq - 1) * sz;
+    const int64_t x_lo = xi_w - sy - sz - 1;
+    const int64_t x_hi = xi_w + 64 + (int64_t)(nb_up + LPS + pf) * sy + (int64_t)Q * sz + 1;
+    const int64_t id_hi = r_w + 64 + (int64_t)(nb_up + LPS + pf) * sy + (int64_t)(nq - 1) * sz;  // ids prefetch reach
+    const bool interior = last_row < n_rows && x_lo >= 0 && x_hi < p.x_len && id_hi <= n_rows + 1024;
+    if (interior) {
+        box3_march<Q, LPS, OFF_NEG1, CENTER_POS>(p, sm, p.x + xi_w, p.ids + p.row_begin + r_w, p.y + p.row_begin + r_w, xi_w,
+                                                 lane, nb, lane * 2 + 1 < cols_ok, nq);
+    } else {
+        box3_edge_tile<Q, OFF_NEG1, CENTER_POS>(p, s_masks, r_w, lane, nb, n_rows, nq, cols_ok);
+    }
+}
+
+// -----------------------------------------------------------------------------
+// Sliding-window kernel, version 4 ("box5"): box3's arithmetic fed from a
+// multi-stage shared-memory ring.  The stall profile of box3 showed the FP64 chains
+// were not the limit: every step exposed L2/HBM latency on its serial setup (window
+// loads, ids -> mask -> vote -> branch) with only ~2.5 warps per scheduler.  Here the
+// CTA's x lines (WC*Q+2 planes x 68 doubles) and pattern ids (WC*Q planes x 64 ints)
+// of line l are copied global -> shared with cp.async (16-byte chunks, L2 only) DEPTH
+// lines ahead of their use, so the per-step critical path only sees shared-memory
+// latency, and the z halo between the warps of a CTA is fetched once per CTA.
+// Interior CTAs only (all copies in range); edge CTAs use the guarded v2 march.
+// Needs strides and offsets that are multiples of 4 rows and 16-byte aligned arrays.
+// -----------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async16(uint32_t dst_smem, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst_smem), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int R, int WC, int Q, int DEPTH, int MINB, bool OFF_NEG1, int CENTER_POS>
+__global__ void __launch_bounds__(WC * 32, MINB) spmv_pattern_box5_kernel(PatternArgs p, int n_planes) {
+    constexpr int T = WC * 32;
+    constexpr int NP = WC * Q;         // planes computed by the CTA
+    constexpr int XP = NP + 2;         // x planes staged (one halo plane each side)
+    constexpr int XW = 68;             // staged doubles per x line: columns a_w-2 .. a_w+65
+    constexpr int XCH = XP * (XW / 2); // 16-byte chunks of x per stage
+    constexpr int ICH = NP * 16;       // 16-byte chunks of ids per stage
+    constexpr int NCH = XCH + ICH;
+    constexpr int PER = (NCH + T - 1) / T;
+    constexpr int S = 3, P = Q + 2;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double *xs = reinterpret_cast<double *>(smem_raw);                              // [DEPTH][XP][XW]
+    int32_t *is = reinterpret_cast<int32_t *>(smem_raw + (size_t)DEPTH * XP * XW * 8);  // [DEPTH][NP][64]
+    __shared__ uint32_t s_masks[kDictSmemPat];
+    for (int i = threadIdx.x; i < p.n_patterns; i += T) s_masks[i] = p.masks[i];
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int a_w = blockIdx.x * 64;
+    const int c0 = blockIdx.z * NP;   // first plane of the CTA
+    const int b0 = blockIdx.y * R;
+    const int nb = min(R, p.plane_lines - b0);
+    const int64_t n_rows = (int64_t)p.row_end - p.row_begin;
+    const int64_t sy64 = p.sy, sz64 = sy64 * p.plane_lines;
+    const int64_t r_c = a_w + sy64 * (b0 + (int64_t)p.plane_lines * c0);  // relative row of (column a_w, line b0, plane c0)
+    const int cols_ok = min(64, p.sy - a_w);
+    const int nq_cta = min(NP, n_planes - c0);
+    const int64_t xi_c = p.g0 + p.row_begin + r_c;
+    // interior CTA: every staged byte (lines -1..nb, planes c0-1..c0+NP) is inside x, every id read inside ids
+    const int64_t x_lo = xi_c - sy64 - sz64 - 2;
+    const int64_t x_hi = xi_c + 66 + (int64_t)nb * sy64 + (int64_t)NP * sz64;
+    const int64_t last_row = r_c + (cols_ok - 1) + (int64_t)(nb - 1) * sy64 + (int64_t)(nq_cta - 1) * sz64;
+    const bool interior = x_lo >= 0 && x_hi < p.x_len && last_row < n_rows && cols_ok == 64;
+    __syncthreads();
+    if (!interior) {  // CTA-uniform: grid edges, slab ends, ragged ranges
+        const int cw = c0 + warp * Q;
+        if (cw < n_planes && r_c + (int64_t)warp * Q * sz64 < n_rows)
+            box3_edge_tile<Q, OFF_NEG1, CENTER_POS>(p, s_masks, r_c + (int64_t)warp * Q * sz64, lane, nb, n_rows,
+                                                    min(Q, n_planes - cw), cols_ok);
+        return;
+    }
+    const int sy = p.sy, sz = sy * p.plane_lines;
+    // ---- per-thread copy plan: chunk c = tid + k*T -> (source offset, shared offset)
+    const double *xg = p.x + xi_c;                       // (column a_w, line b0, plane c0)
+    const int32_t *ig = p.ids + p.row_begin + r_c;
+    int src_off[PER];       // elements, relative to xg (doubles) or ig (ints), for line 0
+    uint32_t dst_off[PER];  // bytes from the start of a stage's x (or ids) area
+    int kind[PER];          // 0 x, 1 ids, 2 none
+    const uint32_t xs_base = (uint32_t)__cvta_generic_to_shared(xs);
+    const uint32_t is_base = (uint32_t)__cvta_generic_to_shared(is);
+#pragma unroll
+    for (int k = 0; k < PER; k++) {
+        const int c = threadIdx.x + k * T;
+        if (c < XCH) {
+            const int pz = c / (XW / 2), j = c % (XW / 2);
+            kind[k] = 0;
+            src_off[k] = (pz - 1) * sz - 2 + 2 * j;
+            dst_off[k] = (uint32_t)((pz * XW + 2 * j) * 8);
+        } else if (c < NCH) {
+            const int q = (c - XCH) / 16, j = (c - XCH) % 16;
+            kind[k] = q < nq_cta ? 1 : 2;
+            src_off[k] = q * sz + 4 * j;
+            dst_off[k] = (uint32_t)((q * 64 + 4 * j) * 4);
+        } else {
+            kind[k] = 2; src_off[k] = 0; dst_off[k] = 0;
+        }
+    }
+    auto fetch = [&](int line) {  // stage line `line` (-1 .. nb) into ring slot (line+1) % DEPTH; always one group
+        if (line <= nb) {
+            const int slot = (line + 1) % DEPTH;
+#pragma unroll
+            for (int k = 0; k < PER; k++) {
+                if (kind[k] == 0)
+                    cp_async16(xs_base + (uint32_t)(slot * XP * XW * 8) + dst_off[k], xg + (src_off[k] + line * sy));
+                else if (kind[k] == 1 && line >= 0 && line < nb)
+                    cp_async16(is_base + (uint32_t)(slot * NP * 64 * 4) + dst_off[k], ig + (src_off[k] + line * sy));
+            }
+        }
+        cp_async_commit();
+    };
+    // ---- consumer view: this warp's planes are staged x planes warp*Q .. warp*Q+Q+1
+    const int pw = warp * Q;
+    const bool warp_on = c0 + pw < n_planes;
+    const int nq = min(Q, n_planes - (c0 + pw));
+    double w[S][P][4];
+    auto load_line = [&](int wslot, int line) {
+        const double *base = xs + ((line + 1) % DEPTH) * (XP * XW) + pw * XW + 2 * lane;
+#pragma unroll
+        for (int pz = 0; pz < P; pz++) {
+            const double *pl = base + pz * XW;
+            const double2 v = *reinterpret_cast<const double2 *>(pl + 2);
+            w[wslot][pz][0] = pl[1];
+            w[wslot][pz][1] = v.x;
+            w[wslot][pz][2] = v.y;
+            w[wslot][pz][3] = pl[4];
+        }
+    };
+#pragma unroll
+    for (int l = -1; l < DEPTH - 1; l++) fetch(l);  // DEPTH groups in flight: lines -1 .. DEPTH-2
+    cp_async_wait<DEPTH - 2>();                     // lines -1 and 0 have landed
+    __syncthreads();
+    load_line(S - 1, -1);
+    load_line(0, 0);
+    double *yw = p.y + p.row_begin + r_c + (int64_t)pw * sz64 + 2 * lane;
+    const double vc = p.v_center, vo = p.v_off;
+    // L2 prefetch only while its farthest address stays inside x and ids
+    const int pf = (x_hi + (int64_t)(DEPTH + p.prefetch) * sy64 < p.x_len &&
+                    last_row + (int64_t)(DEPTH + p.prefetch) * sy64 < n_rows) ? p.prefetch : 0;
+#pragma unroll 1
+    for (int j0 = 0; j0 < nb; j0 += S) {
+#pragma unroll
+        for (int k = 0; k < S; k++) {
+            const int j = j0 + k;
+            if (j < nb) {  // CTA-uniform
+                cp_async_wait<DEPTH - 3>();  // line j+1 has landed (groups up to line j+DEPTH-2 are committed)
+                __syncthreads();             // ... for every thread's copies; slot of line j-1 is free again
+                fetch(j + DEPTH - 1);
+                if (pf > 0 && lane < 8) {    // a little further ahead: HBM -> L2, one request per 128-byte line
+                    const int line = j + DEPTH - 1 + pf;
+#pragma unroll
+                    for (int q = 0; q < Q; q++) {
+                        prefetch_l2(xg + ((pw + q) * sz + line * sy + 16 * lane));
+                        if (lane < 2) prefetch_l2(ig + ((pw + q) * sz + line * sy + 32 * lane));
+                    }
+                    if (warp == 0) prefetch_l2(xg + (-sz + line * sy + 16 * lane));
+                    if (warp == WC - 1) prefetch_l2(xg + (NP * sz + line * sy + 16 * lane));
+                }
+                load_line((k + 1) % S, j + 1);
+                if (warp_on) {
+                    int id[1][Q][2];
+                    uint32_t mk[1][Q][2];
+                    bool zl[1][Q], zr[1][Q], other = false, anyl = false, anyr = false;
+                    const int32_t *idl = is + ((j + 1) % DEPTH) * (NP * 64) + pw * 64 + 2 * lane;
+#pragma unroll
+                    for (int q = 0; q < Q; q++) {
+                        int2 v = make_int2(-1, -1);
+                        if (q < nq) v = *reinterpret_cast<const int2 *>(idl + q * 64);
+                        id[0][q][0] = v.x;
+                        id[0][q][1] = v.y;
+#pragma unroll
+                        for (int i = 0; i < 2; i++)  // exception rows (id < 0) are computed as full rows and not stored
+                            mk[0][q][i] = id[0][q][i] >= 0 ? s_masks[id[0][q][i]] : kFullBox;
+                        zl[0][q] = mk[0][q][0] == (kFullBox & ~kLBits);
+                        zr[0][q] = mk[0][q][1] == (kFullBox & ~kRBits);
+                        other = other || !(mk[0][q][0] == kFullBox || zl[0][q]) || !(mk[0][q][1] == kFullBox || zr[0][q]);
+                        anyl = anyl || zl[0][q];
+                        anyr = anyr || zr[0][q];
+                    }
+                    double acc[1][Q][2];
+                    const unsigned vote = __ballot_sync(0xffffffffu, other) ? 4u
+                                          : ((__ballot_sync(0xffffffffu, anyl) ? 1u : 0u) | (__ballot_sync(0xffffffffu, anyr) ? 2u : 0u));
+                    if (vote == 0) box3_chain<Q, S, 1, OFF_NEG1, CENTER_POS, 0, false, false>(w, k, mk, zl, zr, vc, vo, acc);
+                    else if (vote == 1) box3_chain<Q, S, 1, OFF_NEG1, CENTER_POS, 0, true, false>(w, k, mk, zl, zr, vc, vo, acc);
+                    else if (vote == 2) box3_chain<Q, S, 1, OFF_NEG1, CENTER_POS, 0, false, true>(w, k, mk, zl, zr, vc, vo, acc);
+                    else {
+                        box3_chain<Q, S, 1, OFF_NEG1, CENTER_POS, 1, false, false>(w, k, mk, zl, zr, vc, vo, acc);
+#pragma unroll
+                        for (int q = 0; q < Q; q++)
+#pragma unroll
+                            for (int i = 0; i < 2; i++)  // patterns outside the box: List 1 per lane
+                                if (mk[0][q][i] == kGenericMask)
+                                    acc[0][q][i] = pattern_row(p, p.disp, p.ends, p.table, id[0][q][i],
+                                                               xi_c + (int64_t)(pw + q) * sz64 + (int64_t)j * sy64 + 2 * lane + i);
+                    }
+#pragma unroll
+                    for (int q = 0; q < Q; q++) {
+                        double *dst = yw + (q * sz + j * sy);
+                        if (id[0][q][0] >= 0 && id[0][q][1] >= 0)
+                            *reinterpret_cast<double2 *>(dst) = make_double2(acc[0][q][0], acc[0][q][1]);
+                        else {
+                            if (id[0][q][0] >= 0) dst[0] = acc[0][q][0];
+                            if (id[0][q][1] >= 0) dst[1] = acc[0][q][1];
+                        }
+                    }
+                }
+            }
+        }
+    }
+    cp_async_wait<0>();
+}
+
 // ---- host-side launchers -----------------------------------------------------------
 static int check_launch(const char *what) {
     cudaError_t e = cudaGetLastError();
@@ -450,6 +946,61 @@ static int launch_box_rw(const spmvb_matrix *a, PatternArgs &p, cudaStream_t st)
     return check_launch("spmv_pattern_box");
 }
 
+// v3 launch: returns 1 when the configuration / alignment is not served (caller falls back to v2)
+template <int R, int WC, int Q, int LPS, int MINB, bool ALLV>
+static int launch_box3(const spmvb_matrix *a, PatternArgs &p, cudaStream_t st) {
+    const int64_t n_rows = (int64_t)p.row_end - p.row_begin;
+    const int64_t sz = (int64_t)p.sy * p.plane_lines;
+    const int n_planes = (int)((n_rows + sz - 1) / sz);
+    const bool neg1 = p.v_off == -1.0;
+    const int cp = a->box.center_pos;
+    if (!ALLV && !(neg1 && cp == 1)) return 1;
+    dim3 grid((p.sy + 63) / 64, (p.plane_lines + R - 1) / R, (n_planes + WC * Q - 1) / (WC * Q));
+    dim3 block(WC * 32);
+#define LAUNCH3(NEG, CP) spmv_pattern_box3_kernel<R, WC, Q, LPS, MINB, NEG, CP><<<grid, block, 0, st>>>(p, n_planes)
+    if constexpr (ALLV) {
+        if (neg1) {
+            if (cp == 0) LAUNCH3(true, 0); else if (cp == 1) LAUNCH3(true, 1); else LAUNCH3(true, 2);
+        } else {
+            if (cp == 0) LAUNCH3(false, 0); else if (cp == 1) LAUNCH3(false, 1); else LAUNCH3(false, 2);
+        }
+    } else {
+        LAUNCH3(true, 1);
+    }
+#undef LAUNCH3
+    return check_launch("spmv_pattern_box3") == SPMVB_OK ? 0 : -1;
+}
+
+// v4 (shared-memory ring) launch: returns 1 when not served
+template <int R, int WC, int Q, int DEPTH, int MINB>
+static int launch_box5(const spmvb_matrix *a, PatternArgs &p, cudaStream_t st) {
+    const int64_t n_rows = (int64_t)p.row_end - p.row_begin;
+    const int64_t sz = (int64_t)p.sy * p.plane_lines;
+    const int n_planes = (int)((n_rows + sz - 1) / sz);
+    if (!(p.v_off == -1.0 && a->box.center_pos == 1)) return 1;
+    if (p.sy % 4 || (p.g0 + p.row_begin) % 4 || p.row_begin % 4) return 1;
+    constexpr int NP = WC * Q;
+    const size_t smem = (size_t)DEPTH * ((NP + 2) * 68 * 8 + NP * 64 * 4);
+    static bool attr_set = false;
+    if (!attr_set) {
+        if (cudaFuncSetAttribute(spmv_pattern_box5_kernel<R, WC, Q, DEPTH, MINB, true, 1>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return -1;
+        attr_set = true;
+    }
+    dim3 grid((p.sy + 63) / 64, (p.plane_lines + R - 1) / R, (n_planes + NP - 1) / NP);
+    spmv_pattern_box5_kernel<R, WC, Q, DEPTH, MINB, true, 1><<<grid, WC * 32, smem, st>>>(p, n_planes);
+    return check_launch("spmv_pattern_box5") == SPMVB_OK ? 0 : -1;
+}
+
+// Conditions of the v3 kernel: vector loads need even strides/offsets and 16-byte aligned
+// arrays; all in-tile offsets must fit 32 bits; masks must fit the shared-memory table.
+static bool box3_ok(const spmvb_matrix *a, const PatternArgs &p) {
+    const int64_t sz = (int64_t)p.sy * p.plane_lines;
+    return (p.sy % 2 == 0) && ((p.g0 + p.row_begin) % 2 == 0) && (p.row_begin % 2 == 0) &&
+           ((uintptr_t)p.x % 16 == 0) && ((uintptr_t)p.y % 16 == 0) && ((uintptr_t)p.ids % 8 == 0) &&
+           a->n_patterns <= kDictSmemPat && 6 * sz + 128 * (int64_t)p.sy + 4096 < INT32_MAX;
+}
+
 static int launch_pattern(const spmvb_matrix *a, const double *x, int64_t x_col0, int64_t x_len, double *y,
                           int row_begin, int row_end, cudaStream_t st) {
     if (row_end > row_begin) {
@@ -469,22 +1020,44 @@ static int launch_pattern(const spmvb_matrix *a, const double *x, int64_t x_col0
         p.v_off = a->box.valid ? a->h_table[a->box.k_off] : 0.0;
         p.v_center = a->box.valid ? a->h_table[a->box.k_center] : 0.0;
         const Options &o = options();
-        p.prefetch = o.box_prefetch >= 0 ? o.box_prefetch : 6;
+        p.prefetch = o.box_prefetch >= 0 ? o.box_prefetch : 2;
+        p.prefetch_l1 = o.box_prefetch_l1;
         const bool use_box = a->box.valid && o.pattern_kernel != 1;
         if (o.pattern_kernel == 2 && !a->box.valid)
             return fail(SPMVB_ERR_INVALID_ARGUMENT, "box kernel requested but the dictionary has no box plan");
         if (use_box) {
-            switch (o.box_march) {  // <R lines, WC warps, Q planes/thread, look-ahead>
-                case 1: SPMVB_TRY((launch_box_rw<32, 8, 1, 1>(a, p, st))); break;
-                case 2: SPMVB_TRY((launch_box_rw<32, 4, 2, 1>(a, p, st))); break;
-                case 3: SPMVB_TRY((launch_box_rw<16, 4, 2, 1>(a, p, st))); break;
-                case 4: SPMVB_TRY((launch_box_rw<32, 4, 2, 0>(a, p, st))); break;
-                case 5: SPMVB_TRY((launch_box_rw<16, 4, 3, 0>(a, p, st))); break;
-                case 6: SPMVB_TRY((launch_box_rw<32, 4, 4, 0>(a, p, st))); break;
-                case 7: SPMVB_TRY((launch_box_rw<16, 4, 4, 0>(a, p, st))); break;
-                case 8: SPMVB_TRY((launch_box_rw<16, 2, 4, 0>(a, p, st))); break;
-                case 9: SPMVB_TRY((launch_box_rw<16, 8, 2, 0>(a, p, st))); break;
-                default: SPMVB_TRY((launch_box_rw<32, 4, 2, 1>(a, p, st))); break;
+            int rc3 = 1;  // 1 = not served by v3
+            if (o.pattern_kernel != 3 && box3_ok(a, p)) {
+                const int64_t n_planes = ((int64_t)row_end - row_begin + (int64_t)p.sy * p.plane_lines - 1) / ((int64_t)p.sy * p.plane_lines);
+                if (n_planes == 1) rc3 = launch_box3<16, 4, 1, 2, 3, false>(a, p, st);  // single-plane ranges (slab boundary planes)
+                else if (o.box_march >= 20) switch (o.box_march) {  // ring kernel <R, WC, Q, DEPTH, min CTAs/SM>
+                    case 20: rc3 = launch_box5<16, 4, 2, 4, 3>(a, p, st); break;
+                    case 21: rc3 = launch_box5<32, 4, 2, 4, 3>(a, p, st); break;
+                    case 22: rc3 = launch_box5<16, 4, 2, 6, 3>(a, p, st); break;
+                    case 23: rc3 = launch_box5<16, 8, 2, 4, 1>(a, p, st); break;
+                    case 24: rc3 = launch_box5<16, 4, 1, 4, 4>(a, p, st); break;
+                    case 25: rc3 = launch_box5<32, 8, 1, 4, 2>(a, p, st); break;
+                    case 26: rc3 = launch_box5<64, 4, 2, 4, 3>(a, p, st); break;
+                    default: rc3 = launch_box5<16, 4, 2, 4, 3>(a, p, st); break;
+                }
+                else switch (o.box_march) {  // <R lines, WC warps, Q planes/thread, lines/step, min CTAs/SM>
+                    case 1: rc3 = launch_box3<16, 4, 2, 1, 3, false>(a, p, st); break;
+                    case 2: rc3 = launch_box3<16, 4, 2, 2, 2, false>(a, p, st); break;
+                    case 3: rc3 = launch_box3<32, 4, 2, 2, 2, false>(a, p, st); break;
+                    case 4: rc3 = launch_box3<16, 8, 2, 2, 1, false>(a, p, st); break;
+                    case 5: rc3 = launch_box3<16, 4, 1, 2, 3, false>(a, p, st); break;
+                    case 6: rc3 = launch_box3<16, 4, 3, 2, 2, false>(a, p, st); break;
+                    case 7: rc3 = launch_box3<8, 4, 2, 1, 3, false>(a, p, st); break;
+                    case 8: rc3 = launch_box3<16, 2, 2, 2, 4, false>(a, p, st); break;
+                    case 9: rc3 = launch_box3<16, 4, 1, 4, 2, false>(a, p, st); break;
+                    case 10: rc3 = launch_box3<8, 4, 2, 2, 2, false>(a, p, st); break;
+                    default: rc3 = launch_box3<8, 4, 2, 1, 3, true>(a, p, st); break;  // best measured at 256^3 (profiles/)
+                }
+                if (rc3 < 0) return SPMVB_ERR_CUDA;
+            }
+            if (rc3 == 1) {  // v2: any stride / alignment / value pattern
+                if (o.box_march == 11) SPMVB_TRY((launch_box_rw<32, 8, 1, 1>(a, p, st)));
+                else SPMVB_TRY((launch_box_rw<16, 8, 2, 0>(a, p, st)));
             }
         } else {
             const int threads = 256;

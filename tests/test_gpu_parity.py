@@ -68,8 +68,9 @@ def test_all_formats_bit_exact(sp, orc, g):
         assert (np.abs(y - ys[0]) / scale).max() <= 1e-13
 
 
-@pytest.mark.parametrize("g", [(4, 4, 4), (6, 6, 6), (33, 9, 5), (40, 37, 11), (32, 32, 32)])
-@pytest.mark.parametrize("kernel", [1, 2])
+@pytest.mark.parametrize("g", [(4, 4, 4), (6, 6, 6), (33, 9, 5), (40, 37, 11), (32, 32, 32), (128, 20, 12), (64, 33, 9),
+                               (192, 17, 10), (100, 18, 11)])
+@pytest.mark.parametrize("kernel", [1, 2, 3])
 def test_pattern_kernels_generic_and_box(sp, orc, g, kernel):
     m = orc.generate_matrix(*g)
     pc = orc.compress_patterns(m, True)
@@ -85,9 +86,10 @@ def test_pattern_kernels_generic_and_box(sp, orc, g, kernel):
     assert np.array_equal(bits(y), bits(orc.spmv(pc, x)))
 
 
-@pytest.mark.parametrize("march", [1, 2, 3, 4, 5, 6, 7, 8, 9])
-def test_box_march_variants(sp, orc, march):
-    m = orc.generate_matrix(40, 37, 11)
+@pytest.mark.parametrize("march", [1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 20, 21, 22, 23, 24, 25, 26])
+@pytest.mark.parametrize("g", [(40, 37, 11), (128, 36, 20), (192, 40, 19)])
+def test_box_march_variants(sp, orc, march, g):
+    m = orc.generate_matrix(*g)
     pc = orc.compress_patterns(m, True)
     d = up_pat(sp, pc)
     x = orc.make_test_vector(m.n, orc.RANDOM, seed=5, lo=-1.0, hi=1.0)
@@ -116,11 +118,37 @@ def test_no_box_plan_for_flat_grids(sp, orc):
 def test_value_pairs_and_centre_position(sp, orc, vals):
     """centre last (off < diag), centre first (off > diag), single-value table, generic multiply."""
     diag, off = vals
+    test_value_pairs_big(sp, orc, vals)
     m = orc.generate_matrix(9, 8, 7, diag, off)
     x = orc.make_test_vector(m.n, orc.RANDOM, seed=11, lo=-1.0, hi=1.0)
     for ref, dev in ((orc.to_ell(m), None), (orc.compress_values(m), None), (orc.compress_patterns(m), None)):
         dev = {orc.Ell: up_ell, orc.Vt: up_vt, orc.Pattern: up_pat}[type(ref)](sp, ref)
         assert np.array_equal(bits(run(sp, dev, x)), bits(orc.spmv(ref, x)))
+
+
+def test_value_pairs_big(sp, orc, vals=(0.5, 3.0)):
+    """Same on a grid wide enough for the guard-free vector march."""
+    diag, off = vals
+    m = orc.generate_matrix(128, 20, 12, diag, off)
+    x = orc.make_test_vector(m.n, orc.RANDOM, seed=11, lo=-1.0, hi=1.0)
+    ref = orc.compress_patterns(m)
+    assert np.array_equal(bits(run(sp, up_pat(sp, ref), x)), bits(orc.spmv(ref, x)))
+
+
+def test_row_ranges_big_grid(sp, orc):
+    """Ragged row ranges on a grid with interior tiles: every partition gives the single-call result."""
+    m = orc.generate_matrix(128, 20, 12)
+    x = orc.make_test_vector(m.n, orc.RANDOM, seed=7, lo=-1.0, hi=1.0)
+    ref = orc.compress_patterns(m)
+    dev = up_pat(sp, ref)
+    full = orc.spmv(ref, x)
+    dx = sp.DeviceVector.from_host(x)
+    dy = sp.DeviceVector.from_host(np.full(m.n, np.nan))
+    plane = 128 * 20
+    cuts = [0, 2, 2 * plane, 2 * plane + 130, 5 * plane + 7, 9 * plane, m.n]
+    for b, e in zip(cuts[:-1], cuts[1:]):
+        sp.spmv_rows(dev, dx, dy, b, e)
+    assert np.array_equal(bits(dy.to_host()), bits(full))
 
 
 def test_row_ranges_untouched_and_bit_identical(sp, orc):
@@ -147,9 +175,10 @@ def test_row_ranges_untouched_and_bit_identical(sp, orc):
             sp.spmv(dev, np.ones(m.n - 1))
 
 
-def test_slab_with_ghost_planes(sp, orc):
+@pytest.mark.parametrize("g", [(12, 10, 9), (128, 18, 9)])
+def test_slab_with_ghost_planes(sp, orc, g):
     """z-slab: local ids/ELL slices with global columns, ghosted local x (x_col0 = first ghost column)."""
-    nx, ny, nz = 12, 10, 9
+    nx, ny, nz = g
     plane = nx * ny
     m = orc.generate_matrix(nx, ny, nz)
     x = orc.make_test_vector(m.n, orc.RANDOM, seed=7, lo=-1.0, hi=1.0)
@@ -170,7 +199,7 @@ def test_slab_with_ghost_planes(sp, orc):
             assert np.array_equal(bits(y), bits(full[key][r0:r1])), (key, z0, z1)
 
 
-@pytest.mark.parametrize("g", [(16, 16, 16), (48, 40, 36)])
+@pytest.mark.parametrize("g", [(16, 16, 16), (48, 40, 36), (128, 20, 12)])
 def test_hybrid_exception_rows(sp, orc, g):
     """Config-4 style matrix: perturbed rows become uncompressed exception rows."""
     m = orc.generate_matrix(*g, perturb=(11, 0.1, 0.1))
@@ -184,7 +213,7 @@ def test_hybrid_exception_rows(sp, orc, g):
     ref = orc.spmv(pc, x)
     exc = pc.exc_rows  # exception rows are summed in ELL slot order == ascending-column (CSR) order
     assert np.array_equal(bits(ref[exc]), bits(orc.spmv(m, x)[exc]))
-    for kernel in (1, 2):
+    for kernel in (1, 2, 3):
         sp.set_option("pattern_kernel", kernel)
         try:
             y = run(sp, d, x)
