@@ -84,7 +84,7 @@ void destroy(spmvb_matrix *a);
 
 struct Options {
     int pattern_kernel = 0;  // 0 auto, 1 generic (List 1), 2 box (v3, else v2), 3 box v2 only
-    int ell_kernel = 0;      // 0 auto (staged), 1 naive thread-per-row
+    int ell_kernel = 0;      // 0 auto (ELL: TMA bulk pipeline, vt: staged), 1 naive, 2 staged vector loads, 3 TMA for vt too
     int box_march = 0;       // 0 default
     int box_prefetch = -1;   // L2 prefetch distance in lines (-1 = default)
     int box_prefetch_l1 = 0; // L1 prefetch distance in lines (0 = off)

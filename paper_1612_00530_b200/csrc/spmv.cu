@@ -36,6 +36,43 @@ __device__ __forceinline__ void prefetch_l1(const void *p) {
     asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
 
+
+// ---- per-row accumulation from a staged tile (shared memory), reference order ---------------
+// The gathers of x are issued in independent batches of B before the ordered sums consume
+// them, so a row costs ~width/B L2 latencies instead of `width`.
+template <int B>
+__device__ __forceinline__ double ell_row(const double *v, const int32_t *c, int width, const double *__restrict__ x,
+                                          int64_t x_col0) {
+    // inc/kernels.hpp:19-20: slot order; padding slots multiply 0.0 by x[own row]
+    double acc = 0.0;
+    for (int base = 0; base < width; base += B) {
+        double xv[B];
+#pragma unroll
+        for (int j = 0; j < B; j++) xv[j] = base + j < width ? __ldg(x + ((int64_t)c[base + j] - x_col0)) : 0.0;
+#pragma unroll
+        for (int j = 0; j < B; j++)
+            if (base + j < width) acc = __dadd_rn(acc, __dmul_rn(v[base + j], xv[j]));
+    }
+    return acc;
+}
+
+template <int B>
+__device__ __forceinline__ double vt_row(const int32_t *c, const int32_t *e, const double *tab, int m,
+                                         const double *__restrict__ x, int64_t x_col0) {
+    // inc/kernels.hpp:20-22: per value group (table order) sum x in stored order, then one product.
+    // (Batching the gathers inside a group was measured slower than this plain loop: 509 vs 470 us
+    // at 256^3 -- the group bookkeeping costs more than the latency it hides at full occupancy.)
+    double acc = 0.0;
+    int idx = 0;
+    for (int k = 0; k < m; k++) {
+        double sum = 0.0;
+        const int end = e[k];
+        for (; idx < end; idx++) sum = __dadd_rn(sum, __ldg(x + ((int64_t)c[idx] - x_col0)));
+        acc = __dadd_rn(acc, __dmul_rn(tab[k], sum));
+    }
+    return acc;
+}
+
 // =============================================================================
 // ELL (inc/ell.hpp:10-24; spmv: inc/kernels.hpp:23,31-32)
 // Row-major n x width.  A tile of kTileRows rows is one contiguous block of each
@@ -70,12 +107,7 @@ __global__ void __launch_bounds__(ROWS) spmv_ell_kernel(const double *__restrict
     __syncthreads();
     const int r = r0 + threadIdx.x;
     if (r < row_begin || r >= row_end) return;
-    const double *v = sv + threadIdx.x * width;
-    const int32_t *c = sc + threadIdx.x * width;
-    double acc = 0.0;
-#pragma unroll 9
-    for (int k = 0; k < width; k++) acc = __dadd_rn(acc, __dmul_rn(v[k], __ldg(x + ((int64_t)c[k] - x_col0))));
-    y[row_map ? row_map[r] : r] = acc;
+    y[row_map ? row_map[r] : r] = ell_row<9>(sv + threadIdx.x * width, sc + threadIdx.x * width, width, x, x_col0);
 }
 
 // Naive thread-per-row form, kept as the A/B baseline ("ell_kernel" = 1).
@@ -122,17 +154,107 @@ __global__ void __launch_bounds__(ROWS) spmv_vt_kernel(const int32_t *__restrict
     __syncthreads();
     const int r = r0 + threadIdx.x;
     if (r < row_begin || r >= row_end) return;
-    const int32_t *c = sc + threadIdx.x * width;
-    const int32_t *e = se + threadIdx.x * m;
-    double acc = 0.0;
-    int idx = 0;
-    for (int k = 0; k < m; k++) {
-        double sum = 0.0;
-        const int end = e[k];
-        for (; idx < end; idx++) sum = __dadd_rn(sum, __ldg(x + ((int64_t)c[idx] - x_col0)));
-        acc = __dadd_rn(acc, __dmul_rn(st[k], sum));
+    y[r] = vt_row<9>(sc + threadIdx.x * width, se + threadIdx.x * m, st, m, x, x_col0);
+}
+
+// =============================================================================
+// TMA (bulk-copy) pipelines for the row-major streams.  A persistent CTA walks
+// 128-row tiles; one elected thread issues `cp.async.bulk` (SASS UBLKCP) copies of
+// the tile's contiguous value / column blocks into a ring of NS shared-memory
+// stages, completion is signalled on an mbarrier per stage (complete_tx), all
+// threads then accumulate their own row from shared memory in the reference
+// order.  While one stage is consumed the other NS-1 are in flight, so HBM never
+// idles during the gather/accumulate phase (the vectorised-load kernels above
+// alternate between a load phase and a compute phase).
+// =============================================================================
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint32_t bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_LOOP:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@p bra DONE;\n\t"
+        "bra WAIT_LOOP;\n"
+        "DONE:\n\t}" ::"r"(bar), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+
+// FMT 0: ELL (a = values f64, b = columns i32, wa = wb = width)
+// FMT 1: vt  (a unused,       b = sorted_columns i32 (wb = width), c = ends i32 (wc = m), table)
+template <int ROWS, int NS, int FMT>
+__global__ void __launch_bounds__(ROWS) spmv_rows_tma_kernel(const double *__restrict__ values,
+                                                            const int32_t *__restrict__ columns,
+                                                            const int32_t *__restrict__ ends,
+                                                            const double *__restrict__ table, int width, int m,
+                                                            const double *__restrict__ x, int64_t x_col0,
+                                                            double *__restrict__ y, int row_begin, int row_end, int tile0,
+                                                            int n_tiles, const int32_t *__restrict__ row_map) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const uint32_t bytes_v = FMT == 0 ? (uint32_t)ROWS * width * 8 : 0;
+    const uint32_t bytes_c = (uint32_t)ROWS * width * 4;
+    const uint32_t bytes_e = FMT == 1 ? (uint32_t)ROWS * m * 4 : 0;
+    const uint32_t stage_bytes = bytes_v + bytes_c + bytes_e;  // each a multiple of 16
+    __shared__ __align__(8) uint64_t full_bar[NS];
+    __shared__ double s_table[FMT == 1 ? 256 : 1];
+    if (FMT == 1)
+        for (int i = threadIdx.x; i < m && i < 256; i += ROWS) s_table[i] = table[i];
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NS; s++) mbar_init(smem_u32(&full_bar[s]), 1);
+        fence_mbar_init();
     }
-    y[r] = acc;
+    __syncthreads();
+    auto issue = [&](int it) {  // elected thread: fetch the it-th tile of this CTA into stage it % NS
+        const int tile = blockIdx.x + it * gridDim.x;
+        if (tile >= n_tiles) return;
+        const int s = it % NS;
+        const int64_t r0 = (int64_t)(tile0 + tile) * ROWS;
+        const uint32_t bar = smem_u32(&full_bar[s]);
+        const uint32_t dst = smem_u32(smem + (size_t)s * stage_bytes);
+        mbar_expect_tx(bar, stage_bytes);
+        if (FMT == 0) bulk_g2s(dst, values + r0 * width, bytes_v, bar);
+        bulk_g2s(dst + bytes_v, columns + r0 * width, bytes_c, bar);
+        if (FMT == 1) bulk_g2s(dst + bytes_v + bytes_c, ends + r0 * m, bytes_e, bar);
+    };
+    if (threadIdx.x == 0)
+        for (int it = 0; it < NS; it++) issue(it);
+    for (int it = 0;; it++) {
+        const int tile = blockIdx.x + it * gridDim.x;
+        if (tile >= n_tiles) break;
+        const int s = it % NS;
+        mbar_wait(smem_u32(&full_bar[s]), (it / NS) & 1);
+        const unsigned char *st = smem + (size_t)s * stage_bytes;
+        const int r = (tile0 + tile) * ROWS + threadIdx.x;
+        if (r >= row_begin && r < row_end) {
+            const int32_t *c = reinterpret_cast<const int32_t *>(st + bytes_v) + threadIdx.x * width;
+            double acc;
+            if (FMT == 0) {
+                const double *v = reinterpret_cast<const double *>(st) + threadIdx.x * width;
+                acc = width == 27 ? ell_row<27>(v, c, 27, x, x_col0) : ell_row<9>(v, c, width, x, x_col0);
+            } else {
+                const int32_t *e = reinterpret_cast<const int32_t *>(st + bytes_v + bytes_c) + threadIdx.x * m;
+                const double *tab = m <= 256 ? s_table : table;
+                acc = vt_row<9>(c, e, tab, m, x, x_col0);
+            }
+            y[row_map ? row_map[r] : r] = acc;
+        }
+        __syncthreads();  // every thread is done with stage s
+        if (threadIdx.x == 0) {
+            fence_proxy_async();  // order the generic-proxy reads before the async-proxy refill
+            issue(it + NS);
+        }
+    }
 }
 
 // =============================================================================
@@ -899,6 +1021,24 @@ static int launch_ell(const double *values, const int32_t *columns, int width, c
     const int tiles = (row_end + kTileRows - 1) / kTileRows - tile0;
     const size_t smem = (size_t)kTileRows * width * 12;
     if (smem > 200 * 1024) return fail(SPMVB_ERR_INVALID_ARGUMENT, "ELL width %d too large for the staged kernel", width);
+    if (options().ell_kernel != 2) {
+        // TMA bulk pipeline (default): persistent CTAs, NS stages of one tile each
+        constexpr int NS = 2;
+        const size_t stage = smem;  // multiple of 16 for any width (128 rows)
+        const size_t need = stage * NS;
+        if (need <= 220 * 1024) {
+            static bool tma_attr = false;
+            if (!tma_attr) {
+                SPMVB_CUDA(cudaFuncSetAttribute(spmv_rows_tma_kernel<kTileRows, NS, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+                tma_attr = true;
+            }
+            const int per_sm = std::max(1, (int)std::min<size_t>(8, (220 * 1024) / (need + 1024)));
+            const int grid = std::min(tiles, 148 * per_sm);
+            spmv_rows_tma_kernel<kTileRows, NS, 0><<<grid, kTileRows, need, st>>>(values, columns, nullptr, nullptr, width, 0, x, x_col0, y,
+                                                                               row_begin, row_end, tile0, tiles, row_map);
+            return check_launch("spmv_ell_tma");
+        }
+    }
     static bool attr_set = false;
     if (!attr_set) {
         SPMVB_CUDA(cudaFuncSetAttribute(spmv_ell_kernel<kTileRows>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -916,6 +1056,24 @@ static int launch_vt(const spmvb_matrix *a, const double *x, int64_t x_col0, dou
     const int tiles = (row_end + kTileRows - 1) / kTileRows - tile0;
     const size_t smem = (size_t)kTileRows * (a->width + a->m) * 4 + (size_t)a->m * 8 + 16;
     if (smem > 200 * 1024) return fail(SPMVB_ERR_INVALID_ARGUMENT, "vt width/table too large for the staged kernel");
+    if (options().ell_kernel == 3) {  // TMA bulk pipeline: measured slower than the staged kernel for vt (545 vs 470 us)
+        constexpr int NS = 2;
+        const size_t stage = (size_t)kTileRows * (a->width + a->m) * 4;
+        const size_t need = stage * NS;
+        if (need <= 200 * 1024) {
+            static bool tma_attr = false;
+            if (!tma_attr) {
+                SPMVB_CUDA(cudaFuncSetAttribute(spmv_rows_tma_kernel<kTileRows, NS, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+                tma_attr = true;
+            }
+            const int per_sm = std::max(1, (int)std::min<size_t>(8, (200 * 1024) / (need + 4096)));
+            const int grid = std::min(tiles, 148 * per_sm);
+            spmv_rows_tma_kernel<kTileRows, NS, 1><<<grid, kTileRows, need, st>>>(
+                nullptr, static_cast<const int32_t *>(a->s[SPMVB_S_SORTED_COLUMNS]), static_cast<const int32_t *>(a->s[SPMVB_S_ENDS]),
+                static_cast<const double *>(a->s[SPMVB_S_TABLE]), a->width, a->m, x, x_col0, y, row_begin, row_end, tile0, tiles, nullptr);
+            return check_launch("spmv_vt_tma");
+        }
+    }
     static bool attr_set = false;
     if (!attr_set) {
         SPMVB_CUDA(cudaFuncSetAttribute(spmv_vt_kernel<kTileRows>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));

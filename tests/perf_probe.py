@@ -76,11 +76,13 @@ if "vt" in fmts or "ell" in fmts:
         vt = orc.compress_values(m)
         d = sp.upload_vt(vt.n, vt.width, vt.table, vt.sorted_columns, vt.ends)
         del vt
-        timeit(d, "vt staged", 132)
+        timeit(d, "vt staged vector loads", 132)
+        timeit(d, "vt tma pipeline", 132, ell_kernel=3)
         del d
     if "ell" in fmts:
         e = orc.to_ell(m)
         d = sp.upload_ell(e.n, e.width, e.nnz, e.values, e.columns)
         del e
-        timeit(d, "ell staged", 340)
+        timeit(d, "ell tma pipeline", 340)
+        timeit(d, "ell staged vector loads", 340, ell_kernel=2)
         timeit(d, "ell naive", 340, ell_kernel=1)

@@ -227,6 +227,27 @@ def test_hybrid_exception_rows(sp, orc, g):
     assert (np.abs(y_ell - ref) / orc.row_abs_scale(m, x)).max() <= 1e-12
 
 
+@pytest.mark.parametrize("ell_kernel", [0, 1, 2, 3])
+def test_ell_vt_kernel_variants(sp, orc, ell_kernel):
+    """TMA bulk pipeline (0), naive (1) and staged vector-load (2) kernels agree bit for bit with the oracle."""
+    for g in [(5, 4, 3), (33, 9, 5), (64, 33, 9), (128, 20, 12)]:
+        m = orc.generate_matrix(*g)
+        x = orc.make_test_vector(m.n, orc.RANDOM, seed=7, lo=-1.0, hi=1.0)
+        ell, vt = orc.to_ell(m), orc.compress_values(m)
+        sp.set_option("ell_kernel", ell_kernel)
+        try:
+            ye, yv = run(sp, up_ell(sp, ell), x), run(sp, up_vt(sp, vt), x)
+            dx = sp.DeviceVector.from_host(x)
+            dy = sp.DeviceVector.from_host(np.full(m.n, 5.0))
+            sp.spmv_rows(up_ell(sp, ell), dx, dy, 3, m.n - 2)  # ragged range
+            part = dy.to_host()
+        finally:
+            sp.set_option("ell_kernel", 0)
+        assert np.array_equal(bits(ye), bits(orc.spmv(ell, x))) and np.array_equal(bits(yv), bits(orc.spmv(vt, x)))
+        assert np.all(part[:3] == 5.0) and np.all(part[-2:] == 5.0)
+        assert np.array_equal(bits(part[3:-2]), bits(orc.spmv(ell, x)[3:-2]))
+
+
 def test_fig_row_and_explicit_rows(sp, orc):
     rows = [[(i, 26.0)] for i in range(66)]
     rows[50] = [(45, -1.0), (49, -1.0), (50, 26.0), (51, -1.0), (65, -1.0)]
