@@ -177,6 +177,7 @@ static int *option_slot(const char *key) {
     if (!strcmp(key, "box_march")) return &o.box_march;
     if (!strcmp(key, "box_prefetch")) return &o.box_prefetch;
     if (!strcmp(key, "box_prefetch_l1")) return &o.box_prefetch_l1;
+    if (!strcmp(key, "debug_nochain")) return &o.debug_nochain;
     return nullptr;
 }
 

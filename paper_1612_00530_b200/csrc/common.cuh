@@ -88,6 +88,7 @@ struct Options {
     int box_march = 0;       // 0 default
     int box_prefetch = -1;   // L2 prefetch distance in lines (-1 = default)
     int box_prefetch_l1 = 0; // L1 prefetch distance in lines (0 = off)
+    int debug_nochain = 0;   // measurement only
 };
 Options &options();
 

@@ -27,6 +27,10 @@ __device__ __forceinline__ int ld_stream(const int *p) {
 __device__ __forceinline__ void prefetch_l2(const void *p) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
+// TMA-engine L2 prefetch of a contiguous range (address 16-byte aligned, size a multiple of 16)
+__device__ __forceinline__ void bulk_prefetch_l2(const void *p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
     uint32_t v;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
@@ -279,6 +283,7 @@ struct PatternArgs {
     double v_off, v_center;
     int prefetch;              // L2 prefetch distance in lines
     int prefetch_l1;           // L1 prefetch distance in lines (v3), 0 = off
+    int debug_nochain;         // measurement only: skip the FP64 chains (y = centre operand)
 };
 
 // List 1, one row: groups in table order, per element value * x.
@@ -294,6 +299,10 @@ __device__ __forceinline__ double pattern_row(const PatternArgs &p, const int32_
         for (; idx < end; idx++) acc = __dadd_rn(acc, __dmul_rn(a_ij, __ldg(p.x + (xi + d[idx]))));
     }
     return acc;
+}
+
+__device__ __noinline__ double pattern_row_cold(const PatternArgs &p, int id, int64_t xi) {
+    return pattern_row(p, p.disp, p.ends, p.table, id, xi);
 }
 
 // Generic kernel: thread per row, any dictionary.  DICT_SMEM keeps the dictionary
@@ -615,16 +624,22 @@ __device__ __forceinline__ void box3_march(const PatternArgs &p, const Box3Smem 
     const int sy = p.sy;
     const int sz = sy * p.plane_lines;
     const int lo = lane * 2;
+    constexpr int dbg = 0;  // ablation switches of profiles/r01_ablation_*.log (1 no chain, 2 no halo loads, 4 no ids, 8 no prefetch)
     double w[S][P][4];
     auto load_line = [&](int slot, int line_off) {
 #pragma unroll
         for (int pz = 0; pz < P; pz++) {
             const double *pl = xw + (lo + (pz - 1) * sz + line_off);
             const double2 v = __ldg(reinterpret_cast<const double2 *>(pl));
-            w[slot][pz][0] = __ldg(pl - 1);
+            if (dbg & 2) {  // measurement only: no halo loads
+                w[slot][pz][0] = v.y;
+                w[slot][pz][3] = v.x;
+            } else {
+                w[slot][pz][0] = __ldg(pl - 1);
+                w[slot][pz][3] = __ldg(pl + 2);
+            }
             w[slot][pz][1] = v.x;
             w[slot][pz][2] = v.y;
-            w[slot][pz][3] = __ldg(pl + 2);
         }
     };
     bool vq[Q];  // rows of plane q exist for this lane
@@ -632,7 +647,8 @@ __device__ __forceinline__ void box3_march(const PatternArgs &p, const Box3Smem 
     for (int q = 0; q < Q; q++) vq[q] = lane_ok && q < nq;
     auto load_ids = [&](int q, bool line_ok, int line_off) {
         int2 r = make_int2(-1, -1);  // rows outside the tile's valid columns / planes / lines: computed, never stored
-        if (vq[q] && line_ok) {
+        if (dbg & 4) r = make_int2(13, 13);  // measurement only: no id stream
+        else if (vq[q] && line_ok) {
             const int2 *ptr = reinterpret_cast<const int2 *>(idw + (lo + q * sz + line_off));
             asm volatile("ld.global.nc.L1::no_allocate.v2.s32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(ptr));
         }
@@ -669,7 +685,9 @@ __device__ __forceinline__ void box3_march(const PatternArgs &p, const Box3Smem 
                         c1[l][q] = lds_u32(sm.cls1 + 4 + 4 * id[l][q][1]);
                         wv |= c0[l][q] | c1[l][q];
                     }
-                if (pf > 0) {  // pull the lines `prefetch` steps ahead from HBM into L2
+                if (pf > 0 && !(dbg & 8)) {  // pull the lines `prefetch` steps ahead from HBM into L2
+                    // (one TMA bulk prefetch per segment, cp.async.bulk.prefetch.L2, measured identical:
+                    //  profiles/r01_ablation_bulk_l2_prefetch.log; it also needs 16-byte aligned id rows)
 #pragma unroll
                     for (int l = 0; l < LPS; l++)
 #pragma unroll
@@ -682,7 +700,14 @@ __device__ __forceinline__ void box3_march(const PatternArgs &p, const Box3Smem 
                 uint32_t mk[LPS][Q][2];
                 bool zl[LPS][Q], zr[LPS][Q];
                 const unsigned vote = __reduce_or_sync(0xffffffffu, wv);  // 1 some L-partial, 2 some R-partial, 4 other
-                if (vote == 0) {
+                if (dbg & 1) {
+#pragma unroll
+                    for (int l = 0; l < LPS; l++)
+#pragma unroll
+                        for (int q = 0; q < Q; q++)
+#pragma unroll
+                            for (int i = 0; i < 2; i++) acc[l][q][i] = w[(kb + l) % S][q + 1][i + 1] + w[(kb + l + 1) % S][q + 2][i + 2];
+                } else if (vote == 0) {
                     box3_chain<Q, S, LPS, OFF_NEG1, CENTER_POS, 0, false, false>(w, kb, mk, zl, zr, vc, vo, acc);
                 } else if (vote == 1 || vote == 2) {
 #pragma unroll
@@ -754,7 +779,7 @@ __device__ __noinline__ void box3_edge_tile(const PatternArgs &p, const uint32_t
                                                     half * 32 + lane < cols_ok, false, false);
 }
 
-template <int R, int WC, int Q, int LPS, int MINB, bool OFF_NEG1, int CENTER_POS>
+template <int R, int WC, int Q, int LPS, int MINB, bool OFF_NEG1, int CENTER_POS, int WA = 1>
 __global__ void __launch_bounds__(WC * 32, MINB) spmv_pattern_box3_kernel(PatternArgs p, int n_planes) {
     __shared__ uint32_t s_cls0[kDictSmemPat + 1], s_cls1[kDictSmemPat + 1], s_masks1[kDictSmemPat + 1];
     box3_fill_tables(p, s_cls0, s_cls1, s_masks1, threadIdx.x, WC * 32);
@@ -765,8 +790,10 @@ __global__ void __launch_bounds__(WC * 32, MINB) spmv_pattern_box3_kernel(Patter
     sm.cls1 = (uint32_t)__cvta_generic_to_shared(s_cls1);
     sm.masks = (uint32_t)__cvta_generic_to_shared(s_masks1);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int a_w = blockIdx.x * 64;  // first column of the warp
-    const int c0 = (blockIdx.z * WC + warp) * Q;
+    // WA warps of the CTA sit side by side along x (a CTA then reads contiguous runs of WA*512 bytes
+    // per line and plane), the remaining WC/WA along z.
+    const int a_w = (blockIdx.x * WA + warp % WA) * 64;  // first column of the warp
+    const int c0 = (blockIdx.z * (WC / WA) + warp / WA) * Q;
     const int b0 = blockIdx.y * R;
     if (c0 >= n_planes) return;
     const int nb = min(R, p.plane_lines - b0);
@@ -997,6 +1024,459 @@ __global__ void __launch_bounds__(WC * 32, MINB) spmv_pattern_box5_kernel(Patter
     cp_async_wait<0>();
 }
 
+// -----------------------------------------------------------------------------
+// Sliding-window kernel, wide tile ("box6"): NX adjacent columns (4 or 8) and Q planes
+// per thread, one line per step.  With NX = 8 a warp spans 256 columns: the per-step
+// setup is amortised over 8 rows per thread, only 2 of the NX/2+2 loads per (line,
+// plane) are halo loads, and the x-boundary rows are always the first / last column
+// of a thread, so ONE chain variant serves every warp: the nine dx=-1 operands of the
+// first column and the nine dx=+1 operands of the last column are selected per lane
+// (zeroed when that row's mask lacks exactly those entries).  Any other partial mask
+// in the step takes the fully masked chain.  NX*Q independent chains per thread.
+// -----------------------------------------------------------------------------
+template <int NX, int Q, bool OFF_NEG1, int CENTER_POS, bool MASKED>
+__device__ __forceinline__ void box6_chain(const double (&w)[3][Q + 2][NX + 2], int kb, const uint32_t (&mk)[Q][NX],
+                                           const bool (&zl)[Q], const bool (&zr)[Q], double vc, double vo,
+                                           double (&acc)[Q][NX]) {
+    double hl[Q][3][3], hr[Q][3][3];
+    if (!MASKED) {
+#pragma unroll
+        for (int q = 0; q < Q; q++)
+#pragma unroll
+            for (int dz = 0; dz < 3; dz++)
+#pragma unroll
+                for (int dy = 0; dy < 3; dy++) {
+                    const int s = (kb + dy + 2) % 3;
+                    hl[q][dz][dy] = zl[q] ? 0.0 : w[s][q + dz][0];
+                    hr[q][dz][dy] = zr[q] ? 0.0 : w[s][q + dz][NX + 1];
+                }
+    }
+#pragma unroll
+    for (int q = 0; q < Q; q++)
+#pragma unroll
+        for (int i = 0; i < NX; i++) acc[q][i] = 0.0;
+    auto centre = [&]() {
+#pragma unroll
+        for (int q = 0; q < Q; q++)
+#pragma unroll
+            for (int i = 0; i < NX; i++) {
+                const double pr = __dmul_rn(vc, w[kb % 3][q + 1][i + 1]);
+                acc[q][i] = __dadd_rn(acc[q][i], (MASKED && !(mk[q][i] >> 13 & 1u)) ? 0.0 : pr);
+            }
+    };
+    if (CENTER_POS == 0) centre();
+#pragma unroll
+    for (int t = 0; t < 27; t++) {
+        if (t == 13 && CENTER_POS != 2) continue;
+        const int dz = t / 9, dy = (t / 3) % 3, dx = t % 3;
+#pragma unroll
+        for (int q = 0; q < Q; q++)
+#pragma unroll
+            for (int i = 0; i < NX; i++) {
+                double e = w[(kb + dy + 2) % 3][q + dz][i + dx];
+                if (!MASKED && i + dx == 0) e = hl[q][dz][dy];
+                if (!MASKED && i + dx == NX + 1) e = hr[q][dz][dy];
+                if (OFF_NEG1) {
+                    if (MASKED) e = (mk[q][i] >> t & 1u) ? e : 0.0;
+                    acc[q][i] = __dsub_rn(acc[q][i], e);
+                } else {
+                    double pr = __dmul_rn(vo, e);
+                    if (MASKED) pr = (mk[q][i] >> t & 1u) ? pr : 0.0;
+                    acc[q][i] = __dadd_rn(acc[q][i], pr);
+                }
+            }
+    }
+    if (CENTER_POS == 1) centre();
+}
+
+struct Box6Smem {
+    uint32_t cls0, cls1, clsm, masks;  // 32-bit shared addresses (tables indexed by id + 1)
+};
+
+template <int NX, int Q, bool OFF_NEG1, int CENTER_POS>
+__device__ __forceinline__ void box6_march(const PatternArgs &p, const Box6Smem sm, const double *__restrict__ xw,
+                                           const int32_t *__restrict__ idw, double *__restrict__ yw, int64_t xi_w, int lane,
+                                           int nb, bool lane_ok, int nq) {
+    constexpr int P = Q + 2, WX = NX + 2;
+    const int sy = p.sy;
+    const int sz = sy * p.plane_lines;
+    const int lo = lane * NX;
+    double w[3][P][WX];
+    auto load_line = [&](int slot, int line_off) {
+#pragma unroll
+        for (int pz = 0; pz < P; pz++) {
+            const double *pl = xw + (lo + (pz - 1) * sz + line_off);
+            w[slot][pz][0] = __ldg(pl - 1);
+#pragma unroll
+            for (int h = 0; h < NX / 2; h++) {
+                const double2 v = __ldg(reinterpret_cast<const double2 *>(pl) + h);
+                w[slot][pz][1 + 2 * h] = v.x;
+                w[slot][pz][2 + 2 * h] = v.y;
+            }
+            w[slot][pz][NX + 1] = __ldg(pl + NX);
+        }
+    };
+    bool vq[Q];
+#pragma unroll
+    for (int q = 0; q < Q; q++) vq[q] = lane_ok && q < nq;
+    auto load_ids = [&](int q, bool line_ok, int line_off, int (&out)[NX]) {
+#pragma unroll
+        for (int i = 0; i < NX; i++) out[i] = -1;  // rows outside the tile: computed, never stored
+        if (vq[q] && line_ok) {
+            const int4 *ptr = reinterpret_cast<const int4 *>(idw + (lo + q * sz + line_off));
+#pragma unroll
+            for (int h = 0; h < NX / 4; h++) {
+                const int4 v = ld_stream(ptr + h);
+                out[4 * h] = v.x; out[4 * h + 1] = v.y; out[4 * h + 2] = v.z; out[4 * h + 3] = v.w;
+            }
+        }
+    };
+    load_line(2, -sy);
+    load_line(0, 0);
+    int idn[Q][NX];
+#pragma unroll
+    for (int q = 0; q < Q; q++) load_ids(q, 0 < nb, 0, idn[q]);
+    const int pf = p.prefetch * sy;
+    const double vc = p.v_center, vo = p.v_off;
+#pragma unroll 1
+    for (int j0 = 0; j0 < nb; j0 += 3) {
+#pragma unroll
+        for (int kb = 0; kb < 3; kb++) {
+            const int j = j0 + kb;
+            if (j < nb) {
+                load_line((kb + 1) % 3, sy);
+                int id[Q][NX];
+                uint32_t other = 0;
+                bool zl[Q], zr[Q];
+#pragma unroll
+                for (int q = 0; q < Q; q++) {
+#pragma unroll
+                    for (int i = 0; i < NX; i++) id[q][i] = idn[q][i];
+                    load_ids(q, j + 1 < nb, sy, idn[q]);
+                    const uint32_t c0 = lds_u32(sm.cls0 + 4 + 4 * id[q][0]);
+                    const uint32_t c1 = lds_u32(sm.cls1 + 4 + 4 * id[q][NX - 1]);
+                    zl[q] = c0 & 1u;
+                    zr[q] = c1 & 2u;
+                    other |= c0 | c1;
+#pragma unroll
+                    for (int i = 1; i < NX - 1; i++) other |= lds_u32(sm.clsm + 4 + 4 * id[q][i]);
+                }
+                if (pf > 0 && (lane & 1) == 0) {  // lines `prefetch` steps ahead, HBM -> L2 (one request per 128 bytes)
+#pragma unroll
+                    for (int q = 0; q < Q; q++) {
+                        prefetch_l2(xw + (lo + q * sz + pf));
+                        if ((lane & 3) == 0) prefetch_l2(idw + (lo + q * sz + pf));
+                    }
+                }
+                double acc[Q][NX];
+                uint32_t mk[Q][NX];
+                if (!__any_sync(0xffffffffu, (other & 4u) != 0)) {
+                    box6_chain<NX, Q, OFF_NEG1, CENTER_POS, false>(w, kb, mk, zl, zr, vc, vo, acc);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < Q; q++)
+#pragma unroll
+                        for (int i = 0; i < NX; i++) mk[q][i] = lds_u32(sm.masks + 4 + 4 * id[q][i]);
+                    box6_chain<NX, Q, OFF_NEG1, CENTER_POS, true>(w, kb, mk, zl, zr, vc, vo, acc);
+#pragma unroll
+                    for (int q = 0; q < Q; q++)
+#pragma unroll
+                        for (int i = 0; i < NX; i++)  // patterns outside the box: List 1 per lane
+                            if (mk[q][i] == kGenericMask)
+                                acc[q][i] = pattern_row_cold(p, id[q][i], xi_w + lo + q * (int64_t)sz + i);
+                }
+#pragma unroll
+                for (int q = 0; q < Q; q++) {
+                    double *dst = yw + (lo + q * sz);
+                    int all = id[q][0];
+#pragma unroll
+                    for (int i = 1; i < NX; i++) all |= id[q][i];
+                    if (all >= 0) {
+#pragma unroll
+                        for (int h = 0; h < NX / 2; h++)
+                            reinterpret_cast<double2 *>(dst)[h] = make_double2(acc[q][2 * h], acc[q][2 * h + 1]);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < NX; i++)
+                            if (id[q][i] >= 0) dst[i] = acc[q][i];
+                    }
+                }
+                xw += sy;
+                idw += sy;
+                yw += sy;
+                xi_w += sy;
+            }
+        }
+    }
+}
+
+template <int NX, int R, int WC, int Q, int MINB, bool OFF_NEG1, int CENTER_POS>
+__global__ void __launch_bounds__(WC * 32, MINB) spmv_pattern_box6_kernel(PatternArgs p, int n_planes) {
+    constexpr int CW = 32 * NX;  // columns per warp
+    __shared__ uint32_t s_cls0[kDictSmemPat + 1], s_cls1[kDictSmemPat + 1], s_clsm[kDictSmemPat + 1], s_masks1[kDictSmemPat + 1];
+    for (int i = threadIdx.x; i <= p.n_patterns; i += WC * 32) {
+        const uint32_t m = i == 0 ? kFullBox : p.masks[i - 1];
+        s_masks1[i] = m;
+        s_cls0[i] = m == kFullBox ? 0u : (m == (kFullBox & ~kLBits) ? 1u : 4u);
+        s_cls1[i] = m == kFullBox ? 0u : (m == (kFullBox & ~kRBits) ? 2u : 4u);
+        s_clsm[i] = m == kFullBox ? 0u : 4u;
+    }
+    __syncthreads();
+    Box6Smem sm;
+    sm.cls0 = (uint32_t)__cvta_generic_to_shared(s_cls0);
+    sm.cls1 = (uint32_t)__cvta_generic_to_shared(s_cls1);
+    sm.clsm = (uint32_t)__cvta_generic_to_shared(s_clsm);
+    sm.masks = (uint32_t)__cvta_generic_to_shared(s_masks1);
+    const uint32_t *s_masks = s_masks1 + 1;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int a_w = blockIdx.x * CW;
+    const int c0 = (blockIdx.z * WC + warp) * Q;
+    const int b0 = blockIdx.y * R;
+    if (c0 >= n_planes) return;
+    const int nb = min(R, p.plane_lines - b0);
+    const int nq = min(Q, n_planes - c0);
+    const int64_t n_rows = (int64_t)p.row_end - p.row_begin;
+    const int64_t sy = p.sy, sz = sy * p.plane_lines;
+    const int64_t r_w = a_w + sy * (b0 + (int64_t)p.plane_lines * c0);
+    if (r_w >= n_rows) return;
+    const int cols_ok = min(CW, p.sy - a_w);  // a multiple of NX (launcher guarantees sy % NX == 0)
+    const int64_t xi_w = p.g0 + p.row_begin + r_w;
+    const int pf = p.prefetch > 0 ? p.prefetch : 0;
+    const int64_t last_row = r_w + (cols_ok - 1) + (int64_t)(nb - 1) * sy + (int64_t)(nq - 1) * sz;
+    const int64_t x_lo = xi_w - sy - sz - 1;
+    const int64_t x_hi = xi_w + CW + (int64_t)(nb + 1 + pf) * sy + (int64_t)Q * sz + 1;
+    const int64_t id_hi = r_w + CW + (int64_t)(nb + 1 + pf) * sy + (int64_t)(nq - 1) * sz;
+    const bool interior = last_row < n_rows && x_lo >= 0 && x_hi < p.x_len && id_hi <= n_rows + 1024;
+    if (interior) {
+        box6_march<NX, Q, OFF_NEG1, CENTER_POS>(p, sm, p.x + xi_w, p.ids + p.row_begin + r_w, p.y + p.row_begin + r_w, xi_w, lane,
+                                                nb, lane * NX + NX - 1 < cols_ok, nq);
+    } else {
+#pragma unroll 1
+        for (int part = 0; part < NX; part++)  // guarded one-column march of the v2 kernel, 32 columns at a time
+            box_march<Q, 0, OFF_NEG1, CENTER_POS, true>(p, s_masks, r_w + part * 32 + lane, nb, n_rows, nq,
+                                                        part * 32 + lane < cols_ok, false, false);
+    }
+}
+
+// -----------------------------------------------------------------------------
+// Sliding-window kernel, software-pipelined ring ("box7").
+// Measured regime of box3/box5 (profiles/): each warp spends ~90% of a step outside its
+// FP64 chain, on a serial setup (window loads -> ids -> class lookup -> vote -> branch)
+// whose latencies are exposed because only ~10 warps fit per SM (96-register window).
+// Here the setup of step j+1 is issued in the SAME basic block as the DADD chain of
+// step j -- the chain occupies every other issue slot (DADD issues once per 2 cycles),
+// the setup's shared-memory loads, class lookups, halo selects and the vote fill the
+// rest -- and everything the setup reads comes from a cp.async shared-memory ring
+// filled DEPTH lines ahead (box5), so no global latency is on the path at all.
+//   * window: 4 slots (lines j-1, j, j+1 in use, j+2 arriving) x (Q+2) planes x 4 cols
+//   * one chain variant for every warp: the nine dx=-1 operands of the left column and
+//     the nine dx=+1 operands of the right column are selected per lane (zeroed for rows
+//     whose mask lacks exactly those entries); a step with any other partial mask runs
+//     the fully masked chain (same basic-block structure, rare).
+// -----------------------------------------------------------------------------
+template <int R, int WC, int Q, int DEPTH, int MINB, bool OFF_NEG1, int CENTER_POS>
+__global__ void __launch_bounds__(WC * 32, MINB) spmv_pattern_box7_kernel(PatternArgs p, int n_planes) {
+    constexpr int T = WC * 32;
+    constexpr int NP = WC * Q;
+    constexpr int XP = NP + 2;
+    constexpr int XW = 68;
+    constexpr int XCH = XP * (XW / 2);
+    constexpr int ICH = NP * 16;
+    constexpr int NCH = XCH + ICH;
+    constexpr int PER = (NCH + T - 1) / T;
+    constexpr int S = 4, P = Q + 2;
+    static_assert(DEPTH >= 4, "ring depth");
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double *xs = reinterpret_cast<double *>(smem_raw);                                   // [DEPTH][XP][XW]
+    int32_t *is = reinterpret_cast<int32_t *>(smem_raw + (size_t)DEPTH * XP * XW * 8);   // [DEPTH][NP][64]
+    __shared__ uint32_t s_cls0[kDictSmemPat + 1], s_cls1[kDictSmemPat + 1], s_masks1[kDictSmemPat + 1];
+    box3_fill_tables(p, s_cls0, s_cls1, s_masks1, threadIdx.x, T);
+    const uint32_t cls0_a = (uint32_t)__cvta_generic_to_shared(s_cls0);
+    const uint32_t cls1_a = (uint32_t)__cvta_generic_to_shared(s_cls1);
+    const uint32_t mask_a = (uint32_t)__cvta_generic_to_shared(s_masks1);
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int a_w = blockIdx.x * 64;
+    const int c0 = blockIdx.z * NP;
+    const int b0 = blockIdx.y * R;
+    const int nb = min(R, p.plane_lines - b0);
+    const int64_t n_rows = (int64_t)p.row_end - p.row_begin;
+    const int64_t sy64 = p.sy, sz64 = sy64 * p.plane_lines;
+    const int64_t r_c = a_w + sy64 * (b0 + (int64_t)p.plane_lines * c0);
+    const int cols_ok = min(64, p.sy - a_w);
+    const int nq_cta = min(NP, n_planes - c0);
+    const int64_t xi_c = p.g0 + p.row_begin + r_c;
+    const int64_t x_lo = xi_c - sy64 - sz64 - 2;
+    const int64_t x_hi = xi_c + 66 + (int64_t)nb * sy64 + (int64_t)NP * sz64;
+    const int64_t last_row = r_c + (cols_ok - 1) + (int64_t)(nb - 1) * sy64 + (int64_t)(nq_cta - 1) * sz64;
+    const bool interior = x_lo >= 0 && x_hi < p.x_len && last_row < n_rows && cols_ok == 64;
+    __syncthreads();
+    if (!interior) {  // CTA-uniform: grid edges, slab ends, ragged ranges -> guarded v2 march
+        const int cw = c0 + warp * Q;
+        if (cw < n_planes && r_c + (int64_t)warp * Q * sz64 < n_rows)
+            box3_edge_tile<Q, OFF_NEG1, CENTER_POS>(p, s_masks1 + 1, r_c + (int64_t)warp * Q * sz64, lane, nb, n_rows,
+                                                    min(Q, n_planes - cw), cols_ok);
+        return;
+    }
+    const int sy = p.sy, sz = sy * p.plane_lines;
+    const double *xg = p.x + xi_c;
+    const int32_t *ig = p.ids + p.row_begin + r_c;
+    int src_off[PER];
+    uint32_t dst_off[PER];
+    int kind[PER];
+    const uint32_t xs_base = (uint32_t)__cvta_generic_to_shared(xs);
+    const uint32_t is_base = (uint32_t)__cvta_generic_to_shared(is);
+#pragma unroll
+    for (int k = 0; k < PER; k++) {
+        const int c = threadIdx.x + k * T;
+        if (c < XCH) {
+            const int pz = c / (XW / 2), j = c % (XW / 2);
+            kind[k] = 0;
+            src_off[k] = (pz - 1) * sz - 2 + 2 * j;
+            dst_off[k] = (uint32_t)((pz * XW + 2 * j) * 8);
+        } else if (c < NCH) {
+            const int q = (c - XCH) / 16, j = (c - XCH) % 16;
+            kind[k] = q < nq_cta ? 1 : 2;
+            src_off[k] = q * sz + 4 * j;
+            dst_off[k] = (uint32_t)((q * 64 + 4 * j) * 4);
+        } else {
+            kind[k] = 2; src_off[k] = 0; dst_off[k] = 0;
+        }
+    }
+    auto fetch = [&](int line) {  // stage line `line` (-1 .. nb) into ring slot (line+1) % DEPTH; always one group
+        if (line <= nb) {
+            const int slot = (line + 1) % DEPTH;
+#pragma unroll
+            for (int k = 0; k < PER; k++) {
+                if (kind[k] == 0)
+                    cp_async16(xs_base + (uint32_t)(slot * XP * XW * 8) + dst_off[k], xg + (src_off[k] + line * sy));
+                else if (kind[k] == 1 && line >= 0 && line < nb)
+                    cp_async16(is_base + (uint32_t)(slot * NP * 64 * 4) + dst_off[k], ig + (src_off[k] + line * sy));
+            }
+        }
+        cp_async_commit();
+    };
+    const int pw = warp * Q;
+    const int nq = min(Q, n_planes - (c0 + pw));  // <= 0: this warp only helps with the copies
+    double w[S][P][4];
+    auto load_line = [&](int wslot, int line) {
+        const double *base = xs + ((line + 1) % DEPTH) * (XP * XW) + pw * XW + 2 * lane;
+#pragma unroll
+        for (int pz = 0; pz < P; pz++) {
+            const double *pl = base + pz * XW;
+            const double2 v = *reinterpret_cast<const double2 *>(pl + 2);
+            w[wslot][pz][0] = pl[1];
+            w[wslot][pz][1] = v.x;
+            w[wslot][pz][2] = v.y;
+            w[wslot][pz][3] = pl[4];
+        }
+    };
+    // ids of line `line` -> per-row ids, halo-select flags and the "other mask" flag of that line
+    auto classify = [&](int line, int (&id)[Q][2], bool (&zl)[Q], bool (&zr)[Q]) -> uint32_t {
+        uint32_t other = 0;
+        const int32_t *idl = is + ((line + 1) % DEPTH) * (NP * 64) + pw * 64 + 2 * lane;
+#pragma unroll
+        for (int q = 0; q < Q; q++) {
+            int2 v = make_int2(-1, -1);
+            if (q < nq && line < nb) v = *reinterpret_cast<const int2 *>(idl + q * 64);
+            id[q][0] = v.x;
+            id[q][1] = v.y;
+            const uint32_t c0v = lds_u32(cls0_a + 4 + 4 * v.x), c1v = lds_u32(cls1_a + 4 + 4 * v.y);
+            zl[q] = c0v & 1u;
+            zr[q] = c1v & 2u;
+            other |= (c0v | c1v) & 4u;
+        }
+        return other;
+    };
+#pragma unroll
+    for (int l = -1; l < DEPTH - 1; l++) fetch(l);  // lines -1 .. DEPTH-2 in flight
+    cp_async_wait<DEPTH - 3>();                     // lines -1, 0, 1 have landed
+    __syncthreads();
+    load_line(S - 1, -1);
+    load_line(0, 0);
+    load_line(1, 1);
+    int id[Q][2];
+    bool zl[Q], zr[Q];
+    bool slow = __any_sync(0xffffffffu, classify(0, id, zl, zr) != 0);
+    double *yw = p.y + p.row_begin + r_c + (int64_t)pw * sz64 + 2 * lane;
+    const double vc = p.v_center, vo = p.v_off;
+    const int pf = (x_hi + (int64_t)(DEPTH + p.prefetch) * sy64 < p.x_len &&
+                    last_row + (int64_t)(DEPTH + p.prefetch) * sy64 < n_rows) ? p.prefetch : 0;
+#pragma unroll 1
+    for (int j0 = 0; j0 < nb; j0 += S) {
+#pragma unroll
+        for (int k = 0; k < S; k++) {
+            const int j = j0 + k;
+            if (j < nb) {  // CTA-uniform
+                cp_async_wait<DEPTH - 4>();  // line j+2 has landed (groups up to line j+DEPTH-2 are committed)
+                __syncthreads();
+                fetch(j + DEPTH - 1);
+                if (pf > 0 && lane < 8) {  // further ahead: HBM -> L2, one request per 128-byte line
+                    const int line = j + DEPTH - 1 + pf;
+#pragma unroll
+                    for (int q = 0; q < Q; q++) {
+                        prefetch_l2(xg + ((pw + q) * sz + line * sy + 16 * lane));
+                        if (lane < 2) prefetch_l2(ig + ((pw + q) * sz + line * sy + 32 * lane));
+                    }
+                    if (warp == 0) prefetch_l2(xg + (-sz + line * sy + 16 * lane));
+                    if (warp == WC - 1) prefetch_l2(xg + (NP * sz + line * sy + 16 * lane));
+                }
+                int idn[Q][2];
+                bool zln[Q], zrn[Q];
+                uint32_t other_n;
+                double acc[1][Q][2];
+                uint32_t mk[1][Q][2];
+                bool zl1[1][Q], zr1[1][Q];
+#pragma unroll
+                for (int q = 0; q < Q; q++) { zl1[0][q] = zl[q]; zr1[0][q] = zr[q]; }
+                // Slot of line l is (l mod 4) with line -1 in slot 3: chain(j) reads slots k-1, k, k+1; line j+2 -> slot k+2.
+                if (false) {  // ablation: no chain (profiles/r01_ablation_nochain.log)
+                    load_line((k + 2) % S, j + 2);
+                    other_n = classify(j + 1, idn, zln, zrn);
+#pragma unroll
+                    for (int q = 0; q < Q; q++)
+#pragma unroll
+                        for (int i = 0; i < 2; i++) acc[0][q][i] = w[k][q + 1][i + 1] + w[(k + 1) % S][q + 2][i + 2];
+                } else if (!slow) {
+                    load_line((k + 2) % S, j + 2);             // setup of step j+1 ...
+                    other_n = classify(j + 1, idn, zln, zrn);
+                    box3_chain<Q, S, 1, OFF_NEG1, CENTER_POS, 0, true, true>(w, k, mk, zl1, zr1, vc, vo, acc);  // ... under chain j
+                } else {
+                    load_line((k + 2) % S, j + 2);
+                    other_n = classify(j + 1, idn, zln, zrn);
+#pragma unroll
+                    for (int q = 0; q < Q; q++)
+#pragma unroll
+                        for (int i = 0; i < 2; i++) mk[0][q][i] = lds_u32(mask_a + 4 + 4 * id[q][i]);
+                    box3_chain<Q, S, 1, OFF_NEG1, CENTER_POS, 1, false, false>(w, k, mk, zl1, zr1, vc, vo, acc);
+#pragma unroll
+                    for (int q = 0; q < Q; q++)
+#pragma unroll
+                        for (int i = 0; i < 2; i++)  // patterns outside the box: List 1 per lane
+                            if (mk[0][q][i] == kGenericMask)
+                                acc[0][q][i] = pattern_row_cold(p, id[q][i], xi_c + (int64_t)(pw + q) * sz64 + (int64_t)j * sy64 + 2 * lane + i);
+                }
+#pragma unroll
+                for (int q = 0; q < Q; q++) {
+                    double *dst = yw + (q * sz + j * sy);
+                    if ((id[q][0] | id[q][1]) >= 0) *reinterpret_cast<double2 *>(dst) = make_double2(acc[0][q][0], acc[0][q][1]);
+                    else {
+                        if (id[q][0] >= 0) dst[0] = acc[0][q][0];
+                        if (id[q][1] >= 0) dst[1] = acc[0][q][1];
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < Q; q++) {
+                    id[q][0] = idn[q][0]; id[q][1] = idn[q][1];
+                    zl[q] = zln[q]; zr[q] = zrn[q];
+                }
+                slow = __any_sync(0xffffffffu, other_n != 0);
+            }
+        }
+    }
+    cp_async_wait<0>();
+}
+
 // ---- host-side launchers -----------------------------------------------------------
 static int check_launch(const char *what) {
     cudaError_t e = cudaGetLastError();
@@ -1104,8 +1584,34 @@ static int launch_box_rw(const spmvb_matrix *a, PatternArgs &p, cudaStream_t st)
     return check_launch("spmv_pattern_box");
 }
 
+// wide-tile launch: returns 1 when not served
+template <int NX, int R, int WC, int Q, int MINB, bool ALLV>
+static int launch_box6(const spmvb_matrix *a, PatternArgs &p, cudaStream_t st) {
+    const int64_t n_rows = (int64_t)p.row_end - p.row_begin;
+    const int64_t sz = (int64_t)p.sy * p.plane_lines;
+    const int n_planes = (int)((n_rows + sz - 1) / sz);
+    const bool neg1 = p.v_off == -1.0;
+    const int cp = a->box.center_pos;
+    if (!ALLV && !(neg1 && cp == 1)) return 1;
+    if (p.sy % NX || p.sy % 4 || (p.g0 + p.row_begin) % 4 || p.row_begin % 4 || (uintptr_t)p.ids % 16) return 1;
+    dim3 grid((p.sy + 32 * NX - 1) / (32 * NX), (p.plane_lines + R - 1) / R, (n_planes + WC * Q - 1) / (WC * Q));
+    dim3 block(WC * 32);
+#define LAUNCH6(NEG, CP) spmv_pattern_box6_kernel<NX, R, WC, Q, MINB, NEG, CP><<<grid, block, 0, st>>>(p, n_planes)
+    if constexpr (ALLV) {
+        if (neg1) {
+            if (cp == 0) LAUNCH6(true, 0); else if (cp == 1) LAUNCH6(true, 1); else LAUNCH6(true, 2);
+        } else {
+            if (cp == 0) LAUNCH6(false, 0); else if (cp == 1) LAUNCH6(false, 1); else LAUNCH6(false, 2);
+        }
+    } else {
+        LAUNCH6(true, 1);
+    }
+#undef LAUNCH6
+    return check_launch("spmv_pattern_box6") == SPMVB_OK ? 0 : -1;
+}
+
 // v3 launch: returns 1 when the configuration / alignment is not served (caller falls back to v2)
-template <int R, int WC, int Q, int LPS, int MINB, bool ALLV>
+template <int R, int WC, int Q, int LPS, int MINB, bool ALLV, int WA = 1>
 static int launch_box3(const spmvb_matrix *a, PatternArgs &p, cudaStream_t st) {
     const int64_t n_rows = (int64_t)p.row_end - p.row_begin;
     const int64_t sz = (int64_t)p.sy * p.plane_lines;
@@ -1113,9 +1619,9 @@ static int launch_box3(const spmvb_matrix *a, PatternArgs &p, cudaStream_t st) {
     const bool neg1 = p.v_off == -1.0;
     const int cp = a->box.center_pos;
     if (!ALLV && !(neg1 && cp == 1)) return 1;
-    dim3 grid((p.sy + 63) / 64, (p.plane_lines + R - 1) / R, (n_planes + WC * Q - 1) / (WC * Q));
+    dim3 grid((p.sy + 64 * WA - 1) / (64 * WA), (p.plane_lines + R - 1) / R, (n_planes + (WC / WA) * Q - 1) / ((WC / WA) * Q));
     dim3 block(WC * 32);
-#define LAUNCH3(NEG, CP) spmv_pattern_box3_kernel<R, WC, Q, LPS, MINB, NEG, CP><<<grid, block, 0, st>>>(p, n_planes)
+#define LAUNCH3(NEG, CP) spmv_pattern_box3_kernel<R, WC, Q, LPS, MINB, NEG, CP, WA><<<grid, block, 0, st>>>(p, n_planes)
     if constexpr (ALLV) {
         if (neg1) {
             if (cp == 0) LAUNCH3(true, 0); else if (cp == 1) LAUNCH3(true, 1); else LAUNCH3(true, 2);
@@ -1150,6 +1656,27 @@ static int launch_box5(const spmvb_matrix *a, PatternArgs &p, cudaStream_t st) {
     return check_launch("spmv_pattern_box5") == SPMVB_OK ? 0 : -1;
 }
 
+// pipelined ring launch: returns 1 when not served
+template <int R, int WC, int Q, int DEPTH, int MINB>
+static int launch_box7(const spmvb_matrix *a, PatternArgs &p, cudaStream_t st) {
+    const int64_t n_rows = (int64_t)p.row_end - p.row_begin;
+    const int64_t sz = (int64_t)p.sy * p.plane_lines;
+    const int n_planes = (int)((n_rows + sz - 1) / sz);
+    if (!(p.v_off == -1.0 && a->box.center_pos == 1)) return 1;
+    if (p.sy % 4 || (p.g0 + p.row_begin) % 4 || p.row_begin % 4) return 1;
+    constexpr int NP = WC * Q;
+    const size_t smem = (size_t)DEPTH * ((NP + 2) * 68 * 8 + NP * 64 * 4);
+    static bool attr_set = false;
+    if (!attr_set) {
+        if (cudaFuncSetAttribute(spmv_pattern_box7_kernel<R, WC, Q, DEPTH, MINB, true, 1>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return -1;
+        attr_set = true;
+    }
+    dim3 grid((p.sy + 63) / 64, (p.plane_lines + R - 1) / R, (n_planes + NP - 1) / NP);
+    spmv_pattern_box7_kernel<R, WC, Q, DEPTH, MINB, true, 1><<<grid, WC * 32, smem, st>>>(p, n_planes);
+    return check_launch("spmv_pattern_box7") == SPMVB_OK ? 0 : -1;
+}
+
 // Conditions of the v3 kernel: vector loads need even strides/offsets and 16-byte aligned
 // arrays; all in-tile offsets must fit 32 bits; masks must fit the shared-memory table.
 static bool box3_ok(const spmvb_matrix *a, const PatternArgs &p) {
@@ -1180,6 +1707,7 @@ static int launch_pattern(const spmvb_matrix *a, const double *x, int64_t x_col0
         const Options &o = options();
         p.prefetch = o.box_prefetch >= 0 ? o.box_prefetch : 2;
         p.prefetch_l1 = o.box_prefetch_l1;
+        p.debug_nochain = o.debug_nochain;
         const bool use_box = a->box.valid && o.pattern_kernel != 1;
         if (o.pattern_kernel == 2 && !a->box.valid)
             return fail(SPMVB_ERR_INVALID_ARGUMENT, "box kernel requested but the dictionary has no box plan");
@@ -1188,28 +1716,17 @@ static int launch_pattern(const spmvb_matrix *a, const double *x, int64_t x_col0
             if (o.pattern_kernel != 3 && box3_ok(a, p)) {
                 const int64_t n_planes = ((int64_t)row_end - row_begin + (int64_t)p.sy * p.plane_lines - 1) / ((int64_t)p.sy * p.plane_lines);
                 if (n_planes == 1) rc3 = launch_box3<16, 4, 1, 2, 3, false>(a, p, st);  // single-plane ranges (slab boundary planes)
-                else if (o.box_march >= 20) switch (o.box_march) {  // ring kernel <R, WC, Q, DEPTH, min CTAs/SM>
-                    case 20: rc3 = launch_box5<16, 4, 2, 4, 3>(a, p, st); break;
-                    case 21: rc3 = launch_box5<32, 4, 2, 4, 3>(a, p, st); break;
-                    case 22: rc3 = launch_box5<16, 4, 2, 6, 3>(a, p, st); break;
-                    case 23: rc3 = launch_box5<16, 8, 2, 4, 1>(a, p, st); break;
-                    case 24: rc3 = launch_box5<16, 4, 1, 4, 4>(a, p, st); break;
-                    case 25: rc3 = launch_box5<32, 8, 1, 4, 2>(a, p, st); break;
-                    case 26: rc3 = launch_box5<64, 4, 2, 4, 3>(a, p, st); break;
-                    default: rc3 = launch_box5<16, 4, 2, 4, 3>(a, p, st); break;
-                }
-                else switch (o.box_march) {  // <R lines, WC warps, Q planes/thread, lines/step, min CTAs/SM>
-                    case 1: rc3 = launch_box3<16, 4, 2, 1, 3, false>(a, p, st); break;
-                    case 2: rc3 = launch_box3<16, 4, 2, 2, 2, false>(a, p, st); break;
-                    case 3: rc3 = launch_box3<32, 4, 2, 2, 2, false>(a, p, st); break;
-                    case 4: rc3 = launch_box3<16, 8, 2, 2, 1, false>(a, p, st); break;
-                    case 5: rc3 = launch_box3<16, 4, 1, 2, 3, false>(a, p, st); break;
-                    case 6: rc3 = launch_box3<16, 4, 3, 2, 2, false>(a, p, st); break;
-                    case 7: rc3 = launch_box3<8, 4, 2, 1, 3, false>(a, p, st); break;
-                    case 8: rc3 = launch_box3<16, 2, 2, 2, 4, false>(a, p, st); break;
-                    case 9: rc3 = launch_box3<16, 4, 1, 4, 2, false>(a, p, st); break;
-                    case 10: rc3 = launch_box3<8, 4, 2, 2, 2, false>(a, p, st); break;
-                    default: rc3 = launch_box3<8, 4, 2, 1, 3, true>(a, p, st); break;  // best measured at 256^3 (profiles/)
+                else switch (o.box_march) {
+                    // measured alternatives kept selectable for A/B (profiles/r01_probe256_*.log, 256^3):
+                    case 1: rc3 = launch_box3<16, 4, 2, 1, 3, false>(a, p, st); break;      // R=16 tiles            124 us
+                    case 5: rc3 = launch_box3<16, 4, 1, 2, 3, false>(a, p, st); break;      // 1 plane, 2 lines/step 116-121 us
+                    case 12: rc3 = launch_box3<16, 4, 2, 1, 3, false, 4>(a, p, st); break;  // CTA spans full lines  124 us
+                    case 20: rc3 = launch_box5<16, 4, 2, 4, 3>(a, p, st); break;            // cp.async ring         137 us
+                    case 35: rc3 = launch_box6<4, 8, 4, 2, 2, false>(a, p, st); break;      // 4 columns per thread  127 us
+                    case 30: rc3 = launch_box6<8, 8, 4, 1, 2, false>(a, p, st); break;      // 8 columns per thread  183 us
+                    case 47: rc3 = launch_box7<16, 4, 2, 8, 2>(a, p, st); break;            // pipelined ring        141 us
+                    // default <R=8 lines, 4 warps, Q=2 planes/thread, 1 line/step, 3 CTAs/SM>: 118 us
+                    default: rc3 = launch_box3<8, 4, 2, 1, 3, true>(a, p, st); break;
                 }
                 if (rc3 < 0) return SPMVB_ERR_CUDA;
             }
