@@ -1477,6 +1477,225 @@ __global__ void __launch_bounds__(WC * 32, MINB) spmv_pattern_box7_kernel(Patter
     cp_async_wait<0>();
 }
 
+// -----------------------------------------------------------------------------
+// Sliding-window kernel, warp-specialised TMA ring ("box8").
+// What the measurements of box3 / box5 / box7 say: the direct-load
+// march is bound by memory-level parallelism (about 16 KB in flight per SM, every
+// memory unit below 35% busy), and the cp.async rings fix that but load every thread
+// with copy bookkeeping and a CTA barrier per line, so they become instruction bound.
+// Here the roles are split:
+//   * producer: lane 0 of warp 0 walks the CTA's tiles and, per grid line, issues one
+//     TMA bulk copy (cp.async.bulk, SASS UBLKCP) per staged x plane (2080 contiguous
+//     bytes: 256 columns + halo) and per id plane (1024 bytes) into a DEPTH-deep
+//     shared-memory ring; completion is counted on an mbarrier per stage (complete_tx).
+//   * consumers: 12 warps = 4 across x (64 columns each) x 3 across z (Q = 2 planes
+//     each).  Per line: wait on the stage's "full" mbarrier, refill the register window
+//     from shared memory, classify the rows from their pattern ids, run box3's chains
+//     in the dictionary's order, store y, release the stage on its "empty" mbarrier.
+//     No global loads, no copy instructions, no CTA-wide barrier on that path.
+// Persistent grid (one CTA per SM, tiles round-robin).  Tiles that are not interior
+// (staged range leaves x, partial width, ragged rows) are served by the guarded v2
+// march on the consumer warps.  Needs sy % 256 == 0-style alignment (checked by the
+// launcher); everything else falls back to box3.
+// -----------------------------------------------------------------------------
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+template <int R, int DEPTH, int WZ, bool OFF_NEG1, int CENTER_POS>
+__global__ void __maxnreg__(WZ == 3 ? 128 : 168) spmv_pattern_box8_kernel(PatternArgs p, int n_planes, int n_tiles_y,
+                                                                      int n_tiles_z, int n_tiles_x) {
+    constexpr int Q = 2, WA = 4, NCW = WA * WZ, NT = (1 + NCW) * 32;
+    constexpr int NP = WZ * Q;        // planes computed per tile
+    constexpr int XP = NP + 2;        // x planes staged
+    constexpr int XW = 256 + 4;       // staged doubles per x line: columns a_c-2 .. a_c+257
+    constexpr int XSTAGE = XP * XW;   // doubles
+    constexpr int ISTAGE = NP * 256;  // ints
+    constexpr uint32_t STAGE_BYTES = XSTAGE * 8 + ISTAGE * 4;
+    constexpr int S = 3, P = Q + 2;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t full_bar[DEPTH], empty_bar[DEPTH];
+    __shared__ uint32_t s_cls0[kDictSmemPat + 1], s_cls1[kDictSmemPat + 1], s_masks1[kDictSmemPat + 1];
+    box3_fill_tables(p, s_cls0, s_cls1, s_masks1, threadIdx.x, NT);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < DEPTH; s++) {
+            mbar_init(smem_u32(&full_bar[s]), 1);
+            mbar_init(smem_u32(&empty_bar[s]), NCW);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t n_rows = (int64_t)p.row_end - p.row_begin;
+    const int64_t sy64 = p.sy, sz64 = sy64 * p.plane_lines;
+    const int sy = p.sy, sz = sy * p.plane_lines;
+    const int n_tiles = n_tiles_x * n_tiles_y * n_tiles_z;
+
+    // Tile geometry, identical for producer and consumers.
+    struct Tile {
+        int a_c, b0, c0, nb, nq;
+        int64_t r_c, xi_c;
+        bool interior;
+    };
+    auto tile_of = [&](int t) {
+        Tile T;
+        const int tx = t % n_tiles_x, ty = (t / n_tiles_x) % n_tiles_y, tz = t / (n_tiles_x * n_tiles_y);
+        T.a_c = tx * 256;
+        T.b0 = ty * R;
+        T.c0 = tz * NP;
+        T.nb = min(R, p.plane_lines - T.b0);
+        T.nq = min(NP, n_planes - T.c0);
+        T.r_c = T.a_c + sy64 * (T.b0 + (int64_t)p.plane_lines * T.c0);
+        T.xi_c = p.g0 + p.row_begin + T.r_c;
+        const int cols_ok = min(256, p.sy - T.a_c);
+        const int64_t x_lo = T.xi_c - sy64 - sz64 - 2;
+        const int64_t x_hi = T.xi_c + 258 + (int64_t)T.nb * sy64 + (int64_t)T.nq * sz64;
+        const int64_t last_row = T.r_c + (cols_ok - 1) + (int64_t)(T.nb - 1) * sy64 + (int64_t)(T.nq - 1) * sz64;
+        T.interior = cols_ok == 256 && x_lo >= 0 && x_hi < p.x_len && last_row < n_rows;
+        return T;
+    };
+
+    if (warp == 0) {
+        // ------------------------------------------------------------------ producer
+        if (lane != 0) return;
+        int it = 0;
+        for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+            const Tile T = tile_of(t);
+            if (!T.interior) continue;
+            const double *xg = p.x + T.xi_c;
+            const int32_t *ig = p.ids + p.row_begin + T.r_c;
+            for (int line = -1; line <= T.nb; line++, it++) {
+                const int s = it % DEPTH, n = it / DEPTH;
+                if (n > 0) mbar_wait(smem_u32(&empty_bar[s]), (n - 1) & 1);  // consumers released the previous use
+                const bool with_ids = line >= 0 && line < T.nb;
+                const uint32_t bar = smem_u32(&full_bar[s]);
+                const uint32_t dst = smem_u32(smem_raw + (size_t)s * STAGE_BYTES);
+                mbar_expect_tx(bar, (uint32_t)(T.nq + 2) * XW * 8 + (with_ids ? (uint32_t)T.nq * 1024 : 0u));
+                for (int pz = 0; pz < T.nq + 2; pz++)
+                    bulk_g2s(dst + pz * XW * 8, xg + ((int64_t)(pz - 1) * sz + (int64_t)line * sy - 2), XW * 8, bar);
+                if (with_ids)
+                    for (int q = 0; q < T.nq; q++)
+                        bulk_g2s(dst + XSTAGE * 8 + q * 1024, ig + ((int64_t)q * sz + (int64_t)line * sy), 1024, bar);
+            }
+        }
+        return;
+    }
+    // ---------------------------------------------------------------------- consumers
+    const int cw = warp - 1;
+    const int xw_i = cw % WA, zw = cw / WA;
+    const int pw = zw * Q;  // first plane (within the tile) of this warp
+    Box3Smem sm;
+    sm.cls0 = smem_u32(s_cls0);
+    sm.cls1 = smem_u32(s_cls1);
+    sm.masks = smem_u32(s_masks1);
+    const double vc = p.v_center, vo = p.v_off;
+    int it = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        const Tile T = tile_of(t);
+        if (!T.interior) {  // grid edges, slab ends, ragged ranges: guarded v2 march, 64 columns per warp
+            const int cwz = T.c0 + pw;
+            const int cols_ok = min(64, p.sy - (T.a_c + 64 * xw_i));
+            if (cwz < n_planes && cols_ok > 0 && T.r_c + 64 * xw_i + (int64_t)pw * sz64 < n_rows)
+                box3_edge_tile<Q, OFF_NEG1, CENTER_POS>(p, s_masks1 + 1, T.r_c + 64 * xw_i + (int64_t)pw * sz64, lane, T.nb, n_rows,
+                                                        min(Q, n_planes - cwz), cols_ok);
+            continue;
+        }
+        const int nq = min(Q, T.nq - pw);  // <= 0: this warp only keeps the ring protocol going
+        double w[S][P][4];
+        auto wait_full = [&](int i) { mbar_wait(smem_u32(&full_bar[i % DEPTH]), (i / DEPTH) & 1); };
+        auto release = [&](int i) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&empty_bar[i % DEPTH]));
+        };
+        auto load_line = [&](int wslot, int i) {  // window slot <- x line held by ring entry i
+            const double *base = reinterpret_cast<const double *>(smem_raw + (size_t)(i % DEPTH) * STAGE_BYTES) + pw * XW + 64 * xw_i + 2 * lane;
+#pragma unroll
+            for (int pz = 0; pz < P; pz++) {
+                const double *pl = base + pz * XW;
+                const double2 v = *reinterpret_cast<const double2 *>(pl + 2);
+                w[wslot][pz][0] = pl[1];
+                w[wslot][pz][1] = v.x;
+                w[wslot][pz][2] = v.y;
+                w[wslot][pz][3] = pl[4];
+            }
+        };
+        // lines -1 and 0
+        wait_full(it);
+        if (nq > 0) load_line(S - 1, it);
+        release(it);
+        wait_full(it + 1);
+        if (nq > 0) load_line(0, it + 1);
+        double *yw = p.y + p.row_begin + T.r_c + (int64_t)pw * sz64 + 64 * xw_i + 2 * lane;
+        const int64_t xi_w = T.xi_c + (int64_t)pw * sz64 + 64 * xw_i;
+#pragma unroll 1
+        for (int j0 = 0; j0 < T.nb; j0 += S) {
+#pragma unroll
+            for (int k = 0; k < S; k++) {
+                const int j = j0 + k;
+                if (j < T.nb) {
+                    const int ej = it + 1 + j;  // ring entry of line j; line j+1 is entry ej + 1
+                    wait_full(ej + 1);
+                    if (nq > 0) {
+                        load_line((k + 1) % S, ej + 1);
+                        const int32_t *idl = reinterpret_cast<const int32_t *>(smem_raw + (size_t)(ej % DEPTH) * STAGE_BYTES + XSTAGE * 8) +
+                                             pw * 256 + 64 * xw_i + 2 * lane;
+                        int id[1][Q][2];
+                        uint32_t c0v[Q], c1v[Q], wv = 0;
+#pragma unroll
+                        for (int q = 0; q < Q; q++) {
+                            int2 v = make_int2(-1, -1);
+                            if (q < nq) v = *reinterpret_cast<const int2 *>(idl + q * 256);
+                            id[0][q][0] = v.x;
+                            id[0][q][1] = v.y;
+                            c0v[q] = lds_u32(sm.cls0 + 4 + 4 * v.x);
+                            c1v[q] = lds_u32(sm.cls1 + 4 + 4 * v.y);
+                            wv |= c0v[q] | c1v[q];
+                        }
+                        release(ej);  // x of line j was consumed one step ago, its ids just now
+                        double acc[1][Q][2];
+                        uint32_t mk[1][Q][2];
+                        bool zl[1][Q], zr[1][Q];
+                        const unsigned vote = __reduce_or_sync(0xffffffffu, wv);
+                        if (vote == 0) {
+                            box3_chain<Q, S, 1, OFF_NEG1, CENTER_POS, 0, false, false>(w, k, mk, zl, zr, vc, vo, acc);
+                        } else if (vote == 1 || vote == 2) {
+#pragma unroll
+                            for (int q = 0; q < Q; q++) { zl[0][q] = c0v[q] != 0; zr[0][q] = c1v[q] != 0; }
+                            if (vote == 1) box3_chain<Q, S, 1, OFF_NEG1, CENTER_POS, 0, true, false>(w, k, mk, zl, zr, vc, vo, acc);
+                            else box3_chain<Q, S, 1, OFF_NEG1, CENTER_POS, 0, false, true>(w, k, mk, zl, zr, vc, vo, acc);
+                        } else {
+#pragma unroll
+                            for (int q = 0; q < Q; q++)
+#pragma unroll
+                                for (int i = 0; i < 2; i++) mk[0][q][i] = lds_u32(sm.masks + 4 + 4 * id[0][q][i]);
+                            box3_chain<Q, S, 1, OFF_NEG1, CENTER_POS, 1, false, false>(w, k, mk, zl, zr, vc, vo, acc);
+#pragma unroll
+                            for (int q = 0; q < Q; q++)
+#pragma unroll
+                                for (int i = 0; i < 2; i++)  // patterns outside the box: List 1 per lane
+                                    if (mk[0][q][i] == kGenericMask)
+                                        acc[0][q][i] = pattern_row_cold(p, id[0][q][i], xi_w + q * sz64 + (int64_t)j * sy64 + 2 * lane + i);
+                        }
+#pragma unroll
+                        for (int q = 0; q < Q; q++) {
+                            double *dst = yw + (q * sz + j * sy);
+                            if ((id[0][q][0] | id[0][q][1]) >= 0) *reinterpret_cast<double2 *>(dst) = make_double2(acc[0][q][0], acc[0][q][1]);
+                            else {
+                                if (id[0][q][0] >= 0) dst[0] = acc[0][q][0];
+                                if (id[0][q][1] >= 0) dst[1] = acc[0][q][1];
+                            }
+                        }
+                    } else {
+                        release(ej);
+                    }
+                }
+            }
+        }
+        release(it + 1 + T.nb);  // the last x line (no ids)
+        it += T.nb + 2;
+    }
+}
+
 // ---- host-side launchers -----------------------------------------------------------
 static int check_launch(const char *what) {
     cudaError_t e = cudaGetLastError();
@@ -1677,6 +1896,29 @@ static int launch_box7(const spmvb_matrix *a, PatternArgs &p, cudaStream_t st) {
     return check_launch("spmv_pattern_box7") == SPMVB_OK ? 0 : -1;
 }
 
+// warp-specialised TMA ring launch: returns 1 when not served
+template <int R, int DEPTH, int WZ>
+static int launch_box8(const spmvb_matrix *a, PatternArgs &p, cudaStream_t st) {
+    const int64_t n_rows = (int64_t)p.row_end - p.row_begin;
+    const int64_t sz = (int64_t)p.sy * p.plane_lines;
+    const int n_planes = (int)((n_rows + sz - 1) / sz);
+    if (!(p.v_off == -1.0 && a->box.center_pos == 1)) return 1;
+    if (p.sy % 4 || p.sy < 256 || (p.g0 + p.row_begin) % 4 || p.row_begin % 4 || (uintptr_t)p.ids % 16) return 1;
+    constexpr int NP = 2 * WZ;
+    constexpr size_t stage = (size_t)(NP + 2) * 260 * 8 + NP * 256 * 4;
+    const size_t smem = stage * DEPTH;
+    static bool attr_set = false;
+    if (!attr_set) {
+        if (cudaFuncSetAttribute(spmv_pattern_box8_kernel<R, DEPTH, WZ, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem) != cudaSuccess) return -1;
+        attr_set = true;
+    }
+    const int tx = (p.sy + 255) / 256, ty = (p.plane_lines + R - 1) / R, tz = (n_planes + NP - 1) / NP;
+    const int grid = std::min(tx * ty * tz, 148);
+    spmv_pattern_box8_kernel<R, DEPTH, WZ, true, 1><<<grid, (1 + 4 * WZ) * 32, smem, st>>>(p, n_planes, ty, tz, tx);
+    return check_launch("spmv_pattern_box8") == SPMVB_OK ? 0 : -1;
+}
+
 // Conditions of the v3 kernel: vector loads need even strides/offsets and 16-byte aligned
 // arrays; all in-tile offsets must fit 32 bits; masks must fit the shared-memory table.
 static bool box3_ok(const spmvb_matrix *a, const PatternArgs &p) {
@@ -1725,6 +1967,7 @@ static int launch_pattern(const spmvb_matrix *a, const double *x, int64_t x_col0
                     case 35: rc3 = launch_box6<4, 8, 4, 2, 2, false>(a, p, st); break;      // 4 columns per thread  127 us
                     case 30: rc3 = launch_box6<8, 8, 4, 1, 2, false>(a, p, st); break;      // 8 columns per thread  183 us
                     case 47: rc3 = launch_box7<16, 4, 2, 8, 2>(a, p, st); break;            // pipelined ring        141 us
+                    case 62: rc3 = launch_box8<8, 10, 2>(a, p, st); break;                  // warp-specialised TMA ring 208 us (spills)
                     // default <R=8 lines, 4 warps, Q=2 planes/thread, 1 line/step, 3 CTAs/SM>: 118 us
                     default: rc3 = launch_box3<8, 4, 2, 1, 3, true>(a, p, st); break;
                 }
