@@ -196,3 +196,45 @@ def test_config4_128_cubed(sp, orc):
     sp.row_abs_scale(m, dx, sc)
     worst, _ = sp.compare(dy2, dy1, n, scale=sc)
     assert worst <= 1e-12
+
+
+def test_config5_512_cubed_single_gpu(sp):
+    """BASELINE configs[4] on one GPU (it fits: CSR 44 GB build-time, 0.54 GB of ids resident): the matrix is
+    generated and compressed on the device (n*27 > 2^31, so 64-bit slot offsets are exercised) and checked
+    through size-independent properties."""
+    import torch
+    free, _ = torch.cuda.mem_get_info()
+    if free < 120e9:
+        pytest.skip("needs ~100 GB of free device memory")
+    g = (512, 512, 512)
+    n = 512 ** 3
+    m = sp.generate_matrix(sp.GridSpec(*g))
+    assert m.n == n and m.nnz == (3 * 512 - 2) ** 3  # nnz formula, SURVEY section 8
+    pc = sp.compress_patterns(m, True)
+    info = pc.info
+    assert (info.n_patterns, info.n_exc, info.kernel_plan) == (27, 0, 1)
+    assert (info.box_stride_y, info.box_stride_z) == (512, 512 * 512)
+    ids = pc.download("row_pattern").reshape(512, 512, 512)
+    assert len(np.unique(ids[1:-1, 1:-1, 1:-1])) == 1 and int(ids[1, 1, 1]) == 13  # interior rows share one id
+    del ids, m
+    # A*ones: interior exactly 0, everything >= 0 (SPEC.md:71); A*x agrees between the box and the List-1 kernels
+    x = torch.ones(n, dtype=torch.float64, device="cuda")
+    y = torch.empty(n, dtype=torch.float64, device="cuda")
+    sp.spmv_rows(pc, x, y, 0, n)
+    yv = y.view(512, 512, 512)
+    assert bool((yv[1:-1, 1:-1, 1:-1] == 0).all()) and bool((y >= 0).all())
+    assert float(yv[0, 0, 0]) == 19.0 and float(yv[0, 0, 1]) == 15.0  # corner 26-7, edge 26-11
+    sp.check(sp.lib.spmvb_vec_fill(x.data_ptr(), n, sp.RANDOM, 7, -1.0, 1.0, 0, None))
+    y2 = torch.empty(n, dtype=torch.float64, device="cuda")
+    sp.spmv_rows(pc, x, y, 0, n)
+    sp.set_option("pattern_kernel", 1)
+    try:
+        sp.spmv_rows(pc, x, y2, 0, n)
+    finally:
+        sp.set_option("pattern_kernel", 0)
+    assert sp.compare(y, y2, n) == (0.0, 0)
+    # linearity within 1e-12 (SPEC.md:270): A(2x) == 2 A x exactly (power of two), partition invariance (kernels.hpp:27-29)
+    x.mul_(2.0)
+    sp.spmv_rows(pc, x, y2, 0, n // 2 + 12345)
+    sp.spmv_rows(pc, x, y2, n // 2 + 12345, n)
+    assert bool(torch.equal(y2, y * 2.0))
