@@ -1,0 +1,178 @@
+// Pattern-format SpMV (inc/compress.hpp:48-76; spmv: inc/kernels.hpp:25,35-36; PAPER.md:797-813
+// List 1): production launchers, kernel selection, and the C-ABI SpMV entry points.
+#include <algorithm>
+
+#include "pattern_kernels.cuh"
+#include "spmv_internal.cuh"
+
+namespace spmvb {
+
+template <int R, int WC, int Q, int LA>
+static int launch_box_rw(const spmvb_matrix *a, PatternArgs &p, cudaStream_t st) {
+    const int64_t n_rows = (int64_t)p.row_end - p.row_begin;
+    const int64_t sz = (int64_t)p.sy * p.plane_lines;
+    const int n_planes = (int)((n_rows + sz - 1) / sz);
+    dim3 grid((p.sy + 31) / 32, (p.plane_lines + R - 1) / R, (n_planes + WC * Q - 1) / (WC * Q));
+    dim3 block(WC * 32);
+    const bool neg1 = p.v_off == -1.0;
+    const int cp = a->box.center_pos;
+#define LAUNCH(NEG, CP) spmv_pattern_box_kernel<R, WC, Q, LA, NEG, CP><<<grid, block, 0, st>>>(p, n_planes)
+    if (neg1) {
+        if (cp == 0) LAUNCH(true, 0); else if (cp == 1) LAUNCH(true, 1); else LAUNCH(true, 2);
+    } else {
+        if (cp == 0) LAUNCH(false, 0); else if (cp == 1) LAUNCH(false, 1); else LAUNCH(false, 2);
+    }
+#undef LAUNCH
+    return check_launch("spmv_pattern_box");
+}
+
+// v3 launch: returns 1 when the configuration / alignment is not served (caller falls back to v2)
+template <int R, int WC, int Q, int LPS, int MINB, bool ALLV, int WA = 1>
+static int launch_box3(const spmvb_matrix *a, PatternArgs &p, cudaStream_t st) {
+    const int64_t n_rows = (int64_t)p.row_end - p.row_begin;
+    const int64_t sz = (int64_t)p.sy * p.plane_lines;
+    const int n_planes = (int)((n_rows + sz - 1) / sz);
+    const bool neg1 = p.v_off == -1.0;
+    const int cp = a->box.center_pos;
+    if (!ALLV && !(neg1 && cp == 1)) return 1;
+    dim3 grid((p.sy + 64 * WA - 1) / (64 * WA), (p.plane_lines + R - 1) / R, (n_planes + (WC / WA) * Q - 1) / ((WC / WA) * Q));
+    dim3 block(WC * 32);
+#define LAUNCH3(NEG, CP) spmv_pattern_box3_kernel<R, WC, Q, LPS, MINB, NEG, CP, WA><<<grid, block, 0, st>>>(p, n_planes)
+    if constexpr (ALLV) {
+        if (neg1) {
+            if (cp == 0) LAUNCH3(true, 0); else if (cp == 1) LAUNCH3(true, 1); else LAUNCH3(true, 2);
+        } else {
+            if (cp == 0) LAUNCH3(false, 0); else if (cp == 1) LAUNCH3(false, 1); else LAUNCH3(false, 2);
+        }
+    } else {
+        LAUNCH3(true, 1);
+    }
+#undef LAUNCH3
+    return check_launch("spmv_pattern_box3") == SPMVB_OK ? 0 : -1;
+}
+
+// Conditions of the v3 kernel: vector loads need even strides/offsets and 16-byte aligned
+// arrays; all in-tile offsets must fit 32 bits; masks must fit the shared-memory table.
+static bool box3_ok(const spmvb_matrix *a, const PatternArgs &p) {
+    const int64_t sz = (int64_t)p.sy * p.plane_lines;
+    return (p.sy % 2 == 0) && ((p.g0 + p.row_begin) % 2 == 0) && (p.row_begin % 2 == 0) &&
+           ((uintptr_t)p.x % 16 == 0) && ((uintptr_t)p.y % 16 == 0) && ((uintptr_t)p.ids % 8 == 0) &&
+           a->n_patterns <= kDictSmemPat && 6 * sz + 128 * (int64_t)p.sy + 4096 < INT32_MAX;
+}
+
+static int launch_pattern(const spmvb_matrix *a, const double *x, int64_t x_col0, int64_t x_len, double *y,
+                          int row_begin, int row_end, cudaStream_t st) {
+    if (row_end > row_begin) {
+        PatternArgs p;
+        p.ids = static_cast<const int32_t *>(a->s[SPMVB_S_ROW_PATTERN]);
+        p.x = x; p.y = y;
+        p.g0 = a->row_offset - x_col0;
+        p.x_len = x_len;
+        p.disp_off = a->d_disp_off32;
+        p.disp = static_cast<const int32_t *>(a->s[SPMVB_S_DISP_FLAT]);
+        p.ends = static_cast<const int32_t *>(a->s[SPMVB_S_ENDS_FLAT]);
+        p.table = static_cast<const double *>(a->s[SPMVB_S_TABLE]);
+        p.masks = a->d_masks;
+        p.n_patterns = a->n_patterns; p.m = a->m; p.disp_total = (int)a->disp_total;
+        p.row_begin = row_begin; p.row_end = row_end;
+        p.sy = a->box.sy; p.plane_lines = a->box.valid ? a->box.sz / a->box.sy : 0;
+        p.v_off = a->box.valid ? a->h_table[a->box.k_off] : 0.0;
+        p.v_center = a->box.valid ? a->h_table[a->box.k_center] : 0.0;
+        const Options &o = options();
+        p.prefetch = o.box_prefetch >= 0 ? o.box_prefetch : 2;
+        p.prefetch_l1 = o.box_prefetch_l1;
+        p.debug_nochain = o.debug_nochain;
+        const bool use_box = a->box.valid && o.pattern_kernel != 1;
+        if (o.pattern_kernel == 2 && !a->box.valid)
+            return fail(SPMVB_ERR_INVALID_ARGUMENT, "box kernel requested but the dictionary has no box plan");
+        if (use_box) {
+            int rc3 = 1;  // 1 = not served by v3
+            if (o.pattern_kernel != 3 && box3_ok(a, p)) {
+                const int64_t n_planes = ((int64_t)row_end - row_begin + (int64_t)p.sy * p.plane_lines - 1) / ((int64_t)p.sy * p.plane_lines);
+                if (n_planes == 1) rc3 = launch_box3<16, 4, 1, 2, 3, false>(a, p, st);  // single-plane ranges (slab boundary planes)
+                else switch (o.box_march) {
+                    // measured alternatives kept selectable for A/B (profiles/r01_probe256_*.log, 256^3):
+                    case 1: rc3 = launch_box3<16, 4, 2, 1, 3, false>(a, p, st); break;      // R=16 tiles            124 us
+                    case 5: rc3 = launch_box3<16, 4, 1, 2, 3, false>(a, p, st); break;      // 1 plane, 2 lines/step 116-121 us
+                    case 12: rc3 = launch_box3<16, 4, 2, 1, 3, false, 4>(a, p, st); break;  // CTA spans full lines  124 us
+                    case 20: case 30: case 35: case 47: case 62:                            // spmv_pattern_lab.cu
+                        rc3 = launch_pattern_lab(o.box_march, a, p, st); break;
+                    // default <R=8 lines, 4 warps, Q=2 planes/thread, 1 line/step, 3 CTAs/SM>: 118 us
+                    default: rc3 = launch_box3<8, 4, 2, 1, 3, true>(a, p, st); break;
+                }
+                if (rc3 < 0) return SPMVB_ERR_CUDA;
+            }
+            if (rc3 == 1) {  // v2: any stride / alignment / value pattern
+                if (o.box_march == 11) SPMVB_TRY((launch_box_rw<32, 8, 1, 1>(a, p, st)));
+                else SPMVB_TRY((launch_box_rw<16, 8, 2, 0>(a, p, st)));
+            }
+        } else {
+            const int threads = 256;
+            const int blocks = (row_end - row_begin + threads - 1) / threads;
+            const bool dict_smem = a->disp_total <= kDictSmemDisp && a->n_patterns <= kDictSmemPat && a->m <= kDictSmemTab;
+            if (dict_smem) spmv_pattern_generic_kernel<true><<<blocks, threads, 0, st>>>(p);
+            else spmv_pattern_generic_kernel<false><<<blocks, threads, 0, st>>>(p);
+            SPMVB_TRY(check_launch("spmv_pattern_generic"));
+        }
+    }
+    if (a->n_exc > 0 && row_end > row_begin) {
+        // exception slots whose rows fall in [row_begin,row_end)
+        const auto &er = a->h_exc_rows;
+        const int e0 = (int)(std::lower_bound(er.begin(), er.end(), row_begin) - er.begin());
+        const int e1 = (int)(std::lower_bound(er.begin(), er.end(), row_end) - er.begin());
+        SPMVB_TRY(launch_ell(static_cast<const double *>(a->s[SPMVB_S_EXC_VALUES]),
+                             static_cast<const int32_t *>(a->s[SPMVB_S_EXC_COLUMNS]), a->w_exc, x, x_col0, y, e0, e1,
+                             static_cast<const int32_t *>(a->s[SPMVB_S_EXC_ROWS]), st));
+    }
+    return SPMVB_OK;
+}
+
+}  // namespace spmvb
+
+using namespace spmvb;
+
+extern "C" {
+
+int spmvb_spmv(const spmvb_matrix *a, const double *x_dev, int64_t x_col0, int64_t x_len, double *y_dev,
+               int32_t row_begin, int32_t row_end, void *stream) {
+    if (!a || !x_dev || !y_dev) return fail(SPMVB_ERR_INVALID_ARGUMENT, "spmv: NULL argument");
+    if (row_begin < 0 || row_end > a->n || row_begin > row_end)
+        return fail(SPMVB_ERR_INVALID_ARGUMENT, "spmv: row range [%d,%d) outside [0,%d)", row_begin, row_end, a->n);
+    cudaStream_t st = as_stream(stream);
+    switch (a->format) {
+        case SPMVB_FMT_ELL:
+            return launch_ell(static_cast<const double *>(a->s[SPMVB_S_VALUES]),
+                              static_cast<const int32_t *>(a->s[SPMVB_S_COLUMNS]), a->width, x_dev, x_col0, y_dev,
+                              row_begin, row_end, nullptr, st);
+        case SPMVB_FMT_VT:
+            return launch_vt(a, x_dev, x_col0, y_dev, row_begin, row_end, st);
+        case SPMVB_FMT_PATTERN:
+            return launch_pattern(a, x_dev, x_col0, x_len, y_dev, row_begin, row_end, st);
+        default:
+            return fail(SPMVB_ERR_INVALID_ARGUMENT, "spmv: format %d has no SpMV kernel", a->format);
+    }
+}
+
+int spmvb_spmv_host(const spmvb_matrix *a, const double *x_host, int64_t x_len, double *y_host) {
+    if (!a || !x_host || !y_host) return fail(SPMVB_ERR_INVALID_ARGUMENT, "spmv_host: NULL argument");
+    if (a->row_offset != 0) return fail(SPMVB_ERR_INVALID_ARGUMENT, "spmv_host: handle is a slab (row_offset != 0)");
+    if (x_len != a->n)  // SPEC.md:212,222,232 "length mismatch"
+        return fail(SPMVB_ERR_INVALID_ARGUMENT, "spmv: x has %lld entries, matrix has %d rows", (long long)x_len, a->n);
+    // persistent device scratch: the matrix stays resident, only x and y cross the bus
+    if (a->scratch_x_len < x_len || !a->scratch_x) {
+        if (a->scratch_x) cudaFree(a->scratch_x);
+        if (a->scratch_y) cudaFree(a->scratch_y);
+        a->scratch_x = a->scratch_y = nullptr;
+        a->scratch_x_len = 0;
+        SPMVB_TRY(spmvb_vec_alloc(x_len, &a->scratch_x));
+        SPMVB_TRY(spmvb_vec_alloc(a->n, &a->scratch_y));
+        a->scratch_x_len = x_len;
+    }
+    SPMVB_CUDA(cudaMemcpyAsync(a->scratch_x, x_host, (size_t)x_len * 8, cudaMemcpyHostToDevice, nullptr));
+    SPMVB_TRY(spmvb_spmv(a, a->scratch_x, 0, x_len, a->scratch_y, 0, a->n, nullptr));
+    SPMVB_CUDA(cudaMemcpyAsync(y_host, a->scratch_y, (size_t)a->n * 8, cudaMemcpyDeviceToHost, nullptr));
+    SPMVB_CUDA(cudaStreamSynchronize(nullptr));
+    return SPMVB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,298 @@
+// SpMV kernels for the row-major streams (ELL and value-table formats), sm_100a, fp64.
+//
+// Arithmetic contract: every product and every sum is rounded
+// separately (__dmul_rn / __dadd_rn, never contracted to FMA), in the reference's documented
+// per-format order (inc/kernels.hpp:19-22): bit-identical to the reference's loop built for
+// baseline x86-64.
+#include <algorithm>
+
+#include "device_utils.cuh"
+#include "spmv_internal.cuh"
+
+namespace spmvb {
+
+// ---- per-row accumulation from a staged tile (shared memory), reference order ---------------
+// The gathers of x are issued in independent batches of B before the ordered sums consume
+// them, so a row costs ~width/B L2 latencies instead of `width`.
+template <int B>
+__device__ __forceinline__ double ell_row(const double *v, const int32_t *c, int width, const double *__restrict__ x,
+                                          int64_t x_col0) {
+    // inc/kernels.hpp:19-20: slot order; padding slots multiply 0.0 by x[own row]
+    double acc = 0.0;
+    for (int base = 0; base < width; base += B) {
+        double xv[B];
+#pragma unroll
+        for (int j = 0; j < B; j++) xv[j] = base + j < width ? __ldg(x + ((int64_t)c[base + j] - x_col0)) : 0.0;
+#pragma unroll
+        for (int j = 0; j < B; j++)
+            if (base + j < width) acc = __dadd_rn(acc, __dmul_rn(v[base + j], xv[j]));
+    }
+    return acc;
+}
+
+template <int B>
+__device__ __forceinline__ double vt_row(const int32_t *c, const int32_t *e, const double *tab, int m,
+                                         const double *__restrict__ x, int64_t x_col0) {
+    // inc/kernels.hpp:20-22: per value group (table order) sum x in stored order, then one product.
+    // (Batching the gathers inside a group was measured slower than this plain loop: 509 vs 470 us
+    // at 256^3 -- the group bookkeeping costs more than the latency it hides at full occupancy.)
+    double acc = 0.0;
+    int idx = 0;
+    for (int k = 0; k < m; k++) {
+        double sum = 0.0;
+        const int end = e[k];
+        for (; idx < end; idx++) sum = __dadd_rn(sum, __ldg(x + ((int64_t)c[idx] - x_col0)));
+        acc = __dadd_rn(acc, __dmul_rn(tab[k], sum));
+    }
+    return acc;
+}
+
+// =============================================================================
+// ELL (inc/ell.hpp:10-24; spmv: inc/kernels.hpp:23,31-32)
+// Row-major n x width.  A tile of kTileRows rows is one contiguous block of each
+// array; it is staged into shared memory with coalesced 128-bit loads, then each
+// thread accumulates its own row in slot order (stride `width` doubles: conflict
+// free for odd widths such as 27).  row_map != nullptr serves the exception block
+// of the hybrid pattern format: tile rows are exception slots, y goes to row_map[e].
+// =============================================================================
+template <int ROWS>
+__global__ void __launch_bounds__(ROWS) spmv_ell_kernel(const double *__restrict__ values,
+                                                       const int32_t *__restrict__ columns, int width,
+                                                       const double *__restrict__ x, int64_t x_col0,
+                                                       double *__restrict__ y, int row_begin, int row_end,
+                                                       int tile0, const int32_t *__restrict__ row_map) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double *sv = reinterpret_cast<double *>(smem);
+    int32_t *sc = reinterpret_cast<int32_t *>(smem + (size_t)ROWS * width * 8);
+    const int r0 = (tile0 + blockIdx.x) * ROWS;
+    const int64_t base = (int64_t)r0 * width;
+    const int rows_here = min(ROWS, row_end - r0);
+    const int nelem = rows_here * width;
+    {
+        const int4 *gv = reinterpret_cast<const int4 *>(values + base);
+        const int nv = (nelem + 1) >> 1;
+#pragma unroll 4
+        for (int i = threadIdx.x; i < nv; i += ROWS) reinterpret_cast<int4 *>(sv)[i] = ld_stream(gv + i);
+        const int4 *gc = reinterpret_cast<const int4 *>(columns + base);
+        const int nc = (nelem + 3) >> 2;
+#pragma unroll 4
+        for (int i = threadIdx.x; i < nc; i += ROWS) reinterpret_cast<int4 *>(sc)[i] = ld_stream(gc + i);
+    }
+    __syncthreads();
+    const int r = r0 + threadIdx.x;
+    if (r < row_begin || r >= row_end) return;
+    y[row_map ? row_map[r] : r] = ell_row<9>(sv + threadIdx.x * width, sc + threadIdx.x * width, width, x, x_col0);
+}
+
+// Naive thread-per-row form, kept as the A/B baseline ("ell_kernel" = 1).
+__global__ void spmv_ell_naive_kernel(const double *__restrict__ values, const int32_t *__restrict__ columns,
+                                      int width, const double *__restrict__ x, int64_t x_col0,
+                                      double *__restrict__ y, int row_begin, int row_end) {
+    const int r = row_begin + blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= row_end) return;
+    const double *v = values + (int64_t)r * width;
+    const int32_t *c = columns + (int64_t)r * width;
+    double acc = 0.0;
+    for (int k = 0; k < width; k++) acc = __dadd_rn(acc, __dmul_rn(v[k], __ldg(x + ((int64_t)c[k] - x_col0))));
+    y[r] = acc;
+}
+
+// =============================================================================
+// Value table (inc/compress.hpp:28-44; spmv: inc/kernels.hpp:24,33-34;
+// SPEC.md:218-221): per row, sum x within each value group in stored order, then
+// one product per group in table order.
+// =============================================================================
+template <int ROWS>
+__global__ void __launch_bounds__(ROWS) spmv_vt_kernel(const int32_t *__restrict__ sorted_columns,
+                                                      const int32_t *__restrict__ ends,
+                                                      const double *__restrict__ table, int width, int m,
+                                                      const double *__restrict__ x, int64_t x_col0,
+                                                      double *__restrict__ y, int row_begin, int row_end,
+                                                      int tile0) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    int32_t *sc = reinterpret_cast<int32_t *>(smem);
+    int32_t *se = sc + (size_t)ROWS * width;
+    double *st = reinterpret_cast<double *>(se + (size_t)ROWS * m);
+    const int r0 = (tile0 + blockIdx.x) * ROWS;
+    const int rows_here = min(ROWS, row_end - r0);
+    {
+        const int4 *gc = reinterpret_cast<const int4 *>(sorted_columns + (int64_t)r0 * width);
+        const int nc = (rows_here * width + 3) >> 2;
+#pragma unroll 4
+        for (int i = threadIdx.x; i < nc; i += ROWS) reinterpret_cast<int4 *>(sc)[i] = ld_stream(gc + i);
+        const int4 *ge = reinterpret_cast<const int4 *>(ends + (int64_t)r0 * m);
+        const int ne = (rows_here * m + 3) >> 2;
+        for (int i = threadIdx.x; i < ne; i += ROWS) reinterpret_cast<int4 *>(se)[i] = ld_stream(ge + i);
+        for (int i = threadIdx.x; i < m; i += ROWS) st[i] = table[i];
+    }
+    __syncthreads();
+    const int r = r0 + threadIdx.x;
+    if (r < row_begin || r >= row_end) return;
+    y[r] = vt_row<9>(sc + threadIdx.x * width, se + threadIdx.x * m, st, m, x, x_col0);
+}
+
+// =============================================================================
+// TMA (bulk-copy) pipelines for the row-major streams.  A persistent CTA walks
+// 128-row tiles; one elected thread issues `cp.async.bulk` (SASS UBLKCP) copies of
+// the tile's contiguous value / column blocks into a ring of NS shared-memory
+// stages, completion is signalled on an mbarrier per stage (complete_tx), all
+// threads then accumulate their own row from shared memory in the reference
+// order.  While one stage is consumed the other NS-1 are in flight, so HBM never
+// idles during the gather/accumulate phase (the vectorised-load kernels above
+// alternate between a load phase and a compute phase).
+// =============================================================================
+// FMT 0: ELL (a = values f64, b = columns i32, wa = wb = width)
+// FMT 1: vt  (a unused,       b = sorted_columns i32 (wb = width), c = ends i32 (wc = m), table)
+template <int ROWS, int NS, int FMT>
+__global__ void __launch_bounds__(ROWS) spmv_rows_tma_kernel(const double *__restrict__ values,
+                                                            const int32_t *__restrict__ columns,
+                                                            const int32_t *__restrict__ ends,
+                                                            const double *__restrict__ table, int width, int m,
+                                                            const double *__restrict__ x, int64_t x_col0,
+                                                            double *__restrict__ y, int row_begin, int row_end, int tile0,
+                                                            int n_tiles, const int32_t *__restrict__ row_map) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const uint32_t bytes_v = FMT == 0 ? (uint32_t)ROWS * width * 8 : 0;
+    const uint32_t bytes_c = (uint32_t)ROWS * width * 4;
+    const uint32_t bytes_e = FMT == 1 ? (uint32_t)ROWS * m * 4 : 0;
+    const uint32_t stage_bytes = bytes_v + bytes_c + bytes_e;  // each a multiple of 16
+    __shared__ __align__(8) uint64_t full_bar[NS];
+    __shared__ double s_table[FMT == 1 ? 256 : 1];
+    if (FMT == 1)
+        for (int i = threadIdx.x; i < m && i < 256; i += ROWS) s_table[i] = table[i];
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NS; s++) mbar_init(smem_u32(&full_bar[s]), 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    auto issue = [&](int it) {  // elected thread: fetch the it-th tile of this CTA into stage it % NS
+        const int tile = blockIdx.x + it * gridDim.x;
+        if (tile >= n_tiles) return;
+        const int s = it % NS;
+        const int64_t r0 = (int64_t)(tile0 + tile) * ROWS;
+        const uint32_t bar = smem_u32(&full_bar[s]);
+        const uint32_t dst = smem_u32(smem + (size_t)s * stage_bytes);
+        mbar_expect_tx(bar, stage_bytes);
+        if (FMT == 0) bulk_g2s(dst, values + r0 * width, bytes_v, bar);
+        bulk_g2s(dst + bytes_v, columns + r0 * width, bytes_c, bar);
+        if (FMT == 1) bulk_g2s(dst + bytes_v + bytes_c, ends + r0 * m, bytes_e, bar);
+    };
+    if (threadIdx.x == 0)
+        for (int it = 0; it < NS; it++) issue(it);
+    for (int it = 0;; it++) {
+        const int tile = blockIdx.x + it * gridDim.x;
+        if (tile >= n_tiles) break;
+        const int s = it % NS;
+        mbar_wait(smem_u32(&full_bar[s]), (it / NS) & 1);
+        const unsigned char *st = smem + (size_t)s * stage_bytes;
+        const int r = (tile0 + tile) * ROWS + threadIdx.x;
+        if (r >= row_begin && r < row_end) {
+            const int32_t *c = reinterpret_cast<const int32_t *>(st + bytes_v) + threadIdx.x * width;
+            double acc;
+            if (FMT == 0) {
+                const double *v = reinterpret_cast<const double *>(st) + threadIdx.x * width;
+                acc = width == 27 ? ell_row<27>(v, c, 27, x, x_col0) : ell_row<9>(v, c, width, x, x_col0);
+            } else {
+                const int32_t *e = reinterpret_cast<const int32_t *>(st + bytes_v + bytes_c) + threadIdx.x * m;
+                const double *tab = m <= 256 ? s_table : table;
+                acc = vt_row<9>(c, e, tab, m, x, x_col0);
+            }
+            y[row_map ? row_map[r] : r] = acc;
+        }
+        __syncthreads();  // every thread is done with stage s
+        if (threadIdx.x == 0) {
+            fence_proxy_async();  // order the generic-proxy reads before the async-proxy refill
+            issue(it + NS);
+        }
+    }
+}
+
+// ---- host-side launchers -----------------------------------------------------------
+int check_launch(const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(SPMVB_ERR_CUDA, "%s launch failed: %s", what, cudaGetErrorString(e));
+    return SPMVB_OK;
+}
+
+int launch_ell(const double *values, const int32_t *columns, int width, const double *x, int64_t x_col0,
+                      double *y, int row_begin, int row_end, const int32_t *row_map, cudaStream_t st) {
+    if (row_end <= row_begin || width == 0) {
+        if (width == 0 && row_end > row_begin && !row_map)
+            SPMVB_CUDA(cudaMemsetAsync(y + row_begin, 0, (size_t)(row_end - row_begin) * 8, st));
+        return SPMVB_OK;
+    }
+    if (options().ell_kernel == 1 && !row_map) {
+        const int threads = 128;
+        spmv_ell_naive_kernel<<<(row_end - row_begin + threads - 1) / threads, threads, 0, st>>>(
+            values, columns, width, x, x_col0, y, row_begin, row_end);
+        return check_launch("spmv_ell_naive");
+    }
+    const int tile0 = row_begin / kTileRows;
+    const int tiles = (row_end + kTileRows - 1) / kTileRows - tile0;
+    const size_t smem = (size_t)kTileRows * width * 12;
+    if (smem > 200 * 1024) return fail(SPMVB_ERR_INVALID_ARGUMENT, "ELL width %d too large for the staged kernel", width);
+    if (options().ell_kernel != 2) {
+        // TMA bulk pipeline (default): persistent CTAs, NS stages of one tile each
+        constexpr int NS = 2;
+        const size_t stage = smem;  // multiple of 16 for any width (128 rows)
+        const size_t need = stage * NS;
+        if (need <= 220 * 1024) {
+            static bool tma_attr = false;
+            if (!tma_attr) {
+                SPMVB_CUDA(cudaFuncSetAttribute(spmv_rows_tma_kernel<kTileRows, NS, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+                tma_attr = true;
+            }
+            const int per_sm = std::max(1, (int)std::min<size_t>(8, (220 * 1024) / (need + 1024)));
+            const int grid = std::min(tiles, 148 * per_sm);
+            spmv_rows_tma_kernel<kTileRows, NS, 0><<<grid, kTileRows, need, st>>>(values, columns, nullptr, nullptr, width, 0, x, x_col0, y,
+                                                                               row_begin, row_end, tile0, tiles, row_map);
+            return check_launch("spmv_ell_tma");
+        }
+    }
+    static bool attr_set = false;
+    if (!attr_set) {
+        SPMVB_CUDA(cudaFuncSetAttribute(spmv_ell_kernel<kTileRows>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr_set = true;
+    }
+    spmv_ell_kernel<kTileRows><<<tiles, kTileRows, smem, st>>>(values, columns, width, x, x_col0, y, row_begin,
+                                                               row_end, tile0, row_map);
+    return check_launch("spmv_ell");
+}
+
+int launch_vt(const spmvb_matrix *a, const double *x, int64_t x_col0, double *y, int row_begin, int row_end,
+                     cudaStream_t st) {
+    if (row_end <= row_begin) return SPMVB_OK;
+    const int tile0 = row_begin / kTileRows;
+    const int tiles = (row_end + kTileRows - 1) / kTileRows - tile0;
+    const size_t smem = (size_t)kTileRows * (a->width + a->m) * 4 + (size_t)a->m * 8 + 16;
+    if (smem > 200 * 1024) return fail(SPMVB_ERR_INVALID_ARGUMENT, "vt width/table too large for the staged kernel");
+    if (options().ell_kernel == 3) {  // TMA bulk pipeline: measured slower than the staged kernel for vt (545 vs 470 us)
+        constexpr int NS = 2;
+        const size_t stage = (size_t)kTileRows * (a->width + a->m) * 4;
+        const size_t need = stage * NS;
+        if (need <= 200 * 1024) {
+            static bool tma_attr = false;
+            if (!tma_attr) {
+                SPMVB_CUDA(cudaFuncSetAttribute(spmv_rows_tma_kernel<kTileRows, NS, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+                tma_attr = true;
+            }
+            const int per_sm = std::max(1, (int)std::min<size_t>(8, (200 * 1024) / (need + 4096)));
+            const int grid = std::min(tiles, 148 * per_sm);
+            spmv_rows_tma_kernel<kTileRows, NS, 1><<<grid, kTileRows, need, st>>>(
+                nullptr, static_cast<const int32_t *>(a->s[SPMVB_S_SORTED_COLUMNS]), static_cast<const int32_t *>(a->s[SPMVB_S_ENDS]),
+                static_cast<const double *>(a->s[SPMVB_S_TABLE]), a->width, a->m, x, x_col0, y, row_begin, row_end, tile0, tiles, nullptr);
+            return check_launch("spmv_vt_tma");
+        }
+    }
+    static bool attr_set = false;
+    if (!attr_set) {
+        SPMVB_CUDA(cudaFuncSetAttribute(spmv_vt_kernel<kTileRows>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr_set = true;
+    }
+    spmv_vt_kernel<kTileRows><<<tiles, kTileRows, smem, st>>>(
+        static_cast<const int32_t *>(a->s[SPMVB_S_SORTED_COLUMNS]), static_cast<const int32_t *>(a->s[SPMVB_S_ENDS]),
+        static_cast<const double *>(a->s[SPMVB_S_TABLE]), a->width, a->m, x, x_col0, y, row_begin, row_end, tile0);
+    return check_launch("spmv_vt");
+}
+
+}  // namespace spmvb
