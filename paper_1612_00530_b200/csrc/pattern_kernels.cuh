@@ -367,11 +367,12 @@ struct Box3Smem {
     uint32_t cls0, cls1, masks;  // 32-bit shared addresses of the three tables
 };
 
-template <int Q, int LPS, bool OFF_NEG1, int CENTER_POS>
+template <int Q, int LPS, bool OFF_NEG1, int CENTER_POS, int LA = 0>
 __device__ __forceinline__ void box3_march(const PatternArgs &p, const Box3Smem sm, const double *__restrict__ xw,
                                            const int32_t *__restrict__ idw, double *__restrict__ yw, int64_t xi_w, int lane,
                                            int nb, bool lane_ok, int nq) {
-    constexpr int S = LPS + 2, P = Q + 2;
+    // window slots: lines jb-1 .. jb+LPS in use by the step, plus LA steps of look-ahead in flight
+    constexpr int S = LPS * (1 + LA) + 2, P = Q + 2;
     constexpr int U = (S % LPS == 0) ? S / LPS : S;  // steps until the slot pattern repeats
     const int sy = p.sy;
     const int sz = sy * p.plane_lines;
@@ -407,7 +408,8 @@ __device__ __forceinline__ void box3_march(const PatternArgs &p, const Box3Smem 
         return r;
     };
     load_line(S - 1, -sy);
-    load_line(0, 0);
+#pragma unroll
+    for (int l = 0; l <= LA * LPS; l++) load_line(l, l * sy);
     int2 idn[LPS][Q];
 #pragma unroll
     for (int l = 0; l < LPS; l++)
@@ -423,7 +425,7 @@ __device__ __forceinline__ void box3_march(const PatternArgs &p, const Box3Smem 
             const int kb = (u * LPS) % S;  // its slot
             if (jb < nb) {
 #pragma unroll
-                for (int l = 0; l < LPS; l++) load_line((kb + 1 + l) % S, (1 + l) * sy);
+                for (int l = 0; l < LPS; l++) load_line((kb + 1 + l + LA * LPS) % S, (1 + l + LA * LPS) * sy);
                 int id[LPS][Q][2];
                 uint32_t c0[LPS][Q], c1[LPS][Q], wv = 0;
 #pragma unroll
@@ -531,7 +533,7 @@ __device__ __noinline__ void box3_edge_tile(const PatternArgs &p, const uint32_t
                                                     half * 32 + lane < cols_ok, false, false);
 }
 
-template <int R, int WC, int Q, int LPS, int MINB, bool OFF_NEG1, int CENTER_POS, int WA = 1>
+template <int R, int WC, int Q, int LPS, int MINB, bool OFF_NEG1, int CENTER_POS, int WA = 1, int LA = 0>
 __global__ void __launch_bounds__(WC * 32, MINB) spmv_pattern_box3_kernel(PatternArgs p, int n_planes) {
     __shared__ uint32_t s_cls0[kDictSmemPat + 1], s_cls1[kDictSmemPat + 1], s_masks1[kDictSmemPat + 1];
     box3_fill_tables(p, s_cls0, s_cls1, s_masks1, threadIdx.x, WC * 32);
@@ -563,11 +565,11 @@ __global__ void __launch_bounds__(WC * 32, MINB) spmv_pattern_box3_kernel(Patter
     const int nb_up = (nb + LPS - 1) / LPS * LPS;
     const int64_t last_row = r_w + (cols_ok - 1) + (int64_t)(nb - 1) * sy + (int64_t)(nq - 1) * sz;
     const int64_t x_lo = xi_w - sy - sz - 1;
-    const int64_t x_hi = xi_w + 64 + (int64_t)(nb_up + LPS + pf) * sy + (int64_t)Q * sz + 1;
+    const int64_t x_hi = xi_w + 64 + (int64_t)(nb_up + LPS * (1 + LA) + pf) * sy + (int64_t)Q * sz + 1;
     const int64_t id_hi = r_w + 64 + (int64_t)(nb_up + LPS + pf) * sy + (int64_t)(nq - 1) * sz;  // ids prefetch reach
     const bool interior = last_row < n_rows && x_lo >= 0 && x_hi < p.x_len && id_hi <= n_rows + 1024;
     if (interior) {
-        box3_march<Q, LPS, OFF_NEG1, CENTER_POS>(p, sm, p.x + xi_w, p.ids + p.row_begin + r_w, p.y + p.row_begin + r_w, xi_w,
+        box3_march<Q, LPS, OFF_NEG1, CENTER_POS, LA>(p, sm, p.x + xi_w, p.ids + p.row_begin + r_w, p.y + p.row_begin + r_w, xi_w,
                                                  lane, nb, lane * 2 + 1 < cols_ok, nq);
     } else {
         box3_edge_tile<Q, OFF_NEG1, CENTER_POS>(p, s_masks, r_w, lane, nb, n_rows, nq, cols_ok);

@@ -27,7 +27,7 @@ static int launch_box_rw(const spmvb_matrix *a, PatternArgs &p, cudaStream_t st)
 }
 
 // v3 launch: returns 1 when the configuration / alignment is not served (caller falls back to v2)
-template <int R, int WC, int Q, int LPS, int MINB, bool ALLV, int WA = 1>
+template <int R, int WC, int Q, int LPS, int MINB, bool ALLV, int WA = 1, int LA = 0>
 static int launch_box3(const spmvb_matrix *a, PatternArgs &p, cudaStream_t st) {
     const int64_t n_rows = (int64_t)p.row_end - p.row_begin;
     const int64_t sz = (int64_t)p.sy * p.plane_lines;
@@ -37,7 +37,7 @@ static int launch_box3(const spmvb_matrix *a, PatternArgs &p, cudaStream_t st) {
     if (!ALLV && !(neg1 && cp == 1)) return 1;
     dim3 grid((p.sy + 64 * WA - 1) / (64 * WA), (p.plane_lines + R - 1) / R, (n_planes + (WC / WA) * Q - 1) / ((WC / WA) * Q));
     dim3 block(WC * 32);
-#define LAUNCH3(NEG, CP) spmv_pattern_box3_kernel<R, WC, Q, LPS, MINB, NEG, CP, WA><<<grid, block, 0, st>>>(p, n_planes)
+#define LAUNCH3(NEG, CP) spmv_pattern_box3_kernel<R, WC, Q, LPS, MINB, NEG, CP, WA, LA><<<grid, block, 0, st>>>(p, n_planes)
     if constexpr (ALLV) {
         if (neg1) {
             if (cp == 0) LAUNCH3(true, 0); else if (cp == 1) LAUNCH3(true, 1); else LAUNCH3(true, 2);
@@ -95,6 +95,7 @@ static int launch_pattern(const spmvb_matrix *a, const double *x, int64_t x_col0
                     case 1: rc3 = launch_box3<16, 4, 2, 1, 3, false>(a, p, st); break;      // R=16 tiles            124 us
                     case 5: rc3 = launch_box3<16, 4, 1, 2, 3, false>(a, p, st); break;      // 1 plane, 2 lines/step 116-121 us
                     case 12: rc3 = launch_box3<16, 4, 2, 1, 3, false, 4>(a, p, st); break;  // CTA spans full lines  124 us
+                    case 70: rc3 = launch_box3<8, 4, 2, 1, 2, false, 1, 1>(a, p, st); break;   // register look-ahead LA=1: 146 us (sweep: profiles/r01_probe256_lookahead_sweep.log)
                     case 20: case 30: case 35: case 47: case 62:                            // spmv_pattern_lab.cu
                         rc3 = launch_pattern_lab(o.box_march, a, p, st); break;
                     // default <R=8 lines, 4 warps, Q=2 planes/thread, 1 line/step, 3 CTAs/SM>: 118 us

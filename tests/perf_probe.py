@@ -62,8 +62,8 @@ if "pattern" in fmts or "generic" in fmts:
     ref = None
     if "pattern" in fmts:
         for march, name in ((0, "box3 default"), (1, "box3 R=16"), (5, "box3 Q=1 2 lines/step"), (12, "box3 full-line CTA"),
-                            (20, "box5 cp.async ring"), (35, "box6 4 cols/thread"), (30, "box6 8 cols/thread"),
-                            (47, "box7 pipelined ring"), (62, "box8 TMA ring 8w R=8")):
+                            (70, "box3 look-ahead 1"), (20, "box5 cp.async ring"), (35, "box6 4 cols/thread"),
+                            (30, "box6 8 cols/thread"), (47, "box7 pipelined ring"), (62, "box8 TMA ring 8w R=8")):
             timeit(d, f"pattern {name}", 20, pattern_kernel=2, box_march=march, box_prefetch=2)
         timeit(d, "pattern box v2 <16,8,2,0> pf=4", 20, pattern_kernel=3, box_march=0, box_prefetch=4)
     if "generic" in fmts:

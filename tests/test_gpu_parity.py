@@ -86,7 +86,7 @@ def test_pattern_kernels_generic_and_box(sp, orc, g, kernel):
     assert np.array_equal(bits(y), bits(orc.spmv(pc, x)))
 
 
-@pytest.mark.parametrize("march", [1, 5, 11, 12, 20, 30, 35, 47, 62])
+@pytest.mark.parametrize("march", [1, 5, 11, 12, 20, 30, 35, 47, 62, 70])
 @pytest.mark.parametrize("g", [(40, 37, 11), (128, 36, 20), (192, 40, 19), (256, 20, 12), (264, 18, 11), (512, 19, 15)])
 def test_box_march_variants(sp, orc, march, g):
     m = orc.generate_matrix(*g)
