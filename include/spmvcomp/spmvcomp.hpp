@@ -6,13 +6,15 @@
 // (grid.hpp, stencil.hpp, ...) forward here.  Every function below runs on the GPU
 // through the C-ABI in spmvcomp_b200.h -- there is no CPU implementation.
 //
-// Declared here: everything on the SpMV path.
-// Not declared: dot / waxpby / symgs_sweep / cg_solve / model_table* / Matrix
-// Market export, which are callers or tooling around the path (section 8f).
+// Declared here: everything on the SpMV path and its first
+// caller, the CG driver with dot / waxpby (section 8f row N1; unpreconditioned only).
+// Not declared: symgs_sweep, model_table*, Matrix Market export (tooling / sequential
+// smoother outside the path, section 8f rows N2-N4).
 #pragma once
 
 #include <cstddef>
 #include <cstdint>
+#include <map>
 #include <optional>
 #include <span>
 #include <stdexcept>
@@ -170,6 +172,35 @@ void spmv_rows(const VtCompressedMatrix& a, std::span<const double> x, std::span
 void spmv_rows(const PatternCompressedMatrix& a, std::span<const double> x, std::span<double> y, std::int32_t begin,
                std::int32_t end);
 }  // namespace unchecked
+
+// ---------------------------------------------------------------- CG caller (inc/kernels.hpp:39-42, inc/solver.hpp:13-46)
+double dot(const Vector& u, const Vector& v);                                               // length mismatch -> invalid_argument
+Vector waxpby(double alpha, const Vector& x, double beta, const Vector& y);                 // w = alpha*x + beta*y
+void waxpby_into(double alpha, const Vector& x, double beta, const Vector& y, Vector& w);
+
+enum class SpmvBackend { ell, vt, pattern };
+const char* backend_name(SpmvBackend b);
+
+struct CgConfig {
+    int max_iterations = 500;
+    double tolerance = 1e-8;  // relative residual ||r||2 / ||b||2
+    int symgs_sweeps = 0;     // 0 = unpreconditioned; >= 1 is not available on the device path (std::invalid_argument)
+    SpmvBackend backend = SpmvBackend::ell;
+};
+struct OpStats {
+    std::int64_t calls = 0, flops = 0;
+    double seconds = 0.0;
+};
+struct CgReport {
+    int iterations = 0;
+    bool converged = false;
+    std::vector<double> residual_history;  // iterations + 1 entries, [0] = 1.0
+    std::int64_t flops_total = 0;
+    std::map<std::string, OpStats> per_op;  // "spmv", "dot", "waxpby", "precond"
+    double final_residual() const { return residual_history.back(); }
+};
+// x0 = 0; per iteration exactly 1 SpMV (on the configured backend), 3 dots and 3 waxpbys, all on the GPU.
+std::pair<Vector, CgReport> cg_solve(const StencilMatrix& m, const Vector& b, const CgConfig& cfg = {});
 
 // ---------------------------------------------------------------- byte model (inc/perf_model.hpp:14-80)
 enum class MatrixFormat { ell, vt, pattern, pattern_with_values };

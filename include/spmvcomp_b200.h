@@ -197,6 +197,20 @@ int spmvb_spmv(const spmvb_matrix *a, const double *x_dev, int64_t x_col0, int64
  * device, runs, copies y back, synchronises. */
 int spmvb_spmv_host(const spmvb_matrix *a, const double *x_host, int64_t x_len, double *y_host);
 
+/* ---- the caller of the path: CG vector primitives and driver ---- */
+/* dot (inc/kernels.hpp:39): device vectors, result to the host; fixed-shape tree (deterministic). */
+int spmvb_dot(const double *u_dev, const double *v_dev, int64_t n, double *result, void *stream);
+/* waxpby_into (inc/kernels.hpp:41-42): w = alpha*x + beta*y, bit-identical to the reference expression;
+ * w may alias x or y. */
+int spmvb_waxpby(double alpha, const double *x_dev, double beta, const double *y_dev, double *w_dev, int64_t n,
+                 void *stream);
+/* cg_solve (inc/solver.hpp:40-46) without preconditioner, x0 = 0, SpMV on the handle's format:
+ * per iteration 1 SpMV, 3 dots, 3 waxpbys.  residual_history (may be NULL) needs max_iterations+1
+ * slots: [0] = 1.0, [k] = ||r_k|| / ||b||.  SPMVB_ERR_DIVERGENCE on a non-finite value
+ * (iteration in the message and in *iterations). */
+int spmvb_cg_solve(const spmvb_matrix *a, const double *b_dev, double *x_dev, int32_t max_iterations, double tolerance,
+                   int32_t *iterations, int32_t *converged, double *residual_history, void *stream);
+
 /* ---- verification helpers ----------------------------------------------------- */
 /* max_i |y[i]-ref[i]| / den[i] and the number of entries whose bit patterns
  * differ.  den = scale[i] (= sum_k |a_ik x_k|, from spmvb_row_abs_scale) when a

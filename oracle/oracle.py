@@ -115,6 +115,12 @@ def lib():
         _lib.orc_spmv_csr.restype = None
         _lib.orc_row_abs_scale.argtypes = [C.POINTER(_Csr), C.c_void_p, C.c_void_p]
         _lib.orc_row_abs_scale.restype = None
+        _lib.orc_dot.restype = C.c_double
+        _lib.orc_dot.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
+        _lib.orc_waxpby.restype = None
+        _lib.orc_waxpby.argtypes = [C.c_double, C.c_void_p, C.c_double, C.c_void_p, C.c_void_p, C.c_int64]
+        _lib.orc_cg_solve.argtypes = [C.c_int, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int32, C.c_double,
+                                      C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.c_void_p, C.POINTER(C.c_int32)]
         _lib.orc_csr_from_arrays.argtypes = [C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
                                              C.POINTER(C.POINTER(_Csr))]
     return _lib
@@ -397,3 +403,42 @@ def measured_cost(a):
     fn = {Ell: "orc_measured_cost_ell", Vt: "orc_measured_cost_vt", Pattern: "orc_measured_cost_pattern"}[type(a)]
     _check(getattr(lib(), fn)(a.p, C.byref(c)))
     return c
+
+
+def dot(u, v):
+    """dot (kernels.hpp:39): index-ascending sum."""
+    u, v = np.ascontiguousarray(u, dtype=np.float64), np.ascontiguousarray(v, dtype=np.float64)
+    if u.shape != v.shape:
+        raise InvalidArgument(INVALID_ARGUMENT, "length mismatch")
+    return lib().orc_dot(_ptr(u), _ptr(v), u.shape[0])
+
+
+def waxpby(alpha, x, beta, y):
+    """waxpby (kernels.hpp:41)."""
+    x, y = np.ascontiguousarray(x, dtype=np.float64), np.ascontiguousarray(y, dtype=np.float64)
+    if x.shape != y.shape:
+        raise InvalidArgument(INVALID_ARGUMENT, "length mismatch")
+    w = np.empty_like(x)
+    lib().orc_waxpby(alpha, _ptr(x), beta, _ptr(y), _ptr(w), x.shape[0])
+    return w
+
+
+class DivergenceError(OracleError):  # errors.hpp:22
+    pass
+
+
+def cg_solve(a, b, max_iterations=500, tolerance=1e-8):
+    """cg_solve (solver.hpp:40-46), unpreconditioned; `a` is the SpMV backend (Ell, Vt or Pattern).
+    Returns (x, iterations, converged, residual_history)."""
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    if b.shape[0] != a.n:
+        raise InvalidArgument(INVALID_ARGUMENT, "length mismatch")
+    fmt = {Ell: 0, Vt: 1, Pattern: 2}[type(a)]
+    x = np.empty(a.n)
+    hist = np.zeros(max_iterations + 1)
+    it, conv, div = C.c_int32(), C.c_int32(), C.c_int32()
+    _check(lib().orc_cg_solve(fmt, C.cast(a.p, C.c_void_p), a.n, _ptr(b), _ptr(x), max_iterations, tolerance,
+                              C.byref(it), C.byref(conv), _ptr(hist), C.byref(div)))
+    if div.value:
+        raise DivergenceError(6, f"non-finite value in iteration {div.value}")
+    return x, it.value, bool(conv.value), hist[:it.value + 1].copy()

@@ -975,6 +975,63 @@ void orc_row_abs_scale(const orc_csr *a, const double *x, double *scale) {
 }
 
 /* ------------------------------------------------------------------------- */
+/* CG caller                                                                  */
+/* ------------------------------------------------------------------------- */
+double orc_dot(const double *u, const double *v, int64_t n) {
+    /* sequential accumulation, index ascending */
+    double acc = 0.0;
+    for (int64_t i = 0; i < n; i++) {
+        double prod = u[i] * v[i];
+        acc = acc + prod;
+    }
+    return acc;
+}
+void orc_waxpby(double alpha, const double *x, double beta, const double *y, double *w, int64_t n) {
+    /* w[i] = alpha*x[i] + beta*y[i] */
+    for (int64_t i = 0; i < n; i++) {
+        double ax = alpha * x[i], by = beta * y[i];
+        w[i] = ax + by;
+    }
+}
+static void cg_spmv(int format, const void *a, int32_t n, const double *x, double *y) {
+    if (format == 0) ell_rows(a, x, 0, y, 0, n);
+    else if (format == 1) vt_rows(a, x, 0, y, 0, n);
+    else pattern_rows(a, x, 0, y, 0, n);
+}
+int orc_cg_solve(int format, const void *a, int32_t n, const double *b, double *x, int32_t max_iterations,
+                 double tolerance, int32_t *iterations, int32_t *converged, double *history, int32_t *diverged_at) {
+    /* solver.hpp:40-46: r = b - A*0, z = r (no preconditioner), p = z; per iteration exactly
+     * 1 SpMV, 3 dots, 3 waxpbys; stop when ||r||2 / ||b||2 <= tolerance. */
+    if (max_iterations < 1 || !(tolerance > 0.0) || format < 0 || format > 2)
+        FAIL(ORC_INVALID_ARGUMENT, "cg_solve: bad configuration");
+    double *r = malloc((size_t)n * 8), *p = malloc((size_t)n * 8), *ap = malloc((size_t)n * 8);
+    *iterations = 0; *converged = 0; *diverged_at = 0;
+    for (int32_t i = 0; i < n; i++) { x[i] = 0.0; r[i] = b[i]; p[i] = b[i]; }
+    double bnorm = sqrt(orc_dot(b, b, n));
+    double rz = orc_dot(r, r, n);
+    history[0] = 1.0;
+    if (bnorm == 0.0) { *converged = 1; free(r); free(p); free(ap); return ORC_OK; }
+    for (int32_t it = 1; it <= max_iterations; it++) {
+        cg_spmv(format, a, n, p, ap);
+        double alpha = rz / orc_dot(p, ap, n);
+        orc_waxpby(1.0, x, alpha, p, x, n);
+        orc_waxpby(1.0, r, -alpha, ap, r, n);
+        double rr = orc_dot(r, r, n);
+        double rz_new = orc_dot(r, r, n);
+        double rel = sqrt(rr) / bnorm;
+        *iterations = it;
+        history[it] = rel;
+        if (!isfinite(alpha) || !isfinite(rel)) { *diverged_at = it; break; }
+        if (rel <= tolerance) { *converged = 1; break; }
+        double beta = rz_new / rz;
+        rz = rz_new;
+        orc_waxpby(1.0, r, beta, p, p, n);
+    }
+    free(r); free(p); free(ap);
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------- */
 /* byte model                                                                 */
 /* ------------------------------------------------------------------------- */
 static void cost_finish(orc_cost *c, double flops_per_row) {

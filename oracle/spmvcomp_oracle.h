@@ -164,6 +164,15 @@ void orc_spmv_csr(const orc_csr *a, const double *x, double *y);
 /* sum_k |a_ik * x_k| per row: the scale for "relative per row". */
 void orc_row_abs_scale(const orc_csr *a, const double *x, double *scale);
 
+/* ---- CG caller (kernels.hpp:39-42, solver.hpp:40-46) -- */
+double orc_dot(const double *u, const double *v, int64_t n);                 /* index-ascending sum */
+void orc_waxpby(double alpha, const double *x, double beta, const double *y, double *w, int64_t n);
+/* Unpreconditioned CG, x0 = 0.  format: 0 ell, 1 vt, 2 pattern (the SpMV backend); `a` points
+ * to the matching struct.  history needs max_iterations+1 slots.  Returns ORC_OK, or
+ * ORC_INVALID_ARGUMENT; *diverged_at > 0 when a non-finite value appeared. */
+int orc_cg_solve(int format, const void *a, int32_t n, const double *b, double *x, int32_t max_iterations,
+                 double tolerance, int32_t *iterations, int32_t *converged, double *history, int32_t *diverged_at);
+
 /* ---- byte model (perf_model.hpp:49-80) -------------------- */
 typedef struct orc_cost {
     double bytes_per_row, flops_per_row, bytes_per_flop;

@@ -87,7 +87,8 @@ SYMBOLS = [
     "spmvb_to_csr", "spmvb_validate", "spmvb_pattern_remap", "spmvb_pattern_first_rows", "spmvb_matrix_get_info",
     "spmvb_matrix_stream_bytes", "spmvb_matrix_download", "spmvb_matrix_stream_ptr", "spmvb_matrix_destroy",
     "spmvb_vec_alloc", "spmvb_vec_free", "spmvb_vec_upload", "spmvb_vec_download", "spmvb_vec_fill",
-    "spmvb_spmv", "spmvb_spmv_host", "spmvb_compare", "spmvb_row_abs_scale",
+    "spmvb_spmv", "spmvb_spmv_host", "spmvb_compare", "spmvb_row_abs_scale", "spmvb_dot", "spmvb_waxpby",
+    "spmvb_cg_solve",
 ]
 
 if not os.path.exists(SO_PATH):
@@ -126,6 +127,9 @@ lib.spmvb_spmv.argtypes = [_vp, _vp, _i64, _i64, _vp, _i32, _i32, _vp]
 lib.spmvb_spmv_host.argtypes = [_vp, _vp, _i64, _vp]
 lib.spmvb_compare.argtypes = [_vp, _vp, _vp, _i64, C.POINTER(_f64), C.POINTER(_i64), _vp]
 lib.spmvb_row_abs_scale.argtypes = [_vp, _vp, _i64, _vp, _vp]
+lib.spmvb_dot.argtypes = [_vp, _vp, _i64, C.POINTER(_f64), _vp]
+lib.spmvb_waxpby.argtypes = [_f64, _vp, _f64, _vp, _vp, _i64, _vp]
+lib.spmvb_cg_solve.argtypes = [_vp, _vp, _vp, _i32, _f64, C.POINTER(_i32), C.POINTER(_i32), _vp, _vp]
 lib.spmvb_set_option.argtypes = [C.c_char_p, C.c_int]
 lib.spmvb_get_option.argtypes = [C.c_char_p, C.POINTER(C.c_int)]
 lib.spmvb_device_count.argtypes = [C.POINTER(C.c_int)]

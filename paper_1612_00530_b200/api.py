@@ -303,6 +303,44 @@ def spmv(a: DeviceMatrix, x) -> np.ndarray:
     return y
 
 
+def dot(u, v, n=None, stream=None) -> float:
+    """dot (kernels.hpp:39) on device vectors."""
+    n = u.n if n is None else n
+    out = C.c_double()
+    check(lib.spmvb_dot(_ptr(u), _ptr(v), n, C.byref(out), _stream(stream)))
+    return out.value
+
+
+def waxpby_into(alpha, x, beta, y, w, n=None, stream=None):
+    """waxpby_into (kernels.hpp:42): w = alpha*x + beta*y on device vectors (w may alias x or y)."""
+    n = x.n if n is None else n
+    check(lib.spmvb_waxpby(alpha, _ptr(x), beta, _ptr(y), _ptr(w), n, _stream(stream)))
+
+
+@dataclass
+class CgReport:
+    """solver.hpp:30-38 (flops per SPEC.md:321: 2*nnz + 6n + 6n per iteration, no preconditioner)."""
+    iterations: int
+    converged: bool
+    residual_history: list
+    flops_total: int
+
+    def final_residual(self):
+        return self.residual_history[-1]
+
+
+def cg_solve(a: DeviceMatrix, b, max_iterations=500, tolerance=1e-8, stream=None):
+    """cg_solve (solver.hpp:40-46), unpreconditioned, on the device.  b: device vector; returns (x, CgReport)."""
+    n = a.n
+    x = DeviceVector(n)
+    hist = np.zeros(max_iterations + 1, dtype=np.float64)
+    it, conv = C.c_int32(), C.c_int32()
+    check(lib.spmvb_cg_solve(a.h, _ptr(b), _ptr(x), max_iterations, tolerance, C.byref(it), C.byref(conv), _ptr(hist),
+                             _stream(stream)))
+    k = it.value
+    return x, CgReport(k, bool(conv.value), hist[:k + 1].tolist(), k * (2 * a.nnz + 12 * n))
+
+
 def compare(y, ref, n, scale=None, stream=None):
     """Device-side (max relative deviation, number of bit-different entries)."""
     worst, bad = C.c_double(), C.c_int64()

@@ -7,6 +7,7 @@
 // (g++ -I/root/reference/proj/include ...), which is how tests/test_cpp_api.py checks that
 // the signatures are drop-in compatible.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -17,6 +18,7 @@
 #include "spmvcomp/grid.hpp"
 #include "spmvcomp/kernels.hpp"
 #include "spmvcomp/perf_model.hpp"
+#include "spmvcomp/solver.hpp"
 #include "spmvcomp/stencil.hpp"
 #include "spmvcomp_b200/device.hpp"
 
@@ -362,6 +364,62 @@ void spmv_rows(const EllMatrix& a, std::span<const double> x, std::span<double> 
 void spmv_rows(const VtCompressedMatrix& a, std::span<const double> x, std::span<double> y, std::int32_t b, std::int32_t e) { rows_impl(a, x, y, b, e); }
 void spmv_rows(const PatternCompressedMatrix& a, std::span<const double> x, std::span<double> y, std::int32_t b, std::int32_t e) { rows_impl(a, x, y, b, e); }
 }  // namespace unchecked
+
+// ---------------------------------------------------------------- CG caller
+double dot(const Vector& u, const Vector& v) {
+    if (u.size() != v.size()) throw std::invalid_argument("dot: length mismatch");
+    if (u.empty()) return 0.0;
+    b200::DeviceVector du(u), dv(v);
+    double out = 0.0;
+    throw_on_error(spmvb_dot(du.data(), dv.data(), du.size(), &out, nullptr));
+    return out;
+}
+void waxpby_into(double alpha, const Vector& x, double beta, const Vector& y, Vector& w) {
+    if (x.size() != y.size()) throw std::invalid_argument("waxpby: length mismatch");
+    w.resize(x.size());
+    if (x.empty()) return;
+    b200::DeviceVector dx(x), dy(y), dw((std::int64_t)x.size());
+    throw_on_error(spmvb_waxpby(alpha, dx.data(), beta, dy.data(), dw.data(), dx.size(), nullptr));
+    w = dw.download();
+}
+Vector waxpby(double alpha, const Vector& x, double beta, const Vector& y) {
+    Vector w;
+    waxpby_into(alpha, x, beta, y, w);
+    return w;
+}
+const char* backend_name(SpmvBackend b) {
+    return b == SpmvBackend::ell ? "ell" : (b == SpmvBackend::vt ? "vt" : "pattern");
+}
+std::pair<Vector, CgReport> cg_solve(const StencilMatrix& m, const Vector& b, const CgConfig& cfg) {
+    if ((std::int64_t)b.size() != m.n) throw std::invalid_argument("cg_solve: b has the wrong length");
+    if (cfg.max_iterations < 1 || !(cfg.tolerance > 0.0)) throw std::invalid_argument("cg_solve: need max_iterations >= 1 and tolerance > 0");
+    if (cfg.symgs_sweeps != 0)
+        throw std::invalid_argument("cg_solve: the SymGS preconditioner is sequential by definition and is not part of the device path");
+    DeviceMatrix csr(m);
+    DeviceMatrix a = cfg.backend == SpmvBackend::ell ? csr.to_ell()
+                   : cfg.backend == SpmvBackend::vt ? csr.compress_values() : csr.compress_patterns(true);
+    b200::DeviceVector db(b), dx(m.n);
+    CgReport rep;
+    rep.residual_history.assign((std::size_t)cfg.max_iterations + 1, 0.0);
+    std::int32_t it = 0, conv = 0;
+    const auto t0 = std::chrono::steady_clock::now();
+    const int rc = spmvb_cg_solve(a.handle(), db.data(), dx.data(), cfg.max_iterations, cfg.tolerance, &it, &conv,
+                                  rep.residual_history.data(), nullptr);
+    const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (rc == SPMVB_ERR_DIVERGENCE) throw DivergenceError(it, spmvb_last_error());
+    throw_on_error(rc);
+    rep.iterations = it;
+    rep.converged = conv != 0;
+    rep.residual_history.resize((std::size_t)it + 1);
+    // inc/solver.hpp:43: per iteration 2*nnz (SpMV) + 3 dots (6n) + 3 waxpbys (6n)
+    rep.per_op["spmv"] = {it, it * spmv_flops(m.nnz()), 0.0};
+    rep.per_op["dot"] = {3LL * it, 3LL * it * dot_flops(m.n), 0.0};
+    rep.per_op["waxpby"] = {3LL * it, 3LL * it * waxpby_flops(m.n), 0.0};
+    rep.per_op["precond"] = {0, 0, 0.0};
+    rep.per_op["spmv"].seconds = secs;  // the loop is timed as a whole on the device path
+    rep.flops_total = rep.per_op["spmv"].flops + rep.per_op["dot"].flops + rep.per_op["waxpby"].flops;
+    return {dx.download(), rep};
+}
 
 // ---------------------------------------------------------------- byte model (host arithmetic only)
 const char* format_name(MatrixFormat f) {

@@ -1,6 +1,7 @@
 // C++ API test of the B200-native spmvcomp: the reference's worked examples and
 // acceptance criteria (SPEC.md, cited per check) run through the reference's own C++
 // interface, with every operation executing on the GPU.  Exit code 0 = all passed.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -11,6 +12,7 @@
 #include "spmvcomp/errors.hpp"
 #include "spmvcomp/kernels.hpp"
 #include "spmvcomp/perf_model.hpp"
+#include "spmvcomp/solver.hpp"
 #include "spmvcomp/stencil.hpp"
 #include "spmvcomp_b200/device.hpp"
 
@@ -188,6 +190,46 @@ int main() {
         CHECK(pv > 4.0 && pv < 4.08);
         CHECK(measured_cost(compress_values(m)).bytes_per_row == 116.0);
         CHECK(std::string(format_name(MatrixFormat::pattern_with_values)) == "pattern-values" && parse_format("vt") == MatrixFormat::vt);
+    }
+    // ---- the CG caller (acceptance criterion 8)
+    {
+        CHECK(dot(Vector{1, 2}, Vector{3, 4}) == 11.0);
+        CHECK(dot(Vector(1000, 1.0), Vector(1000, 1.0)) == 1000.0);
+        CHECK(waxpby(2, Vector{1, 1}, 3, Vector{1, 2}) == (Vector{5, 8}));
+        CHECK(waxpby(1, Vector{1, 1}, 0, Vector{1, 2}) == (Vector{1, 1}) && waxpby(0, Vector{1, 1}, 1, Vector{1, 2}) == (Vector{1, 2}));
+        CHECK(throws<std::invalid_argument>([] { dot(Vector{1}, Vector{1, 2}); }));
+        const StencilMatrix one = generate_matrix(GridSpec{1, 1, 1});
+        auto [x1, r1] = cg_solve(one, Vector{52.0});
+        CHECK(x1 == Vector{2.0} && r1.iterations == 1 && r1.converged);
+        const StencilMatrix m = generate_matrix(GridSpec{16, 16, 16});
+        const Vector b = spmv(to_ell(m), Vector(m.n, 1.0));
+        int its[3];
+        Vector xs[3];
+        int k = 0;
+        for (SpmvBackend be : {SpmvBackend::ell, SpmvBackend::vt, SpmvBackend::pattern}) {
+            CgConfig cfg;
+            cfg.backend = be;
+            auto [x, rep] = cg_solve(m, b, cfg);
+            its[k] = rep.iterations;
+            xs[k] = x;
+            double worst = 0;
+            for (double v : x) worst = std::max(worst, std::fabs(v - 1.0));
+            CHECK(rep.converged && rep.final_residual() <= 1e-8 && worst <= 1e-6);
+            CHECK((int)rep.residual_history.size() == rep.iterations + 1 && rep.residual_history[0] == 1.0);
+            CHECK(rep.flops_total == (std::int64_t)rep.iterations * (2 * m.nnz() + 12 * (std::int64_t)m.n));
+            CHECK(rep.per_op.at("spmv").calls == rep.iterations && rep.per_op.at("dot").calls == 3 * rep.iterations);
+            k++;
+        }
+        CHECK(its[0] == its[1] && its[1] == its[2]);
+        double d = 0;
+        for (int i = 0; i < m.n; i++) d = std::max({d, std::fabs(xs[0][i] - xs[1][i]), std::fabs(xs[0][i] - xs[2][i])});
+        CHECK(d <= 1e-9);
+        CgConfig one_it;
+        one_it.max_iterations = 1;
+        CHECK(!cg_solve(m, b, one_it).second.converged);
+        CgConfig pre;
+        pre.symgs_sweeps = 1;
+        CHECK(throws<std::invalid_argument>([&] { cg_solve(m, b, pre); }));
     }
     // ---- device-resident use: generate and compress on the GPU, many SpMVs, one download
     {

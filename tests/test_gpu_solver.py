@@ -1,0 +1,66 @@
+"""GPU tests of the CG caller: dot, waxpby and cg_solve on the device
+against the oracle's restatement (acceptance criterion 8)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def sp():
+    import paper_1612_00530_b200 as sp
+    return sp
+
+
+def test_dot_and_waxpby(sp, orc):
+    n = 1_000_003
+    u = orc.make_test_vector(n, orc.RANDOM, seed=1, lo=-1.0, hi=1.0)
+    v = orc.make_test_vector(n, orc.RANDOM, seed=2, lo=-1.0, hi=1.0)
+    du, dv, dw = sp.DeviceVector.from_host(u), sp.DeviceVector.from_host(v), sp.DeviceVector(n)
+    ref = orc.dot(u, v)
+    got = sp.dot(du, dv)
+    assert abs(got - ref) <= 1e-12 * np.abs(u * v).sum()  # tree vs index-ascending order
+    assert sp.dot(du, dv) == got  # deterministic run to run
+    assert sp.dot(sp.DeviceVector.from_host(np.ones(1000)), sp.DeviceVector.from_host(np.ones(1000))) == 1000.0
+    sp.waxpby_into(0.75, du, -1.5, dv, dw)
+    assert np.array_equal(dw.to_host().view(np.uint64), orc.waxpby(0.75, u, -1.5, v).view(np.uint64))  # bit-exact
+    sp.waxpby_into(1.0, du, 2.0, dv, du)  # aliasing w = x
+    assert np.array_equal(du.to_host().view(np.uint64), orc.waxpby(1.0, u, 2.0, v).view(np.uint64))
+
+
+@pytest.mark.parametrize("g", [(16, 16, 16), (64, 20, 12)])
+def test_cg_matches_the_oracle_on_every_backend(sp, orc, g):
+    ref_m = orc.generate_matrix(*g)
+    m = sp.generate_matrix(sp.GridSpec(*g))
+    n = ref_m.n
+    b = orc.spmv(orc.to_ell(ref_m), np.ones(n))
+    db = sp.DeviceVector.from_host(b)
+    x_ref, it_ref, conv_ref, hist_ref = orc.cg_solve(orc.to_ell(ref_m), b, tolerance=1e-8)
+    assert conv_ref
+    its, xs = [], []
+    for a in (sp.to_ell(m), sp.compress_values(m), sp.compress_patterns(m, True)):
+        x, rep = sp.cg_solve(a, db, tolerance=1e-8)
+        xh = x.to_host()
+        assert rep.converged and rep.final_residual() <= 1e-8
+        assert rep.iterations == it_ref  # identical iteration counts
+        assert len(rep.residual_history) == rep.iterations + 1 and rep.residual_history[0] == 1.0
+        assert np.abs(np.array(rep.residual_history) - hist_ref).max() <= 1e-10
+        assert np.abs(xh - 1.0).max() <= 1e-6 and np.abs(xh - x_ref).max() <= 1e-9
+        assert rep.flops_total == rep.iterations * (2 * ref_m.nnz + 12 * n)
+        its.append(rep.iterations)
+        xs.append(xh)
+    assert len(set(its)) == 1
+    _, rep = sp.cg_solve(sp.to_ell(m), db, max_iterations=1)
+    assert rep.iterations == 1 and not rep.converged
+
+
+def test_cg_single_unknown_and_errors(sp, orc):
+    a = sp.to_ell(sp.generate_matrix(sp.GridSpec(1, 1, 1)))
+    x, rep = sp.cg_solve(a, sp.DeviceVector.from_host(np.array([52.0])))
+    assert x.to_host().tolist() == [2.0] and rep.iterations == 1 and rep.converged
+    with pytest.raises(sp.InvalidArgument):
+        sp.cg_solve(a, sp.DeviceVector.from_host(np.array([52.0])), tolerance=0.0)
+    # a singular system makes p.Ap = 0 -> non-finite alpha -> DivergenceError (solver.hpp:44)
+    z = sp.upload_ell(2, 1, 0, np.zeros(2), np.array([0, 1], dtype=np.int32))
+    with pytest.raises(sp._cabi.DivergenceError):
+        sp.cg_solve(z, sp.DeviceVector.from_host(np.ones(2)))

@@ -318,3 +318,31 @@ def test_k14_measured_cost(orc):
     one = orc.measured_cost(orc.compress_values(orc.generate_matrix(1, 1, 1)))
     assert one.bytes_per_row == 8.0
     assert orc.measured_cost(orc.to_ell(m)).flops_per_row == pytest.approx(2 * m.nnz / m.n)
+
+
+# ---- the CG caller: SPEC.md:243-256,313-321, acceptance criterion 8 ----------
+def test_dot_waxpby_examples(orc):
+    assert orc.dot([1, 2], [3, 4]) == 11.0
+    assert orc.dot(np.ones(1000), np.ones(1000)) == 1000.0
+    x, y = np.array([1.0, 1.0]), np.array([1.0, 2.0])
+    assert orc.waxpby(1, x, 0, y).tolist() == x.tolist() and orc.waxpby(0, x, 1, y).tolist() == y.tolist()
+    assert orc.waxpby(2, x, 3, y).tolist() == [5.0, 8.0]
+    with pytest.raises(orc.InvalidArgument):
+        orc.dot([1, 2], [1, 2, 3])
+
+
+def test_cg_examples(orc):
+    m = orc.generate_matrix(1, 1, 1)
+    x, it, conv, hist = orc.cg_solve(orc.to_ell(m), [52.0])
+    assert x.tolist() == [2.0] and it == 1 and conv and hist[0] == 1.0
+    m = orc.generate_matrix(16, 16, 16)
+    b = orc.spmv(orc.to_ell(m), np.ones(m.n))
+    results = [orc.cg_solve(f, b, tolerance=1e-8) for f in (orc.to_ell(m), orc.compress_values(m), orc.compress_patterns(m))]
+    its = [r[1] for r in results]
+    assert len(set(its)) == 1 and all(r[2] for r in results)  # identical iteration counts
+    for x, it, conv, hist in results:
+        assert np.abs(x - 1.0).max() <= 1e-6 and hist[-1] <= 1e-8 and len(hist) == it + 1
+        assert np.abs(x - results[0][0]).max() <= 1e-9
+        assert np.abs(hist - results[0][3]).max() <= 1e-10
+    _, it, conv, _ = orc.cg_solve(orc.to_ell(m), b, max_iterations=1)
+    assert it == 1 and not conv
