@@ -11,12 +11,14 @@ sys.path.insert(0, ".")
 import paper_1612_00530_b200 as sp  # noqa: E402
 from oracle import oracle as orc  # noqa: E402
 
-n1 = int(sys.argv[1]) if len(sys.argv) > 1 else 128
+dims = [int(v) for v in (sys.argv[1] if len(sys.argv) > 1 else "128").split("x")]
+g = tuple(dims * 3) if len(dims) == 1 else tuple(dims)
+n1 = g[0]
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 50
 fmts = sys.argv[3].split(",") if len(sys.argv) > 3 else ["pattern", "generic", "vt", "ell"]
-g = (n1, n1, n1)
-n = n1 ** 3
-nnz = (3 * n1 - 2) ** 3
+n = g[0] * g[1] * g[2]
+nnz = (3 * g[0] - 2) * (3 * g[1] - 2) * (3 * g[2] - 2)
+print("grid", g, "rows", n, flush=True)
 t0 = time.time()
 pc = orc.compress_patterns_grid(*g, values_in_pattern=True)
 print(f"oracle pattern build {time.time()-t0:.1f}s", flush=True)
@@ -51,7 +53,7 @@ def timeit(a, label, bytes_per_row, **opts):
     e.record()
     torch.cuda.synchronize()
     b2b = s.elapsed_time(e) * 1e3 / reps
-    print(f"{label:34s} flushed med {med:9.1f} us  min {ts[0]:9.1f} | b2b {b2b:9.1f} us  "
+    print(f"{label:34s} flushed med {med:9.1f} us  min {ts[0]:9.1f} | b2b {b2b:9.1f} us ({b2b * 1e3 / n:6.3f} ns/krow) "
           f"{2*nnz/b2b/1e3:9.1f} GF/s  {bytes_per_row*n/b2b/1e3:8.1f} GB/s ({bytes_per_row} B/row)", flush=True)
     for k in opts:
         sp.set_option(k, 0 if k != "box_prefetch" else -1)
