@@ -56,6 +56,8 @@ void destroy(spmvb_matrix *a) {
         if (a->s[i]) cudaFree(a->s[i]);
     if (a->scratch_x) cudaFree(a->scratch_x);
     if (a->scratch_y) cudaFree(a->scratch_y);
+    for (auto &st : a->pipe_streams) if (st) cudaStreamDestroy(st);
+    for (auto &ev : a->pipe_events) if (ev) cudaEventDestroy(ev);
     if (a->d_masks) cudaFree(a->d_masks);
     if (a->d_disp_off32) cudaFree(a->d_disp_off32);
     delete a;

@@ -68,6 +68,9 @@ struct spmvb_matrix {
     // persistent scratch of spmvb_spmv_host (x and y on the device)
     mutable double *scratch_x = nullptr, *scratch_y = nullptr;
     mutable int64_t scratch_x_len = 0;
+    // streams / events of the pipelined host-buffer SpMV (created on first use)
+    mutable cudaStream_t pipe_streams[3] = {};
+    mutable cudaEvent_t pipe_events[32] = {};
     spmvb::BoxPlan box;
     uint32_t *d_masks = nullptr;      // device copy of box.masks
     int32_t *d_disp_off32 = nullptr;  // 32-bit copy of disp_offsets for the kernels

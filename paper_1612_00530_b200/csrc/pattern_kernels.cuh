@@ -30,6 +30,7 @@ struct PatternArgs {
     const uint32_t *masks;     // n_patterns (box plan)
     int n_patterns, m, disp_total;
     int row_begin, row_end;
+    int64_t ids_avail;         // rows of the id stream from row_begin to its end (prefetch-reach guard)
     // box plan
     int sy, plane_lines;       // sy = stride of dy; plane_lines = sz / sy
     double v_off, v_center;
@@ -567,7 +568,7 @@ __global__ void __launch_bounds__(WC * 32, MINB) spmv_pattern_box3_kernel(Patter
     const int64_t x_lo = xi_w - sy - sz - 1;
     const int64_t x_hi = xi_w + 64 + (int64_t)(nb_up + LPS * (1 + LA) + pf) * sy + (int64_t)Q * sz + 1;
     const int64_t id_hi = r_w + 64 + (int64_t)(nb_up + LPS + pf) * sy + (int64_t)(nq - 1) * sz;  // ids prefetch reach
-    const bool interior = last_row < n_rows && x_lo >= 0 && x_hi < p.x_len && id_hi <= n_rows + 1024;
+    const bool interior = last_row < n_rows && x_lo >= 0 && x_hi < p.x_len && id_hi <= p.ids_avail + 1024;
     if (interior) {
         box3_march<Q, LPS, OFF_NEG1, CENTER_POS, LA>(p, sm, p.x + xi_w, p.ids + p.row_begin + r_w, p.y + p.row_begin + r_w, xi_w,
                                                  lane, nb, lane * 2 + 1 < cols_ok, nq);

@@ -75,6 +75,7 @@ static int launch_pattern(const spmvb_matrix *a, const double *x, int64_t x_col0
         p.masks = a->d_masks;
         p.n_patterns = a->n_patterns; p.m = a->m; p.disp_total = (int)a->disp_total;
         p.row_begin = row_begin; p.row_end = row_end;
+        p.ids_avail = (int64_t)a->n - row_begin;
         p.sy = a->box.sy; p.plane_lines = a->box.valid ? a->box.sz / a->box.sy : 0;
         p.v_off = a->box.valid ? a->h_table[a->box.k_off] : 0.0;
         p.v_center = a->box.valid ? a->h_table[a->box.k_center] : 0.0;
@@ -169,10 +170,49 @@ int spmvb_spmv_host(const spmvb_matrix *a, const double *x_host, int64_t x_len, 
         SPMVB_TRY(spmvb_vec_alloc(a->n, &a->scratch_y));
         a->scratch_x_len = x_len;
     }
-    SPMVB_CUDA(cudaMemcpyAsync(a->scratch_x, x_host, (size_t)x_len * 8, cudaMemcpyHostToDevice, nullptr));
-    SPMVB_TRY(spmvb_spmv(a, a->scratch_x, 0, x_len, a->scratch_y, 0, a->n, nullptr));
-    SPMVB_CUDA(cudaMemcpyAsync(y_host, a->scratch_y, (size_t)a->n * 8, cudaMemcpyDeviceToHost, nullptr));
-    SPMVB_CUDA(cudaStreamSynchronize(nullptr));
+    const int64_t n = a->n;
+    // Reach of a row into x: known exactly for the pattern format (largest |displacement| of the dictionary,
+    // no exception rows).  Then the call is pipelined over row chunks: while chunk c computes, x for the later
+    // chunks is still arriving and y of the earlier chunks is already leaving (PCIe is full duplex).
+    int64_t reach = -1;
+    if (a->format == SPMVB_FMT_PATTERN && a->n_exc == 0 && n >= (1 << 20)) {
+        reach = 0;
+        for (int32_t d : a->h_disp_flat) reach = std::max<int64_t>(reach, d < 0 ? -(int64_t)d : d);
+    }
+    if (reach < 0 || reach * 8 > n) {  // plain path: copy, run, copy
+        SPMVB_CUDA(cudaMemcpyAsync(a->scratch_x, x_host, (size_t)x_len * 8, cudaMemcpyHostToDevice, nullptr));
+        SPMVB_TRY(spmvb_spmv(a, a->scratch_x, 0, x_len, a->scratch_y, 0, a->n, nullptr));
+        SPMVB_CUDA(cudaMemcpyAsync(y_host, a->scratch_y, (size_t)a->n * 8, cudaMemcpyDeviceToHost, nullptr));
+        SPMVB_CUDA(cudaStreamSynchronize(nullptr));
+        return SPMVB_OK;
+    }
+    constexpr int kChunks = 16;
+    if (!a->pipe_streams[0]) {
+        for (int i = 0; i < 3; i++) SPMVB_CUDA(cudaStreamCreateWithFlags(&a->pipe_streams[i], cudaStreamNonBlocking));
+        for (int i = 0; i < 2 * kChunks; i++) SPMVB_CUDA(cudaEventCreateWithFlags(&a->pipe_events[i], cudaEventDisableTiming));
+    }
+    cudaStream_t s_in = a->pipe_streams[0], s_run = a->pipe_streams[1], s_out = a->pipe_streams[2];
+    // chunk boundaries on whole planes of the box plan when there is one (tiles then stay aligned), multiples of 4 rows otherwise
+    const int64_t unit = a->box.valid ? (int64_t)a->box.sz : 4;
+    const int64_t units = (n + unit - 1) / unit;
+    const int64_t per = std::max<int64_t>(1, (units + kChunks - 1) / kChunks) * unit;
+    int64_t sent = 0;
+    int c = 0;
+    for (int64_t r0 = 0; r0 < n; r0 += per, c++) {
+        const int64_t r1 = std::min(n, r0 + per);
+        const int64_t need = std::min(n, r1 + reach);
+        if (need > sent) {
+            SPMVB_CUDA(cudaMemcpyAsync(a->scratch_x + sent, x_host + sent, (size_t)(need - sent) * 8, cudaMemcpyHostToDevice, s_in));
+            sent = need;
+        }
+        SPMVB_CUDA(cudaEventRecord(a->pipe_events[2 * c], s_in));
+        SPMVB_CUDA(cudaStreamWaitEvent(s_run, a->pipe_events[2 * c], 0));
+        SPMVB_TRY(spmvb_spmv(a, a->scratch_x, 0, x_len, a->scratch_y, (int32_t)r0, (int32_t)r1, s_run));
+        SPMVB_CUDA(cudaEventRecord(a->pipe_events[2 * c + 1], s_run));
+        SPMVB_CUDA(cudaStreamWaitEvent(s_out, a->pipe_events[2 * c + 1], 0));
+        SPMVB_CUDA(cudaMemcpyAsync(y_host + r0, a->scratch_y + r0, (size_t)(r1 - r0) * 8, cudaMemcpyDeviceToHost, s_out));
+    }
+    SPMVB_CUDA(cudaStreamSynchronize(s_out));
     return SPMVB_OK;
 }
 

@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(WC * 32, MINB) spmv_pattern_box6_kernel(Patter
     const int64_t x_lo = xi_w - sy - sz - 1;
     const int64_t x_hi = xi_w + CW + (int64_t)(nb + 1 + pf) * sy + (int64_t)Q * sz + 1;
     const int64_t id_hi = r_w + CW + (int64_t)(nb + 1 + pf) * sy + (int64_t)(nq - 1) * sz;
-    const bool interior = last_row < n_rows && x_lo >= 0 && x_hi < p.x_len && id_hi <= n_rows + 1024;
+    const bool interior = last_row < n_rows && x_lo >= 0 && x_hi < p.x_len && id_hi <= p.ids_avail + 1024;
     if (interior) {
         box6_march<NX, Q, OFF_NEG1, CENTER_POS>(p, sm, p.x + xi_w, p.ids + p.row_begin + r_w, p.y + p.row_begin + r_w, xi_w, lane,
                                                 nb, lane * NX + NX - 1 < cols_ok, nq);
