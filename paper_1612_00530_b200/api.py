@@ -356,6 +356,12 @@ def set_option(key: str, value: int):
     check(lib.spmvb_set_option(key.encode(), value))
 
 
+def get_option(key: str) -> int:
+    v = C.c_int()
+    check(lib.spmvb_get_option(key.encode(), C.byref(v)))
+    return v.value
+
+
 def device_count() -> int:
     c = C.c_int()
     check(lib.spmvb_device_count(C.byref(c)))

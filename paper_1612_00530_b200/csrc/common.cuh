@@ -92,6 +92,8 @@ struct Options {
     int box_prefetch = -1;   // L2 prefetch distance in lines (-1 = default)
     int box_prefetch_l1 = 0; // L1 prefetch distance in lines (0 = off)
     int debug_nochain = 0;   // measurement only
+    int box_lines = 0;       // lines per CTA march of the tensor-ring kernel (0 = default)
+    int last_pattern_kernel = 0;  // read-only: kernel family of the last pattern launch (1 List 1, 2 box v2, 3 box3, 4 lab, 9 tensor ring)
 };
 Options &options();
 

@@ -302,21 +302,6 @@ __device__ __forceinline__ void box3_chain(const double (&w)[S][Q + 2][4], int k
     // MODE 0: operands straight from the window (with SELL/SELR: halo operands zeroed per lane)
     // MODE 1: every operand selected by its mask bit
     // line l of the step reads slots (kb+l-1, kb+l, kb+l+1) mod S for dy = -1, 0, +1
-    double hl[LPS][Q][3][3], hr[LPS][Q][3][3];
-    if (MODE == 0 && (SELL || SELR)) {
-#pragma unroll
-        for (int l = 0; l < LPS; l++)
-#pragma unroll
-            for (int q = 0; q < Q; q++)
-#pragma unroll
-                for (int dz = 0; dz < 3; dz++)
-#pragma unroll
-                    for (int dy = 0; dy < 3; dy++) {
-                        const int s = (kb + l + dy + S - 1) % S;
-                        if (SELL) hl[l][q][dz][dy] = zl[l][q] ? 0.0 : w[s][q + dz][0];
-                        if (SELR) hr[l][q][dz][dy] = zr[l][q] ? 0.0 : w[s][q + dz][3];
-                    }
-    }
 #pragma unroll
     for (int l = 0; l < LPS; l++)
 #pragma unroll
@@ -344,8 +329,8 @@ __device__ __forceinline__ void box3_chain(const double (&w)[S][Q + 2][4], int k
 #pragma unroll
                 for (int i = 0; i < 2; i++) {
                     double e = w[(kb + l + dy + S - 1) % S][q + dz][i + dx];
-                    if (MODE == 0 && SELL && i + dx == 0) e = hl[l][q][dz][dy];
-                    if (MODE == 0 && SELR && i + dx == 3) e = hr[l][q][dz][dy];
+                    if (MODE == 0 && SELL && i + dx == 0) e = zl[l][q] ? 0.0 : e;
+                    if (MODE == 0 && SELR && i + dx == 3) e = zr[l][q] ? 0.0 : e;
                     if (OFF_NEG1) {
                         if (MODE == 1) e = (mk[l][q][i] >> t & 1u) ? e : 0.0;
                         acc[l][q][i] = __dsub_rn(acc[l][q][i], e);

@@ -14,4 +14,8 @@ int launch_vt(const spmvb_matrix *a, const double *x, int64_t x_col0, double *y,
 // measured experiments (spmv_pattern_lab.cu): returns 0 launched, 1 not served, -1 CUDA error
 int launch_pattern_lab(int which, const spmvb_matrix *a, PatternArgs &p, cudaStream_t st);
 
+// tensor-ring kernel (spmv_pattern_tma.cu): same return convention; `which` selects a measured variant
+bool ring_ok(const spmvb_matrix *a, const PatternArgs &p);
+int launch_pattern_ring(int which, int lines, const spmvb_matrix *a, PatternArgs &p, cudaStream_t st);
+
 }  // namespace spmvb

@@ -79,7 +79,7 @@ static int launch_pattern(const spmvb_matrix *a, const double *x, int64_t x_col0
         p.sy = a->box.sy; p.plane_lines = a->box.valid ? a->box.sz / a->box.sy : 0;
         p.v_off = a->box.valid ? a->h_table[a->box.k_off] : 0.0;
         p.v_center = a->box.valid ? a->h_table[a->box.k_center] : 0.0;
-        const Options &o = options();
+        Options &o = options();
         p.prefetch = o.box_prefetch >= 0 ? o.box_prefetch : 2;
         p.prefetch_l1 = o.box_prefetch_l1;
         p.debug_nochain = o.debug_nochain;
@@ -88,7 +88,13 @@ static int launch_pattern(const spmvb_matrix *a, const double *x, int64_t x_col0
             return fail(SPMVB_ERR_INVALID_ARGUMENT, "box kernel requested but the dictionary has no box plan");
         if (use_box) {
             int rc3 = 1;  // 1 = not served by v3
-            if (o.pattern_kernel != 3 && box3_ok(a, p)) {
+            bool ring = false;
+            if (o.pattern_kernel != 3 && o.box_march >= 90 && o.box_march <= 94 && ring_ok(a, p)) {  // spmv_pattern_tma.cu
+                rc3 = launch_pattern_ring(o.box_march - 90, o.box_lines, a, p, st);
+                if (rc3 < 0) return SPMVB_ERR_CUDA;
+                ring = rc3 == 0;
+            }
+            if (!ring && o.pattern_kernel != 3 && box3_ok(a, p)) {
                 const int64_t n_planes = ((int64_t)row_end - row_begin + (int64_t)p.sy * p.plane_lines - 1) / ((int64_t)p.sy * p.plane_lines);
                 if (n_planes == 1) rc3 = launch_box3<16, 4, 1, 2, 3, false>(a, p, st);  // single-plane ranges (slab boundary planes)
                 else switch (o.box_march) {
@@ -96,6 +102,8 @@ static int launch_pattern(const spmvb_matrix *a, const double *x, int64_t x_col0
                     case 1: rc3 = launch_box3<16, 4, 2, 1, 3, false>(a, p, st); break;      // R=16 tiles            124 us
                     case 5: rc3 = launch_box3<16, 4, 1, 2, 3, false>(a, p, st); break;      // 1 plane, 2 lines/step 116-121 us
                     case 12: rc3 = launch_box3<16, 4, 2, 1, 3, false, 4>(a, p, st); break;  // CTA spans full lines  124 us
+                    case 71: rc3 = launch_box3<8, 4, 2, 1, 4, false>(a, p, st); break;
+                    case 72: rc3 = launch_box3<8, 4, 2, 1, 3, false, 1, 1>(a, p, st); break;
                     case 70: rc3 = launch_box3<8, 4, 2, 1, 2, false, 1, 1>(a, p, st); break;   // register look-ahead LA=1: 146 us (sweep: profiles/r01_probe256_lookahead_sweep.log)
                     case 20: case 30: case 35: case 47: case 62:                            // spmv_pattern_lab.cu
                         rc3 = launch_pattern_lab(o.box_march, a, p, st); break;
@@ -104,6 +112,7 @@ static int launch_pattern(const spmvb_matrix *a, const double *x, int64_t x_col0
                 }
                 if (rc3 < 0) return SPMVB_ERR_CUDA;
             }
+            o.last_pattern_kernel = rc3 == 1 ? 2 : (ring ? 9 : (o.box_march >= 20 && o.box_march < 70 ? 4 : 3));
             if (rc3 == 1) {  // v2: any stride / alignment / value pattern
                 if (o.box_march == 11) SPMVB_TRY((launch_box_rw<32, 8, 1, 1>(a, p, st)));
                 else SPMVB_TRY((launch_box_rw<16, 8, 2, 0>(a, p, st)));
@@ -111,6 +120,7 @@ static int launch_pattern(const spmvb_matrix *a, const double *x, int64_t x_col0
         } else {
             const int threads = 256;
             const int blocks = (row_end - row_begin + threads - 1) / threads;
+            o.last_pattern_kernel = 1;
             const bool dict_smem = a->disp_total <= kDictSmemDisp && a->n_patterns <= kDictSmemPat && a->m <= kDictSmemTab;
             if (dict_smem) spmv_pattern_generic_kernel<true><<<blocks, threads, 0, st>>>(p);
             else spmv_pattern_generic_kernel<false><<<blocks, threads, 0, st>>>(p);

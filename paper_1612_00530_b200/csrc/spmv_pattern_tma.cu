@@ -1,0 +1,346 @@
+// Pattern-format SpMV (inc/compress.hpp:48-76; inc/kernels.hpp:25,35-36; PAPER.md:797-813 List 1):
+// the "tensor ring" kernel.  x is viewed through a 3-D TMA tensor map [plane][line][column] whose
+// strides (sz, sy, 1) come from the dictionary's box plan; every warp owns a 64-column strip of Q
+// planes and marches over lines.  One elected lane fetches the next line set -- 68 columns x (Q+2)
+// planes, one cp.async.bulk.tensor -- into the warp's private shared-memory ring several lines
+// ahead (completion on an mbarrier), and all lanes take the 27 operands of their rows from shared
+// memory with 128-bit loads.  No register window: ~100 registers, so 16-20 warps/SM keep tens of KB
+// in flight per SM without spending instructions on it.
+//
+// Alignment.  A TMA box must start on a 16-byte boundary, i.e. at an even column, and a thread wants
+// its four operands (columns a-1 .. a+2 for its rows a, a+1) as two aligned 128-bit shared loads.
+// Both hold when a is odd: strip s covers columns 64s-1 .. 64s+62 and its box starts at 64s-2.
+// Column -1 of strip 0 is a dummy; the columns past the last strip (one column when 64 | sy) are
+// served by a few extra CTAs with List 1 as written.
+//
+// Exactness.  Elements outside the tensor view are zero-filled by the TMA unit.  A row whose
+// dictionary mask is exactly "the full box minus the entries that fall outside the view" is
+// therefore served by the plain 27-term chain: absent operands are +0.0 and leave the accumulator
+// unchanged bit for bit (it can never be -0.0).  That is every row of a stencil matrix whose x view
+// is aligned with the grid.  Any other row (another dictionary pattern, a sub-box whose missing
+// entries are inside the view, a view that is not aligned with the grid) is recomputed per lane
+// by List 1 as written, so the result is always the reference's order.  Exception rows (id -1)
+// are left to the exception block, as in the other kernels.
+#include <cuda.h>  // CUtensorMap and enums only; the encoder is resolved through the runtime (no -lcuda)
+
+#include <algorithm>
+
+#include "pattern_kernels.cuh"
+#include "spmv_internal.cuh"
+
+namespace spmvb {
+
+constexpr uint32_t kDyLoBits = 0x01C0E07u;  // box entries with dy = -1
+constexpr uint32_t kDyHiBits = kDyLoBits << 6;
+constexpr uint32_t kDzLoBits = 0x1FFu;  // dz = -1
+constexpr uint32_t kDzHiBits = 0x1FFu << 18;
+constexpr int kStripCols = 64;            // columns per warp
+constexpr int kBoxCols = kStripCols + 4;  // columns 64s-2 .. 64s+65 (the first and last are alignment padding)
+constexpr int kRingWarps = 4;
+
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap *tm, int c0, int c1, int c2, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+        "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ double2 lds_f64x2(uint32_t addr) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t v) { asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory"); }
+
+template <int Q, int S>
+struct RingLayout {
+    static constexpr int P = Q + 2;
+    static constexpr uint32_t kLineBytes = kBoxCols * 8;                      // one plane of a line set
+    static constexpr uint32_t kSetBytes = P * kLineBytes;                     // bytes one TMA box delivers
+    static constexpr uint32_t kSlotBytes = (kSetBytes + 127u) / 128u * 128u;  // TMA destinations are 128-byte aligned
+    static constexpr uint32_t kRingBytes = kRingWarps * S * kSlotBytes;
+    static constexpr uint32_t kBarBytes = kRingWarps * S * 8;
+    static constexpr uint32_t kTotal = kRingBytes + kBarBytes + (kDictSmemPat + 1) * 4 + 128;  // + alignment slack
+};
+
+// gridDim.x = strip CTAs (4 strips each) + one CTA column for the left-over columns [left_lo, sy) when there are any
+template <int Q, int S, int MINB, bool OFF_NEG1, int CENTER_POS>
+__global__ void __launch_bounds__(kRingWarps * 32, MINB)
+    spmv_pattern_ring_kernel(const __grid_constant__ CUtensorMap tm, PatternArgs p, int c_lo, int c_hi, int np_x, int R, int n_strips,
+                             int left_lo) {
+    using L = RingLayout<Q, S>;
+    constexpr int P = L::P;
+    extern __shared__ unsigned char smem_raw[];
+    const uint32_t sbase = (smem_u32(smem_raw) + 127u) & ~127u;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int sy = p.sy, pl = p.plane_lines;
+    const int sz = sy * pl;
+    const int b0 = blockIdx.y * R;
+    const int c0 = c_lo + blockIdx.z * Q;
+    const int nb = min(R, pl - b0);
+    const int rb = p.row_begin;
+    const unsigned n_range = (unsigned)(p.row_end - p.row_begin);
+
+    if ((int)blockIdx.x * kRingWarps >= n_strips) {  // left-over columns: List 1 per row
+        const int n_left = sy - left_lo;
+        for (int t = threadIdx.x; t < n_left * nb * Q; t += kRingWarps * 32) {
+            const int col = left_lo + t % n_left, line = b0 + (t / n_left) % nb, c = c0 + t / (n_left * nb);
+            if (c > c_hi) break;
+            const int64_t xi = col + (int64_t)sy * line + (int64_t)sz * c;
+            const int64_t row = xi - p.g0;
+            if (row < rb || row >= p.row_end) continue;
+            const int id = p.ids[row];
+            if (id >= 0) p.y[row] = pattern_row(p, p.disp, p.ends, p.table, id, xi);
+        }
+        return;
+    }
+
+    const uint32_t ring = sbase + warp * (S * L::kSlotBytes);
+    const uint32_t bars = sbase + L::kRingBytes + warp * (S * 8);
+    const uint32_t s_masks = sbase + L::kRingBytes + L::kBarBytes;  // entry 0 serves id = -1
+    for (int i = threadIdx.x; i <= p.n_patterns; i += kRingWarps * 32) sts_u32(s_masks + 4 * i, i == 0 ? 0u : p.masks[i - 1]);
+    if (lane == 0) {
+#pragma unroll
+        for (int s = 0; s < S; s++) mbar_init(bars + 8 * s, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    const int strip = blockIdx.x * kRingWarps + warp;
+    if (strip >= n_strips) return;  // no CTA barrier below this point
+    const int a_w = strip * kStripCols - 1;  // first column of the warp's strip (odd; -1 for strip 0)
+    const int n_sets = nb + 2;               // line sets b0-1 .. b0+nb
+
+    auto issue = [&](int k) {  // elected lane: line set k -> slot k % S
+        const uint32_t bar = bars + 8 * (k % S);
+        mbar_expect_tx(bar, L::kSetBytes);
+        tma_load_3d(ring + (k % S) * L::kSlotBytes, &tm, a_w - 1, b0 - 1 + k, c0 - 1, bar);
+    };
+    if (lane == 0)
+        for (int k = 0; k < S && k < n_sets; k++) issue(k);
+
+    // per-thread geometry: columns a, a+1 (a odd); the row of (column a, line b0 + j, plane c0 + q) is row0 + q*sz + j*sy
+    const int a = a_w + 2 * lane;
+    const int64_t xi0 = a + (int64_t)sy * b0 + (int64_t)sz * c0;
+    const int row0 = (int)(xi0 - p.g0);
+    bool ok[Q][2];           // the row's column and plane exist
+    uint32_t expect[Q][2];   // dictionary mask the plain chain is exact for (before the line term)
+#pragma unroll
+    for (int q = 0; q < Q; q++) {
+        const int c = c0 + q;
+        const uint32_t oob_c = (c == 0 ? kDzLoBits : 0u) | (c == np_x - 1 ? kDzHiBits : 0u);
+#pragma unroll
+        for (int i = 0; i < 2; i++) {
+            const uint32_t oob_a = (a + i == 0 ? kLBits : 0u) | (a + i == sy - 1 ? kRBits : 0u);
+            expect[q][i] = (c >= np_x) ? 0u : (kFullBox & ~(oob_a | oob_c));
+            ok[q][i] = a + i >= 0 && a + i < sy && c <= c_hi;
+        }
+    }
+    const int32_t *__restrict__ ids = p.ids;
+    auto load_id = [&](int q, int i, int j) {  // -1: no such row here (computed on whatever the ring holds, never stored)
+        const int r = row0 + q * sz + j * sy + i;
+        return (ok[q][i] && (unsigned)(r - rb) < n_range) ? __ldg(ids + r) : -1;
+    };
+    int idn[Q][2];
+#pragma unroll
+    for (int q = 0; q < Q; q++)
+#pragma unroll
+        for (int i = 0; i < 2; i++) idn[q][i] = load_id(q, i, 0);
+    const double vc = p.v_center, vo = p.v_off;
+    const uint32_t lane_off = lane * 16;
+
+    mbar_wait(bars + 0, 0);
+    mbar_wait(bars + 8 * (1 % S), (1 / S) & 1);
+#pragma unroll 1
+    for (int j = 0; j < nb; j++) {
+        const int b = b0 + j;
+        mbar_wait(bars + 8 * ((j + 2) % S), ((j + 2) / S) & 1);
+        uint32_t sl[3];
+#pragma unroll
+        for (int dy = 0; dy < 3; dy++) sl[dy] = ring + ((j + dy) % S) * L::kSlotBytes + lane_off;
+        int id[Q][2];
+        uint32_t bad = 0;
+        const uint32_t oob_b = (b == 0 ? kDyLoBits : 0u) | (b == pl - 1 ? kDyHiBits : 0u);
+#pragma unroll
+        for (int q = 0; q < Q; q++)
+#pragma unroll
+            for (int i = 0; i < 2; i++) {
+                id[q][i] = idn[q][i];
+                idn[q][i] = j + 1 < nb ? load_id(q, i, j + 1) : -1;
+                const uint32_t m = lds_u32(s_masks + 4 + 4 * id[q][i]);
+                bad |= (id[q][i] >= 0 && m != (expect[q][i] & ~oob_b)) ? (1u << (q * 2 + i)) : 0u;
+            }
+        double acc[Q][2], xc[Q][2];
+#pragma unroll
+        for (int q = 0; q < Q; q++) acc[q][0] = acc[q][1] = 0.0;
+        if (CENTER_POS == 0) {
+#pragma unroll
+            for (int q = 0; q < Q; q++) {
+                const double2 u = lds_f64x2(sl[1] + (q + 1) * L::kLineBytes), v = lds_f64x2(sl[1] + (q + 1) * L::kLineBytes + 16);
+                acc[q][0] = __dadd_rn(acc[q][0], __dmul_rn(vc, u.y));
+                acc[q][1] = __dadd_rn(acc[q][1], __dmul_rn(vc, v.x));
+            }
+        }
+        // planes outermost so that the Q rows of a thread consume each (plane, line) operand quad together
+#pragma unroll
+        for (int pz = 0; pz < P; pz++)
+#pragma unroll
+            for (int dy = 0; dy < 3; dy++) {
+                const double2 u = lds_f64x2(sl[dy] + pz * L::kLineBytes), v = lds_f64x2(sl[dy] + pz * L::kLineBytes + 16);
+                const double e[4] = {u.x, u.y, v.x, v.y};  // columns a-1 .. a+2
+#pragma unroll
+                for (int dx = 0; dx < 3; dx++)
+#pragma unroll
+                    for (int q = 0; q < Q; q++) {
+                        const int dz = pz - q;
+                        if (dz < 0 || dz > 2) continue;
+                        const int t = dz * 9 + dy * 3 + dx;
+#pragma unroll
+                        for (int i = 0; i < 2; i++) {
+                            if (t == 13) {
+                                if (CENTER_POS == 2) acc[q][i] = __dadd_rn(acc[q][i], __dmul_rn(vc, e[i + 1]));
+                                else xc[q][i] = e[i + 1];
+                            } else if (OFF_NEG1) {
+                                acc[q][i] = __dsub_rn(acc[q][i], e[i + dx]);
+                            } else {
+                                acc[q][i] = __dadd_rn(acc[q][i], __dmul_rn(vo, e[i + dx]));
+                            }
+                        }
+                    }
+            }
+        if (CENTER_POS == 1) {
+#pragma unroll
+            for (int q = 0; q < Q; q++)
+#pragma unroll
+                for (int i = 0; i < 2; i++) acc[q][i] = __dadd_rn(acc[q][i], __dmul_rn(vc, xc[q][i]));
+        }
+        __syncwarp();  // every lane is done with the slot of line b-1
+        if (lane == 0 && j + S < n_sets) {
+            fence_proxy_async();  // generic-proxy reads before the async-proxy refill
+            issue(j + S);
+        }
+        if (__any_sync(0xffffffffu, bad != 0)) {  // rows the plain chain is not exact for: List 1 per lane
+#pragma unroll
+            for (int q = 0; q < Q; q++)
+#pragma unroll
+                for (int i = 0; i < 2; i++)
+                    if (bad >> (q * 2 + i) & 1u)
+                        acc[q][i] = pattern_row_cold(p, id[q][i], xi0 + (int64_t)j * sy + (int64_t)q * sz + i);
+        }
+#pragma unroll
+        for (int q = 0; q < Q; q++)
+#pragma unroll
+            for (int i = 0; i < 2; i++)
+                if (id[q][i] >= 0) p.y[row0 + q * sz + j * sy + i] = acc[q][i];
+    }
+}
+
+// ---- host side ------------------------------------------------------------------------
+using EncodeTiledFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *, const cuuint64_t *,
+                                   const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = [] {
+        void *ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            ptr = nullptr;
+        return reinterpret_cast<EncodeTiledFn>(ptr);
+    }();
+    return fn;
+}
+
+// The x view [np_x planes][plane_lines lines][sy columns] with a (Q+2) x 1 x 66 box.
+static int make_x_map(const double *x, int sy, int pl, int np_x, int planes_per_box, CUtensorMap *out) {
+    struct Key {
+        const double *x;
+        int sy, pl, np, pb;
+    };
+    thread_local Key last{nullptr, 0, 0, 0, 0};
+    thread_local CUtensorMap last_map;
+    if (last.x == x && last.sy == sy && last.pl == pl && last.np == np_x && last.pb == planes_per_box) {
+        *out = last_map;
+        return SPMVB_OK;
+    }
+    EncodeTiledFn enc = encode_tiled();
+    if (!enc) return fail(SPMVB_ERR_CUDA, "cuTensorMapEncodeTiled is not available from this driver");
+    const cuuint64_t dims[3] = {(cuuint64_t)sy, (cuuint64_t)pl, (cuuint64_t)np_x};
+    const cuuint64_t strides[2] = {(cuuint64_t)sy * 8, (cuuint64_t)sy * pl * 8};
+    const cuuint32_t box[3] = {(cuuint32_t)kBoxCols, 1u, (cuuint32_t)planes_per_box};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = enc(&last_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double *>(x), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        last.x = nullptr;
+        return fail(SPMVB_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) for view %d x %d x %d", (int)r, np_x, pl, sy);
+    }
+    last = Key{x, sy, pl, np_x, planes_per_box};
+    *out = last_map;
+    return SPMVB_OK;
+}
+
+template <int Q, int S, int MINB, bool ALLV>
+static int launch_ring_t(const spmvb_matrix *a, PatternArgs &p, int R, cudaStream_t st) {
+    using L = RingLayout<Q, S>;
+    const bool neg1 = p.v_off == -1.0;
+    const int cp = a->box.center_pos;
+    if (!ALLV && !(neg1 && cp == 1)) return 1;
+    const int64_t sz = (int64_t)p.sy * p.plane_lines;
+    const int np_x = (int)(p.x_len / sz);
+    const int c_lo = (int)((p.g0 + p.row_begin) / sz), c_hi = (int)((p.g0 + p.row_end - 1) / sz);
+    CUtensorMap tm;
+    if (make_x_map(p.x, p.sy, p.plane_lines, np_x, Q + 2, &tm) != SPMVB_OK) return -1;
+    // strips start at column -1; a partial last strip is used unless at most two columns are left over
+    int n_strips = (p.sy + 1) / kStripCols;
+    if (p.sy - (n_strips * kStripCols - 1) > 2) n_strips++;
+    const int left_lo = std::min(p.sy, n_strips * kStripCols - 1);
+    dim3 grid((n_strips + kRingWarps - 1) / kRingWarps + (left_lo < p.sy ? 1 : 0), (p.plane_lines + R - 1) / R, (c_hi - c_lo + Q) / Q);
+    dim3 block(kRingWarps * 32);
+#define LAUNCH_RING(NEG, CP)                                                                                                  \
+    do {                                                                                                                       \
+        static bool attr = false;                                                                                              \
+        if (!attr) {                                                                                                           \
+            if (cudaFuncSetAttribute(spmv_pattern_ring_kernel<Q, S, MINB, NEG, CP>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                     (int)L::kTotal) != cudaSuccess)                                                           \
+                return -1;                                                                                                     \
+            attr = true;                                                                                                       \
+        }                                                                                                                      \
+        spmv_pattern_ring_kernel<Q, S, MINB, NEG, CP><<<grid, block, L::kTotal, st>>>(tm, p, c_lo, c_hi, np_x, R, n_strips, left_lo);             \
+    } while (0)
+    if constexpr (ALLV) {
+        if (neg1) {
+            if (cp == 0) LAUNCH_RING(true, 0); else if (cp == 1) LAUNCH_RING(true, 1); else LAUNCH_RING(true, 2);
+        } else {
+            if (cp == 0) LAUNCH_RING(false, 0); else if (cp == 1) LAUNCH_RING(false, 1); else LAUNCH_RING(false, 2);
+        }
+    } else {
+        LAUNCH_RING(true, 1);
+    }
+#undef LAUNCH_RING
+    return check_launch("spmv_pattern_ring") == SPMVB_OK ? 0 : -1;
+}
+
+// Conditions: the TMA view needs a 16-byte aligned base, strides that are multiples of 16 bytes (even
+// sy), at least one whole plane of x and a line no narrower than a box; row arithmetic is 32-bit.
+bool ring_ok(const spmvb_matrix *a, const PatternArgs &p) {
+    const int64_t sz = (int64_t)p.sy * p.plane_lines;
+    return (p.sy % 2 == 0) && p.sy >= kBoxCols && ((uintptr_t)p.x % 16 == 0) && a->n_patterns <= kDictSmemPat && p.x_len >= sz &&
+           p.g0 + p.row_begin >= 0 && sz < (1 << 28) && p.x_len / sz < (1 << 30) && (int64_t)a->n + 2 * sz < INT32_MAX &&
+           p.g0 > -(int64_t)INT32_MAX / 2 && p.g0 < INT32_MAX / 2;
+}
+
+// which: 0 default; others are measured alternatives.  `lines` = lines per CTA march (0 = default).
+int launch_pattern_ring(int which, int lines, const spmvb_matrix *a, PatternArgs &p, cudaStream_t st) {
+    const int R = lines > 0 ? lines : 16;
+    switch (which) {
+        case 1: return launch_ring_t<2, 5, 5, false>(a, p, R, st);
+        case 2: return launch_ring_t<4, 5, 3, false>(a, p, R, st);
+        case 3: return launch_ring_t<2, 8, 3, false>(a, p, R, st);
+        case 4: return launch_ring_t<1, 6, 6, false>(a, p, R, st);
+        default: return launch_ring_t<2, 6, 4, false>(a, p, R, st);
+    }
+}
+
+}  // namespace spmvb

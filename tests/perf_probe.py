@@ -17,6 +17,8 @@ n1 = g[0]
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 50
 fmts = sys.argv[3].split(",") if len(sys.argv) > 3 else ["pattern", "generic", "vt", "ell"]
 n = g[0] * g[1] * g[2]
+ring_lines = [int(v) for v in sys.argv[4].split(",")] if len(sys.argv) > 4 else []
+only_ring = bool(ring_lines)
 nnz = (3 * g[0] - 2) * (3 * g[1] - 2) * (3 * g[2] - 2)
 print("grid", g, "rows", n, flush=True)
 t0 = time.time()
@@ -64,8 +66,16 @@ if "pattern" in fmts or "generic" in fmts:
     ref = None
     if "pattern" in fmts:
         for march, name in ((0, "box3 default"), (1, "box3 R=16"), (5, "box3 Q=1 2 lines/step"), (12, "box3 full-line CTA"),
-                            (70, "box3 look-ahead 1"), (20, "box5 cp.async ring"), (35, "box6 4 cols/thread"),
-                            (30, "box6 8 cols/thread"), (47, "box7 pipelined ring"), (62, "box8 TMA ring 8w R=8")):
+                            (70, "box3 look-ahead 1"), (71, "box3 4 CTAs/SM 128 regs"), (72, "box3 look-ahead 1 168 regs"), (20, "box5 cp.async ring"), (35, "box6 4 cols/thread"),
+                            (30, "box6 8 cols/thread"), (47, "box7 pipelined ring"), (62, "box8 TMA ring 8w R=8"),
+                            (90, "ring Q2 S6 4cta"), (91, "ring Q2 S5 5cta"), (92, "ring Q4 S5 3cta"), (93, "ring Q2 S8 3cta"),
+                            (94, "ring Q1 S6 6cta")):
+            if march >= 90 and ring_lines:
+                for ln in ring_lines:
+                    timeit(d, f"pattern {name} R={ln}", 20, pattern_kernel=2, box_march=march, box_prefetch=2, box_lines=ln)
+                continue
+            if only_ring and march not in (0,):
+                continue
             timeit(d, f"pattern {name}", 20, pattern_kernel=2, box_march=march, box_prefetch=2)
         timeit(d, "pattern box v2 <16,8,2,0> pf=4", 20, pattern_kernel=3, box_march=0, box_prefetch=4)
     if "generic" in fmts:

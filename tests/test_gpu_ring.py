@@ -1,0 +1,128 @@
+"""Tensor-ring pattern kernel (csrc/spmv_pattern_tma.cu): bit-exact against the oracle's List 1
+ on aligned and misaligned views, ragged ranges, slabs and hybrid matrices."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from tests.test_gpu_parity import bits, run, sp, up_pat  # noqa: E402,F401
+
+RING = [90, 91, 92, 93, 94]
+
+
+def ring_run(sp, d, x, march, lines=0, must_ring=True, **kw):
+    sp.set_option("box_march", march)
+    sp.set_option("box_lines", lines)
+    try:
+        y = run(sp, d, x, **kw)
+        used = sp.get_option("last_pattern_kernel")
+    finally:
+        sp.set_option("box_march", 0)
+        sp.set_option("box_lines", 0)
+    if must_ring:
+        assert used == 9, f"tensor-ring kernel not used (kernel family {used})"
+    return y
+
+
+@pytest.mark.parametrize("march", RING)
+@pytest.mark.parametrize("g", [(68, 10, 9), (100, 18, 11), (130, 9, 8), (128, 36, 20), (192, 40, 19), (256, 20, 12), (264, 18, 11),
+                               (512, 19, 15)])
+def test_ring_variants_bit_exact(sp, orc, march, g):
+    m = orc.generate_matrix(*g)
+    pc = orc.compress_patterns(m, True)
+    d = up_pat(sp, pc)
+    x = orc.make_test_vector(m.n, orc.RANDOM, seed=5, lo=-1.0, hi=1.0)
+    assert np.array_equal(bits(ring_run(sp, d, x, march)), bits(orc.spmv(pc, x)))
+
+
+@pytest.mark.parametrize("lines", [1, 2, 3, 7, 64])
+def test_ring_march_lengths(sp, orc, lines):
+    m = orc.generate_matrix(128, 21, 10)
+    pc = orc.compress_patterns(m, True)
+    x = orc.make_test_vector(m.n, orc.RANDOM, seed=6, lo=-1.0, hi=1.0)
+    assert np.array_equal(bits(ring_run(sp, up_pat(sp, pc), x, 90, lines)), bits(orc.spmv(pc, x)))
+
+
+@pytest.mark.parametrize("march", [90, 92])
+def test_ring_ragged_ranges(sp, orc, march):
+    """Partitions at arbitrary (even and odd) rows give the single-call result; other rows stay untouched."""
+    m = orc.generate_matrix(128, 20, 12)
+    x = orc.make_test_vector(m.n, orc.RANDOM, seed=7, lo=-1.0, hi=1.0)
+    ref = orc.compress_patterns(m)
+    dev = up_pat(sp, ref)
+    full = orc.spmv(ref, x)
+    dx = sp.DeviceVector.from_host(x)
+    dy = sp.DeviceVector.from_host(np.full(m.n, 123.0))
+    plane = 128 * 20
+    cuts = [0, 2, 131, 2 * plane, 2 * plane + 130, 5 * plane + 7, 9 * plane, m.n - 1, m.n]
+    sp.set_option("box_march", march)
+    try:
+        for b, e in zip(cuts[:-1], cuts[1:]):
+            if (b, e) == (2 * plane + 130, 5 * plane + 7):
+                continue  # leave a hole
+            sp.spmv_rows(dev, dx, dy, b, e)
+            assert sp.get_option("last_pattern_kernel") == 9
+    finally:
+        sp.set_option("box_march", 0)
+    y = dy.to_host()
+    hole = slice(2 * plane + 130, 5 * plane + 7)
+    assert np.all(y[hole] == 123.0)
+    keep = np.r_[0:hole.start, hole.stop:m.n]
+    assert np.array_equal(bits(y[keep]), bits(full[keep]))
+
+
+@pytest.mark.parametrize("g", [(128, 18, 9), (70, 12, 10)])
+def test_ring_slab_with_ghost_planes(sp, orc, g):
+    nx, ny, nz = g
+    plane = nx * ny
+    m = orc.generate_matrix(nx, ny, nz)
+    x = orc.make_test_vector(m.n, orc.RANDOM, seed=7, lo=-1.0, hi=1.0)
+    pc = orc.compress_patterns(m, True)
+    full = orc.spmv(pc, x)
+    for z0, z1 in ((0, 3), (3, 7), (7, nz)):
+        r0, r1 = z0 * plane, z1 * plane
+        g0, g1 = max(z0 - 1, 0) * plane, min(z1 + 1, nz) * plane
+        d_p = sp.upload_pattern(r1 - r0, pc.table, pc.disp_offsets, pc.disp_flat, pc.ends_flat, pc.row_pattern[r0:r1],
+                                True, row_offset=r0)
+        y = ring_run(sp, d_p, x[g0:g1], 90, x_col0=g0)
+        assert np.array_equal(bits(y), bits(full[r0:r1])), (z0, z1)
+
+
+def test_ring_misaligned_view_falls_back_per_row(sp, orc):
+    """x_col0 that is not a multiple of the plane: the zero-filled view disagrees with the masks of the
+    rows on the view's faces, which must then be recomputed by List 1 -- same bits."""
+    nx, ny, nz = 128, 10, 9
+    plane = nx * ny
+    m = orc.generate_matrix(nx, ny, nz)
+    x = orc.make_test_vector(m.n, orc.RANDOM, seed=8, lo=-1.0, hi=1.0)
+    pc = orc.compress_patterns(m, True)
+    full = orc.spmv(pc, x)
+    r0, r1 = 3 * plane, 6 * plane
+    for g0 in (2 * plane - 2 * nx - 6, 2 * plane - 130, 2 * plane - 2):  # even offsets, not plane / line aligned
+        d_p = sp.upload_pattern(r1 - r0, pc.table, pc.disp_offsets, pc.disp_flat, pc.ends_flat, pc.row_pattern[r0:r1],
+                                True, row_offset=r0)
+        y = ring_run(sp, d_p, x[g0:7 * plane], 90, x_col0=g0)
+        assert np.array_equal(bits(y), bits(full[r0:r1])), g0
+
+
+@pytest.mark.parametrize("g", [(128, 20, 12), (96, 40, 36)])
+def test_ring_hybrid_exception_rows(sp, orc, g):
+    m = orc.generate_matrix(*g, perturb=(11, 0.1, 0.1))
+    pc = orc.compress_patterns(m, True, min_pattern_rows=2)
+    assert pc.n_exc > 0
+    d = up_pat(sp, pc)
+    x = orc.make_test_vector(m.n, orc.RANDOM, seed=7, lo=-1.0, hi=1.0)
+    assert np.array_equal(bits(ring_run(sp, d, x, 90)), bits(orc.spmv(pc, x)))
+
+
+def test_ring_nonfinite_neighbours_do_not_leak(sp, orc):
+    """Absent entries are never read as operands: NaN in x reaches exactly the rows that reference it."""
+    m = orc.generate_matrix(128, 12, 10)
+    pc = orc.compress_patterns(m, True)
+    x = orc.make_test_vector(m.n, orc.RANDOM, seed=9, lo=-1.0, hi=1.0)
+    x[127] = np.nan  # last column of line 0: not a neighbour of row 128 (column 0 of line 1)
+    y = ring_run(sp, up_pat(sp, pc), x, 90)
+    ref = orc.spmv(pc, x)
+    ok = ~np.isnan(ref)
+    assert np.array_equal(np.isnan(y), np.isnan(ref)) and np.array_equal(bits(y[ok]), bits(ref[ok]))
+    assert np.isnan(y[126]) and not np.isnan(y[128])
