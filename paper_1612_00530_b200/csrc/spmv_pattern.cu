@@ -89,8 +89,11 @@ static int launch_pattern(const spmvb_matrix *a, const double *x, int64_t x_col0
         if (use_box) {
             int rc3 = 1;  // 1 = not served by v3
             bool ring = false;
-            if (o.pattern_kernel != 3 && o.box_march >= 90 && o.box_march <= 94 && ring_ok(a, p)) {  // spmv_pattern_tma.cu
-                rc3 = launch_pattern_ring(o.box_march - 90, o.box_lines, a, p, st);
+            // tensor-ring kernel (spmv_pattern_tma.cu): default for ranges of at least 8 planes; 90..94 force a variant
+            const int64_t planes = ((int64_t)row_end - row_begin) / ((int64_t)p.sy * p.plane_lines);
+            const bool want_ring = (o.box_march == 0 && planes >= 8) || (o.box_march >= 90 && o.box_march <= 94);
+            if (o.pattern_kernel != 3 && want_ring && ring_ok(a, p)) {
+                rc3 = launch_pattern_ring(o.box_march >= 90 ? o.box_march - 90 : 0, o.box_lines, a, p, st);
                 if (rc3 < 0) return SPMVB_ERR_CUDA;
                 ring = rc3 == 0;
             }
@@ -107,7 +110,8 @@ static int launch_pattern(const spmvb_matrix *a, const double *x, int64_t x_col0
                     case 70: rc3 = launch_box3<8, 4, 2, 1, 2, false, 1, 1>(a, p, st); break;   // register look-ahead LA=1: 146 us (sweep: profiles/r01_probe256_lookahead_sweep.log)
                     case 20: case 30: case 35: case 47: case 62:                            // spmv_pattern_lab.cu
                         rc3 = launch_pattern_lab(o.box_march, a, p, st); break;
-                    // default <R=8 lines, 4 warps, Q=2 planes/thread, 1 line/step, 3 CTAs/SM>: 118 us
+                    case 3: rc3 = launch_box3<8, 4, 2, 1, 3, true>(a, p, st); break;           // box3 default, forced
+                    // <R=8 lines, 4 warps, Q=2 planes/thread, 1 line/step, 3 CTAs/SM>: 118-123 us
                     default: rc3 = launch_box3<8, 4, 2, 1, 3, true>(a, p, st); break;
                 }
                 if (rc3 < 0) return SPMVB_ERR_CUDA;

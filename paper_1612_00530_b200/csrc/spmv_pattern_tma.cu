@@ -24,6 +24,7 @@
 #include <cuda.h>  // CUtensorMap and enums only; the encoder is resolved through the runtime (no -lcuda)
 
 #include <algorithm>
+#include <type_traits>
 
 #include "pattern_kernels.cuh"
 #include "spmv_internal.cuh"
@@ -62,8 +63,57 @@ struct RingLayout {
     static constexpr uint32_t kTotal = kRingBytes + kBarBytes + (kDictSmemPat + 1) * 4 + 128;  // + alignment slack
 };
 
+// Rare path of the direct variant, kept out of line so that its registers do not weigh on the main loop: the sums
+// of one step again, every operand selected by its row's own 27-bit mask (absent entries contribute +0.0), operands
+// re-read from the three line slots of the ring; the rows stay interleaved as in the main chain.
+template <int Q, bool OFF_NEG1, int CENTER_POS, uint32_t LINE_BYTES>
+__device__ __noinline__ void ring_masked_step(uint32_t sl0, uint32_t sl1, uint32_t sl2, const uint32_t *mk, double vc, double vo,
+                                              double *out) {
+    constexpr int P = Q + 2;
+    const uint32_t sl[3] = {sl0, sl1, sl2};
+    double acc[Q][2], xc[Q][2];
+#pragma unroll
+    for (int q = 0; q < Q; q++) {
+        const double2 u = lds_f64x2(sl[1] + (q + 1) * LINE_BYTES), v = lds_f64x2(sl[1] + (q + 1) * LINE_BYTES + 16);
+        xc[q][0] = (mk[q * 2] >> 13 & 1u) ? __dmul_rn(vc, u.y) : 0.0;
+        xc[q][1] = (mk[q * 2 + 1] >> 13 & 1u) ? __dmul_rn(vc, v.x) : 0.0;
+        acc[q][0] = acc[q][1] = 0.0;
+        if (CENTER_POS == 0) acc[q][0] = __dadd_rn(acc[q][0], xc[q][0]), acc[q][1] = __dadd_rn(acc[q][1], xc[q][1]);
+    }
+#pragma unroll
+    for (int pz = 0; pz < P; pz++)
+#pragma unroll
+        for (int dy = 0; dy < 3; dy++) {
+            const double2 u = lds_f64x2(sl[dy] + pz * LINE_BYTES), v = lds_f64x2(sl[dy] + pz * LINE_BYTES + 16);
+            const double e[4] = {u.x, u.y, v.x, v.y};
+#pragma unroll
+            for (int dx = 0; dx < 3; dx++)
+#pragma unroll
+                for (int q = 0; q < Q; q++) {
+                    const int dz = pz - q;
+                    if (dz < 0 || dz > 2) continue;
+                    const int t = dz * 9 + dy * 3 + dx;
+#pragma unroll
+                    for (int i = 0; i < 2; i++) {
+                        const bool on = mk[q * 2 + i] >> t & 1u;
+                        if (t == 13) {
+                            if (CENTER_POS == 2) acc[q][i] = __dadd_rn(acc[q][i], xc[q][i]);
+                        } else if (OFF_NEG1) {
+                            acc[q][i] = __dsub_rn(acc[q][i], on ? e[i + dx] : 0.0);
+                        } else {
+                            acc[q][i] = __dadd_rn(acc[q][i], on ? __dmul_rn(vo, e[i + dx]) : 0.0);
+                        }
+                    }
+                }
+        }
+#pragma unroll
+    for (int q = 0; q < Q; q++)
+#pragma unroll
+        for (int i = 0; i < 2; i++) out[q * 2 + i] = CENTER_POS == 1 ? __dadd_rn(acc[q][i], xc[q][i]) : acc[q][i];
+}
+
 // gridDim.x = strip CTAs (4 strips each) + one CTA column for the left-over columns [left_lo, sy) when there are any
-template <int Q, int S, int MINB, bool OFF_NEG1, int CENTER_POS>
+template <int Q, int S, int MINB, bool OFF_NEG1, int CENTER_POS, int DB = 1, int PF = 1, int IDA = 2>
 __global__ void __launch_bounds__(kRingWarps * 32, MINB)
     spmv_pattern_ring_kernel(const __grid_constant__ CUtensorMap tm, PatternArgs p, int c_lo, int c_hi, int np_x, int R, int n_strips,
                              int left_lo) {
@@ -75,12 +125,13 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
     const int sy = p.sy, pl = p.plane_lines;
     const int sz = sy * pl;
     const int b0 = blockIdx.y * R;
-    const int c0 = c_lo + blockIdx.z * Q;
+    // plane groups: the last one first, then 0, 1, ... (the groups on the grid faces may take the slower paths)
+    const int c0 = c_lo + (int)((blockIdx.z + gridDim.z - 1) % gridDim.z) * Q;
     const int nb = min(R, pl - b0);
     const int rb = p.row_begin;
     const unsigned n_range = (unsigned)(p.row_end - p.row_begin);
 
-    if ((int)blockIdx.x * kRingWarps >= n_strips) {  // left-over columns: List 1 per row
+    if ((int)blockIdx.x * kRingWarps >= n_strips) {  // left-over columns, thread per row
         const int n_left = sy - left_lo;
         for (int t = threadIdx.x; t < n_left * nb * Q; t += kRingWarps * 32) {
             const int col = left_lo + t % n_left, line = b0 + (t / n_left) % nb, c = c0 + t / (n_left * nb);
@@ -89,7 +140,33 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
             const int64_t row = xi - p.g0;
             if (row < rb || row >= p.row_end) continue;
             const int id = p.ids[row];
-            if (id >= 0) p.y[row] = pattern_row(p, p.disp, p.ends, p.table, id, xi);
+            if (id < 0) continue;
+            const uint32_t m = p.masks[id];
+            const uint32_t oob = (col == 0 ? kLBits : 0u) | (col == sy - 1 ? kRBits : 0u) | (line == 0 ? kDyLoBits : 0u) |
+                                 (line == pl - 1 ? kDyHiBits : 0u) | (c == 0 ? kDzLoBits : 0u) | (c == np_x - 1 ? kDzHiBits : 0u);
+            if (c < np_x && m == (kFullBox & ~oob)) {
+                // same rule as the strips: the row's entries are exactly the in-view box entries; all gathers in one batch
+                double xv[27];
+#pragma unroll
+                for (int e = 0; e < 27; e++)
+                    xv[e] = (m >> e & 1u) ? __ldg(p.x + (xi + (e % 3 - 1) + (int64_t)sy * ((e / 3) % 3 - 1) + (int64_t)sz * (e / 9 - 1))) : 0.0;
+                double acc = 0.0;
+                if (CENTER_POS == 0) acc = __dadd_rn(acc, __dmul_rn(p.v_center, xv[13]));
+#pragma unroll
+                for (int e = 0; e < 27; e++) {
+                    if (e == 13) {
+                        if (CENTER_POS == 2) acc = __dadd_rn(acc, __dmul_rn(p.v_center, xv[13]));
+                    } else if (OFF_NEG1) {
+                        acc = __dsub_rn(acc, xv[e]);
+                    } else {
+                        acc = __dadd_rn(acc, __dmul_rn(p.v_off, xv[e]));
+                    }
+                }
+                if (CENTER_POS == 1) acc = __dadd_rn(acc, __dmul_rn(p.v_center, xv[13]));
+                p.y[row] = acc;
+            } else {
+                p.y[row] = pattern_row(p, p.disp, p.ends, p.table, id, xi);
+            }
         }
         return;
     }
@@ -123,7 +200,7 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
     const int64_t xi0 = a + (int64_t)sy * b0 + (int64_t)sz * c0;
     const int row0 = (int)(xi0 - p.g0);
     bool ok[Q][2];           // the row's column and plane exist
-    uint32_t expect[Q][2];   // dictionary mask the plain chain is exact for (before the line term)
+    uint32_t expect[Q][2];   // dictionary mask the plain chain is exact for, before the line term; 0 for rows that do not exist
 #pragma unroll
     for (int q = 0; q < Q; q++) {
         const int c = c0 + q;
@@ -131,22 +208,125 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
 #pragma unroll
         for (int i = 0; i < 2; i++) {
             const uint32_t oob_a = (a + i == 0 ? kLBits : 0u) | (a + i == sy - 1 ? kRBits : 0u);
-            expect[q][i] = (c >= np_x) ? 0u : (kFullBox & ~(oob_a | oob_c));
             ok[q][i] = a + i >= 0 && a + i < sy && c <= c_hi;
+            expect[q][i] = (c >= np_x || !ok[q][i]) ? 0u : (kFullBox & ~(oob_a | oob_c));
         }
     }
     const int32_t *__restrict__ ids = p.ids;
-    auto load_id = [&](int q, int i, int j) {  // -1: no such row here (computed on whatever the ring holds, never stored)
+    double *__restrict__ y = p.y;
+    // -1: no such row here (computed on whatever the ring holds, never stored)
+    auto load_id = [&](int q, int i, int j) {
         const int r = row0 + q * sz + j * sy + i;
-        return (ok[q][i] && (unsigned)(r - rb) < n_range) ? __ldg(ids + r) : -1;
+        return (ok[q][i] && j < nb && (unsigned)(r - rb) < n_range) ? __ldg(ids + r) : -1;
     };
-    int idn[Q][2];
+    if (PF) {  // pull the tile's id rows into L2 while the first line sets are in flight (3 points cover a 256-byte row)
+        const int r_strip = row0 - 2 * lane + (a_w < 0 ? 1 : 0);
+        for (int t = lane; t < nb * Q * 3; t += 32) {
+            const int r = r_strip + (t / 3 % nb) * sy + (t / (3 * nb)) * sz + (t % 3) * 31;
+            if ((unsigned)(r - rb) < n_range) prefetch_l2(ids + r);
+        }
+    }
+    int idn[Q][2], idn2[Q][2];  // ids of the next two lines (the id stream is fetched two steps ahead)
 #pragma unroll
     for (int q = 0; q < Q; q++)
 #pragma unroll
-        for (int i = 0; i < 2; i++) idn[q][i] = load_id(q, i, 0);
+        for (int i = 0; i < 2; i++) {
+            idn[q][i] = load_id(q, i, 0);
+            if (IDA == 2) idn2[q][i] = load_id(q, i, 1);
+        }
     const double vc = p.v_center, vo = p.v_off;
     const uint32_t lane_off = lane * 16;
+
+    if constexpr (DB == 2) {
+        // Register window: the x values of lines b-1, b, b+1 x P planes x 4 columns stay in registers and only the
+        // new line is read from the ring each step (one third of the shared-memory traffic of the direct variant).
+        double w[3][P][4];
+        auto load_set = [&](auto slot, int k) {  // line set k: ring -> window slot
+            const uint32_t base = ring + (k % S) * L::kSlotBytes + lane_off;
+#pragma unroll
+            for (int pz = 0; pz < P; pz++) {
+                const double2 u = lds_f64x2(base + pz * L::kLineBytes), v = lds_f64x2(base + pz * L::kLineBytes + 16);
+                w[decltype(slot)::value][pz][0] = u.x, w[decltype(slot)::value][pz][1] = u.y;
+                w[decltype(slot)::value][pz][2] = v.x, w[decltype(slot)::value][pz][3] = v.y;
+            }
+        };
+        auto refill = [&](int k) {  // the slot of set k has been consumed
+            if (k + S < n_sets) issue(k + S);
+        };
+        mbar_wait(bars + 0, 0);
+        load_set(std::integral_constant<int, 0>{}, 0);
+        mbar_wait(bars + 8 * (1 % S), (1 / S) & 1);
+        load_set(std::integral_constant<int, 1>{}, 1);
+        auto step = [&](auto uc, int j) {
+            constexpr int u = decltype(uc)::value;  // j % 3: lines b-1, b, b+1 sit in window slots u, u+1, u+2 (mod 3)
+            const int b = b0 + j;
+            mbar_wait(bars + 8 * ((j + 2) % S), ((j + 2) / S) & 1);
+            load_set(std::integral_constant<int, (u + 2) % 3>{}, j + 2);
+            int id[Q][2];
+            uint32_t bad = 0;
+            const uint32_t in_b = ~((b == 0 ? kDyLoBits : 0u) | (b == pl - 1 ? kDyHiBits : 0u));
+#pragma unroll
+            for (int q = 0; q < Q; q++)
+#pragma unroll
+                for (int i = 0; i < 2; i++) {
+                    id[q][i] = idn[q][i];
+                    if (IDA == 2) idn[q][i] = idn2[q][i], idn2[q][i] = load_id(q, i, j + 2);
+                    else idn[q][i] = load_id(q, i, j + 1);
+                    bad |= lds_u32(s_masks + 4 + 4 * id[q][i]) ^ (expect[q][i] & in_b);  // id -1 reads entry 0 = 0
+                }
+            double acc[Q][2];
+#pragma unroll
+            for (int q = 0; q < Q; q++) acc[q][0] = acc[q][1] = 0.0;
+            auto centre = [&]() {
+#pragma unroll
+                for (int q = 0; q < Q; q++)
+#pragma unroll
+                    for (int i = 0; i < 2; i++) acc[q][i] = __dadd_rn(acc[q][i], __dmul_rn(vc, w[(u + 1) % 3][q + 1][i + 1]));
+            };
+            if (CENTER_POS == 0) centre();
+#pragma unroll
+            for (int t = 0; t < 27; t++) {
+                if (t == 13 && CENTER_POS != 2) continue;
+                const int dz = t / 9, dy = (t / 3) % 3, dx = t % 3;
+#pragma unroll
+                for (int q = 0; q < Q; q++)
+#pragma unroll
+                    for (int i = 0; i < 2; i++) {
+                        const double ev = w[(u + dy) % 3][q + dz][i + dx];
+                        if (t == 13) acc[q][i] = __dadd_rn(acc[q][i], __dmul_rn(vc, ev));
+                        else if (OFF_NEG1) acc[q][i] = __dsub_rn(acc[q][i], ev);
+                        else acc[q][i] = __dadd_rn(acc[q][i], __dmul_rn(vo, ev));
+                    }
+            }
+            if (CENTER_POS == 1) centre();
+            __syncwarp();  // every lane has consumed the new line (its values fed this step's sums)
+            if (lane == 0) {
+                fence_proxy_async();  // generic-proxy reads before the async-proxy refill
+                if (j == 0) refill(0), refill(1);
+                refill(j + 2);
+            }
+            if (__any_sync(0xffffffffu, bad != 0)) {  // some row the plain chain may not be exact for: List 1 for those
+#pragma unroll
+                for (int q = 0; q < Q; q++)
+#pragma unroll
+                    for (int i = 0; i < 2; i++)
+                        if (id[q][i] >= 0 && lds_u32(s_masks + 4 + 4 * id[q][i]) != (expect[q][i] & in_b))
+                            acc[q][i] = pattern_row_cold(p, id[q][i], xi0 + (int64_t)j * sy + (int64_t)q * sz + i);
+            }
+#pragma unroll
+            for (int q = 0; q < Q; q++)
+#pragma unroll
+                for (int i = 0; i < 2; i++)
+                    if (id[q][i] >= 0) y[row0 + q * sz + j * sy + i] = acc[q][i];
+        };
+#pragma unroll 1
+        for (int j0 = 0; j0 < nb; j0 += 3) {
+            step(std::integral_constant<int, 0>{}, j0);
+            if (j0 + 1 < nb) step(std::integral_constant<int, 1>{}, j0 + 1);
+            if (j0 + 2 < nb) step(std::integral_constant<int, 2>{}, j0 + 2);
+        }
+        return;
+    }
 
     mbar_wait(bars + 0, 0);
     mbar_wait(bars + 8 * (1 % S), (1 / S) & 1);
@@ -159,78 +339,108 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
         for (int dy = 0; dy < 3; dy++) sl[dy] = ring + ((j + dy) % S) * L::kSlotBytes + lane_off;
         int id[Q][2];
         uint32_t bad = 0;
-        const uint32_t oob_b = (b == 0 ? kDyLoBits : 0u) | (b == pl - 1 ? kDyHiBits : 0u);
+        const uint32_t in_b = ~((b == 0 ? kDyLoBits : 0u) | (b == pl - 1 ? kDyHiBits : 0u));
 #pragma unroll
         for (int q = 0; q < Q; q++)
 #pragma unroll
             for (int i = 0; i < 2; i++) {
                 id[q][i] = idn[q][i];
-                idn[q][i] = j + 1 < nb ? load_id(q, i, j + 1) : -1;
-                const uint32_t m = lds_u32(s_masks + 4 + 4 * id[q][i]);
-                bad |= (id[q][i] >= 0 && m != (expect[q][i] & ~oob_b)) ? (1u << (q * 2 + i)) : 0u;
+                if (IDA == 2) idn[q][i] = idn2[q][i], idn2[q][i] = load_id(q, i, j + 2);
+                else idn[q][i] = load_id(q, i, j + 1);
+                bad |= lds_u32(s_masks + 4 + 4 * id[q][i]) ^ (expect[q][i] & in_b);  // id -1 reads entry 0 = 0
             }
-        double acc[Q][2], xc[Q][2];
+        double acc[Q][2];
+        // The sums of the step.  Planes outermost, so that the Q rows of a thread consume each (plane, line) operand
+        // quad together; with DB the quads of plane pz+1 are fetched from shared memory while plane pz is being summed.
+        {
+            double xc[Q][2];
 #pragma unroll
-        for (int q = 0; q < Q; q++) acc[q][0] = acc[q][1] = 0.0;
-        if (CENTER_POS == 0) {
+            for (int q = 0; q < Q; q++) acc[q][0] = acc[q][1] = 0.0;
+            if (CENTER_POS == 0) {
 #pragma unroll
-            for (int q = 0; q < Q; q++) {
-                const double2 u = lds_f64x2(sl[1] + (q + 1) * L::kLineBytes), v = lds_f64x2(sl[1] + (q + 1) * L::kLineBytes + 16);
-                acc[q][0] = __dadd_rn(acc[q][0], __dmul_rn(vc, u.y));
-                acc[q][1] = __dadd_rn(acc[q][1], __dmul_rn(vc, v.x));
+                for (int q = 0; q < Q; q++) {
+                    const double2 u = lds_f64x2(sl[1] + (q + 1) * L::kLineBytes), v = lds_f64x2(sl[1] + (q + 1) * L::kLineBytes + 16);
+                    acc[q][0] = __dadd_rn(acc[q][0], __dmul_rn(vc, u.y));
+                    acc[q][1] = __dadd_rn(acc[q][1], __dmul_rn(vc, v.x));
+                }
             }
-        }
-        // planes outermost so that the Q rows of a thread consume each (plane, line) operand quad together
+            double e[2][3][4];  // [buffer][dy][columns a-1 .. a+2]
+            auto load_plane = [&](int buf, int pz) {
 #pragma unroll
-        for (int pz = 0; pz < P; pz++)
+                for (int dy = 0; dy < 3; dy++) {
+                    const double2 u = lds_f64x2(sl[dy] + pz * L::kLineBytes), v = lds_f64x2(sl[dy] + pz * L::kLineBytes + 16);
+                    e[buf][dy][0] = u.x, e[buf][dy][1] = u.y, e[buf][dy][2] = v.x, e[buf][dy][3] = v.y;
+                }
+            };
+            if (DB == 1) load_plane(0, 0);
 #pragma unroll
-            for (int dy = 0; dy < 3; dy++) {
-                const double2 u = lds_f64x2(sl[dy] + pz * L::kLineBytes), v = lds_f64x2(sl[dy] + pz * L::kLineBytes + 16);
-                const double e[4] = {u.x, u.y, v.x, v.y};  // columns a-1 .. a+2
+            for (int pz = 0; pz < P; pz++) {
+                if (DB == 1) {
+                    if (pz + 1 < P) load_plane((pz + 1) & 1, pz + 1);
+                } else {
+                    load_plane(pz & 1, pz);
+                }
 #pragma unroll
-                for (int dx = 0; dx < 3; dx++)
+                for (int dy = 0; dy < 3; dy++)
 #pragma unroll
-                    for (int q = 0; q < Q; q++) {
-                        const int dz = pz - q;
-                        if (dz < 0 || dz > 2) continue;
-                        const int t = dz * 9 + dy * 3 + dx;
+                    for (int dx = 0; dx < 3; dx++)
 #pragma unroll
-                        for (int i = 0; i < 2; i++) {
-                            if (t == 13) {
-                                if (CENTER_POS == 2) acc[q][i] = __dadd_rn(acc[q][i], __dmul_rn(vc, e[i + 1]));
-                                else xc[q][i] = e[i + 1];
-                            } else if (OFF_NEG1) {
-                                acc[q][i] = __dsub_rn(acc[q][i], e[i + dx]);
-                            } else {
-                                acc[q][i] = __dadd_rn(acc[q][i], __dmul_rn(vo, e[i + dx]));
+                        for (int q = 0; q < Q; q++) {
+                            const int dz = pz - q;
+                            if (dz < 0 || dz > 2) continue;
+                            const int t = dz * 9 + dy * 3 + dx;
+#pragma unroll
+                            for (int i = 0; i < 2; i++) {
+                                const double ev = e[pz & 1][dy][i + dx];
+                                if (t == 13) {
+                                    if (CENTER_POS == 2) acc[q][i] = __dadd_rn(acc[q][i], __dmul_rn(vc, ev));
+                                    else xc[q][i] = ev;
+                                } else if (OFF_NEG1) {
+                                    acc[q][i] = __dsub_rn(acc[q][i], ev);
+                                } else {
+                                    acc[q][i] = __dadd_rn(acc[q][i], __dmul_rn(vo, ev));
+                                }
                             }
                         }
-                    }
             }
-        if (CENTER_POS == 1) {
+            if (CENTER_POS == 1) {
+#pragma unroll
+                for (int q = 0; q < Q; q++)
+#pragma unroll
+                    for (int i = 0; i < 2; i++) acc[q][i] = __dadd_rn(acc[q][i], __dmul_rn(vc, xc[q][i]));
+            }
+        }
+        if (__any_sync(0xffffffffu, bad != 0)) {
+            // Some row the plain chain may not be exact for.  Sub-boxes whose entries are all inside the view (e.g. the
+            // grid faces when x carries ghost planes beyond them): the sums again with every operand selected by the
+            // row's mask.  Rows of other patterns, or with entries outside the view: List 1 as written.
+            uint32_t mk[Q * 2];
+            double am[Q * 2];
 #pragma unroll
             for (int q = 0; q < Q; q++)
 #pragma unroll
-                for (int i = 0; i < 2; i++) acc[q][i] = __dadd_rn(acc[q][i], __dmul_rn(vc, xc[q][i]));
+                for (int i = 0; i < 2; i++) mk[q * 2 + i] = lds_u32(s_masks + 4 + 4 * id[q][i]);
+            ring_masked_step<Q, OFF_NEG1, CENTER_POS, L::kLineBytes>(sl[0], sl[1], sl[2], mk, vc, vo, am);
+#pragma unroll
+            for (int q = 0; q < Q; q++)
+#pragma unroll
+                for (int i = 0; i < 2; i++) {
+                    const uint32_t m = mk[q * 2 + i];
+                    if (id[q][i] >= 0 && (m == kGenericMask || (m & ~(expect[q][i] & in_b)) != 0))
+                        am[q * 2 + i] = pattern_row_cold(p, id[q][i], xi0 + (int64_t)j * sy + (int64_t)q * sz + i);
+                    acc[q][i] = am[q * 2 + i];
+                }
         }
         __syncwarp();  // every lane is done with the slot of line b-1
         if (lane == 0 && j + S < n_sets) {
             fence_proxy_async();  // generic-proxy reads before the async-proxy refill
             issue(j + S);
         }
-        if (__any_sync(0xffffffffu, bad != 0)) {  // rows the plain chain is not exact for: List 1 per lane
-#pragma unroll
-            for (int q = 0; q < Q; q++)
-#pragma unroll
-                for (int i = 0; i < 2; i++)
-                    if (bad >> (q * 2 + i) & 1u)
-                        acc[q][i] = pattern_row_cold(p, id[q][i], xi0 + (int64_t)j * sy + (int64_t)q * sz + i);
-        }
 #pragma unroll
         for (int q = 0; q < Q; q++)
 #pragma unroll
             for (int i = 0; i < 2; i++)
-                if (id[q][i] >= 0) p.y[row0 + q * sz + j * sy + i] = acc[q][i];
+                if (id[q][i] >= 0) y[row0 + q * sz + j * sy + i] = acc[q][i];
     }
 }
 
@@ -281,7 +491,7 @@ static int make_x_map(const double *x, int sy, int pl, int np_x, int planes_per_
     return SPMVB_OK;
 }
 
-template <int Q, int S, int MINB, bool ALLV>
+template <int Q, int S, int MINB, bool ALLV, int DB = 1, int PF = 1, int IDA = 2>
 static int launch_ring_t(const spmvb_matrix *a, PatternArgs &p, int R, cudaStream_t st) {
     using L = RingLayout<Q, S>;
     const bool neg1 = p.v_off == -1.0;
@@ -302,12 +512,12 @@ static int launch_ring_t(const spmvb_matrix *a, PatternArgs &p, int R, cudaStrea
     do {                                                                                                                       \
         static bool attr = false;                                                                                              \
         if (!attr) {                                                                                                           \
-            if (cudaFuncSetAttribute(spmv_pattern_ring_kernel<Q, S, MINB, NEG, CP>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+            if (cudaFuncSetAttribute(spmv_pattern_ring_kernel<Q, S, MINB, NEG, CP, DB, PF, IDA>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                      (int)L::kTotal) != cudaSuccess)                                                           \
                 return -1;                                                                                                     \
             attr = true;                                                                                                       \
         }                                                                                                                      \
-        spmv_pattern_ring_kernel<Q, S, MINB, NEG, CP><<<grid, block, L::kTotal, st>>>(tm, p, c_lo, c_hi, np_x, R, n_strips, left_lo);             \
+        spmv_pattern_ring_kernel<Q, S, MINB, NEG, CP, DB, PF, IDA><<<grid, block, L::kTotal, st>>>(tm, p, c_lo, c_hi, np_x, R, n_strips, left_lo);             \
     } while (0)
     if constexpr (ALLV) {
         if (neg1) {
@@ -331,15 +541,16 @@ bool ring_ok(const spmvb_matrix *a, const PatternArgs &p) {
            p.g0 > -(int64_t)INT32_MAX / 2 && p.g0 < INT32_MAX / 2;
 }
 
-// which: 0 default; others are measured alternatives.  `lines` = lines per CTA march (0 = default).
+// which: 0 = default configuration; others are measured alternatives (profiles/r01_probe256_tensor_ring*.log).
+// `lines` = lines per CTA march (0 = default).
 int launch_pattern_ring(int which, int lines, const spmvb_matrix *a, PatternArgs &p, cudaStream_t st) {
     const int R = lines > 0 ? lines : 16;
     switch (which) {
-        case 1: return launch_ring_t<2, 5, 5, false>(a, p, R, st);
-        case 2: return launch_ring_t<4, 5, 3, false>(a, p, R, st);
-        case 3: return launch_ring_t<2, 8, 3, false>(a, p, R, st);
-        case 4: return launch_ring_t<1, 6, 6, false>(a, p, R, st);
-        default: return launch_ring_t<2, 6, 4, false>(a, p, R, st);
+        case 1: return launch_ring_t<2, 6, 4, false>(a, p, R, st);           // 2 planes/thread, 16 warps/SM     105 us
+        case 2: return launch_ring_t<2, 5, 5, false>(a, p, R, st);           // 2 planes/thread, 20 warps/SM     104 us
+        case 3: return launch_ring_t<2, 6, 3, false, 2, 1, 1>(a, p, R, st);  // register window fed by the ring  123 us
+        case 4: return launch_ring_t<2, 4, 3, false, 2, 0, 1>(a, p, R, st);
+        default: return launch_ring_t<4, 5, 3, true>(a, p, R, st);           // 4 planes/thread, 12 warps/SM      93 us
     }
 }
 

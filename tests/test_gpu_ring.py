@@ -126,3 +126,40 @@ def test_ring_nonfinite_neighbours_do_not_leak(sp, orc):
     ok = ~np.isnan(ref)
     assert np.array_equal(np.isnan(y), np.isnan(ref)) and np.array_equal(bits(y[ok]), bits(ref[ok]))
     assert np.isnan(y[126]) and not np.isnan(y[128])
+
+
+@pytest.mark.parametrize("vals", [(26.0, -1.0), (-4.0, 1.5), (2.0, 2.0), (0.5, 3.0), (-1.0, -1.0), (-3.0, -1.0)])
+def test_ring_value_pairs_and_centre_position(sp, orc, vals):
+    """centre last / first / in place, off-diagonal -1 and general: the default variant serves them all."""
+    diag, off = vals
+    m = orc.generate_matrix(128, 11, 10, diag, off)
+    x = orc.make_test_vector(m.n, orc.RANDOM, seed=11, lo=-1.0, hi=1.0)
+    ref = orc.compress_patterns(m)
+    assert np.array_equal(bits(ring_run(sp, up_pat(sp, ref), x, 0)), bits(orc.spmv(ref, x)))
+
+
+def test_ring_is_the_default_for_large_ranges(sp, orc):
+    m = orc.generate_matrix(128, 12, 10)
+    pc = orc.compress_patterns(m, True)
+    d = up_pat(sp, pc)
+    x = orc.make_test_vector(m.n, orc.RANDOM, seed=5, lo=-1.0, hi=1.0)
+    y = run(sp, d, x)
+    assert sp.get_option("last_pattern_kernel") == 9
+    assert np.array_equal(bits(y), bits(orc.spmv(pc, x)))
+    dx, dy = sp.DeviceVector.from_host(x), sp.DeviceVector.from_host(np.zeros(m.n))
+    sp.spmv_rows(d, dx, dy, 0, 3 * 128 * 12)  # a few planes: sliding-window kernel
+    assert sp.get_option("last_pattern_kernel") == 3
+
+
+@pytest.mark.parametrize("march", [0, 91, 93])
+def test_ring_ghost_planes_beyond_the_grid_faces(sp, orc, march):
+    """x padded by one (unreferenced) plane at each end, x_col0 = -plane (the single-rank SlabLayout): the rows
+    of the first and last grid plane are sub-boxes whose missing entries are inside the view."""
+    nx, ny, nz = 128, 12, 10
+    plane = nx * ny
+    m = orc.generate_matrix(nx, ny, nz)
+    pc = orc.compress_patterns(m, True)
+    x = orc.make_test_vector(m.n, orc.RANDOM, seed=12, lo=-1.0, hi=1.0)
+    xg = np.concatenate([np.full(plane, np.nan), x, np.full(plane, np.nan)])  # ghosts must never be read as operands
+    y = ring_run(sp, up_pat(sp, pc), xg, march, x_col0=-plane, n_rows=m.n)
+    assert np.array_equal(bits(y), bits(orc.spmv(pc, x)))
