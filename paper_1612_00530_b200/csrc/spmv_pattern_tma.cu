@@ -52,12 +52,17 @@ __device__ __forceinline__ double2 lds_f64x2(uint32_t addr) {
 }
 __device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t v) { asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory"); }
 
-template <int Q, int S>
+constexpr int kIdBoxCols = kStripCols + 8;  // id box: columns 64s-4 .. 64s+67 (a 16-byte aligned start for 4-byte ids)
+
+template <int Q, int S, bool IDT>
 struct RingLayout {
     static constexpr int P = Q + 2;
-    static constexpr uint32_t kLineBytes = kBoxCols * 8;                      // one plane of a line set
-    static constexpr uint32_t kSetBytes = P * kLineBytes;                     // bytes one TMA box delivers
-    static constexpr uint32_t kSlotBytes = (kSetBytes + 127u) / 128u * 128u;  // TMA destinations are 128-byte aligned
+    static constexpr uint32_t kLineBytes = kBoxCols * 8;                    // one plane of a line set of x
+    static constexpr uint32_t kXBytes = (P * kLineBytes + 127u) / 128u * 128u;  // TMA destinations are 128-byte aligned
+    static constexpr uint32_t kIdLineBytes = kIdBoxCols * 4;
+    static constexpr uint32_t kIdBytes = IDT ? Q * kIdLineBytes : 0;        // the ids of the set's line ride along
+    static constexpr uint32_t kSetBytes = P * kLineBytes + kIdBytes;        // bytes the TMA boxes of one set deliver
+    static constexpr uint32_t kSlotBytes = kXBytes + (kIdBytes + 127u) / 128u * 128u;
     static constexpr uint32_t kRingBytes = kRingWarps * S * kSlotBytes;
     static constexpr uint32_t kBarBytes = kRingWarps * S * 8;
     static constexpr uint32_t kTotal = kRingBytes + kBarBytes + (kDictSmemPat + 1) * 4 + 128;  // + alignment slack
@@ -115,9 +120,10 @@ __device__ __noinline__ void ring_masked_step(uint32_t sl0, uint32_t sl1, uint32
 // gridDim.x = strip CTAs (4 strips each) + one CTA column for the left-over columns [left_lo, sy) when there are any
 template <int Q, int S, int MINB, bool OFF_NEG1, int CENTER_POS, int DB = 1, int PF = 1, int IDA = 2>
 __global__ void __launch_bounds__(kRingWarps * 32, MINB)
-    spmv_pattern_ring_kernel(const __grid_constant__ CUtensorMap tm, PatternArgs p, int c_lo, int c_hi, int np_x, int R, int n_strips,
-                             int left_lo) {
-    using L = RingLayout<Q, S>;
+    spmv_pattern_ring_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm_ids, PatternArgs p, int c_lo,
+                             int c_hi, int np_x, int R, int n_strips, int left_lo, int id_plane0) {
+    constexpr bool IDT = IDA == 0;  // ids through the ring (their own tensor view) instead of per-thread loads
+    using L = RingLayout<Q, S, IDT>;
     constexpr int P = L::P;
     extern __shared__ unsigned char smem_raw[];
     const uint32_t sbase = (smem_u32(smem_raw) + 127u) & ~127u;
@@ -191,6 +197,7 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
         const uint32_t bar = bars + 8 * (k % S);
         mbar_expect_tx(bar, L::kSetBytes);
         tma_load_3d(ring + (k % S) * L::kSlotBytes, &tm, a_w - 1, b0 - 1 + k, c0 - 1, bar);
+        if (IDT) tma_load_3d(ring + (k % S) * L::kSlotBytes + L::kXBytes, &tm_ids, a_w - 3, b0 - 1 + k, c0 - id_plane0, bar);
     };
     if (lane == 0)
         for (int k = 0; k < S && k < n_sets; k++) issue(k);
@@ -219,21 +226,42 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
         const int r = row0 + q * sz + j * sy + i;
         return (ok[q][i] && j < nb && (unsigned)(r - rb) < n_range) ? __ldg(ids + r) : -1;
     };
-    if (PF) {  // pull the tile's id rows into L2 while the first line sets are in flight (3 points cover a 256-byte row)
+    if (PF && !IDT) {  // pull the tile's id rows into L2 while the first line sets are in flight (3 points cover a 256-byte row)
         const int r_strip = row0 - 2 * lane + (a_w < 0 ? 1 : 0);
         for (int t = lane; t < nb * Q * 3; t += 32) {
             const int r = r_strip + (t / 3 % nb) * sy + (t / (3 * nb)) * sz + (t % 3) * 31;
             if ((unsigned)(r - rb) < n_range) prefetch_l2(ids + r);
         }
     }
-    int idn[Q][2], idn2[Q][2];  // ids of the next two lines (the id stream is fetched two steps ahead)
+    int idn[Q][2], idn2[Q][2];  // ids of the next two lines (IDA = 2: the id stream is fetched two steps ahead)
+    if (!IDT) {
 #pragma unroll
-    for (int q = 0; q < Q; q++)
+        for (int q = 0; q < Q; q++)
 #pragma unroll
-        for (int i = 0; i < 2; i++) {
-            idn[q][i] = load_id(q, i, 0);
-            if (IDA == 2) idn2[q][i] = load_id(q, i, 1);
+            for (int i = 0; i < 2; i++) {
+                idn[q][i] = load_id(q, i, 0);
+                if (IDA == 2) idn2[q][i] = load_id(q, i, 1);
+            }
+    }
+    // the id of (plane q, column i) of line b0 + j: from the ring (set j+1 carries the ids of its line) or the registers
+    auto ring_id = [&](int q, int i, int j) {  // IDT: id of line b0 + j, read from set j + 1
+        const int r = row0 + q * sz + j * sy + i;
+        const int v = (int)lds_u32(ring + ((j + 1) % S) * L::kSlotBytes + L::kXBytes + q * L::kIdLineBytes + (3 + 2 * lane + i) * 4);
+        return (ok[q][i] && (unsigned)(r - rb) < n_range) ? v : -1;
+    };
+    auto next_id = [&](int q, int i, int j) {
+        if (IDT) {
+            if (DB != 2) return ring_id(q, i, j);
+            // window variant: the slot of set j+1 was released a step ago; ids are taken one step early, with the window line
+            const int v = idn[q][i];
+            idn[q][i] = ring_id(q, i, j + 1);
+            return v;
         }
+        const int v = idn[q][i];
+        if (IDA == 2) idn[q][i] = idn2[q][i], idn2[q][i] = load_id(q, i, j + 2);
+        else idn[q][i] = load_id(q, i, j + 1);
+        return v;
+    };
     const double vc = p.v_center, vo = p.v_off;
     const uint32_t lane_off = lane * 16;
 
@@ -257,6 +285,12 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
         load_set(std::integral_constant<int, 0>{}, 0);
         mbar_wait(bars + 8 * (1 % S), (1 / S) & 1);
         load_set(std::integral_constant<int, 1>{}, 1);
+        if (IDT) {
+#pragma unroll
+            for (int q = 0; q < Q; q++)
+#pragma unroll
+                for (int i = 0; i < 2; i++) idn[q][i] = ring_id(q, i, 0);
+        }
         auto step = [&](auto uc, int j) {
             constexpr int u = decltype(uc)::value;  // j % 3: lines b-1, b, b+1 sit in window slots u, u+1, u+2 (mod 3)
             const int b = b0 + j;
@@ -269,9 +303,7 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
             for (int q = 0; q < Q; q++)
 #pragma unroll
                 for (int i = 0; i < 2; i++) {
-                    id[q][i] = idn[q][i];
-                    if (IDA == 2) idn[q][i] = idn2[q][i], idn2[q][i] = load_id(q, i, j + 2);
-                    else idn[q][i] = load_id(q, i, j + 1);
+                    id[q][i] = next_id(q, i, j);
                     bad |= lds_u32(s_masks + 4 + 4 * id[q][i]) ^ (expect[q][i] & in_b);  // id -1 reads entry 0 = 0
                 }
             double acc[Q][2];
@@ -344,9 +376,7 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
         for (int q = 0; q < Q; q++)
 #pragma unroll
             for (int i = 0; i < 2; i++) {
-                id[q][i] = idn[q][i];
-                if (IDA == 2) idn[q][i] = idn2[q][i], idn2[q][i] = load_id(q, i, j + 2);
-                else idn[q][i] = load_id(q, i, j + 1);
+                id[q][i] = next_id(q, i, j);
                 bad |= lds_u32(s_masks + 4 + 4 * id[q][i]) ^ (expect[q][i] & in_b);  // id -1 reads entry 0 = 0
             }
         double acc[Q][2];
@@ -461,47 +491,64 @@ static EncodeTiledFn encode_tiled() {
     return fn;
 }
 
-// The x view [np_x planes][plane_lines lines][sy columns] with a (Q+2) x 1 x 66 box.
-static int make_x_map(const double *x, int sy, int pl, int np_x, int planes_per_box, CUtensorMap *out) {
+// A [planes][plane_lines lines][sy columns] view of `base` with a box of box_cols x 1 x box_planes elements
+// (x: fp64, 68 columns, Q+2 planes; ids: int32, 72 columns, Q planes).  One cached map per thread and kind.
+static int make_view_map(int kind, const void *base, int sy, int pl, int planes, int box_cols, int box_planes, CUtensorMap *out) {
     struct Key {
-        const double *x;
-        int sy, pl, np, pb;
+        const void *base;
+        int sy, pl, np, bc, bp;
     };
-    thread_local Key last{nullptr, 0, 0, 0, 0};
-    thread_local CUtensorMap last_map;
-    if (last.x == x && last.sy == sy && last.pl == pl && last.np == np_x && last.pb == planes_per_box) {
-        *out = last_map;
+    thread_local Key last[2] = {{nullptr, 0, 0, 0, 0, 0}, {nullptr, 0, 0, 0, 0, 0}};
+    thread_local CUtensorMap last_map[2];
+    Key &k = last[kind];
+    if (k.base == base && k.sy == sy && k.pl == pl && k.np == planes && k.bc == box_cols && k.bp == box_planes) {
+        *out = last_map[kind];
         return SPMVB_OK;
     }
     EncodeTiledFn enc = encode_tiled();
     if (!enc) return fail(SPMVB_ERR_CUDA, "cuTensorMapEncodeTiled is not available from this driver");
-    const cuuint64_t dims[3] = {(cuuint64_t)sy, (cuuint64_t)pl, (cuuint64_t)np_x};
-    const cuuint64_t strides[2] = {(cuuint64_t)sy * 8, (cuuint64_t)sy * pl * 8};
-    const cuuint32_t box[3] = {(cuuint32_t)kBoxCols, 1u, (cuuint32_t)planes_per_box};
+    const cuuint64_t esz = kind == 0 ? 8 : 4;
+    const cuuint64_t dims[3] = {(cuuint64_t)sy, (cuuint64_t)pl, (cuuint64_t)planes};
+    const cuuint64_t strides[2] = {(cuuint64_t)sy * esz, (cuuint64_t)sy * pl * esz};
+    const cuuint32_t box[3] = {(cuuint32_t)box_cols, 1u, (cuuint32_t)box_planes};
     const cuuint32_t estr[3] = {1, 1, 1};
-    const CUresult r = enc(&last_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double *>(x), dims, strides, box, estr,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    const CUresult r = enc(&last_map[kind], kind == 0 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_INT32, 3,
+                           const_cast<void *>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
-        last.x = nullptr;
-        return fail(SPMVB_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) for view %d x %d x %d", (int)r, np_x, pl, sy);
+        k.base = nullptr;
+        return fail(SPMVB_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) for view %d x %d x %d", (int)r, planes, pl, sy);
     }
-    last = Key{x, sy, pl, np_x, planes_per_box};
-    *out = last_map;
+    k = Key{base, sy, pl, planes, box_cols, box_planes};
+    *out = last_map[kind];
     return SPMVB_OK;
+}
+
+// The id stream can ride through the ring when its rows form whole planes of the same view: g0 a multiple of the
+// plane, a whole number of planes of rows, 16-byte aligned base and line stride.
+static bool ids_view_ok(const spmvb_matrix *a, const PatternArgs &p) {
+    const int64_t sz = (int64_t)p.sy * p.plane_lines;
+    return p.g0 >= 0 && p.g0 % sz == 0 && (int64_t)a->n % sz == 0 && p.sy % 4 == 0 && (uintptr_t)p.ids % 16 == 0;
 }
 
 template <int Q, int S, int MINB, bool ALLV, int DB = 1, int PF = 1, int IDA = 2>
 static int launch_ring_t(const spmvb_matrix *a, PatternArgs &p, int R, cudaStream_t st) {
-    using L = RingLayout<Q, S>;
+    using L = RingLayout<Q, S, IDA == 0>;
     const bool neg1 = p.v_off == -1.0;
     const int cp = a->box.center_pos;
     if (!ALLV && !(neg1 && cp == 1)) return 1;
+    if (IDA == 0 && !ids_view_ok(a, p)) return 1;
     const int64_t sz = (int64_t)p.sy * p.plane_lines;
     const int np_x = (int)(p.x_len / sz);
     const int c_lo = (int)((p.g0 + p.row_begin) / sz), c_hi = (int)((p.g0 + p.row_end - 1) / sz);
-    CUtensorMap tm;
-    if (make_x_map(p.x, p.sy, p.plane_lines, np_x, Q + 2, &tm) != SPMVB_OK) return -1;
+    const int id_plane0 = (int)(p.g0 / sz);
+    CUtensorMap tm, tm_ids;
+    if (make_view_map(0, p.x, p.sy, p.plane_lines, np_x, kBoxCols, Q + 2, &tm) != SPMVB_OK) return -1;
+    if (IDA == 0) {
+        if (make_view_map(1, p.ids, p.sy, p.plane_lines, (int)(a->n / sz), kIdBoxCols, Q, &tm_ids) != SPMVB_OK) return -1;
+    } else {
+        tm_ids = tm;  // unused
+    }
     // strips start at column -1; a partial last strip is used unless at most two columns are left over
     int n_strips = (p.sy + 1) / kStripCols;
     if (p.sy - (n_strips * kStripCols - 1) > 2) n_strips++;
@@ -517,7 +564,7 @@ static int launch_ring_t(const spmvb_matrix *a, PatternArgs &p, int R, cudaStrea
                 return -1;                                                                                                     \
             attr = true;                                                                                                       \
         }                                                                                                                      \
-        spmv_pattern_ring_kernel<Q, S, MINB, NEG, CP, DB, PF, IDA><<<grid, block, L::kTotal, st>>>(tm, p, c_lo, c_hi, np_x, R, n_strips, left_lo);             \
+        spmv_pattern_ring_kernel<Q, S, MINB, NEG, CP, DB, PF, IDA><<<grid, block, L::kTotal, st>>>(tm, tm_ids, p, c_lo, c_hi, np_x, R, n_strips, left_lo, id_plane0);             \
     } while (0)
     if constexpr (ALLV) {
         if (neg1) {
@@ -545,12 +592,17 @@ bool ring_ok(const spmvb_matrix *a, const PatternArgs &p) {
 // `lines` = lines per CTA march (0 = default).
 int launch_pattern_ring(int which, int lines, const spmvb_matrix *a, PatternArgs &p, cudaStream_t st) {
     const int R = lines > 0 ? lines : 16;
+    int rc = 1;
     switch (which) {
-        case 1: return launch_ring_t<2, 6, 4, false>(a, p, R, st);           // 2 planes/thread, 16 warps/SM     105 us
-        case 2: return launch_ring_t<2, 5, 5, false>(a, p, R, st);           // 2 planes/thread, 20 warps/SM     104 us
-        case 3: return launch_ring_t<2, 6, 3, false, 2, 1, 1>(a, p, R, st);  // register window fed by the ring  123 us
-        case 4: return launch_ring_t<2, 4, 3, false, 2, 0, 1>(a, p, R, st);
-        default: return launch_ring_t<4, 5, 3, true>(a, p, R, st);           // 4 planes/thread, 12 warps/SM      93 us
+        case 1: return launch_ring_t<2, 6, 4, false>(a, p, R, st);  // 2 planes/thread, 16 warps/SM, ids by per-thread loads  101-105 us
+        case 2: return launch_ring_t<4, 5, 3, true>(a, p, R, st);   // 4 planes/thread, 12 warps/SM, ids by per-thread loads   93-96 us
+        case 3:                                                     // register window fed by the ring                       100-107 us
+            rc = launch_ring_t<2, 5, 3, false, 2, 0, 0>(a, p, R, st);
+            return rc == 1 ? launch_ring_t<2, 6, 3, false, 2, 1, 1>(a, p, R, st) : rc;
+        case 4: return launch_ring_t<2, 6, 3, false, 2, 1, 1>(a, p, R, st);
+        default:  // 4 planes/thread, 12 warps/SM, ids through the ring when their rows are whole planes of the view        88 us
+            rc = launch_ring_t<4, 4, 3, true, 1, 0, 0>(a, p, R, st);
+            return rc == 1 ? launch_ring_t<4, 5, 3, true>(a, p, R, st) : rc;
     }
 }
 
