@@ -133,8 +133,75 @@ void analyse_box_plan(spmvb_matrix *a) {
     }
 }
 
+// Smallest and largest global column referenced by the rows of a pattern handle (ids + per-pattern displacement
+// extremes, plus the exception block).  out[0] = min, out[1] = max.
+__global__ void column_range_kernel(const int32_t *__restrict__ ids, int n, int64_t row_offset, const int32_t *__restrict__ pmin,
+                                    const int32_t *__restrict__ pmax, const int32_t *__restrict__ exc_cols, int64_t n_exc_entries,
+                                    long long *out) {
+    long long lo = INT64_MAX, hi = INT64_MIN;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x, t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (int64_t r = t0; r < n; r += stride) {
+        const int id = ids[r];
+        if (id >= 0) {
+            lo = min(lo, (long long)(row_offset + r + pmin[id]));
+            hi = max(hi, (long long)(row_offset + r + pmax[id]));
+        }
+    }
+    for (int64_t e = t0; e < n_exc_entries; e += stride) {
+        lo = min(lo, (long long)exc_cols[e]);
+        hi = max(hi, (long long)exc_cols[e]);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (lo != INT64_MAX) atomicMin(out, lo);
+        if (hi != INT64_MIN) atomicMax(out + 1, hi);
+    }
+}
+
+static int compute_column_range(spmvb_matrix *a) {
+    a->col_min = 0;
+    a->col_max = -1;
+    const int P = a->n_patterns;
+    if (a->n <= 0 || P <= 0 || !a->s[SPMVB_S_ROW_PATTERN]) return SPMVB_OK;
+    std::vector<int32_t> ext(2 * (size_t)P);
+    for (int p = 0; p < P; p++) {
+        int32_t lo = 0, hi = 0;
+        const int64_t b = a->h_disp_offsets[p], e = a->h_disp_offsets[p + 1];
+        if (e > b) {
+            lo = hi = a->h_disp_flat[b];
+            for (int64_t t = b; t < e; t++) lo = std::min(lo, a->h_disp_flat[t]), hi = std::max(hi, a->h_disp_flat[t]);
+        }
+        ext[p] = lo;
+        ext[P + p] = hi;
+    }
+    int32_t *d_ext = nullptr;
+    long long *d_out = nullptr;
+    SPMVB_CUDA(cudaMalloc(&d_ext, ext.size() * sizeof(int32_t)));
+    SPMVB_CUDA(cudaMalloc(&d_out, 2 * sizeof(long long)));
+    const long long init[2] = {INT64_MAX, INT64_MIN};
+    long long res[2];
+    cudaError_t e1 = cudaMemcpy(d_ext, ext.data(), ext.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+    cudaError_t e2 = cudaMemcpy(d_out, init, sizeof(init), cudaMemcpyHostToDevice);
+    if (e1 == cudaSuccess && e2 == cudaSuccess) {
+        column_range_kernel<<<592, 256>>>(static_cast<const int32_t *>(a->s[SPMVB_S_ROW_PATTERN]), a->n, a->row_offset, d_ext, d_ext + P,
+                                          static_cast<const int32_t *>(a->s[SPMVB_S_EXC_COLUMNS]), (int64_t)a->n_exc * a->w_exc, d_out);
+        e1 = cudaGetLastError();
+        e2 = cudaMemcpy(res, d_out, sizeof(res), cudaMemcpyDeviceToHost);
+    }
+    cudaFree(d_ext);
+    cudaFree(d_out);
+    if (e1 != cudaSuccess || e2 != cudaSuccess)
+        return fail(SPMVB_ERR_CUDA, "column range scan failed: %s", cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
+    if (res[0] <= res[1]) a->col_min = res[0], a->col_max = res[1];
+    return SPMVB_OK;
+}
+
 int finish_pattern_handle(spmvb_matrix *a) {
     analyse_box_plan(a);
+    SPMVB_TRY(compute_column_range(a));
     const int P = a->n_patterns;
     std::vector<uint32_t> masks = a->box.masks;
     if (masks.empty()) masks.assign(std::max(P, 1), kGenericMask);

@@ -58,6 +58,7 @@ struct spmvb_matrix {
     int32_t device = 0;
     int32_t n = 0, width = 0, m = 0, n_patterns = 0, n_exc = 0, w_exc = 0, values_in_pattern = 0;
     int64_t nnz = 0, row_offset = 0, disp_total = 0, n_cols = 0;
+    int64_t col_min = 0, col_max = -1;  // pattern handles: range of global columns the rows reference (col_max < col_min: unknown)
     void *s[SPMVB_S_COUNT_] = {};
     uint64_t bytes[SPMVB_S_COUNT_] = {};
     // host mirrors of the small pattern-side tables

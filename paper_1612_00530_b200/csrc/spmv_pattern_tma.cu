@@ -45,6 +45,10 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap *tm,
         "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
         : "memory");
 }
+// TMA-engine prefetch of the same box into L2 only
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap *tm, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(tm), "r"(c0), "r"(c1), "r"(c2) : "memory");
+}
 __device__ __forceinline__ double2 lds_f64x2(uint32_t addr) {
     double2 v;
     asm volatile("ld.shared.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
@@ -474,6 +478,300 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
     }
 }
 
+// -----------------------------------------------------------------------------------------
+// Persistent form of the direct variant (the default).  The (strip, plane group) columns of the
+// view, pl lines each, form one sequence of line steps; it is cut into equal contiguous chunks,
+// one per resident warp (a single wave of CTAs), so that every warp does the same amount of work
+// and nothing is left for a tail.  A chunk that crosses a column end is two marches.  The rows of
+// the left-over columns are dealt out to the warps and summed while the first line sets are in
+// flight.  The ring (slot = set number mod S, parity from the set number) runs on across marches.
+// -----------------------------------------------------------------------------------------
+template <bool OFF_NEG1, int CENTER_POS>
+__device__ __forceinline__ void ring_leftover_row(const PatternArgs &p, int col, int line, int c, int np_x) {
+    const int sy = p.sy, pl = p.plane_lines;
+    const int64_t sz = (int64_t)sy * pl;
+    const int64_t xi = col + (int64_t)sy * line + sz * c;
+    const int64_t row = xi - p.g0;
+    if (row < p.row_begin || row >= p.row_end) return;
+    const int id = p.ids[row];
+    if (id < 0) return;
+    const uint32_t m = p.masks[id];
+    const uint32_t oob = (col == 0 ? kLBits : 0u) | (col == sy - 1 ? kRBits : 0u) | (line == 0 ? kDyLoBits : 0u) |
+                         (line == pl - 1 ? kDyHiBits : 0u) | (c == 0 ? kDzLoBits : 0u) | (c == np_x - 1 ? kDzHiBits : 0u);
+    if (c < np_x && m == (kFullBox & ~oob)) {
+        // same rule as the strips: the row's entries are exactly the in-view box entries; all gathers in one batch
+        double xv[27];
+#pragma unroll
+        for (int e = 0; e < 27; e++)
+            xv[e] = (m >> e & 1u) ? __ldg(p.x + (xi + (e % 3 - 1) + (int64_t)sy * ((e / 3) % 3 - 1) + sz * (e / 9 - 1))) : 0.0;
+        double acc = 0.0;
+        if (CENTER_POS == 0) acc = __dadd_rn(acc, __dmul_rn(p.v_center, xv[13]));
+#pragma unroll
+        for (int e = 0; e < 27; e++) {
+            if (e == 13) {
+                if (CENTER_POS == 2) acc = __dadd_rn(acc, __dmul_rn(p.v_center, xv[13]));
+            } else if (OFF_NEG1) {
+                acc = __dsub_rn(acc, xv[e]);
+            } else {
+                acc = __dadd_rn(acc, __dmul_rn(p.v_off, xv[e]));
+            }
+        }
+        if (CENTER_POS == 1) acc = __dadd_rn(acc, __dmul_rn(p.v_center, xv[13]));
+        p.y[row] = acc;
+    } else {
+        p.y[row] = pattern_row(p, p.disp, p.ends, p.table, id, xi);
+    }
+}
+
+template <int Q, int S, int MINB, bool OFF_NEG1, int CENTER_POS, bool IDT, int PFD = 0, int DBG = 0, bool CTAC = false>
+__global__ void __launch_bounds__(kRingWarps * 32, MINB)
+    spmv_pattern_ringp_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm_ids, PatternArgs p, int c_lo,
+                              int c_hi, int np_x, int n_strips, int left_lo, int id_plane0, int total_steps, int steps_per_warp) {
+    using L = RingLayout<Q, S, IDT>;
+    constexpr int P = L::P;
+    extern __shared__ unsigned char smem_raw[];
+    const uint32_t sbase = (smem_u32(smem_raw) + 127u) & ~127u;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int sy = p.sy, pl = p.plane_lines;
+    const int sz = sy * pl;
+    const int rb = p.row_begin;
+    const unsigned n_range = (unsigned)(p.row_end - p.row_begin);
+    const uint32_t ring = sbase + warp * (S * L::kSlotBytes);
+    const uint32_t bars = sbase + L::kRingBytes + warp * (S * 8);
+    const uint32_t s_masks = sbase + L::kRingBytes + L::kBarBytes;  // entry 0 serves id = -1
+    for (int i = threadIdx.x; i <= p.n_patterns; i += kRingWarps * 32) sts_u32(s_masks + 4 * i, i == 0 ? 0u : p.masks[i - 1]);
+    if (lane == 0) {
+#pragma unroll
+        for (int s = 0; s < S; s++) mbar_init(bars + 8 * s, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();  // the only CTA barrier: the warps are independent from here on
+
+    const int gw = blockIdx.x * kRingWarps + warp, n_warps = gridDim.x * kRingWarps;
+    const int n_sg = (n_strips + kRingWarps - 1) / kRingWarps;  // CTAC: columns are (group of 4 strips, plane group)
+    const int32_t *__restrict__ ids = p.ids;
+    double *__restrict__ y = p.y;
+    const double vc = p.v_center, vo = p.v_off;
+    const uint32_t lane_off = lane * 16;
+    uint32_t gs = 0;  // sets issued so far by this warp: slot = set number % S, parity = (set number / S) & 1
+    bool first = true;
+    // CTAC: the chunk belongs to the CTA and its four warps take the four strips of the same lines (they then read
+    // whole contiguous lines of x together); otherwise every warp has a chunk of its own.
+    int s_pos = (CTAC ? (int)blockIdx.x : gw) * steps_per_warp;
+    const int s_end = min(total_steps, s_pos + steps_per_warp);
+#pragma unroll 1
+    while (s_pos < s_end || first) {
+        const bool have = s_pos < s_end;
+        const int col_idx = have ? s_pos / pl : 0;
+        const int b0 = have ? s_pos - col_idx * pl : 0;
+        const int nb = have ? min(pl - b0, s_end - s_pos) : 0;
+        const int strip = CTAC ? (col_idx % n_sg) * kRingWarps + warp : col_idx % n_strips;
+        const int c0 = c_lo + (col_idx / (CTAC ? n_sg : n_strips)) * Q;
+        if (CTAC && have && strip >= n_strips) {  // no such strip in this group: nothing to march, but the left-over share remains
+            s_pos += nb;
+            if (s_pos < s_end || !first) continue;
+        }
+        const int a_w = strip * kStripCols - 1;  // first column of the strip (odd; -1 for strip 0)
+        const int n_sets = nb + 2;               // line sets b0-1 .. b0+nb
+        auto issue = [&](int k) {  // elected lane: line set k of this march -> slot (gs + k) % S
+            const uint32_t slot = (gs + k) % S, bar = bars + 8 * slot;
+            mbar_expect_tx(bar, L::kSetBytes);
+            tma_load_3d(ring + slot * L::kSlotBytes, &tm, a_w - 1, b0 - 1 + k, c0 - 1, bar);
+            if (IDT) tma_load_3d(ring + slot * L::kSlotBytes + L::kXBytes, &tm_ids, a_w - 3, b0 - 1 + k, c0 - id_plane0, bar);
+        };
+        auto prefetch = [&](int k) {  // the box of line set k into L2, PFD sets ahead of its fetch
+            tma_prefetch_3d(&tm, a_w - 1, b0 - 1 + k, c0 - 1);
+            if (IDT) tma_prefetch_3d(&tm_ids, a_w - 3, b0 - 1 + k, c0 - id_plane0);
+        };
+        if (have && lane == 0) {
+            for (int k = 0; k < S && k < n_sets; k++) issue(k);
+            if (PFD > 0)
+                for (int k = S; k < S + PFD && k < n_sets; k++) prefetch(k);
+        }
+        if (first) {  // this warp's share of the left-over columns, while its first line sets are in flight
+            first = false;
+            const int n_left = sy - left_lo;
+            const int total_left = n_left * pl * (c_hi - c_lo + 1);
+            for (int t = gw * 32 + lane; t < total_left; t += n_warps * 32)
+                ring_leftover_row<OFF_NEG1, CENTER_POS>(p, left_lo + t % n_left, (t / n_left) % pl, c_lo + t / (n_left * pl), np_x);
+            if (!have) break;
+        }
+
+        // per-thread geometry: columns a, a+1 (a odd); the row of (column a, line b0 + j, plane c0 + q) is row0 + q*sz + j*sy
+        const int a = a_w + 2 * lane;
+        const int64_t xi0 = a + (int64_t)sy * b0 + (int64_t)sz * c0;
+        const int row0 = (int)(xi0 - p.g0);
+        bool ok[Q][2];           // the row's column and plane exist
+        uint32_t expect[Q][2];   // dictionary mask the plain chain is exact for, before the line term; 0 for rows that do not exist
+#pragma unroll
+        for (int q = 0; q < Q; q++) {
+            const int c = c0 + q;
+            const uint32_t oob_c = (c == 0 ? kDzLoBits : 0u) | (c == np_x - 1 ? kDzHiBits : 0u);
+#pragma unroll
+            for (int i = 0; i < 2; i++) {
+                const uint32_t oob_a = (a + i == 0 ? kLBits : 0u) | (a + i == sy - 1 ? kRBits : 0u);
+                ok[q][i] = a + i >= 0 && a + i < sy && c <= c_hi;
+                expect[q][i] = (c >= np_x || !ok[q][i]) ? 0u : (kFullBox & ~(oob_a | oob_c));
+            }
+        }
+        // -1: no such row here (computed on whatever the ring holds, never stored)
+        auto load_id = [&](int q, int i, int j) {
+            const int r = row0 + q * sz + j * sy + i;
+            return (ok[q][i] && j < nb && (unsigned)(r - rb) < n_range) ? __ldg(ids + r) : -1;
+        };
+        int idn[Q][2], idn2[Q][2];  // !IDT: the id stream is fetched two steps ahead into registers
+        if (!IDT) {
+#pragma unroll
+            for (int q = 0; q < Q; q++)
+#pragma unroll
+                for (int i = 0; i < 2; i++) idn[q][i] = load_id(q, i, 0), idn2[q][i] = load_id(q, i, 1);
+        }
+        auto wait_set = [&](int k) { mbar_wait(bars + 8 * ((gs + k) % S), ((gs + k) / S) & 1); };
+        wait_set(0);
+        wait_set(1);
+#pragma unroll 1
+        for (int j = 0; j < nb; j++) {
+            const int b = b0 + j;
+            wait_set(j + 2);
+            uint32_t sl[3];
+#pragma unroll
+            for (int dy = 0; dy < 3; dy++) sl[dy] = ring + ((gs + j + dy) % S) * L::kSlotBytes + lane_off;
+            if (DBG >= 3) {  // measurement only: the data movement alone (ring fetches, waits, y stores)
+                if (DBG == 3) {
+                    const double2 u = lds_f64x2(sl[1] + L::kLineBytes);
+#pragma unroll
+                    for (int q = 0; q < Q; q++)
+#pragma unroll
+                        for (int i = 0; i < 2; i++)
+                            if (ok[q][i]) y[row0 + q * sz + j * sy + i] = u.y;
+                }
+                __syncwarp();
+                if (lane == 0 && j + S < n_sets) {
+                    fence_proxy_async();
+                    issue(j + S);
+                }
+                continue;
+            }
+            int id[Q][2];
+            uint32_t bad = 0;
+            const uint32_t in_b = ~((b == 0 ? kDyLoBits : 0u) | (b == pl - 1 ? kDyHiBits : 0u));
+#pragma unroll
+            for (int q = 0; q < Q; q++)
+#pragma unroll
+                for (int i = 0; i < 2; i++) {
+                    if (IDT) {  // set j+1 carries the ids of its line
+                        const int r = row0 + q * sz + j * sy + i;
+                        const int v = (int)lds_u32(sl[1] - lane_off + L::kXBytes + q * L::kIdLineBytes + (3 + 2 * lane + i) * 4);
+                        id[q][i] = (ok[q][i] && (unsigned)(r - rb) < n_range) ? v : -1;
+                    } else {
+                        id[q][i] = idn[q][i];
+                        idn[q][i] = idn2[q][i], idn2[q][i] = load_id(q, i, j + 2);
+                    }
+                    bad |= lds_u32(s_masks + 4 + 4 * id[q][i]) ^ (expect[q][i] & in_b);  // id -1 reads entry 0 = 0
+                }
+            double acc[Q][2];
+            // The sums of the step.  Planes outermost, so that the Q rows of a thread consume each (plane, line) operand
+            // quad together; the quads of plane pz+1 are fetched from shared memory while plane pz is being summed.
+            {
+                double xc[Q][2];
+#pragma unroll
+                for (int q = 0; q < Q; q++) acc[q][0] = acc[q][1] = 0.0;
+                if (CENTER_POS == 0) {
+#pragma unroll
+                    for (int q = 0; q < Q; q++) {
+                        const double2 u = lds_f64x2(sl[1] + (q + 1) * L::kLineBytes), v = lds_f64x2(sl[1] + (q + 1) * L::kLineBytes + 16);
+                        acc[q][0] = __dadd_rn(acc[q][0], __dmul_rn(vc, u.y));
+                        acc[q][1] = __dadd_rn(acc[q][1], __dmul_rn(vc, v.x));
+                    }
+                }
+                double e[2][3][4];  // [buffer][dy][columns a-1 .. a+2]
+                auto load_plane = [&](int buf, int pz) {
+#pragma unroll
+                    for (int dy = 0; dy < 3; dy++) {
+                        if (DBG == 2 && !(pz == 1 && dy == 1)) {  // measurement only: one operand quad per step
+                            e[buf][dy][0] = e[buf][dy][1] = e[buf][dy][2] = e[buf][dy][3] = vc;
+                            continue;
+                        }
+                        const double2 u = lds_f64x2(sl[dy] + pz * L::kLineBytes), v = lds_f64x2(sl[dy] + pz * L::kLineBytes + 16);
+                        e[buf][dy][0] = u.x, e[buf][dy][1] = u.y, e[buf][dy][2] = v.x, e[buf][dy][3] = v.y;
+                    }
+                };
+                load_plane(0, 0);
+#pragma unroll
+                for (int pz = 0; pz < P; pz++) {
+                    if (pz + 1 < P) load_plane((pz + 1) & 1, pz + 1);
+#pragma unroll
+                    for (int dy = 0; dy < 3; dy++)
+#pragma unroll
+                        for (int dx = 0; dx < 3; dx++)
+#pragma unroll
+                            for (int q = 0; q < Q; q++) {
+                                const int dz = pz - q;
+                                if (dz < 0 || dz > 2) continue;
+                                const int t = dz * 9 + dy * 3 + dx;
+#pragma unroll
+                                for (int i = 0; i < 2; i++) {
+                                    const double ev = e[pz & 1][dy][i + dx];
+                                    if (t == 13) {
+                                        if (CENTER_POS == 2) acc[q][i] = __dadd_rn(acc[q][i], __dmul_rn(vc, ev));
+                                        else xc[q][i] = ev;
+                                    } else if (DBG == 1) {  // measurement only: no dependent FP64 chain
+                                        if (dx == 1 && dy == 1) acc[q][i] = __dsub_rn(acc[q][i], ev);
+                                    } else if (OFF_NEG1) {
+                                        acc[q][i] = __dsub_rn(acc[q][i], ev);
+                                    } else {
+                                        acc[q][i] = __dadd_rn(acc[q][i], __dmul_rn(vo, ev));
+                                    }
+                                }
+                            }
+                }
+                if (CENTER_POS == 1) {
+#pragma unroll
+                    for (int q = 0; q < Q; q++)
+#pragma unroll
+                        for (int i = 0; i < 2; i++) acc[q][i] = __dadd_rn(acc[q][i], __dmul_rn(vc, xc[q][i]));
+                }
+            }
+            if (__any_sync(0xffffffffu, bad != 0)) {
+                // Some row the plain chain may not be exact for.  Sub-boxes whose entries are all inside the view (e.g. the
+                // grid faces when x carries ghost planes beyond them): the sums again with every operand selected by the
+                // row's mask.  Rows of other patterns, or with entries outside the view: List 1 as written.
+                uint32_t mk[Q * 2];
+                double am[Q * 2];
+#pragma unroll
+                for (int q = 0; q < Q; q++)
+#pragma unroll
+                    for (int i = 0; i < 2; i++) mk[q * 2 + i] = lds_u32(s_masks + 4 + 4 * id[q][i]);
+                ring_masked_step<Q, OFF_NEG1, CENTER_POS, L::kLineBytes>(sl[0], sl[1], sl[2], mk, vc, vo, am);
+#pragma unroll
+                for (int q = 0; q < Q; q++)
+#pragma unroll
+                    for (int i = 0; i < 2; i++) {
+                        const uint32_t m = mk[q * 2 + i];
+                        if (id[q][i] >= 0 && (m == kGenericMask || (m & ~(expect[q][i] & in_b)) != 0))
+                            am[q * 2 + i] = pattern_row_cold(p, id[q][i], xi0 + (int64_t)j * sy + (int64_t)q * sz + i);
+                        acc[q][i] = am[q * 2 + i];
+                    }
+            }
+            __syncwarp();  // every lane is done with the slot of line b-1
+            if (lane == 0 && j + S < n_sets) {
+                fence_proxy_async();  // generic-proxy reads before the async-proxy refill
+                issue(j + S);
+                if (PFD > 0 && j + S + PFD < n_sets) prefetch(j + S + PFD);
+            }
+            // (16-byte stores of the aligned pairs (a+1, a+2) through a lane shuffle were measured slower: 81 vs 78 us)
+#pragma unroll
+            for (int q = 0; q < Q; q++)
+#pragma unroll
+                for (int i = 0; i < 2; i++)
+                    if (id[q][i] >= 0) y[row0 + q * sz + j * sy + i] = acc[q][i];
+        }
+        gs += n_sets;
+        s_pos += nb;
+        __syncwarp();
+    }
+}
+
 // ---- host side ------------------------------------------------------------------------
 using EncodeTiledFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *, const cuuint64_t *,
                                    const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -524,6 +822,27 @@ static int make_view_map(int kind, const void *base, int sy, int pl, int planes,
     return SPMVB_OK;
 }
 
+// The view of x only needs the planes that hold columns the matrix references.  Planes before / after them (e.g. the
+// ghost planes a slab layout keeps beyond the faces of the global grid) are cut off, so that the entries the face
+// rows lack fall outside the view -- zero-filled, i.e. the plain chain is exact there too.  Shifts x / g0 / x_len of
+// a copy of the arguments by whole planes; every consumer (List 1 included) stays consistent.
+static PatternArgs clip_view(const spmvb_matrix *a, const PatternArgs &p) {
+    PatternArgs q = p;
+    if (a->col_max < a->col_min) return q;
+    const int64_t sz = (int64_t)p.sy * p.plane_lines;
+    const int64_t x_col0 = a->row_offset - p.g0;
+    const int64_t lo = std::max<int64_t>(0, a->col_min - x_col0), hi = std::min<int64_t>(p.x_len - 1, a->col_max - x_col0);
+    if (hi < lo) return q;
+    const int64_t k_lo = lo / sz;
+    int64_t planes = hi / sz - k_lo + 1;
+    if ((k_lo + planes) * sz > p.x_len) planes = (p.x_len - k_lo * sz) / sz;  // whole planes only
+    if (planes < 1 || p.g0 - k_lo * sz + p.row_begin < 0) return q;
+    q.x = p.x + k_lo * sz;
+    q.g0 = p.g0 - k_lo * sz;
+    q.x_len = planes * sz;
+    return q;
+}
+
 // The id stream can ride through the ring when its rows form whole planes of the same view: g0 a multiple of the
 // plane, a whole number of planes of rows, 16-byte aligned base and line stride.
 static bool ids_view_ok(const spmvb_matrix *a, const PatternArgs &p) {
@@ -532,7 +851,8 @@ static bool ids_view_ok(const spmvb_matrix *a, const PatternArgs &p) {
 }
 
 template <int Q, int S, int MINB, bool ALLV, int DB = 1, int PF = 1, int IDA = 2>
-static int launch_ring_t(const spmvb_matrix *a, PatternArgs &p, int R, cudaStream_t st) {
+static int launch_ring_t(const spmvb_matrix *a, PatternArgs &p_in, int R, cudaStream_t st) {
+    PatternArgs p = clip_view(a, p_in);
     using L = RingLayout<Q, S, IDA == 0>;
     const bool neg1 = p.v_off == -1.0;
     const int cp = a->box.center_pos;
@@ -579,6 +899,66 @@ static int launch_ring_t(const spmvb_matrix *a, PatternArgs &p, int R, cudaStrea
     return check_launch("spmv_pattern_ring") == SPMVB_OK ? 0 : -1;
 }
 
+template <int Q, int S, int MINB, bool IDT, int PFD = 0, int DBG = 0, bool CTAC = false>
+static int launch_ringp_t(const spmvb_matrix *a, PatternArgs &p_in, int chunk, cudaStream_t st) {
+    PatternArgs p = clip_view(a, p_in);
+    using L = RingLayout<Q, S, IDT>;
+    const bool neg1 = p.v_off == -1.0;
+    const int cp = a->box.center_pos;
+    if (IDT && !ids_view_ok(a, p)) return 1;
+    const int64_t sz = (int64_t)p.sy * p.plane_lines;
+    const int np_x = (int)(p.x_len / sz);
+    const int c_lo = (int)((p.g0 + p.row_begin) / sz), c_hi = (int)((p.g0 + p.row_end - 1) / sz);
+    const int id_plane0 = (int)(p.g0 / sz);
+    CUtensorMap tm, tm_ids;
+    if (make_view_map(0, p.x, p.sy, p.plane_lines, np_x, kBoxCols, Q + 2, &tm) != SPMVB_OK) return -1;
+    if (IDT) {
+        if (make_view_map(1, p.ids, p.sy, p.plane_lines, (int)(a->n / sz), kIdBoxCols, Q, &tm_ids) != SPMVB_OK) return -1;
+    } else {
+        tm_ids = tm;  // unused
+    }
+    int n_strips = (p.sy + 1) / kStripCols;
+    if (p.sy - (n_strips * kStripCols - 1) > 2) n_strips++;
+    const int left_lo = std::min(p.sy, n_strips * kStripCols - 1);
+    const int n_cols = CTAC ? (n_strips + kRingWarps - 1) / kRingWarps : n_strips;
+    const int units = CTAC ? 1 : kRingWarps;  // chunks per CTA
+    const int64_t total64 = (int64_t)n_cols * ((c_hi - c_lo + Q) / Q) * p.plane_lines;
+    if (total64 >= INT32_MAX) return 1;
+    const int total = (int)total64;
+    static int n_sm = 0;
+    if (n_sm == 0) {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
+    }
+    // one wave of CTAs; every warp gets the same number of line steps (at least `min_steps`, so that small problems
+    // do not pay two halo line sets for a handful of steps)
+    const int min_steps = 8;
+#define LAUNCH_RINGP(NEG, CP)                                                                                                   \
+    do {                                                                                                                         \
+        static int per_sm = 0;                                                                                                   \
+        if (per_sm == 0) {                                                                                                       \
+            if (cudaFuncSetAttribute(spmv_pattern_ringp_kernel<Q, S, MINB, NEG, CP, IDT, PFD, DBG, CTAC>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                     (int)L::kTotal) != cudaSuccess ||                                                           \
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmv_pattern_ringp_kernel<Q, S, MINB, NEG, CP, IDT, PFD, DBG, CTAC>,      \
+                                                              kRingWarps * 32, L::kTotal) != cudaSuccess || per_sm <= 0)         \
+                return -1;                                                                                                       \
+        }                                                                                                                        \
+        int grid = n_sm * per_sm;                                                                                                \
+        grid = std::max(1, std::min(grid, (total + min_steps * units - 1) / (min_steps * units)));                              \
+        const int spw = chunk > 0 ? chunk : (total + grid * units - 1) / (grid * units);                                         \
+        if (chunk > 0) grid = (total + spw * units - 1) / (spw * units);                                                         \
+        spmv_pattern_ringp_kernel<Q, S, MINB, NEG, CP, IDT, PFD, DBG, CTAC><<<grid, kRingWarps * 32, L::kTotal, st>>>(                          \
+            tm, tm_ids, p, c_lo, c_hi, np_x, n_strips, left_lo, id_plane0, total, spw);                                          \
+    } while (0)
+    if (neg1) {
+        if (cp == 0) LAUNCH_RINGP(true, 0); else if (cp == 1) LAUNCH_RINGP(true, 1); else LAUNCH_RINGP(true, 2);
+    } else {
+        if (cp == 0) LAUNCH_RINGP(false, 0); else if (cp == 1) LAUNCH_RINGP(false, 1); else LAUNCH_RINGP(false, 2);
+    }
+#undef LAUNCH_RINGP
+    return check_launch("spmv_pattern_ringp") == SPMVB_OK ? 0 : -1;
+}
+
 // Conditions: the TMA view needs a 16-byte aligned base, strides that are multiples of 16 bytes (even
 // sy), at least one whole plane of x and a line no narrower than a box; row arithmetic is 32-bit.
 bool ring_ok(const spmvb_matrix *a, const PatternArgs &p) {
@@ -600,9 +980,29 @@ int launch_pattern_ring(int which, int lines, const spmvb_matrix *a, PatternArgs
             rc = launch_ring_t<2, 5, 3, false, 2, 0, 0>(a, p, R, st);
             return rc == 1 ? launch_ring_t<2, 6, 3, false, 2, 1, 1>(a, p, R, st) : rc;
         case 4: return launch_ring_t<2, 6, 3, false, 2, 1, 1>(a, p, R, st);
-        default:  // 4 planes/thread, 12 warps/SM, ids through the ring when their rows are whole planes of the view        88 us
-            rc = launch_ring_t<4, 4, 3, true, 1, 0, 0>(a, p, R, st);
+        case 6: return launch_ringp_t<4, 4, 3, true, 2>(a, p, lines, st);     // + TMA L2 prefetch 2 sets ahead: 95 us (4 ahead: 105 us)
+        case 7: return launch_ringp_t<4, 4, 3, true, 0, 1>(a, p, lines, st);  // measurement only (wrong results): no FP64 chains
+        case 8: return launch_ringp_t<4, 4, 3, true, 0, 2>(a, p, lines, st);  // measurement only (wrong results): one operand quad per step
+        case 9: return launch_ringp_t<4, 4, 3, true, 0, 3>(a, p, lines, st);  // measurement only: ring fetches + y stores, nothing else
+        case 10: return launch_ringp_t<4, 4, 3, true, 0, 4>(a, p, lines, st); // measurement only: ring fetches only
+        case 11:  // a chunk per warp instead of per CTA: 87 us
+            rc = launch_ringp_t<4, 4, 3, true>(a, p, lines, st);
+            return rc == 1 ? launch_ringp_t<4, 5, 3, false>(a, p, lines, st) : rc;
+        case 14:  // CTA chunks, 2 planes/thread, 6 slots: 90 us
+            rc = launch_ringp_t<2, 6, 3, true, 0, 0, true>(a, p, lines, st);
+            return rc == 1 ? launch_ringp_t<4, 5, 3, false, 0, 0, true>(a, p, lines, st) : rc;
+        case 15: return launch_ringp_t<2, 5, 4, true, 0, 0, true>(a, p, lines, st);   // CTA chunks, 2 planes/thread, 5 slots, 16 warps
+        case 16: return launch_ringp_t<4, 5, 2, true, 0, 0, true>(a, p, lines, st);   // CTA chunks, 4 planes/thread, 5 slots, 8 warps
+        case 17: return launch_ringp_t<4, 5, 3, false, 0, 0, true>(a, p, lines, st);  // CTA chunks, 4 planes/thread, 5 slots, ids by loads
+        case 12: return launch_ringp_t<4, 4, 3, true, 0, 4, true>(a, p, lines, st);  // ... fetch only
+        case 13: return launch_ringp_t<4, 4, 3, true, 0, 3, true>(a, p, lines, st);  // ... fetch + store only
+        case 5:  // non-persistent form of the default (CTA tiles of R lines, dynamic CTA scheduling)                          88 us
+            rc = launch_ring_t<4, 4, 3, false, 1, 0, 0>(a, p, R, st);
             return rc == 1 ? launch_ring_t<4, 5, 3, true>(a, p, R, st) : rc;
+        default:  // persistent: 4 planes/thread, 12 warps/SM, equal chunks of line steps per warp; ids through the ring when
+                  // their rows are whole planes of the view, else two steps ahead in registers.  `lines` = chunk length.
+            rc = launch_ringp_t<4, 4, 3, true, 0, 0, true>(a, p, lines, st);
+            return rc == 1 ? launch_ringp_t<4, 5, 3, false, 0, 0, true>(a, p, lines, st) : rc;
     }
 }
 

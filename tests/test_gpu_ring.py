@@ -7,7 +7,7 @@ pytestmark = pytest.mark.gpu
 
 from tests.test_gpu_parity import bits, run, sp, up_pat  # noqa: E402,F401
 
-RING = [90, 91, 92, 93, 94]
+RING = [90, 91, 92, 93, 94, 95, 101, 104, 107]
 
 
 def ring_run(sp, d, x, march, lines=0, must_ring=True, **kw):
