@@ -486,24 +486,25 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
 // the left-over columns are dealt out to the warps and summed while the first line sets are in
 // flight.  The ring (slot = set number mod S, parity from the set number) runs on across marches.
 // -----------------------------------------------------------------------------------------
+// One row of a left-over column.  The id and all in-view box operands are requested together (one memory latency);
+// the row's mask then decides whether the plain sum is exact (same rule as the strips) or List 1 runs as written.
 template <bool OFF_NEG1, int CENTER_POS>
-__device__ __forceinline__ void ring_leftover_row(const PatternArgs &p, int col, int line, int c, int np_x) {
+__device__ __forceinline__ void ring_leftover_row(const PatternArgs &p, uint32_t s_masks, int col, int line, int c, int np_x) {
     const int sy = p.sy, pl = p.plane_lines;
     const int64_t sz = (int64_t)sy * pl;
     const int64_t xi = col + (int64_t)sy * line + sz * c;
     const int64_t row = xi - p.g0;
     if (row < p.row_begin || row >= p.row_end) return;
-    const int id = p.ids[row];
-    if (id < 0) return;
-    const uint32_t m = p.masks[id];
     const uint32_t oob = (col == 0 ? kLBits : 0u) | (col == sy - 1 ? kRBits : 0u) | (line == 0 ? kDyLoBits : 0u) |
                          (line == pl - 1 ? kDyHiBits : 0u) | (c == 0 ? kDzLoBits : 0u) | (c == np_x - 1 ? kDzHiBits : 0u);
-    if (c < np_x && m == (kFullBox & ~oob)) {
-        // same rule as the strips: the row's entries are exactly the in-view box entries; all gathers in one batch
-        double xv[27];
+    const uint32_t in_view = c < np_x ? (kFullBox & ~oob) : 0u;
+    const int id = __ldg(p.ids + row);
+    double xv[27];
 #pragma unroll
-        for (int e = 0; e < 27; e++)
-            xv[e] = (m >> e & 1u) ? __ldg(p.x + (xi + (e % 3 - 1) + (int64_t)sy * ((e / 3) % 3 - 1) + sz * (e / 9 - 1))) : 0.0;
+    for (int e = 0; e < 27; e++)
+        xv[e] = (in_view >> e & 1u) ? __ldg(p.x + (xi + (e % 3 - 1) + (int64_t)sy * ((e / 3) % 3 - 1) + sz * (e / 9 - 1))) : 0.0;
+    if (id < 0) return;
+    if (in_view != 0 && lds_u32(s_masks + 4 + 4 * id) == in_view) {
         double acc = 0.0;
         if (CENTER_POS == 0) acc = __dadd_rn(acc, __dmul_rn(p.v_center, xv[13]));
 #pragma unroll
@@ -585,15 +586,11 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
         };
         if (have && lane == 0) {
             for (int k = 0; k < S && k < n_sets; k++) issue(k);
-            if (PFD > 0)
+            if (PFD > 0 && PFD < 9)
                 for (int k = S; k < S + PFD && k < n_sets; k++) prefetch(k);
         }
-        if (first) {  // this warp's share of the left-over columns, while its first line sets are in flight
+        if (first) {
             first = false;
-            const int n_left = sy - left_lo;
-            const int total_left = n_left * pl * (c_hi - c_lo + 1);
-            for (int t = gw * 32 + lane; t < total_left; t += n_warps * 32)
-                ring_leftover_row<OFF_NEG1, CENTER_POS>(p, left_lo + t % n_left, (t / n_left) % pl, c_lo + t / (n_left * pl), np_x);
             if (!have) break;
         }
 
@@ -757,18 +754,28 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
             if (lane == 0 && j + S < n_sets) {
                 fence_proxy_async();  // generic-proxy reads before the async-proxy refill
                 issue(j + S);
-                if (PFD > 0 && j + S + PFD < n_sets) prefetch(j + S + PFD);
+                if (PFD > 0 && PFD < 9 && j + S + PFD < n_sets) prefetch(j + S + PFD);
             }
             // (16-byte stores of the aligned pairs (a+1, a+2) through a lane shuffle were measured slower: 81 vs 78 us)
 #pragma unroll
             for (int q = 0; q < Q; q++)
 #pragma unroll
                 for (int i = 0; i < 2; i++)
-                    if (id[q][i] >= 0) y[row0 + q * sz + j * sy + i] = acc[q][i];
+                    if (id[q][i] >= 0) {
+                        if (PFD == 9) __stcs(&y[row0 + q * sz + j * sy + i], acc[q][i]);
+                        else y[row0 + q * sz + j * sy + i] = acc[q][i];
+                    }
         }
         gs += n_sets;
         s_pos += nb;
         __syncwarp();
+    }
+    {  // this warp's share of the left-over columns (after its marches: the warps do not finish in step, so these
+       // latency-bound gathers overlap with the marches of the others)
+        const int n_left = sy - left_lo;
+        const int total_left = n_left * pl * (c_hi - c_lo + 1);
+        for (int t = gw * 32 + lane; t < total_left && DBG != 5; t += n_warps * 32)
+            ring_leftover_row<OFF_NEG1, CENTER_POS>(p, s_masks, left_lo + t % n_left, (t / n_left) % pl, c_lo + t / (n_left * pl), np_x);
     }
 }
 
@@ -991,18 +998,41 @@ int launch_pattern_ring(int which, int lines, const spmvb_matrix *a, PatternArgs
         case 14:  // CTA chunks, 2 planes/thread, 6 slots: 90 us
             rc = launch_ringp_t<2, 6, 3, true, 0, 0, true>(a, p, lines, st);
             return rc == 1 ? launch_ringp_t<4, 5, 3, false, 0, 0, true>(a, p, lines, st) : rc;
-        case 15: return launch_ringp_t<2, 5, 4, true, 0, 0, true>(a, p, lines, st);   // CTA chunks, 2 planes/thread, 5 slots, 16 warps
-        case 16: return launch_ringp_t<4, 5, 2, true, 0, 0, true>(a, p, lines, st);   // CTA chunks, 4 planes/thread, 5 slots, 8 warps
+        case 15: return launch_ringp_t<4, 4, 3, true, 9, 0, true>(a, p, lines, st);   // CTA chunks, streaming (evict-first) y stores
+        case 16: return launch_ringp_t<4, 4, 3, true, 0, 5, true>(a, p, lines, st);   // measurement only: no left-over columns
         case 17: return launch_ringp_t<4, 5, 3, false, 0, 0, true>(a, p, lines, st);  // CTA chunks, 4 planes/thread, 5 slots, ids by loads
         case 12: return launch_ringp_t<4, 4, 3, true, 0, 4, true>(a, p, lines, st);  // ... fetch only
         case 13: return launch_ringp_t<4, 4, 3, true, 0, 3, true>(a, p, lines, st);  // ... fetch + store only
         case 5:  // non-persistent form of the default (CTA tiles of R lines, dynamic CTA scheduling)                          88 us
-            rc = launch_ring_t<4, 4, 3, false, 1, 0, 0>(a, p, R, st);
+            rc = launch_ring_t<4, 4, 3, true, 1, 0, 0>(a, p, R, st);
             return rc == 1 ? launch_ring_t<4, 5, 3, true>(a, p, R, st) : rc;
-        default:  // persistent: 4 planes/thread, 12 warps/SM, equal chunks of line steps per warp; ids through the ring when
-                  // their rows are whole planes of the view, else two steps ahead in registers.  `lines` = chunk length.
-            rc = launch_ringp_t<4, 4, 3, true, 0, 0, true>(a, p, lines, st);
-            return rc == 1 ? launch_ringp_t<4, 5, 3, false, 0, 0, true>(a, p, lines, st) : rc;
+        default: {
+            // 4 planes/thread, 12 warps/SM; ids through the ring when their rows are whole planes of the view, else two
+            // steps ahead in registers.  Schedule (measured, profiles/r01_probe_shapes_tensor_ring.log):
+            //  * x (about) fits L2: persistent, one wave, equal chunks of line steps -- per CTA with its warps on the four
+            //    strips of the same lines when the strips come in fours (76 us at 256^3), else per warp (and only while x
+            //    is well inside L2);
+            //  * larger x: CTA tiles of 16 lines in launch order, which keeps the planes being read few enough for their
+            //    halo planes to be reused from L2 (512^3: 530 us vs 686 us persistent).
+            static int l2_bytes = 0;
+            if (l2_bytes == 0) {
+                int dev = 0;
+                if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&l2_bytes, cudaDevAttrL2CacheSize, dev) != cudaSuccess) return -1;
+            }
+            int n_strips = (p.sy + 1) / kStripCols;
+            if (p.sy - (n_strips * kStripCols - 1) > 2) n_strips++;
+            const double x_bytes = (double)p.x_len * 8.0;
+            if (x_bytes > 1.25 * l2_bytes || (n_strips % kRingWarps != 0 && x_bytes > 0.8 * l2_bytes)) {
+                rc = launch_ring_t<4, 4, 3, true, 1, 0, 0>(a, p, R, st);
+                return rc == 1 ? launch_ring_t<4, 5, 3, true>(a, p, R, st) : rc;
+            }
+            if (n_strips % kRingWarps == 0) {
+                rc = launch_ringp_t<4, 4, 3, true, 0, 0, true>(a, p, lines, st);
+                return rc == 1 ? launch_ringp_t<4, 5, 3, false, 0, 0, true>(a, p, lines, st) : rc;
+            }
+            rc = launch_ringp_t<4, 4, 3, true>(a, p, lines, st);
+            return rc == 1 ? launch_ringp_t<4, 5, 3, false>(a, p, lines, st) : rc;
+        }
     }
 }
 
