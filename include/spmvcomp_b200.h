@@ -109,8 +109,16 @@ const char *spmvb_last_error(void);
 int spmvb_version(void);
 int spmvb_device_count(int *count);
 int spmvb_set_device(int device);
-/* Tuning knobs for A/B measurement ("pattern_kernel": 0 auto, 1 generic, 2 box;
- * "ell_kernel": 0 auto ...).  Unknown keys -> SPMVB_ERR_INVALID_ARGUMENT. */
+/* Tuning knobs for A/B measurement; results never depend on them.  Unknown keys -> SPMVB_ERR_INVALID_ARGUMENT.
+ *   "pattern_kernel": 0 auto, 1 List 1 as written (thread per row), 2 box plan required, 3 one-column box kernel only
+ *   "box_march":      0 auto (tensor ring for ranges of >= 8 planes, else the register sliding window);
+ *                     3 sliding window forced; 90..110 variants / ablations of the tensor ring, 1..72 of the
+ *                     sliding window (listed with their measured times in csrc/spmv_pattern*.cu)
+ *   "box_lines":      lines per CTA tile / chunk length of the tensor ring (0 = default)
+ *   "ell_kernel":     0 auto (ELL: TMA bulk pipeline, vt: staged), 1 naive, 2 staged vector loads, 3 TMA for vt too
+ *   "box_prefetch", "box_prefetch_l1": L2 / L1 prefetch distance of the sliding-window kernels
+ *   "last_pattern_kernel" (read): family of the last pattern launch: 1 List 1, 2 one-column box, 3 sliding window,
+ *                     4 lab variant, 9 tensor ring */
 int spmvb_set_option(const char *key, int value);
 int spmvb_get_option(const char *key, int *value);
 
