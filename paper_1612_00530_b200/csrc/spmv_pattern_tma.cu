@@ -449,21 +449,27 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
             // grid faces when x carries ghost planes beyond them): the sums again with every operand selected by the
             // row's mask.  Rows of other patterns, or with entries outside the view: List 1 as written.
             uint32_t mk[Q * 2];
-            double am[Q * 2];
-#pragma unroll
-            for (int q = 0; q < Q; q++)
-#pragma unroll
-                for (int i = 0; i < 2; i++) mk[q * 2 + i] = lds_u32(s_masks + 4 + 4 * id[q][i]);
-            ring_masked_step<Q, OFF_NEG1, CENTER_POS, L::kLineBytes>(sl[0], sl[1], sl[2], mk, vc, vo, am);
+            bool real = false;  // rows without an id (exception rows, range ends) raise the flag too, but need nothing
 #pragma unroll
             for (int q = 0; q < Q; q++)
 #pragma unroll
                 for (int i = 0; i < 2; i++) {
-                    const uint32_t m = mk[q * 2 + i];
-                    if (id[q][i] >= 0 && (m == kGenericMask || (m & ~(expect[q][i] & in_b)) != 0))
-                        am[q * 2 + i] = pattern_row_cold(p, id[q][i], xi0 + (int64_t)j * sy + (int64_t)q * sz + i);
-                    acc[q][i] = am[q * 2 + i];
+                    mk[q * 2 + i] = lds_u32(s_masks + 4 + 4 * id[q][i]);
+                    real = real || (id[q][i] >= 0 && mk[q * 2 + i] != (expect[q][i] & in_b));
                 }
+            if (__any_sync(0xffffffffu, real)) {
+                double am[Q * 2];
+                ring_masked_step<Q, OFF_NEG1, CENTER_POS, L::kLineBytes>(sl[0], sl[1], sl[2], mk, vc, vo, am);
+#pragma unroll
+                for (int q = 0; q < Q; q++)
+#pragma unroll
+                    for (int i = 0; i < 2; i++) {
+                        const uint32_t m = mk[q * 2 + i];
+                        if (id[q][i] >= 0 && (m == kGenericMask || (m & ~(expect[q][i] & in_b)) != 0))
+                            am[q * 2 + i] = pattern_row_cold(p, id[q][i], xi0 + (int64_t)j * sy + (int64_t)q * sz + i);
+                        acc[q][i] = am[q * 2 + i];
+                    }
+            }
         }
         __syncwarp();  // every lane is done with the slot of line b-1
         if (lane == 0 && j + S < n_sets) {
@@ -734,21 +740,27 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
                 // grid faces when x carries ghost planes beyond them): the sums again with every operand selected by the
                 // row's mask.  Rows of other patterns, or with entries outside the view: List 1 as written.
                 uint32_t mk[Q * 2];
-                double am[Q * 2];
-#pragma unroll
-                for (int q = 0; q < Q; q++)
-#pragma unroll
-                    for (int i = 0; i < 2; i++) mk[q * 2 + i] = lds_u32(s_masks + 4 + 4 * id[q][i]);
-                ring_masked_step<Q, OFF_NEG1, CENTER_POS, L::kLineBytes>(sl[0], sl[1], sl[2], mk, vc, vo, am);
+                bool real = false;  // rows without an id (exception rows, range ends) raise the flag too, but need nothing
 #pragma unroll
                 for (int q = 0; q < Q; q++)
 #pragma unroll
                     for (int i = 0; i < 2; i++) {
-                        const uint32_t m = mk[q * 2 + i];
-                        if (id[q][i] >= 0 && (m == kGenericMask || (m & ~(expect[q][i] & in_b)) != 0))
-                            am[q * 2 + i] = pattern_row_cold(p, id[q][i], xi0 + (int64_t)j * sy + (int64_t)q * sz + i);
-                        acc[q][i] = am[q * 2 + i];
+                        mk[q * 2 + i] = lds_u32(s_masks + 4 + 4 * id[q][i]);
+                        real = real || (id[q][i] >= 0 && mk[q * 2 + i] != (expect[q][i] & in_b));
                     }
+                if (__any_sync(0xffffffffu, real)) {
+                    double am[Q * 2];
+                    ring_masked_step<Q, OFF_NEG1, CENTER_POS, L::kLineBytes>(sl[0], sl[1], sl[2], mk, vc, vo, am);
+#pragma unroll
+                    for (int q = 0; q < Q; q++)
+#pragma unroll
+                        for (int i = 0; i < 2; i++) {
+                            const uint32_t m = mk[q * 2 + i];
+                            if (id[q][i] >= 0 && (m == kGenericMask || (m & ~(expect[q][i] & in_b)) != 0))
+                                am[q * 2 + i] = pattern_row_cold(p, id[q][i], xi0 + (int64_t)j * sy + (int64_t)q * sz + i);
+                            acc[q][i] = am[q * 2 + i];
+                        }
+                }
             }
             __syncwarp();  // every lane is done with the slot of line b-1
             if (lane == 0 && j + S < n_sets) {
