@@ -115,6 +115,7 @@ int spmvb_set_device(int device);
  *                     3 sliding window forced; 90..110 variants / ablations of the tensor ring, 1..72 of the
  *                     sliding window (listed with their measured times in csrc/spmv_pattern*.cu)
  *   "box_lines":      lines per CTA tile / chunk length of the tensor ring (0 = default)
+ *   "host_chunks":    row chunks of the pipelined spmvb_spmv_host (0 = default 8)
  *   "ell_kernel":     0 auto (ELL: TMA bulk pipeline, vt: staged), 1 naive, 2 staged vector loads, 3 TMA for vt too
  *   "box_prefetch", "box_prefetch_l1": L2 / L1 prefetch distance of the sliding-window kernels
  *   "last_pattern_kernel" (read): family of the last pattern launch: 1 List 1, 2 one-column box, 3 sliding window,

@@ -248,6 +248,7 @@ static int *option_slot(const char *key) {
     if (!strcmp(key, "box_prefetch_l1")) return &o.box_prefetch_l1;
     if (!strcmp(key, "debug_nochain")) return &o.debug_nochain;
     if (!strcmp(key, "box_lines")) return &o.box_lines;
+    if (!strcmp(key, "host_chunks")) return &o.host_chunks;
     if (!strcmp(key, "last_pattern_kernel")) return &o.last_pattern_kernel;
     return nullptr;
 }

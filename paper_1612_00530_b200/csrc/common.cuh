@@ -71,7 +71,7 @@ struct spmvb_matrix {
     mutable int64_t scratch_x_len = 0;
     // streams / events of the pipelined host-buffer SpMV (created on first use)
     mutable cudaStream_t pipe_streams[3] = {};
-    mutable cudaEvent_t pipe_events[32] = {};
+    mutable cudaEvent_t pipe_events[128] = {};
     spmvb::BoxPlan box;
     uint32_t *d_masks = nullptr;      // device copy of box.masks
     int32_t *d_disp_off32 = nullptr;  // 32-bit copy of disp_offsets for the kernels
@@ -94,6 +94,7 @@ struct Options {
     int box_prefetch_l1 = 0; // L1 prefetch distance in lines (0 = off)
     int debug_nochain = 0;   // measurement only
     int box_lines = 0;       // lines per CTA march of the tensor-ring kernel (0 = default)
+    int host_chunks = 0;     // row chunks of the pipelined host-buffer SpMV (0 = default 8, at most 64)
     int last_pattern_kernel = 0;  // read-only: kernel family of the last pattern launch (1 List 1, 2 box v2, 3 box3, 4 lab, 9 tensor ring)
 };
 Options &options();

@@ -200,10 +200,11 @@ int spmvb_spmv_host(const spmvb_matrix *a, const double *x_host, int64_t x_len, 
         SPMVB_CUDA(cudaStreamSynchronize(nullptr));
         return SPMVB_OK;
     }
-    constexpr int kChunks = 16;
+    constexpr int kMaxChunks = 64;
+    const int kChunks = std::min(kMaxChunks, options().host_chunks > 0 ? options().host_chunks : 8);
     if (!a->pipe_streams[0]) {
         for (int i = 0; i < 3; i++) SPMVB_CUDA(cudaStreamCreateWithFlags(&a->pipe_streams[i], cudaStreamNonBlocking));
-        for (int i = 0; i < 2 * kChunks; i++) SPMVB_CUDA(cudaEventCreateWithFlags(&a->pipe_events[i], cudaEventDisableTiming));
+        for (int i = 0; i < 2 * kMaxChunks; i++) SPMVB_CUDA(cudaEventCreateWithFlags(&a->pipe_events[i], cudaEventDisableTiming));
     }
     cudaStream_t s_in = a->pipe_streams[0], s_run = a->pipe_streams[1], s_out = a->pipe_streams[2];
     // chunk boundaries on whole planes of the box plan when there is one (tiles then stay aligned), multiples of 4 rows otherwise
@@ -214,7 +215,8 @@ int spmvb_spmv_host(const spmvb_matrix *a, const double *x_host, int64_t x_len, 
     int c = 0;
     for (int64_t r0 = 0; r0 < n; r0 += per, c++) {
         const int64_t r1 = std::min(n, r0 + per);
-        const int64_t need = std::min(n, r1 + reach);
+        // whole 4 KB blocks: a copy that starts at an odd element runs at 80 % of the PCIe rate (tests/e2e_probe.py)
+        const int64_t need = std::min(n, (r1 + reach + 511) / 512 * 512);
         if (need > sent) {
             SPMVB_CUDA(cudaMemcpyAsync(a->scratch_x + sent, x_host + sent, (size_t)(need - sent) * 8, cudaMemcpyHostToDevice, s_in));
             sent = need;
