@@ -20,7 +20,13 @@
         }                                                                            \
     } while (0)
 
-constexpr int S = 4, Q = 4, P = Q + 2;
+#ifndef RING_S
+#define RING_S 4
+#endif
+#ifndef MINB
+#define MINB 3
+#endif
+constexpr int S = RING_S, Q = 4, P = Q + 2;
 constexpr uint32_t XB = 68 * 8 * P, XBP = (XB + 127) / 128 * 128, IB = 72 * 4 * Q, SLOT = XBP + (IB + 127) / 128 * 128;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -39,7 +45,7 @@ __device__ __forceinline__ void tma3(uint32_t dst, const CUtensorMap *tm, int c0
 // MODE 0 = Y march, 1 = Z march.  Work unit of a CTA: (group of 4 strips, block of Q planes [Y] / Q lines [Z]) x a range of
 // march steps.  Units are enumerated with the unit index fastest across CTAs: blockIdx.x -> (unit, march chunk).
 template <int MODE>
-__global__ void __launch_bounds__(128, 3)
+__global__ void __launch_bounds__(128, MINB)
     skeleton(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUtensorMap ti, double *__restrict__ y, int sy, int pl, int np,
              int n_units, int chunk, int persistent, int total_steps, int do_store) {
     extern __shared__ unsigned char raw[];
