@@ -147,6 +147,60 @@ class SlabSpmv:
             self.kernel(x_local, y_local, hi, n)
 
 
+class SlabCg:
+    """Unpreconditioned CG (solver.hpp:40-46) over z-slabs: the SpMV is SlabSpmv (halo of the search
+    direction exchanged every iteration, overlapped with the interior rows), the three dots of an iteration are local
+    dots summed over the ranks with one all_reduce each, the three waxpbys are local.  x0 = 0; stops when
+    ||r||2 / ||b||2 <= tolerance.  Same operation sequence as the single-device `cg_solve`, so iteration counts agree
+    across backends; the dot products are summed in a different order, so the iterates agree to rounding.
+
+    ops.dot(u, v) -> float and ops.waxpby(alpha, x, beta, y, w) work on owned-row vectors (the product passes the CUDA
+    kernels, the CPU tests the oracle's); vectors are torch tensors, `p` carries the ghost planes."""
+
+    def __init__(self, layout: SlabLayout, spmv: "SlabSpmv", ops, dist=None, torch=None):
+        self.L, self.spmv, self.ops, self.dist, self.torch = layout, spmv, ops, dist, torch
+
+    def _sum(self, v):
+        if self.dist is None or self.L.world == 1:
+            return v
+        t = self.torch.tensor([v], dtype=self.torch.float64)
+        self.dist.all_reduce(t)  # SUM; the same value on every rank
+        return float(t[0])
+
+    def solve(self, b_local, x_local, p_ghosted, r_local, ap_local, max_iterations=500, tolerance=1e-8):
+        """b, x, r, ap: owned rows (n_local); p_ghosted: x_len entries with ghost planes.  Returns
+        (iterations, converged, residual_history).  Raises ArithmeticError on a non-finite value (DivergenceError)."""
+        if max_iterations < 1 or not tolerance > 0.0:
+            raise ValueError("cg_solve: bad configuration")
+        L, ops = self.L, self.ops
+        p = L.owned(p_ghosted)
+        ops.waxpby(0.0, b_local, 0.0, b_local, x_local)   # x = 0
+        ops.waxpby(1.0, b_local, 0.0, b_local, r_local)   # r = b
+        ops.waxpby(1.0, b_local, 0.0, b_local, p)         # p = b
+        bnorm = self._sum(ops.dot(b_local, b_local)) ** 0.5
+        rz = self._sum(ops.dot(r_local, r_local))
+        history = [1.0]
+        if bnorm == 0.0:
+            return 0, True, history
+        for it in range(1, max_iterations + 1):
+            self.spmv.spmv(p_ghosted, ap_local)
+            alpha = rz / self._sum(ops.dot(p, ap_local))
+            ops.waxpby(1.0, x_local, alpha, p, x_local)
+            ops.waxpby(1.0, r_local, -alpha, ap_local, r_local)
+            rr = self._sum(ops.dot(r_local, r_local))
+            rz_new = rr
+            rel = rr ** 0.5 / bnorm
+            history.append(rel)
+            if not (alpha == alpha and abs(alpha) != float("inf") and rel == rel and rel != float("inf")):
+                raise ArithmeticError(f"non-finite value in iteration {it}")
+            if rel <= tolerance:
+                return it, True, history
+            beta = rz_new / rz
+            rz = rz_new
+            ops.waxpby(1.0, r_local, beta, p, p)
+        return max_iterations, False, history
+
+
 def build_slab_pattern(sp, layout: SlabLayout, dist=None, diagonal=26.0, off_diagonal=-1.0, perturb=None,
                        values_in_pattern=True, min_pattern_rows=1, stream=None, keep_csr=False):
     """Device-side build of one rank's compressed slab: generate the slab's rows, compress

@@ -64,3 +64,43 @@ def test_cg_single_unknown_and_errors(sp, orc):
     z = sp.upload_ell(2, 1, 0, np.zeros(2), np.array([0, 1], dtype=np.int32))
     with pytest.raises(sp._cabi.DivergenceError):
         sp.cg_solve(z, sp.DeviceVector.from_host(np.ones(2)))
+
+
+def test_slab_cg_driver_on_the_device(sp, orc):
+    """The distributed CG driver (slab.py:SlabCg) with the CUDA kernels as its operations, one slab: the same iteration
+    count and history as the single-call device solver, and the known solution."""
+    import torch
+    g = (128, 12, 10)
+    L = sp.SlabLayout(*g, 0, 1)
+    n = L.n_local
+    pc = sp.build_slab_pattern(sp, L, None, keep_csr=False)
+    xs = orc.make_test_vector(n, orc.RANDOM, seed=3, lo=-1.0, hi=1.0)
+    ref = orc.compress_patterns_grid(*g, values_in_pattern=True)
+    b = orc.spmv(ref, xs)
+
+    class Ops:
+        @staticmethod
+        def dot(u, v):
+            out = sp.C.c_double()
+            sp.check(sp.lib.spmvb_dot(sp.C.c_void_p(u.data_ptr()), sp.C.c_void_p(v.data_ptr()), u.numel(), sp.C.byref(out), None))
+            return out.value
+
+        @staticmethod
+        def waxpby(alpha, x, beta, y, w):
+            sp.check(sp.lib.spmvb_waxpby(alpha, sp.C.c_void_p(x.data_ptr()), beta, sp.C.c_void_p(y.data_ptr()),
+                                         sp.C.c_void_p(w.data_ptr()), x.numel(), None))
+
+    def kernel(xl, yl, b0, e0):
+        sp.spmv_rows(pc, xl, yl, b0, e0, x_col0=L.x_col0, x_len=L.x_len)
+
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    z = lambda k: torch.zeros(k, dtype=torch.float64, device="cuda")  # noqa: E731
+    b_d, x_d, r_d, ap_d, p_g = dev(b), z(n), z(n), z(n), z(L.x_len)
+    cg = sp.SlabCg(L, sp.SlabSpmv(L, kernel), Ops, None, torch)
+    it, conv, hist = cg.solve(b_d, x_d, p_g, r_d, ap_d, max_iterations=300, tolerance=1e-10)
+    torch.cuda.synchronize()
+    x1, rep = sp.cg_solve(sp.upload_pattern(ref.n, ref.table, ref.disp_offsets, ref.disp_flat, ref.ends_flat, ref.row_pattern, True),
+                          sp.DeviceVector.from_host(b), max_iterations=300, tolerance=1e-10)
+    assert conv and rep.converged and it == rep.iterations
+    assert np.allclose(hist, rep.residual_history, rtol=1e-9, atol=0.0)
+    assert np.abs(x_d.cpu().numpy() - xs).max() <= 1e-7

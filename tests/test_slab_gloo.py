@@ -122,3 +122,51 @@ def test_merge_dictionaries_orders_by_global_first_row():
     merged, maps = merge_dictionaries([a, b])
     assert merged == [((0, 1), (1, 2)), ((-1, 0), (1, 2)), ((-1, 0, 1), (2, 3))]
     assert maps == [[0, 1], [1, 2]]
+
+
+def _cg_worker(rank, world, port, grid, out_dir):
+    from oracle import oracle as orc
+    from paper_1612_00530_b200.slab import SlabCg
+    os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        nx, ny, nz = grid
+        L = SlabLayout(nx, ny, nz, rank, world)
+        r0, r1 = L.row_range
+        whole = orc.compress_patterns_grid(nx, ny, nz, values_in_pattern=True)
+        xs = orc.make_test_vector(nx * ny * nz, orc.RANDOM, seed=3, lo=-1.0, hi=1.0)
+        bg = orc.spmv(whole, xs)  # right-hand side with a known solution
+
+        def kernel(xl, yl, b, e):
+            orc.spmv_rows(whole, xl.numpy(), _View(yl.numpy(), r0), r0 + b, r0 + e, x_col0=L.x_col0)
+
+        class Ops:  # the oracle's dot / waxpby on the owned rows
+            @staticmethod
+            def dot(u, v):
+                return orc.dot(u.numpy(), v.numpy())
+
+            @staticmethod
+            def waxpby(alpha, x, beta, y, w):
+                w.numpy()[:] = orc.waxpby(alpha, x.numpy(), beta, y.numpy())
+
+        z = lambda n: torch.zeros(n, dtype=torch.float64)  # noqa: E731
+        b_local = torch.from_numpy(bg[r0:r1].copy())
+        x_local, r_local, ap_local, p_g = z(L.n_local), z(L.n_local), z(L.n_local), z(L.x_len)
+        cg = SlabCg(L, SlabSpmv(L, kernel, dist), Ops, dist, torch)
+        it, conv, hist = cg.solve(b_local, x_local, p_g, r_local, ap_local, max_iterations=200, tolerance=1e-10)
+        x_ref, it_ref, conv_ref, hist_ref = orc.cg_solve(whole, bg, max_iterations=200, tolerance=1e-10)
+        assert conv and conv_ref and it == it_ref, (it, it_ref)       # identical iteration counts
+        assert np.allclose(hist, hist_ref, rtol=1e-6, atol=0.0)
+        assert np.abs(x_local.numpy() - x_ref[r0:r1]).max() <= 1e-9 * np.abs(x_ref).max()
+        assert np.abs(x_local.numpy() - xs[r0:r1]).max() <= 1e-7
+        open(os.path.join(out_dir, f"cg{rank}"), "w").write("ok")
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,grid", [(2, (6, 5, 8)), (3, (5, 4, 7))])
+def test_slab_cg_over_gloo(tmp_path, world, grid):
+    """Distributed CG: per-iteration halo exchange of the search direction + all_reduce of the three dots."""
+    port = _free_port()
+    mp.spawn(_cg_worker, args=(world, port, grid, str(tmp_path)), nprocs=world, join=True)
+    assert all((tmp_path / f"cg{r}").exists() for r in range(world))
