@@ -1,0 +1,281 @@
+// spmvcomp command-line harness (SPEC.md:425-500 [MODULE] bench_cli) on the device path.
+//   spmvcomp_cli generate  --grid NX NY NZ
+//   spmvcomp_cli bench     --grid NX NY NZ --format ell|vt|pattern|pattern-values [--reps R] [--out json|csv] [--seed S]
+//   spmvcomp_cli solve     --grid NX NY NZ [--backend ell|vt|pattern] [--tol T] [--max-iter K]
+//   spmvcomp_cli model     --bandwidth GB/s [--formats ell,vt,pattern,pattern-values]
+//   spmvcomp_cli calibrate
+// Exit codes: 0 success, 1 verification / convergence failure, 2 usage error.
+// The matrix file arguments of the reference CLI are replaced by --grid: the serialized formats are
+// not part of this build, the generator runs on the device instead.  `generate` therefore only sizes the matrix.
+// Verification before timing: bench prints nothing but an error when the compressed kernel's y
+// differs from the ELL backend's by more than 1e-12 relative per row (scale = sum |a_ik x_k|).
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "spmvcomp/spmvcomp.hpp"
+#include "spmvcomp_b200.h"
+
+namespace {
+
+struct Usage {
+    std::string msg;
+};
+struct Failure {
+    std::string msg;
+};
+
+void ck(int rc, const char *what) {
+    if (rc != SPMVB_OK) throw Failure{std::string(what) + ": " + spmvb_last_error()};
+}
+
+struct Args {
+    int nx = 0, ny = 0, nz = 0, reps = 100, max_iter = 500;
+    bool have_grid = false;
+    std::string format = "pattern-values", backend = "pattern", out = "json", formats = "ell,vt,pattern,pattern-values";
+    double tol = 1e-8, bandwidth = 0.0;
+    unsigned long long seed = 7;
+};
+
+Args parse(int argc, char **argv) {
+    Args a;
+    for (int i = 2; i < argc; i++) {
+        const std::string k = argv[i];
+        auto need = [&](int n) {
+            if (i + n >= argc) throw Usage{"missing value for " + k};
+        };
+        if (k == "--grid") {
+            need(3);
+            a.nx = std::atoi(argv[i + 1]), a.ny = std::atoi(argv[i + 2]), a.nz = std::atoi(argv[i + 3]);
+            a.have_grid = true;
+            i += 3;
+        } else if (k == "--format") { need(1); a.format = argv[++i];
+        } else if (k == "--backend") { need(1); a.backend = argv[++i];
+        } else if (k == "--reps") { need(1); a.reps = std::atoi(argv[++i]);
+        } else if (k == "--out") { need(1); a.out = argv[++i];
+        } else if (k == "--seed") { need(1); a.seed = std::strtoull(argv[++i], nullptr, 10);
+        } else if (k == "--tol") { need(1); a.tol = std::atof(argv[++i]);
+        } else if (k == "--max-iter") { need(1); a.max_iter = std::atoi(argv[++i]);
+        } else if (k == "--bandwidth") { need(1); a.bandwidth = std::atof(argv[++i]);
+        } else if (k == "--formats") { need(1); a.formats = argv[++i];
+        } else throw Usage{"unknown option " + k};
+    }
+    return a;
+}
+
+spmvcomp::GridSpec grid_of(const Args &a) {
+    if (!a.have_grid) throw Usage{"--grid NX NY NZ is required"};
+    spmvcomp::GridSpec g{a.nx, a.ny, a.nz};
+    spmvcomp::validate(g);  // std::invalid_argument on dims < 1 or more than 2^31-1 rows (grid.hpp:35-47)
+    return g;
+}
+
+struct Handle {  // device handle with scope-bound lifetime
+    spmvb_matrix *h = nullptr;
+    Handle() = default;
+    Handle(const Handle &) = delete;
+    ~Handle() { if (h) spmvb_matrix_destroy(h); }
+};
+struct DVec {
+    double *p = nullptr;
+    explicit DVec(int64_t n) { ck(spmvb_vec_alloc(n, &p), "vec_alloc"); }
+    DVec(const DVec &) = delete;
+    ~DVec() { if (p) spmvb_vec_free(p); }
+};
+
+void generate_csr(const spmvcomp::GridSpec &g, Handle &csr) {
+    spmvb_grid sg{};
+    sg.nx = g.nx, sg.ny = g.ny, sg.nz = g.nz, sg.diagonal = 26.0, sg.off_diagonal = -1.0;
+    ck(spmvb_generate_csr(&sg, 0, g.rows(), nullptr, &csr.h), "generate");
+}
+
+void build_format(const Handle &csr, const std::string &fmt, Handle &out) {
+    spmvb_compress_options o{};
+    o.value_table_limit = 256, o.min_pattern_rows = 1;
+    if (fmt == "ell") ck(spmvb_csr_to_ell(csr.h, 0, nullptr, &out.h), "to_ell");
+    else if (fmt == "vt") ck(spmvb_csr_compress_values(csr.h, &o, 0, nullptr, &out.h), "compress_values");
+    else if (fmt == "pattern" || fmt == "pattern-values") {
+        o.values_in_pattern = fmt == "pattern-values";
+        ck(spmvb_csr_compress_patterns(csr.h, &o, nullptr, &out.h), "compress_patterns");
+    } else throw Usage{"unknown format " + fmt};
+}
+
+double sync_read(const double *dev) {  // a synchronous one-element download: waits for everything queued before it
+    double v = 0.0;
+    ck(spmvb_vec_download(&v, dev, 1, nullptr), "vec_download");
+    return v;
+}
+
+// matrix bytes per row as the byte model counts them (perf_model.hpp:49-57): what `effective_bandwidth` is quoted on
+double model_bytes_per_row(const std::string &fmt, const spmvb_matrix_info &inf) {
+    if (fmt == "ell") return 12.0 * inf.width;
+    if (fmt == "vt") return 4.0 * (inf.width + inf.m);
+    if (fmt == "pattern") return 4.0 + 4.0 * inf.m;
+    return 4.0;
+}
+
+int cmd_generate(const Args &a) {
+    const spmvcomp::GridSpec g = grid_of(a);
+    const long long nnz = (3LL * g.nx - 2) * (3LL * g.ny - 2) * (3LL * g.nz - 2);
+    std::printf("{\"grid\": [%d, %d, %d], \"rows\": %lld, \"nnz\": %lld, \"csr_bytes\": %lld}\n", g.nx, g.ny, g.nz, (long long)g.rows(),
+                nnz, 8LL * (g.rows() + 1) + 12LL * nnz);
+    return 0;
+}
+
+int cmd_bench(const Args &a) {
+    const spmvcomp::GridSpec g = grid_of(a);
+    if (a.reps < 1) throw Usage{"--reps must be >= 1"};
+    if (a.out != "json" && a.out != "csv") throw Usage{"--out must be json or csv"};
+    if (a.format != "ell" && a.format != "vt" && a.format != "pattern" && a.format != "pattern-values")
+        throw Usage{"unknown format " + a.format};
+    const int64_t n = g.rows();
+    Handle csr, ell, fmt;
+    generate_csr(g, csr);
+    build_format(csr, "ell", ell);
+    const bool is_ell = a.format == "ell";
+    if (!is_ell) build_format(csr, a.format, fmt);
+    const spmvb_matrix *run = is_ell ? ell.h : fmt.h;
+    spmvb_matrix_info inf{}, einf{};
+    ck(spmvb_matrix_get_info(run, &inf), "info");
+    ck(spmvb_matrix_get_info(ell.h, &einf), "info");
+    DVec x(n), y(n), y_ell(n), scale(n);
+    ck(spmvb_vec_fill(x.p, n, 2, a.seed, -1.0, 1.0, 0, nullptr), "vec_fill");  // random, U[-1,1)
+    // verification gate against the ELL backend
+    ck(spmvb_spmv(ell.h, x.p, 0, n, y_ell.p, 0, (int32_t)n, nullptr), "spmv ell");
+    ck(spmvb_spmv(run, x.p, 0, n, y.p, 0, (int32_t)n, nullptr), "spmv");
+    ck(spmvb_row_abs_scale(csr.h, x.p, 0, scale.p, nullptr), "row_abs_scale");
+    double worst = 0.0;
+    int64_t differing = 0;
+    ck(spmvb_compare(y.p, y_ell.p, scale.p, n, &worst, &differing, nullptr), "compare");
+    double checksum = 0.0, checksum_ell = 0.0;
+    ck(spmvb_dot(y.p, y.p, n, &checksum, nullptr), "dot");
+    ck(spmvb_dot(y_ell.p, y_ell.p, n, &checksum_ell, nullptr), "dot");
+    if (!(worst <= 1e-12) || !(std::fabs(checksum - checksum_ell) <= 1e-13 * std::fabs(checksum_ell)))
+        throw Failure{"verification failed: max scaled deviation from the ELL backend " + std::to_string(worst)};
+    // timing: one warm-up excluded, monotonic clock around reps back-to-back launches
+    ck(spmvb_spmv(run, x.p, 0, n, y.p, 0, (int32_t)n, nullptr), "spmv");
+    sync_read(y.p);
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int r = 0; r < a.reps; r++) ck(spmvb_spmv(run, x.p, 0, n, y.p, 0, (int32_t)n, nullptr), "spmv");
+    sync_read(y.p);
+    const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    double checksum_after = 0.0;
+    ck(spmvb_dot(y.p, y.p, n, &checksum_after, nullptr), "dot");
+    if (checksum_after != checksum) throw Failure{"verification failed: checksum changed between repetitions"};
+    const double gflops = 2.0 * (double)inf.nnz * a.reps / sec / 1e9;
+    const double bpr = model_bytes_per_row(a.format, inf);
+    const double eff_bw = bpr * (double)n * a.reps / sec / 1e9;
+    const double ratio = 12.0 * einf.width / bpr;
+    if (a.out == "json")
+        std::printf("{\"format\": \"%s\", \"grid\": [%d, %d, %d], \"repetitions\": %d, \"wall_time\": %.9g, \"achieved_gflops\": %.6g, "
+                    "\"effective_bandwidth_gbs\": %.6g, \"compression_ratio\": %.6g, \"bytes_per_row\": %.6g, \"checksum\": %.17g, "
+                    "\"checksum_ell\": %.17g, \"max_scaled_deviation_vs_ell\": %.3g, \"rows\": %lld, \"nnz\": %lld}\n",
+                    a.format.c_str(), g.nx, g.ny, g.nz, a.reps, sec, gflops, eff_bw, ratio, bpr, checksum, checksum_ell, worst, (long long)n,
+                    (long long)inf.nnz);
+    else {
+        std::printf("format,nx,ny,nz,repetitions,wall_time,achieved_gflops,effective_bandwidth_gbs,compression_ratio,bytes_per_row,checksum\n");
+        std::printf("%s,%d,%d,%d,%d,%.9g,%.6g,%.6g,%.6g,%.6g,%.17g\n", a.format.c_str(), g.nx, g.ny, g.nz, a.reps, sec, gflops, eff_bw, ratio, bpr,
+                    checksum);
+    }
+    return 0;
+}
+
+int cmd_solve(const Args &a) {
+    const spmvcomp::GridSpec g = grid_of(a);
+    if (a.max_iter < 1 || !(a.tol > 0.0)) throw Usage{"--max-iter >= 1 and --tol > 0 are required"};
+    if (a.backend != "ell" && a.backend != "vt" && a.backend != "pattern") throw Usage{"unknown backend " + a.backend};
+    const int64_t n = g.rows();
+    Handle csr, ell, fmt;
+    generate_csr(g, csr);
+    build_format(csr, "ell", ell);
+    if (a.backend != "ell") build_format(csr, a.backend == "pattern" ? "pattern-values" : a.backend, fmt);
+    const spmvb_matrix *run = a.backend == "ell" ? ell.h : fmt.h;
+    DVec ones(n), b(n), x(n);
+    ck(spmvb_vec_fill(ones.p, n, 0, 0, 0.0, 1.0, 0, nullptr), "vec_fill");
+    ck(spmvb_spmv(ell.h, ones.p, 0, n, b.p, 0, (int32_t)n, nullptr), "spmv");  // b = A * ones
+    std::vector<double> hist((size_t)a.max_iter + 1);
+    int32_t it = 0, conv = 0;
+    const int rc = spmvb_cg_solve(run, b.p, x.p, a.max_iter, a.tol, &it, &conv, hist.data(), nullptr);
+    if (rc == SPMVB_ERR_DIVERGENCE) {
+        std::fprintf(stderr, "divergence: %s\n", spmvb_last_error());
+        return 1;
+    }
+    ck(rc, "cg_solve");
+    spmvb_matrix_info inf{};
+    ck(spmvb_matrix_get_info(run, &inf), "info");
+    std::printf("{\"backend\": \"%s\", \"grid\": [%d, %d, %d], \"iterations\": %d, \"converged\": %s, \"final_residual\": %.6g, "
+                "\"flops_total\": %lld}\n",
+                a.backend.c_str(), g.nx, g.ny, g.nz, it, conv ? "true" : "false", hist[(size_t)it],
+                (long long)it * (2LL * inf.nnz + 12LL * n));
+    return conv ? 0 : 1;
+}
+
+int cmd_model(const Args &a) {
+    if (!(a.bandwidth > 0.0)) throw Usage{"--bandwidth GB/s (> 0) is required"};
+    spmvcomp::MachineSpec mach;
+    mach.read_bandwidth = a.bandwidth * 1e9;
+    std::printf("%-16s %14s %14s %16s\n", "format", "bytes/row", "bytes/flop", "roofline Gflops");
+    size_t pos = 0;
+    while (pos <= a.formats.size()) {
+        const size_t c = a.formats.find(',', pos);
+        const std::string name = a.formats.substr(pos, c == std::string::npos ? std::string::npos : c - pos);
+        pos = c == std::string::npos ? a.formats.size() + 1 : c + 1;
+        if (name.empty()) continue;
+        const auto f = spmvcomp::parse_format(name);
+        if (!f) throw Usage{"unknown format " + name};
+        const spmvcomp::FormatCost cost = spmvcomp::format_cost(*f, 27, 2);  // interior row of the 27-point stencil, table [-1, 26]
+        const spmvcomp::RooflineEstimate r = spmvcomp::roofline(cost, mach);
+        std::printf("%-16s %14.6g %14.6g %16.6g\n", name.c_str(), cost.bytes_per_row, cost.bytes_per_flop, r.predicted_flops / 1e9);
+    }
+    return 0;
+}
+
+int cmd_calibrate() {
+    // device analogue of the STREAM-style sweep: w = 1*x + 0*y over 64 M doubles reads 16 and writes 8 bytes per element
+    const int64_t n = 64LL << 20;
+    DVec x(n), y(n), w(n);
+    ck(spmvb_vec_fill(x.p, n, 0, 0, 0.0, 1.0, 0, nullptr), "vec_fill");
+    ck(spmvb_vec_fill(y.p, n, 0, 0, 0.0, 1.0, 0, nullptr), "vec_fill");
+    ck(spmvb_waxpby(1.0, x.p, 0.0, y.p, w.p, n, nullptr), "waxpby");
+    sync_read(w.p);
+    const int reps = 20;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int r = 0; r < reps; r++) ck(spmvb_waxpby(1.0, x.p, 0.0, y.p, w.p, n, nullptr), "waxpby");
+    sync_read(w.p);
+    const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    std::printf("{\"device_stream_bandwidth_gbs\": %.6g, \"kernel\": \"waxpby\", \"bytes_per_element\": 24, \"elements\": %lld}\n",
+                24.0 * (double)n * reps / sec / 1e9, (long long)n);
+    return 0;
+}
+
+}  // namespace
+
+int main(int argc, char **argv) {
+    try {
+        if (argc < 2) throw Usage{"subcommand required: generate | bench | solve | model | calibrate"};
+        const std::string cmd = argv[1];
+        const Args a = parse(argc, argv);
+        if (cmd == "generate") return cmd_generate(a);
+        if (cmd == "bench") return cmd_bench(a);
+        if (cmd == "solve") return cmd_solve(a);
+        if (cmd == "model") return cmd_model(a);
+        if (cmd == "calibrate") return cmd_calibrate();
+        throw Usage{"unknown subcommand " + cmd};
+    } catch (const Usage &u) {
+        std::fprintf(stderr, "usage error: %s\n", u.msg.c_str());
+        return 2;
+    } catch (const std::invalid_argument &e) {
+        std::fprintf(stderr, "invalid argument: %s\n", e.what());
+        return 2;
+    } catch (const Failure &f) {
+        std::fprintf(stderr, "%s\n", f.msg.c_str());
+        return 1;
+    } catch (const std::exception &e) {
+        std::fprintf(stderr, "error: %s\n", e.what());
+        return 1;
+    }
+}

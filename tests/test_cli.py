@@ -1,0 +1,97 @@
+"""The command-line harness (SPEC.md:425-500 [MODULE] bench_cli): `spmvcomp_cli`.
+model / generate / usage errors run anywhere; bench, solve and calibrate need the GPU."""
+import json
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CLI = os.path.join(ROOT, "paper_1612_00530_b200", "spmvcomp_cli")
+
+
+def run(*args):
+    r = subprocess.run([CLI, *map(str, args)], capture_output=True, text=True, timeout=600)
+    return r.returncode, r.stdout, r.stderr
+
+
+def table(out):
+    rows = {}
+    for line in out.strip().splitlines()[1:]:
+        f = line.split()
+        rows[f[0]] = [float(v) for v in f[1:]]
+    return rows
+
+
+def test_cli_is_built():
+    assert os.access(CLI, os.X_OK), "spmvcomp_cli missing: run __graft_entry__.build()"
+
+
+def test_model_reproduces_the_paper_column():
+    """`model --bandwidth 75` -> 12.5 / 34.9 / 337.5 (+ pattern-values) (K13)."""
+    rc, out, _ = run("model", "--bandwidth", 75)
+    assert rc == 0
+    t = table(out)
+    assert [t[k][0] for k in ("ell", "vt", "pattern", "pattern-values")] == [324.0, 116.0, 12.0, 4.0]
+    assert t["ell"][2] == 12.5 and abs(t["vt"][2] - 34.9) < 0.05 and t["pattern"][2] == 337.5 and t["pattern-values"][2] == 1012.5
+    rc, out2, _ = run("model", "--bandwidth", 150)
+    t2 = table(out2)
+    assert all(abs(t2[k][2] - 2 * t[k][2]) < 1e-3 * t[k][2] for k in t)  # linearity
+    rc, out3, _ = run("model", "--bandwidth", 85, "--formats", "ell")
+    assert abs(table(out3)["ell"][2] - 14.17) < 0.005
+
+
+def test_generate_sizes_and_overflow_guard():
+    rc, out, _ = run("generate", "--grid", 4, 4, 4)
+    assert rc == 0 and json.loads(out)["rows"] == 64 and json.loads(out)["nnz"] == 1000
+    rc, out, _ = run("generate", "--grid", 1, 1, 1)
+    assert rc == 0 and json.loads(out) == {"grid": [1, 1, 1], "rows": 1, "nnz": 1, "csr_bytes": 28}
+    rc, _, err = run("generate", "--grid", 100000, 100000, 100000)
+    assert rc != 0 and "rows" in err  # SPEC.md:442 sizing error, nonzero exit
+
+
+def test_usage_errors_exit_2():
+    for args in (("frobnicate",), (), ("bench", "--grid", 4, 4), ("model",), ("bench", "--grid", 4, 4, 4, "--format", "csr5"),
+                 ("solve", "--grid", 4, 4, 4, "--max-iter", 0)):
+        rc, _, err = run(*args)
+        assert rc == 2 and err, args
+
+
+@pytest.mark.gpu
+def test_bench_reports_and_compression_ratios():
+    reps = {}
+    for fmt in ("ell", "vt", "pattern", "pattern-values"):
+        rc, out, err = run("bench", "--grid", 32, 32, 32, "--format", fmt, "--reps", 10)
+        assert rc == 0, err
+        reps[fmt] = json.loads(out)
+        assert reps[fmt]["achieved_gflops"] > 0 and reps[fmt]["repetitions"] == 10
+        assert reps[fmt]["max_scaled_deviation_vs_ell"] <= 1e-12
+    assert abs(reps["vt"]["compression_ratio"] - 324 / 116) <= 0.02 * 324 / 116
+    assert abs(reps["pattern-values"]["compression_ratio"] - 81) <= 0.05 * 81
+    assert reps["pattern"]["compression_ratio"] == 27.0 and reps["ell"]["compression_ratio"] == 1.0
+    rc, out1, _ = run("bench", "--grid", 32, 32, 32, "--format", "vt", "--reps", 1)
+    assert json.loads(out1)["checksum"] == reps["vt"]["checksum"]                      # SPEC.md:452 determinism
+    rc, csv, _ = run("bench", "--grid", 16, 16, 16, "--format", "pattern", "--reps", 2, "--out", "csv")
+    head, row = csv.strip().splitlines()
+    assert rc == 0 and head.split(",")[:5] == ["format", "nx", "ny", "nz", "repetitions"] and row.startswith("pattern,16,16,16,2,")
+
+
+@pytest.mark.gpu
+def test_solve_backend_invariance_and_exit_codes():
+    its = {}
+    for backend in ("ell", "vt", "pattern"):
+        rc, out, err = run("solve", "--grid", 16, 16, 16, "--backend", backend, "--tol", 1e-8)
+        assert rc == 0, err
+        rep = json.loads(out)
+        assert rep["converged"] is True and rep["final_residual"] <= 1e-8
+        its[backend] = rep["iterations"]
+    assert its["ell"] == its["pattern"] == its["vt"]
+    rc, out, _ = run("solve", "--grid", 16, 16, 16, "--max-iter", 1)
+    assert rc == 1 and json.loads(out)["converged"] is False
+
+
+@pytest.mark.gpu
+def test_calibrate_reports_a_positive_stable_bandwidth():
+    a = json.loads(run("calibrate")[1])["device_stream_bandwidth_gbs"]
+    b = json.loads(run("calibrate")[1])["device_stream_bandwidth_gbs"]
+    assert a > 0 and abs(a - b) <= 0.2 * max(a, b)
