@@ -1,30 +1,31 @@
 // Pattern-format SpMV (inc/compress.hpp:48-76; inc/kernels.hpp:25,35-36; PAPER.md:797-813 List 1):
-// the "tensor ring" kernel.  x is viewed through a 3-D TMA tensor map [plane][line][column] whose
-// strides (sz, sy, 1) come from the dictionary's box plan; every warp owns a 64-column strip of Q
-// planes and marches over lines.  One elected lane fetches the next line set -- 68 columns x (Q+2)
-// planes, one cp.async.bulk.tensor -- into the warp's private shared-memory ring several lines
-// ahead (completion on an mbarrier), and all lanes take the 27 operands of their rows from shared
-// memory with 128-bit loads.  No register window: ~100 registers, so 16-20 warps/SM keep tens of KB
-// in flight per SM without spending instructions on it.
+// the "tensor ring" kernel, the default for ranges of at least 8 planes.  x is viewed through a 3-D
+// TMA tensor map [plane][line][column] whose strides (sz, sy, 1) come from the dictionary's box plan;
+// every warp owns a 64-column strip of Q planes and marches over lines.  One elected lane fetches the
+// next line set -- 68 columns x (Q+2) planes of x and, through a second int32 view, the 72 x Q pattern
+// ids of that line, one cp.async.bulk.tensor each -- into the warp's private shared-memory ring
+// (completion on an mbarrier), and all lanes take the 27 operands of their rows from shared memory with
+// 128-bit loads.  No register window and no per-thread global loads.  DESIGN.md section 6 has the
+// measurements, the ablations and the dead ends.
 //
 // Alignment.  A TMA box must start on a 16-byte boundary, i.e. at an even column, and a thread wants
 // its four operands (columns a-1 .. a+2 for its rows a, a+1) as two aligned 128-bit shared loads.
 // Both hold when a is odd: strip s covers columns 64s-1 .. 64s+62 and its box starts at 64s-2.
 // Column -1 of strip 0 is a dummy; the columns past the last strip (one column when 64 | sy) are
-// served by a few extra CTAs with List 1 as written.
+// summed row by row from global memory after the marches.
 //
 // Exactness.  Elements outside the tensor view are zero-filled by the TMA unit.  A row whose
 // dictionary mask is exactly "the full box minus the entries that fall outside the view" is
 // therefore served by the plain 27-term chain: absent operands are +0.0 and leave the accumulator
 // unchanged bit for bit (it can never be -0.0).  That is every row of a stencil matrix whose x view
-// is aligned with the grid.  Any other row (another dictionary pattern, a sub-box whose missing
-// entries are inside the view, a view that is not aligned with the grid) is recomputed per lane
-// by List 1 as written, so the result is always the reference's order.  Exception rows (id -1)
-// are left to the exception block, as in the other kernels.
+// is aligned with the grid.  A row whose entries are another sub-box inside the view is summed again
+// with every operand selected by its mask bit; any other row (another dictionary pattern, entries
+// outside the view, a view that is not aligned with the grid) is recomputed by List 1 as written, so
+// the result is always the reference's order.  Exception rows (id -1) are left to the exception
+// block, as in the other kernels.
 #include <cuda.h>  // CUtensorMap and enums only; the encoder is resolved through the runtime (no -lcuda)
 
 #include <algorithm>
-#include <type_traits>
 
 #include "pattern_kernels.cuh"
 #include "spmv_internal.cuh"
@@ -121,369 +122,6 @@ __device__ __noinline__ void ring_masked_step(uint32_t sl0, uint32_t sl1, uint32
         for (int i = 0; i < 2; i++) out[q * 2 + i] = CENTER_POS == 1 ? __dadd_rn(acc[q][i], xc[q][i]) : acc[q][i];
 }
 
-// gridDim.x = strip CTAs (4 strips each) + one CTA column for the left-over columns [left_lo, sy) when there are any
-template <int Q, int S, int MINB, bool OFF_NEG1, int CENTER_POS, int DB = 1, int PF = 1, int IDA = 2>
-__global__ void __launch_bounds__(kRingWarps * 32, MINB)
-    spmv_pattern_ring_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm_ids, PatternArgs p, int c_lo,
-                             int c_hi, int np_x, int R, int n_strips, int left_lo, int id_plane0) {
-    constexpr bool IDT = IDA == 0;  // ids through the ring (their own tensor view) instead of per-thread loads
-    using L = RingLayout<Q, S, IDT>;
-    constexpr int P = L::P;
-    extern __shared__ unsigned char smem_raw[];
-    const uint32_t sbase = (smem_u32(smem_raw) + 127u) & ~127u;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int sy = p.sy, pl = p.plane_lines;
-    const int sz = sy * pl;
-    const int b0 = blockIdx.y * R;
-    // plane groups: the last one first, then 0, 1, ... (the groups on the grid faces may take the slower paths)
-    const int c0 = c_lo + (int)((blockIdx.z + gridDim.z - 1) % gridDim.z) * Q;
-    const int nb = min(R, pl - b0);
-    const int rb = p.row_begin;
-    const unsigned n_range = (unsigned)(p.row_end - p.row_begin);
-
-    if ((int)blockIdx.x * kRingWarps >= n_strips) {  // left-over columns, thread per row
-        const int n_left = sy - left_lo;
-        for (int t = threadIdx.x; t < n_left * nb * Q; t += kRingWarps * 32) {
-            const int col = left_lo + t % n_left, line = b0 + (t / n_left) % nb, c = c0 + t / (n_left * nb);
-            if (c > c_hi) break;
-            const int64_t xi = col + (int64_t)sy * line + (int64_t)sz * c;
-            const int64_t row = xi - p.g0;
-            if (row < rb || row >= p.row_end) continue;
-            const int id = p.ids[row];
-            if (id < 0) continue;
-            const uint32_t m = p.masks[id];
-            const uint32_t oob = (col == 0 ? kLBits : 0u) | (col == sy - 1 ? kRBits : 0u) | (line == 0 ? kDyLoBits : 0u) |
-                                 (line == pl - 1 ? kDyHiBits : 0u) | (c == 0 ? kDzLoBits : 0u) | (c == np_x - 1 ? kDzHiBits : 0u);
-            if (c < np_x && m == (kFullBox & ~oob)) {
-                // same rule as the strips: the row's entries are exactly the in-view box entries; all gathers in one batch
-                double xv[27];
-#pragma unroll
-                for (int e = 0; e < 27; e++)
-                    xv[e] = (m >> e & 1u) ? __ldg(p.x + (xi + (e % 3 - 1) + (int64_t)sy * ((e / 3) % 3 - 1) + (int64_t)sz * (e / 9 - 1))) : 0.0;
-                double acc = 0.0;
-                if (CENTER_POS == 0) acc = __dadd_rn(acc, __dmul_rn(p.v_center, xv[13]));
-#pragma unroll
-                for (int e = 0; e < 27; e++) {
-                    if (e == 13) {
-                        if (CENTER_POS == 2) acc = __dadd_rn(acc, __dmul_rn(p.v_center, xv[13]));
-                    } else if (OFF_NEG1) {
-                        acc = __dsub_rn(acc, xv[e]);
-                    } else {
-                        acc = __dadd_rn(acc, __dmul_rn(p.v_off, xv[e]));
-                    }
-                }
-                if (CENTER_POS == 1) acc = __dadd_rn(acc, __dmul_rn(p.v_center, xv[13]));
-                p.y[row] = acc;
-            } else {
-                p.y[row] = pattern_row(p, p.disp, p.ends, p.table, id, xi);
-            }
-        }
-        return;
-    }
-
-    const uint32_t ring = sbase + warp * (S * L::kSlotBytes);
-    const uint32_t bars = sbase + L::kRingBytes + warp * (S * 8);
-    const uint32_t s_masks = sbase + L::kRingBytes + L::kBarBytes;  // entry 0 serves id = -1
-    for (int i = threadIdx.x; i <= p.n_patterns; i += kRingWarps * 32) sts_u32(s_masks + 4 * i, i == 0 ? 0u : p.masks[i - 1]);
-    if (lane == 0) {
-#pragma unroll
-        for (int s = 0; s < S; s++) mbar_init(bars + 8 * s, 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-
-    const int strip = blockIdx.x * kRingWarps + warp;
-    if (strip >= n_strips) return;  // no CTA barrier below this point
-    const int a_w = strip * kStripCols - 1;  // first column of the warp's strip (odd; -1 for strip 0)
-    const int n_sets = nb + 2;               // line sets b0-1 .. b0+nb
-
-    auto issue = [&](int k) {  // elected lane: line set k -> slot k % S
-        const uint32_t bar = bars + 8 * (k % S);
-        mbar_expect_tx(bar, L::kSetBytes);
-        tma_load_3d(ring + (k % S) * L::kSlotBytes, &tm, a_w - 1, b0 - 1 + k, c0 - 1, bar);
-        if (IDT) tma_load_3d(ring + (k % S) * L::kSlotBytes + L::kXBytes, &tm_ids, a_w - 3, b0 - 1 + k, c0 - id_plane0, bar);
-    };
-    if (lane == 0)
-        for (int k = 0; k < S && k < n_sets; k++) issue(k);
-
-    // per-thread geometry: columns a, a+1 (a odd); the row of (column a, line b0 + j, plane c0 + q) is row0 + q*sz + j*sy
-    const int a = a_w + 2 * lane;
-    const int64_t xi0 = a + (int64_t)sy * b0 + (int64_t)sz * c0;
-    const int row0 = (int)(xi0 - p.g0);
-    bool ok[Q][2];           // the row's column and plane exist
-    uint32_t expect[Q][2];   // dictionary mask the plain chain is exact for, before the line term; 0 for rows that do not exist
-#pragma unroll
-    for (int q = 0; q < Q; q++) {
-        const int c = c0 + q;
-        const uint32_t oob_c = (c == 0 ? kDzLoBits : 0u) | (c == np_x - 1 ? kDzHiBits : 0u);
-#pragma unroll
-        for (int i = 0; i < 2; i++) {
-            const uint32_t oob_a = (a + i == 0 ? kLBits : 0u) | (a + i == sy - 1 ? kRBits : 0u);
-            ok[q][i] = a + i >= 0 && a + i < sy && c <= c_hi;
-            expect[q][i] = (c >= np_x || !ok[q][i]) ? 0u : (kFullBox & ~(oob_a | oob_c));
-        }
-    }
-    const int32_t *__restrict__ ids = p.ids;
-    double *__restrict__ y = p.y;
-    // -1: no such row here (computed on whatever the ring holds, never stored)
-    auto load_id = [&](int q, int i, int j) {
-        const int r = row0 + q * sz + j * sy + i;
-        return (ok[q][i] && j < nb && (unsigned)(r - rb) < n_range) ? __ldg(ids + r) : -1;
-    };
-    if (PF && !IDT) {  // pull the tile's id rows into L2 while the first line sets are in flight (3 points cover a 256-byte row)
-        const int r_strip = row0 - 2 * lane + (a_w < 0 ? 1 : 0);
-        for (int t = lane; t < nb * Q * 3; t += 32) {
-            const int r = r_strip + (t / 3 % nb) * sy + (t / (3 * nb)) * sz + (t % 3) * 31;
-            if ((unsigned)(r - rb) < n_range) prefetch_l2(ids + r);
-        }
-    }
-    int idn[Q][2], idn2[Q][2];  // ids of the next two lines (IDA = 2: the id stream is fetched two steps ahead)
-    if (!IDT) {
-#pragma unroll
-        for (int q = 0; q < Q; q++)
-#pragma unroll
-            for (int i = 0; i < 2; i++) {
-                idn[q][i] = load_id(q, i, 0);
-                if (IDA == 2) idn2[q][i] = load_id(q, i, 1);
-            }
-    }
-    // the id of (plane q, column i) of line b0 + j: from the ring (set j+1 carries the ids of its line) or the registers
-    auto ring_id = [&](int q, int i, int j) {  // IDT: id of line b0 + j, read from set j + 1
-        const int r = row0 + q * sz + j * sy + i;
-        const int v = (int)lds_u32(ring + ((j + 1) % S) * L::kSlotBytes + L::kXBytes + q * L::kIdLineBytes + (3 + 2 * lane + i) * 4);
-        return (ok[q][i] && (unsigned)(r - rb) < n_range) ? v : -1;
-    };
-    auto next_id = [&](int q, int i, int j) {
-        if (IDT) {
-            if (DB != 2) return ring_id(q, i, j);
-            // window variant: the slot of set j+1 was released a step ago; ids are taken one step early, with the window line
-            const int v = idn[q][i];
-            idn[q][i] = ring_id(q, i, j + 1);
-            return v;
-        }
-        const int v = idn[q][i];
-        if (IDA == 2) idn[q][i] = idn2[q][i], idn2[q][i] = load_id(q, i, j + 2);
-        else idn[q][i] = load_id(q, i, j + 1);
-        return v;
-    };
-    const double vc = p.v_center, vo = p.v_off;
-    const uint32_t lane_off = lane * 16;
-
-    if constexpr (DB == 2) {
-        // Register window: the x values of lines b-1, b, b+1 x P planes x 4 columns stay in registers and only the
-        // new line is read from the ring each step (one third of the shared-memory traffic of the direct variant).
-        double w[3][P][4];
-        auto load_set = [&](auto slot, int k) {  // line set k: ring -> window slot
-            const uint32_t base = ring + (k % S) * L::kSlotBytes + lane_off;
-#pragma unroll
-            for (int pz = 0; pz < P; pz++) {
-                const double2 u = lds_f64x2(base + pz * L::kLineBytes), v = lds_f64x2(base + pz * L::kLineBytes + 16);
-                w[decltype(slot)::value][pz][0] = u.x, w[decltype(slot)::value][pz][1] = u.y;
-                w[decltype(slot)::value][pz][2] = v.x, w[decltype(slot)::value][pz][3] = v.y;
-            }
-        };
-        auto refill = [&](int k) {  // the slot of set k has been consumed
-            if (k + S < n_sets) issue(k + S);
-        };
-        mbar_wait(bars + 0, 0);
-        load_set(std::integral_constant<int, 0>{}, 0);
-        mbar_wait(bars + 8 * (1 % S), (1 / S) & 1);
-        load_set(std::integral_constant<int, 1>{}, 1);
-        if (IDT) {
-#pragma unroll
-            for (int q = 0; q < Q; q++)
-#pragma unroll
-                for (int i = 0; i < 2; i++) idn[q][i] = ring_id(q, i, 0);
-        }
-        auto step = [&](auto uc, int j) {
-            constexpr int u = decltype(uc)::value;  // j % 3: lines b-1, b, b+1 sit in window slots u, u+1, u+2 (mod 3)
-            const int b = b0 + j;
-            mbar_wait(bars + 8 * ((j + 2) % S), ((j + 2) / S) & 1);
-            load_set(std::integral_constant<int, (u + 2) % 3>{}, j + 2);
-            int id[Q][2];
-            uint32_t bad = 0;
-            const uint32_t in_b = ~((b == 0 ? kDyLoBits : 0u) | (b == pl - 1 ? kDyHiBits : 0u));
-#pragma unroll
-            for (int q = 0; q < Q; q++)
-#pragma unroll
-                for (int i = 0; i < 2; i++) {
-                    id[q][i] = next_id(q, i, j);
-                    bad |= lds_u32(s_masks + 4 + 4 * id[q][i]) ^ (expect[q][i] & in_b);  // id -1 reads entry 0 = 0
-                }
-            double acc[Q][2];
-#pragma unroll
-            for (int q = 0; q < Q; q++) acc[q][0] = acc[q][1] = 0.0;
-            auto centre = [&]() {
-#pragma unroll
-                for (int q = 0; q < Q; q++)
-#pragma unroll
-                    for (int i = 0; i < 2; i++) acc[q][i] = __dadd_rn(acc[q][i], __dmul_rn(vc, w[(u + 1) % 3][q + 1][i + 1]));
-            };
-            if (CENTER_POS == 0) centre();
-#pragma unroll
-            for (int t = 0; t < 27; t++) {
-                if (t == 13 && CENTER_POS != 2) continue;
-                const int dz = t / 9, dy = (t / 3) % 3, dx = t % 3;
-#pragma unroll
-                for (int q = 0; q < Q; q++)
-#pragma unroll
-                    for (int i = 0; i < 2; i++) {
-                        const double ev = w[(u + dy) % 3][q + dz][i + dx];
-                        if (t == 13) acc[q][i] = __dadd_rn(acc[q][i], __dmul_rn(vc, ev));
-                        else if (OFF_NEG1) acc[q][i] = __dsub_rn(acc[q][i], ev);
-                        else acc[q][i] = __dadd_rn(acc[q][i], __dmul_rn(vo, ev));
-                    }
-            }
-            if (CENTER_POS == 1) centre();
-            __syncwarp();  // every lane has consumed the new line (its values fed this step's sums)
-            if (lane == 0) {
-                fence_proxy_async();  // generic-proxy reads before the async-proxy refill
-                if (j == 0) refill(0), refill(1);
-                refill(j + 2);
-            }
-            if (__any_sync(0xffffffffu, bad != 0)) {  // some row the plain chain may not be exact for: List 1 for those
-#pragma unroll
-                for (int q = 0; q < Q; q++)
-#pragma unroll
-                    for (int i = 0; i < 2; i++)
-                        if (id[q][i] >= 0 && lds_u32(s_masks + 4 + 4 * id[q][i]) != (expect[q][i] & in_b))
-                            acc[q][i] = pattern_row_cold(p, id[q][i], xi0 + (int64_t)j * sy + (int64_t)q * sz + i);
-            }
-#pragma unroll
-            for (int q = 0; q < Q; q++)
-#pragma unroll
-                for (int i = 0; i < 2; i++)
-                    if (id[q][i] >= 0) y[row0 + q * sz + j * sy + i] = acc[q][i];
-        };
-#pragma unroll 1
-        for (int j0 = 0; j0 < nb; j0 += 3) {
-            step(std::integral_constant<int, 0>{}, j0);
-            if (j0 + 1 < nb) step(std::integral_constant<int, 1>{}, j0 + 1);
-            if (j0 + 2 < nb) step(std::integral_constant<int, 2>{}, j0 + 2);
-        }
-        return;
-    }
-
-    mbar_wait(bars + 0, 0);
-    mbar_wait(bars + 8 * (1 % S), (1 / S) & 1);
-#pragma unroll 1
-    for (int j = 0; j < nb; j++) {
-        const int b = b0 + j;
-        mbar_wait(bars + 8 * ((j + 2) % S), ((j + 2) / S) & 1);
-        uint32_t sl[3];
-#pragma unroll
-        for (int dy = 0; dy < 3; dy++) sl[dy] = ring + ((j + dy) % S) * L::kSlotBytes + lane_off;
-        int id[Q][2];
-        uint32_t bad = 0;
-        const uint32_t in_b = ~((b == 0 ? kDyLoBits : 0u) | (b == pl - 1 ? kDyHiBits : 0u));
-#pragma unroll
-        for (int q = 0; q < Q; q++)
-#pragma unroll
-            for (int i = 0; i < 2; i++) {
-                id[q][i] = next_id(q, i, j);
-                bad |= lds_u32(s_masks + 4 + 4 * id[q][i]) ^ (expect[q][i] & in_b);  // id -1 reads entry 0 = 0
-            }
-        double acc[Q][2];
-        // The sums of the step.  Planes outermost, so that the Q rows of a thread consume each (plane, line) operand
-        // quad together; with DB the quads of plane pz+1 are fetched from shared memory while plane pz is being summed.
-        {
-            double xc[Q][2];
-#pragma unroll
-            for (int q = 0; q < Q; q++) acc[q][0] = acc[q][1] = 0.0;
-            if (CENTER_POS == 0) {
-#pragma unroll
-                for (int q = 0; q < Q; q++) {
-                    const double2 u = lds_f64x2(sl[1] + (q + 1) * L::kLineBytes), v = lds_f64x2(sl[1] + (q + 1) * L::kLineBytes + 16);
-                    acc[q][0] = __dadd_rn(acc[q][0], __dmul_rn(vc, u.y));
-                    acc[q][1] = __dadd_rn(acc[q][1], __dmul_rn(vc, v.x));
-                }
-            }
-            double e[2][3][4];  // [buffer][dy][columns a-1 .. a+2]
-            auto load_plane = [&](int buf, int pz) {
-#pragma unroll
-                for (int dy = 0; dy < 3; dy++) {
-                    const double2 u = lds_f64x2(sl[dy] + pz * L::kLineBytes), v = lds_f64x2(sl[dy] + pz * L::kLineBytes + 16);
-                    e[buf][dy][0] = u.x, e[buf][dy][1] = u.y, e[buf][dy][2] = v.x, e[buf][dy][3] = v.y;
-                }
-            };
-            if (DB == 1) load_plane(0, 0);
-#pragma unroll
-            for (int pz = 0; pz < P; pz++) {
-                if (DB == 1) {
-                    if (pz + 1 < P) load_plane((pz + 1) & 1, pz + 1);
-                } else {
-                    load_plane(pz & 1, pz);
-                }
-#pragma unroll
-                for (int dy = 0; dy < 3; dy++)
-#pragma unroll
-                    for (int dx = 0; dx < 3; dx++)
-#pragma unroll
-                        for (int q = 0; q < Q; q++) {
-                            const int dz = pz - q;
-                            if (dz < 0 || dz > 2) continue;
-                            const int t = dz * 9 + dy * 3 + dx;
-#pragma unroll
-                            for (int i = 0; i < 2; i++) {
-                                const double ev = e[pz & 1][dy][i + dx];
-                                if (t == 13) {
-                                    if (CENTER_POS == 2) acc[q][i] = __dadd_rn(acc[q][i], __dmul_rn(vc, ev));
-                                    else xc[q][i] = ev;
-                                } else if (OFF_NEG1) {
-                                    acc[q][i] = __dsub_rn(acc[q][i], ev);
-                                } else {
-                                    acc[q][i] = __dadd_rn(acc[q][i], __dmul_rn(vo, ev));
-                                }
-                            }
-                        }
-            }
-            if (CENTER_POS == 1) {
-#pragma unroll
-                for (int q = 0; q < Q; q++)
-#pragma unroll
-                    for (int i = 0; i < 2; i++) acc[q][i] = __dadd_rn(acc[q][i], __dmul_rn(vc, xc[q][i]));
-            }
-        }
-        if (__any_sync(0xffffffffu, bad != 0)) {
-            // Some row the plain chain may not be exact for.  Sub-boxes whose entries are all inside the view (e.g. the
-            // grid faces when x carries ghost planes beyond them): the sums again with every operand selected by the
-            // row's mask.  Rows of other patterns, or with entries outside the view: List 1 as written.
-            uint32_t mk[Q * 2];
-            bool real = false;  // rows without an id (exception rows, range ends) raise the flag too, but need nothing
-#pragma unroll
-            for (int q = 0; q < Q; q++)
-#pragma unroll
-                for (int i = 0; i < 2; i++) {
-                    mk[q * 2 + i] = lds_u32(s_masks + 4 + 4 * id[q][i]);
-                    real = real || (id[q][i] >= 0 && mk[q * 2 + i] != (expect[q][i] & in_b));
-                }
-            if (__any_sync(0xffffffffu, real)) {
-                double am[Q * 2];
-                ring_masked_step<Q, OFF_NEG1, CENTER_POS, L::kLineBytes>(sl[0], sl[1], sl[2], mk, vc, vo, am);
-#pragma unroll
-                for (int q = 0; q < Q; q++)
-#pragma unroll
-                    for (int i = 0; i < 2; i++) {
-                        const uint32_t m = mk[q * 2 + i];
-                        if (id[q][i] >= 0 && (m == kGenericMask || (m & ~(expect[q][i] & in_b)) != 0))
-                            am[q * 2 + i] = pattern_row_cold(p, id[q][i], xi0 + (int64_t)j * sy + (int64_t)q * sz + i);
-                        acc[q][i] = am[q * 2 + i];
-                    }
-            }
-        }
-        __syncwarp();  // every lane is done with the slot of line b-1
-        if (lane == 0 && j + S < n_sets) {
-            fence_proxy_async();  // generic-proxy reads before the async-proxy refill
-            issue(j + S);
-        }
-#pragma unroll
-        for (int q = 0; q < Q; q++)
-#pragma unroll
-            for (int i = 0; i < 2; i++)
-                if (id[q][i] >= 0) y[row0 + q * sz + j * sy + i] = acc[q][i];
-    }
-}
-
 // -----------------------------------------------------------------------------------------
 // Persistent form of the direct variant (the default).  The (strip, plane group) columns of the
 // view, pl lines each, form one sequence of line steps; it is cut into equal contiguous chunks,
@@ -533,7 +171,7 @@ __device__ __forceinline__ void ring_leftover_row(const PatternArgs &p, uint32_t
 template <int Q, int S, int MINB, bool OFF_NEG1, int CENTER_POS, bool IDT, int PFD = 0, int DBG = 0, bool CTAC = false>
 __global__ void __launch_bounds__(kRingWarps * 32, MINB)
     spmv_pattern_ringp_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm_ids, PatternArgs p, int c_lo,
-                              int c_hi, int np_x, int n_strips, int left_lo, int id_plane0, int total_steps, int steps_per_warp) {
+                              int c_hi, int np_x, int n_strips, int left_lo, int id_plane0, int total_steps, int steps_per_warp, int tile_lines) {
     using L = RingLayout<Q, S, IDT>;
     constexpr int P = L::P;
     extern __shared__ unsigned char smem_raw[];
@@ -561,23 +199,36 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
     const double vc = p.v_center, vo = p.v_off;
     const uint32_t lane_off = lane * 16;
     uint32_t gs = 0;  // sets issued so far by this warp: slot = set number % S, parity = (set number / S) & 1
-    bool first = true;
-    // CTAC: the chunk belongs to the CTA and its four warps take the four strips of the same lines (they then read
-    // whole contiguous lines of x together); otherwise every warp has a chunk of its own.
-    int s_pos = (CTAC ? (int)blockIdx.x : gw) * steps_per_warp;
+    // CTAC: a work unit belongs to the CTA and its four warps take the four strips of the same lines (they then read
+    // whole contiguous lines of x together); otherwise every warp has units of its own.
+    // tile_lines == 0: one contiguous chunk of the column-major step sequence per unit (steps_per_warp steps);
+    // tile_lines  > 0: tiles of that many lines, columns fastest, dealt out round-robin -- the tiles in flight then
+    //                  stay within a few plane groups of each other (halo planes are re-read from L2).
+    const int me = CTAC ? (int)blockIdx.x : gw, n_me = CTAC ? (int)gridDim.x : n_warps;
+    const int n_cols = (CTAC ? n_sg : n_strips) * ((c_hi - c_lo + Q) / Q);
+    const int n_tiles = tile_lines > 0 ? n_cols * ((pl + tile_lines - 1) / tile_lines) : 0;
+    int tile = me;
+    int s_pos = me * steps_per_warp;
     const int s_end = min(total_steps, s_pos + steps_per_warp);
 #pragma unroll 1
-    while (s_pos < s_end || first) {
-        const bool have = s_pos < s_end;
-        const int col_idx = have ? s_pos / pl : 0;
-        const int b0 = have ? s_pos - col_idx * pl : 0;
-        const int nb = have ? min(pl - b0, s_end - s_pos) : 0;
+    while (true) {
+        int col_idx, b0, nb;
+        if (tile_lines > 0) {
+            if (tile >= n_tiles) break;
+            col_idx = tile % n_cols;
+            b0 = (tile / n_cols) * tile_lines;
+            nb = min(tile_lines, pl - b0);
+            tile += n_me;
+        } else {
+            if (s_pos >= s_end) break;
+            col_idx = s_pos / pl;
+            b0 = s_pos - col_idx * pl;
+            nb = min(pl - b0, s_end - s_pos);
+            s_pos += nb;
+        }
         const int strip = CTAC ? (col_idx % n_sg) * kRingWarps + warp : col_idx % n_strips;
         const int c0 = c_lo + (col_idx / (CTAC ? n_sg : n_strips)) * Q;
-        if (CTAC && have && strip >= n_strips) {  // no such strip in this group: nothing to march, but the left-over share remains
-            s_pos += nb;
-            if (s_pos < s_end || !first) continue;
-        }
+        if (CTAC && strip >= n_strips) continue;  // no such strip in this group
         const int a_w = strip * kStripCols - 1;  // first column of the strip (odd; -1 for strip 0)
         const int n_sets = nb + 2;               // line sets b0-1 .. b0+nb
         auto issue = [&](int k) {  // elected lane: line set k of this march -> slot (gs + k) % S
@@ -590,14 +241,10 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
             tma_prefetch_3d(&tm, a_w - 1, b0 - 1 + k, c0 - 1);
             if (IDT) tma_prefetch_3d(&tm_ids, a_w - 3, b0 - 1 + k, c0 - id_plane0);
         };
-        if (have && lane == 0) {
+        if (lane == 0) {
             for (int k = 0; k < S && k < n_sets; k++) issue(k);
             if (PFD > 0 && PFD < 9)
                 for (int k = S; k < S + PFD && k < n_sets; k++) prefetch(k);
-        }
-        if (first) {
-            first = false;
-            if (!have) break;
         }
 
         // per-thread geometry: columns a, a+1 (a odd); the row of (column a, line b0 + j, plane c0 + q) is row0 + q*sz + j*sy
@@ -779,7 +426,6 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
                     }
         }
         gs += n_sets;
-        s_pos += nb;
         __syncwarp();
     }
     {  // this warp's share of the left-over columns (after its marches: the warps do not finish in step, so these
@@ -869,57 +515,8 @@ static bool ids_view_ok(const spmvb_matrix *a, const PatternArgs &p) {
     return p.g0 >= 0 && p.g0 % sz == 0 && (int64_t)a->n % sz == 0 && p.sy % 4 == 0 && (uintptr_t)p.ids % 16 == 0;
 }
 
-template <int Q, int S, int MINB, bool ALLV, int DB = 1, int PF = 1, int IDA = 2>
-static int launch_ring_t(const spmvb_matrix *a, PatternArgs &p_in, int R, cudaStream_t st) {
-    PatternArgs p = clip_view(a, p_in);
-    using L = RingLayout<Q, S, IDA == 0>;
-    const bool neg1 = p.v_off == -1.0;
-    const int cp = a->box.center_pos;
-    if (!ALLV && !(neg1 && cp == 1)) return 1;
-    if (IDA == 0 && !ids_view_ok(a, p)) return 1;
-    const int64_t sz = (int64_t)p.sy * p.plane_lines;
-    const int np_x = (int)(p.x_len / sz);
-    const int c_lo = (int)((p.g0 + p.row_begin) / sz), c_hi = (int)((p.g0 + p.row_end - 1) / sz);
-    const int id_plane0 = (int)(p.g0 / sz);
-    CUtensorMap tm, tm_ids;
-    if (make_view_map(0, p.x, p.sy, p.plane_lines, np_x, kBoxCols, Q + 2, &tm) != SPMVB_OK) return -1;
-    if (IDA == 0) {
-        if (make_view_map(1, p.ids, p.sy, p.plane_lines, (int)(a->n / sz), kIdBoxCols, Q, &tm_ids) != SPMVB_OK) return -1;
-    } else {
-        tm_ids = tm;  // unused
-    }
-    // strips start at column -1; a partial last strip is used unless at most two columns are left over
-    int n_strips = (p.sy + 1) / kStripCols;
-    if (p.sy - (n_strips * kStripCols - 1) > 2) n_strips++;
-    const int left_lo = std::min(p.sy, n_strips * kStripCols - 1);
-    dim3 grid((n_strips + kRingWarps - 1) / kRingWarps + (left_lo < p.sy ? 1 : 0), (p.plane_lines + R - 1) / R, (c_hi - c_lo + Q) / Q);
-    dim3 block(kRingWarps * 32);
-#define LAUNCH_RING(NEG, CP)                                                                                                  \
-    do {                                                                                                                       \
-        static bool attr = false;                                                                                              \
-        if (!attr) {                                                                                                           \
-            if (cudaFuncSetAttribute(spmv_pattern_ring_kernel<Q, S, MINB, NEG, CP, DB, PF, IDA>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                     (int)L::kTotal) != cudaSuccess)                                                           \
-                return -1;                                                                                                     \
-            attr = true;                                                                                                       \
-        }                                                                                                                      \
-        spmv_pattern_ring_kernel<Q, S, MINB, NEG, CP, DB, PF, IDA><<<grid, block, L::kTotal, st>>>(tm, tm_ids, p, c_lo, c_hi, np_x, R, n_strips, left_lo, id_plane0);             \
-    } while (0)
-    if constexpr (ALLV) {
-        if (neg1) {
-            if (cp == 0) LAUNCH_RING(true, 0); else if (cp == 1) LAUNCH_RING(true, 1); else LAUNCH_RING(true, 2);
-        } else {
-            if (cp == 0) LAUNCH_RING(false, 0); else if (cp == 1) LAUNCH_RING(false, 1); else LAUNCH_RING(false, 2);
-        }
-    } else {
-        LAUNCH_RING(true, 1);
-    }
-#undef LAUNCH_RING
-    return check_launch("spmv_pattern_ring") == SPMVB_OK ? 0 : -1;
-}
-
 template <int Q, int S, int MINB, bool IDT, int PFD = 0, int DBG = 0, bool CTAC = false>
-static int launch_ringp_t(const spmvb_matrix *a, PatternArgs &p_in, int chunk, cudaStream_t st) {
+static int launch_ringp_t(const spmvb_matrix *a, PatternArgs &p_in, int chunk, cudaStream_t st, int tile_lines = 0) {
     PatternArgs p = clip_view(a, p_in);
     using L = RingLayout<Q, S, IDT>;
     const bool neg1 = p.v_off == -1.0;
@@ -963,11 +560,15 @@ static int launch_ringp_t(const spmvb_matrix *a, PatternArgs &p_in, int chunk, c
                 return -1;                                                                                                       \
         }                                                                                                                        \
         int grid = n_sm * per_sm;                                                                                                \
-        grid = std::max(1, std::min(grid, (total + min_steps * units - 1) / (min_steps * units)));                              \
+        if (tile_lines > 0) {                                                                                                    \
+            const int n_tiles = n_cols * ((c_hi - c_lo + Q) / Q) * ((p.plane_lines + tile_lines - 1) / tile_lines);              \
+            grid = std::max(1, std::min(grid, (n_tiles + units - 1) / units));                                                   \
+        } else                                                                                                                   \
+            grid = std::max(1, std::min(grid, (total + min_steps * units - 1) / (min_steps * units)));                          \
         const int spw = chunk > 0 ? chunk : (total + grid * units - 1) / (grid * units);                                         \
         if (chunk > 0) grid = (total + spw * units - 1) / (spw * units);                                                         \
         spmv_pattern_ringp_kernel<Q, S, MINB, NEG, CP, IDT, PFD, DBG, CTAC><<<grid, kRingWarps * 32, L::kTotal, st>>>(                          \
-            tm, tm_ids, p, c_lo, c_hi, np_x, n_strips, left_lo, id_plane0, total, spw);                                          \
+            tm, tm_ids, p, c_lo, c_hi, np_x, n_strips, left_lo, id_plane0, total, spw, tile_lines);                                          \
     } while (0)
     if (neg1) {
         if (cp == 0) LAUNCH_RINGP(true, 0); else if (cp == 1) LAUNCH_RINGP(true, 1); else LAUNCH_RINGP(true, 2);
@@ -987,18 +588,12 @@ bool ring_ok(const spmvb_matrix *a, const PatternArgs &p) {
            p.g0 > -(int64_t)INT32_MAX / 2 && p.g0 < INT32_MAX / 2;
 }
 
-// which: 0 = default configuration; others are measured alternatives (profiles/r01_probe256_tensor_ring*.log).
-// `lines` = lines per CTA march (0 = default).
+// which: 0 = default configuration; others are measured alternatives and ablations (profiles/r01_probe256_ring_ablations.log,
+// r01_probe_shapes_tensor_ring.log).  `lines` = chunk length (contiguous schedule) or tile length (round-robin schedule).
 int launch_pattern_ring(int which, int lines, const spmvb_matrix *a, PatternArgs &p, cudaStream_t st) {
-    const int R = lines > 0 ? lines : 16;
     int rc = 1;
+    const int tl = lines > 0 ? lines : 16;
     switch (which) {
-        case 1: return launch_ring_t<2, 6, 4, false>(a, p, R, st);  // 2 planes/thread, 16 warps/SM, ids by per-thread loads  101-105 us
-        case 2: return launch_ring_t<4, 5, 3, true>(a, p, R, st);   // 4 planes/thread, 12 warps/SM, ids by per-thread loads   93-96 us
-        case 3:                                                     // register window fed by the ring                       100-107 us
-            rc = launch_ring_t<2, 5, 3, false, 2, 0, 0>(a, p, R, st);
-            return rc == 1 ? launch_ring_t<2, 6, 3, false, 2, 1, 1>(a, p, R, st) : rc;
-        case 4: return launch_ring_t<2, 6, 3, false, 2, 1, 1>(a, p, R, st);
         case 6: return launch_ringp_t<4, 4, 3, true, 2>(a, p, lines, st);     // + TMA L2 prefetch 2 sets ahead: 95 us (4 ahead: 105 us)
         case 7: return launch_ringp_t<4, 4, 3, true, 0, 1>(a, p, lines, st);  // measurement only (wrong results): no FP64 chains
         case 8: return launch_ringp_t<4, 4, 3, true, 0, 2>(a, p, lines, st);  // measurement only (wrong results): one operand quad per step
@@ -1007,25 +602,29 @@ int launch_pattern_ring(int which, int lines, const spmvb_matrix *a, PatternArgs
         case 11:  // a chunk per warp instead of per CTA: 87 us
             rc = launch_ringp_t<4, 4, 3, true>(a, p, lines, st);
             return rc == 1 ? launch_ringp_t<4, 5, 3, false>(a, p, lines, st) : rc;
+        case 12: return launch_ringp_t<4, 4, 3, true, 0, 4, true>(a, p, lines, st);  // CTA chunks, fetch only
+        case 13: return launch_ringp_t<4, 4, 3, true, 0, 3, true>(a, p, lines, st);  // CTA chunks, fetch + store only
         case 14:  // CTA chunks, 2 planes/thread, 6 slots: 90 us
             rc = launch_ringp_t<2, 6, 3, true, 0, 0, true>(a, p, lines, st);
             return rc == 1 ? launch_ringp_t<4, 5, 3, false, 0, 0, true>(a, p, lines, st) : rc;
-        case 15: return launch_ringp_t<4, 4, 3, true, 9, 0, true>(a, p, lines, st);   // CTA chunks, streaming (evict-first) y stores
-        case 16: return launch_ringp_t<4, 4, 3, true, 0, 5, true>(a, p, lines, st);   // measurement only: no left-over columns
-        case 17: return launch_ringp_t<4, 5, 3, false, 0, 0, true>(a, p, lines, st);  // CTA chunks, 4 planes/thread, 5 slots, ids by loads
-        case 12: return launch_ringp_t<4, 4, 3, true, 0, 4, true>(a, p, lines, st);  // ... fetch only
-        case 13: return launch_ringp_t<4, 4, 3, true, 0, 3, true>(a, p, lines, st);  // ... fetch + store only
-        case 5:  // non-persistent form of the default (CTA tiles of R lines, dynamic CTA scheduling)                          88 us
-            rc = launch_ring_t<4, 4, 3, true, 1, 0, 0>(a, p, R, st);
-            return rc == 1 ? launch_ring_t<4, 5, 3, true>(a, p, R, st) : rc;
+        case 15: return launch_ringp_t<4, 4, 3, true, 9, 0, true>(a, p, lines, st);   // CTA chunks, streaming (evict-first) y stores: no change
+        case 16: return launch_ringp_t<4, 4, 3, true, 0, 5, true>(a, p, lines, st);   // measurement only: fetch only, no left-over columns
+        case 17: return launch_ringp_t<4, 5, 3, false, 0, 0, true>(a, p, lines, st);  // CTA chunks, 5 slots, ids by per-thread loads: 81 us
+        case 18:  // tiles of `lines` (default 16) lines dealt out round-robin, a tile per CTA: 85-87 us (512^3: 530-575 us)
+            rc = launch_ringp_t<4, 4, 3, true, 0, 0, true>(a, p, 0, st, tl);
+            return rc == 1 ? launch_ringp_t<4, 5, 3, false, 0, 0, true>(a, p, 0, st, tl) : rc;
+        case 19:  // ... a tile per warp
+            rc = launch_ringp_t<4, 4, 3, true>(a, p, 0, st, tl);
+            return rc == 1 ? launch_ringp_t<4, 5, 3, false>(a, p, 0, st, tl) : rc;
         default: {
-            // 4 planes/thread, 12 warps/SM; ids through the ring when their rows are whole planes of the view, else two
-            // steps ahead in registers.  Schedule (measured, profiles/r01_probe_shapes_tensor_ring.log):
-            //  * x (about) fits L2: persistent, one wave, equal chunks of line steps -- per CTA with its warps on the four
-            //    strips of the same lines when the strips come in fours (76 us at 256^3), else per warp (and only while x
-            //    is well inside L2);
-            //  * larger x: CTA tiles of 16 lines in launch order, which keeps the planes being read few enough for their
-            //    halo planes to be reused from L2 (512^3: 530 us vs 686 us persistent).
+            // 4 planes/thread, 12 warps/SM, one wave of persistent CTAs; ids through the ring when their rows are whole planes
+            // of the view, else two steps ahead in registers.  Schedule (measured per shape,
+            // profiles/r01_probe_shapes_tensor_ring.log):
+            //  * x (about) fits L2: the (strip group, plane group) x line sequence cut into equal contiguous chunks -- per CTA
+            //    with its warps on the four strips of the same lines when the strips come in fours (76 us at 256^3), else per
+            //    warp (and only while x is well inside L2);
+            //  * larger x: tiles of 16 lines, columns fastest, dealt out round-robin, which keeps the planes being read few
+            //    enough for their halo planes to be re-read from L2 (512^3: 530-575 us vs 686 us with contiguous chunks).
             static int l2_bytes = 0;
             if (l2_bytes == 0) {
                 int dev = 0;
@@ -1033,17 +632,16 @@ int launch_pattern_ring(int which, int lines, const spmvb_matrix *a, PatternArgs
             }
             int n_strips = (p.sy + 1) / kStripCols;
             if (p.sy - (n_strips * kStripCols - 1) > 2) n_strips++;
+            const bool fours = n_strips % kRingWarps == 0;
             const double x_bytes = (double)p.x_len * 8.0;
-            if (x_bytes > 1.25 * l2_bytes || (n_strips % kRingWarps != 0 && x_bytes > 0.8 * l2_bytes)) {
-                rc = launch_ring_t<4, 4, 3, true, 1, 0, 0>(a, p, R, st);
-                return rc == 1 ? launch_ring_t<4, 5, 3, true>(a, p, R, st) : rc;
+            const int tile_lines = (x_bytes > 1.25 * l2_bytes || (!fours && x_bytes > 0.8 * l2_bytes)) ? tl : 0;
+            const int chunk = tile_lines ? 0 : lines;
+            if (fours) {
+                rc = launch_ringp_t<4, 4, 3, true, 0, 0, true>(a, p, chunk, st, tile_lines);
+                return rc == 1 ? launch_ringp_t<4, 5, 3, false, 0, 0, true>(a, p, chunk, st, tile_lines) : rc;
             }
-            if (n_strips % kRingWarps == 0) {
-                rc = launch_ringp_t<4, 4, 3, true, 0, 0, true>(a, p, lines, st);
-                return rc == 1 ? launch_ringp_t<4, 5, 3, false, 0, 0, true>(a, p, lines, st) : rc;
-            }
-            rc = launch_ringp_t<4, 4, 3, true>(a, p, lines, st);
-            return rc == 1 ? launch_ringp_t<4, 5, 3, false>(a, p, lines, st) : rc;
+            rc = launch_ringp_t<4, 4, 3, true>(a, p, chunk, st, tile_lines);
+            return rc == 1 ? launch_ringp_t<4, 5, 3, false>(a, p, chunk, st, tile_lines) : rc;
         }
     }
 }

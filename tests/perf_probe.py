@@ -65,11 +65,15 @@ if "pattern" in fmts or "generic" in fmts:
     d = sp.upload_pattern(pc.n, pc.table, pc.disp_offsets, pc.disp_flat, pc.ends_flat, pc.row_pattern, True)
     ref = None
     if "pattern" in fmts:
-        for march, name in ((0, "default (persistent ring, CTA chunks)"), (3, "box3 <8,4,2,1,3>"), (1, "box3 R=16"), (5, "box3 Q=1 2 lines/step"), (12, "box3 full-line CTA"),
-                            (70, "box3 look-ahead 1"), (71, "box3 4 CTAs/SM 128 regs"), (72, "box3 look-ahead 1 168 regs"), (20, "box5 cp.async ring"), (35, "box6 4 cols/thread"),
+        for march, name in ((0, "default (tensor ring)"), (3, "sliding window box3 <8,4,2,1,3>"), (1, "box3 R=16"), (5, "box3 Q=1 2 lines/step"),
+                            (12, "box3 full-line CTA"), (70, "box3 look-ahead 1"), (20, "box5 cp.async ring"), (35, "box6 4 cols/thread"),
                             (30, "box6 8 cols/thread"), (47, "box7 pipelined ring"), (62, "box8 TMA ring 8w R=8"),
-                            (90, "ring persistent"), (95, "ring Q4 S4 tma-ids tiles"), (96, "ring persistent +L2pf2"), (97, "ABLATION no FP chains"), (98, "ABLATION one LDS quad/step"), (99, "ABLATION fetch+store only"), (100, "ABLATION fetch only"), (101, "ring persistent warp chunks"), (102, "ABLATION CTA chunks fetch only"), (103, "ABLATION CTA chunks fetch+store"), (104, "CTA chunks Q2 S6 12w"), (105, "CTA chunks st.cs stores"), (106, "ABLATION no leftover column"), (107, "CTA chunks Q4 S5 ldg-ids"), (91, "ring Q2 S6 ldg-ids"), (92, "ring Q4 S5 ldg-ids"), (93, "ring window Q2 S5 tma-ids"),
-                            (94, "ring window Q2 S6 ldg-ids")):
+                            (101, "ring: chunk per warp"), (108, "ring: round-robin tiles per CTA"), (109, "ring: round-robin tiles per warp"),
+                            (104, "ring: 2 planes/thread, 6 slots"), (107, "ring: 5 slots, ids by loads"), (96, "ring: + TMA L2 prefetch 2"),
+                            (105, "ring: st.cs stores"), (97, "ABLATION (chunk/warp) no FP chains"),
+                            (98, "ABLATION (chunk/warp) one LDS quad/step"), (99, "ABLATION (chunk/warp) fetch+store only"),
+                            (100, "ABLATION (chunk/warp) fetch only"), (103, "ABLATION fetch+store only"), (102, "ABLATION fetch only"),
+                            (106, "ABLATION fetch only, no left-over column")):
             if march >= 90 and ring_lines:
                 for ln in ring_lines:
                     timeit(d, f"pattern {name} R={ln}", 20, pattern_kernel=2, box_march=march, box_prefetch=2, box_lines=ln)
