@@ -91,7 +91,7 @@ static int launch_pattern(const spmvb_matrix *a, const double *x, int64_t x_col0
             bool ring = false;
             // tensor-ring kernel (spmv_pattern_tma.cu): default for ranges of at least 8 planes; 90..94 force a variant
             const int64_t planes = ((int64_t)row_end - row_begin) / ((int64_t)p.sy * p.plane_lines);
-            const bool want_ring = (o.box_march == 0 && planes >= 8) || (o.box_march >= 90 && o.box_march <= 110);
+            const bool want_ring = (o.box_march == 0 && planes >= 8) || (o.box_march >= 90 && o.box_march <= 120);
             if (o.pattern_kernel != 3 && want_ring && ring_ok(a, p)) {
                 rc3 = launch_pattern_ring(o.box_march >= 90 ? o.box_march - 90 : 0, o.box_lines, a, p, st);
                 if (rc3 < 0) return SPMVB_ERR_CUDA;

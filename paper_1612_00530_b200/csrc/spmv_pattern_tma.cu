@@ -579,6 +579,17 @@ static int launch_ringp_t(const spmvb_matrix *a, PatternArgs &p_in, int chunk, c
     return check_launch("spmv_pattern_ringp") == SPMVB_OK ? 0 : -1;
 }
 
+#ifdef SPMVB_RING_TU_Q6
+// Second translation unit (spmv_pattern_tma6.cu): the 6-planes-per-thread instantiations, so that the two halves build in parallel.
+// mode 0: chunk per CTA (with the ids-by-loads fallback); 1: per CTA, lab; 2: per warp, lab.
+int launch_ring_q6(int mode, const spmvb_matrix *a, PatternArgs &p, int chunk, cudaStream_t st, int tile_lines) {
+    if (mode == 2) return launch_ringp_t<6, 4, 2, true>(a, p, chunk, st, tile_lines);
+    const int rc = launch_ringp_t<6, 4, 2, true, 0, 0, true>(a, p, chunk, st, tile_lines);
+    return rc == 1 && mode == 0 ? launch_ringp_t<6, 5, 2, false, 0, 0, true>(a, p, chunk, st, tile_lines) : rc;
+}
+#else
+int launch_ring_q6(int mode, const spmvb_matrix *a, PatternArgs &p, int chunk, cudaStream_t st, int tile_lines);
+
 // Conditions: the TMA view needs a 16-byte aligned base, strides that are multiples of 16 bytes (even
 // sy), at least one whole plane of x and a line no narrower than a box; row arithmetic is 32-bit.
 bool ring_ok(const spmvb_matrix *a, const PatternArgs &p) {
@@ -613,16 +624,24 @@ int launch_pattern_ring(int which, int lines, const spmvb_matrix *a, PatternArgs
         case 18:  // tiles of `lines` (default 16) lines dealt out round-robin, a tile per CTA: 85-87 us (512^3: 530-575 us)
             rc = launch_ringp_t<4, 4, 3, true, 0, 0, true>(a, p, 0, st, tl);
             return rc == 1 ? launch_ringp_t<4, 5, 3, false, 0, 0, true>(a, p, 0, st, tl) : rc;
+        case 20:  // 4 planes/thread, 12 warps/SM, chunk per CTA (the default before 6 planes/thread): 77 us
+            rc = launch_ringp_t<4, 4, 3, true, 0, 0, true>(a, p, lines, st);
+            return rc == 1 ? launch_ringp_t<4, 5, 3, false, 0, 0, true>(a, p, lines, st) : rc;
+        // (3 / 5 / 7 / 8 planes per thread, chunk per CTA: 80.6 / 76.2 / 74.0 / 84.1 us at 256^3, r01_probe_planes_per_thread.log)
+        case 25: return launch_ring_q6(1, a, p, 0, st, tl);      // 6 planes/thread, round-robin tiles per CTA
+        case 26: return launch_ring_q6(2, a, p, lines, st, 0);   // 6 planes/thread, chunk per warp
+        case 27: return launch_ring_q6(2, a, p, 0, st, tl);      // 6 planes/thread, round-robin tiles per warp
         case 19:  // ... a tile per warp
             rc = launch_ringp_t<4, 4, 3, true>(a, p, 0, st, tl);
             return rc == 1 ? launch_ringp_t<4, 5, 3, false>(a, p, 0, st, tl) : rc;
         default: {
-            // 4 planes/thread, 12 warps/SM, one wave of persistent CTAs; ids through the ring when their rows are whole planes
-            // of the view, else two steps ahead in registers.  Schedule (measured per shape,
-            // profiles/r01_probe_shapes_tensor_ring.log):
+            // One wave of persistent CTAs; ids through the ring when their rows are whole planes of the view, else two steps
+            // ahead in registers.  Schedule and planes per thread (measured per shape,
+            // profiles/r01_probe_shapes_tensor_ring.log, r01_probe_planes_per_thread.log):
             //  * x (about) fits L2: the (strip group, plane group) x line sequence cut into equal contiguous chunks -- per CTA
-            //    with its warps on the four strips of the same lines when the strips come in fours (76 us at 256^3), else per
-            //    warp (and only while x is well inside L2);
+            //    with its warps on the four strips of the same lines when the strips come in fours (6 planes/thread, 8 warps/SM:
+            //    73 us at 256^3; 4 planes/thread, 12 warps/SM: 77 us), else per warp with 4 planes/thread (and only while x is
+            //    well inside L2);
             //  * larger x: tiles of 16 lines, columns fastest, dealt out round-robin, which keeps the planes being read few
             //    enough for their halo planes to be re-read from L2 (512^3: 530-575 us vs 686 us with contiguous chunks).
             static int l2_bytes = 0;
@@ -636,6 +655,9 @@ int launch_pattern_ring(int which, int lines, const spmvb_matrix *a, PatternArgs
             const double x_bytes = (double)p.x_len * 8.0;
             const int tile_lines = (x_bytes > 1.25 * l2_bytes || (!fours && x_bytes > 0.8 * l2_bytes)) ? tl : 0;
             const int chunk = tile_lines ? 0 : lines;
+            if (fours && tile_lines == 0) {  // 6 planes/thread at 8 warps/SM: 5-10 % faster than 4 at 12 on every shape tried
+                return launch_ring_q6(0, a, p, chunk, st, 0);
+            }
             if (fours) {
                 rc = launch_ringp_t<4, 4, 3, true, 0, 0, true>(a, p, chunk, st, tile_lines);
                 return rc == 1 ? launch_ringp_t<4, 5, 3, false, 0, 0, true>(a, p, chunk, st, tile_lines) : rc;
@@ -645,5 +667,7 @@ int launch_pattern_ring(int which, int lines, const spmvb_matrix *a, PatternArgs
         }
     }
 }
+
+#endif  // SPMVB_RING_TU_Q6
 
 }  // namespace spmvb

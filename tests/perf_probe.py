@@ -69,7 +69,7 @@ if "pattern" in fmts or "generic" in fmts:
                             (12, "box3 full-line CTA"), (70, "box3 look-ahead 1"), (20, "box5 cp.async ring"), (35, "box6 4 cols/thread"),
                             (30, "box6 8 cols/thread"), (47, "box7 pipelined ring"), (62, "box8 TMA ring 8w R=8"),
                             (101, "ring: chunk per warp"), (108, "ring: round-robin tiles per CTA"), (109, "ring: round-robin tiles per warp"),
-                            (104, "ring: 2 planes/thread, 6 slots"), (107, "ring: 5 slots, ids by loads"), (96, "ring: + TMA L2 prefetch 2"),
+                            (104, "ring: 2 planes/thread, 6 slots"), (110, "ring: 4 planes/thread 12w, chunk/CTA"), (115, "ring: 6 planes, rr tiles/CTA"), (116, "ring: 6 planes, chunk/warp"), (117, "ring: 6 planes, rr tiles/warp"), (107, "ring: 5 slots, ids by loads"), (96, "ring: + TMA L2 prefetch 2"),
                             (105, "ring: st.cs stores"), (97, "ABLATION (chunk/warp) no FP chains"),
                             (98, "ABLATION (chunk/warp) one LDS quad/step"), (99, "ABLATION (chunk/warp) fetch+store only"),
                             (100, "ABLATION (chunk/warp) fetch only"), (103, "ABLATION fetch+store only"), (102, "ABLATION fetch only"),

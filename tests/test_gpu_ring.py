@@ -7,7 +7,7 @@ pytestmark = pytest.mark.gpu
 
 from tests.test_gpu_parity import bits, run, sp, up_pat  # noqa: E402,F401
 
-RING = [90, 101, 104, 107, 108, 109]  # default schedule, chunk per warp, 2 planes/thread, ids by loads, round-robin tiles
+RING = [90, 101, 104, 107, 108, 109, 110]  # default schedule, chunk per warp, 2 planes/thread, ids by loads, round-robin tiles
 
 
 def ring_run(sp, d, x, march, lines=0, must_ring=True, **kw):
@@ -88,17 +88,18 @@ def test_ring_slab_with_ghost_planes(sp, orc, g):
         assert np.array_equal(bits(y), bits(full[r0:r1])), (z0, z1)
 
 
-def test_ring_misaligned_view_falls_back_per_row(sp, orc):
+@pytest.mark.parametrize("nx", [128, 256])  # 256: strips in fours -> 6 planes/thread, ids by per-thread loads
+def test_ring_misaligned_view_falls_back_per_row(sp, orc, nx):
     """x_col0 that is not a multiple of the plane: the zero-filled view disagrees with the masks of the
     rows on the view's faces, which must then be recomputed by List 1 -- same bits."""
-    nx, ny, nz = 128, 10, 9
+    ny, nz = 10, 9
     plane = nx * ny
     m = orc.generate_matrix(nx, ny, nz)
     x = orc.make_test_vector(m.n, orc.RANDOM, seed=8, lo=-1.0, hi=1.0)
     pc = orc.compress_patterns(m, True)
     full = orc.spmv(pc, x)
     r0, r1 = 3 * plane, 6 * plane
-    for g0 in (2 * plane - 2 * nx - 6, 2 * plane - 130, 2 * plane - 2):  # even offsets, not plane / line aligned
+    for g0 in (2 * plane - 2 * nx - 6, 2 * plane - nx - 2, 2 * plane - 2):  # even offsets, not plane / line aligned
         d_p = sp.upload_pattern(r1 - r0, pc.table, pc.disp_offsets, pc.disp_flat, pc.ends_flat, pc.row_pattern[r0:r1],
                                 True, row_offset=r0)
         y = ring_run(sp, d_p, x[g0:7 * plane], 90, x_col0=g0)
