@@ -357,7 +357,7 @@ def run_b200(args):
                    "l2": "inputs (20 B/row * 16.8M rows = 335 MB per SpMV) exceed the 126 MB L2; no flush needed",
                    "build_seconds": round(build_s, 2)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": ncu_traffic(), "peak_source": peak_src, "kernel": "spmv_pattern_ringp_kernel<4,4,3> (persistent tensor ring)",
+                     "traffic": ncu_traffic(), "peak_source": peak_src, "kernel": "spmv_pattern_ringp_kernel<6,4,2> (persistent tensor ring)",
                      "kernel_ms": kernel_ms, "algorithmic_bytes_per_launch": alg_bytes,
                      "equivalent_ell_gbs": 340.0 * n / (kernel_ms * 1e-3) / 1e9,
                      "uncompressed_ell_roofline_gflops": ell_roofline,
