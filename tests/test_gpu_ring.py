@@ -164,3 +164,46 @@ def test_ring_ghost_planes_beyond_the_grid_faces(sp, orc, march):
     xg = np.concatenate([np.full(plane, np.nan), x, np.full(plane, np.nan)])  # ghosts must never be read as operands
     y = ring_run(sp, up_pat(sp, pc), xg, march, x_col0=-plane, n_rows=m.n)
     assert np.array_equal(bits(y), bits(orc.spmv(pc, x)))
+
+
+def test_ring_randomised_shapes_ranges_and_views(sp, orc):
+    """Random grids (partial strips, one or two left-over columns, strips in fours, plane counts that are not a
+    multiple of the planes per thread), row ranges cut anywhere and x views with and without ghost planes: the
+    default dispatch (tensor ring where it applies) is bit-identical to List 1 on the CPU."""
+    rng = np.random.default_rng(20260117)
+    used_ring = 0
+    for trial in range(36):
+        nx = int(rng.choice([256, 512, 256, 68, 70, 126, 128, 130, 192, 194, 258, 320, 384]))
+        ny = int(rng.integers(2, 9))
+        nz = int(rng.integers(8, 23))
+        m = orc.generate_matrix(nx, ny, nz)
+        pc = orc.compress_patterns(m, True)
+        n, plane = m.n, nx * ny
+        x = orc.make_test_vector(n, orc.RANDOM, seed=100 + trial, lo=-1.0, hi=1.0)
+        full = orc.spmv(pc, x)
+        # a slab of planes [z0, z1) with ghost planes (or more) on either side, possibly beyond the grid faces
+        z0 = int(rng.integers(0, 3))
+        z1 = nz - int(rng.integers(0, 3))
+        r0, r1 = z0 * plane, z1 * plane
+        below, above = int(rng.integers(1, 3)), int(rng.integers(1, 3))
+        g_lo, g_hi = (z0 - below) * plane, (z1 + above) * plane
+        xl = np.full(g_hi - g_lo, np.nan)  # positions outside the grid are never referenced
+        lo, hi = max(g_lo, 0), min(g_hi, n)
+        xl[lo - g_lo:hi - g_lo] = x[lo:hi]
+        d = sp.upload_pattern(r1 - r0, pc.table, pc.disp_offsets, pc.disp_flat, pc.ends_flat, pc.row_pattern[r0:r1], True,
+                              row_offset=r0)
+        nl = r1 - r0
+        cuts = sorted({0, nl, *(int(v) for v in rng.integers(0, nl + 1, size=2))})
+        dx = sp.DeviceVector.from_host(xl)
+        for march in (0, 90):  # the default dispatch, and the tensor ring forced also for ranges of a few planes
+            dy = sp.DeviceVector.from_host(np.full(nl, np.nan))
+            sp.set_option("box_march", march)
+            try:
+                for b, e in zip(cuts[:-1], cuts[1:]):
+                    sp.spmv_rows(d, dx, dy, b, e, x_col0=g_lo)
+                    used_ring += march == 90 and sp.get_option("last_pattern_kernel") == 9
+            finally:
+                sp.set_option("box_march", 0)
+            y = dy.to_host()
+            assert np.array_equal(bits(y), bits(full[r0:r1])), (trial, march, nx, ny, nz, z0, z1, below, above, cuts)
+    assert used_ring >= 60
