@@ -34,6 +34,20 @@ int fail(int code, const char *fmt, ...);
 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Per-device "done once" state (function attributes and occupancy are properties of a kernel *on a device*;
+// a process may drive several devices through spmvb_set_device).
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDevices) d = 0;
+    return d;
+}
+template <typename T>
+struct PerDevice {
+    T v[kMaxDevices] = {};
+    T &get() { return v[current_device()]; }
+};
+
 // Rows per CTA tile of the row-major ELL-like streams.  Device allocations of
 // those streams are padded to a whole number of tiles so a tile can always be
 // fetched with full 16-byte vector loads.

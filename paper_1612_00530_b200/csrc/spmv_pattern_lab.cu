@@ -906,11 +906,11 @@ static int launch_box5(const spmvb_matrix *a, PatternArgs &p, cudaStream_t st) {
     if (p.sy % 4 || (p.g0 + p.row_begin) % 4 || p.row_begin % 4) return 1;
     constexpr int NP = WC * Q;
     const size_t smem = (size_t)DEPTH * ((NP + 2) * 68 * 8 + NP * 64 * 4);
-    static bool attr_set = false;
-    if (!attr_set) {
+    static PerDevice<bool> attr_set;
+    if (!attr_set.get()) {
         if (cudaFuncSetAttribute(spmv_pattern_box5_kernel<R, WC, Q, DEPTH, MINB, true, 1>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return -1;
-        attr_set = true;
+        attr_set.get() = true;
     }
     dim3 grid((p.sy + 63) / 64, (p.plane_lines + R - 1) / R, (n_planes + NP - 1) / NP);
     spmv_pattern_box5_kernel<R, WC, Q, DEPTH, MINB, true, 1><<<grid, WC * 32, smem, st>>>(p, n_planes);
@@ -927,11 +927,11 @@ static int launch_box7(const spmvb_matrix *a, PatternArgs &p, cudaStream_t st) {
     if (p.sy % 4 || (p.g0 + p.row_begin) % 4 || p.row_begin % 4) return 1;
     constexpr int NP = WC * Q;
     const size_t smem = (size_t)DEPTH * ((NP + 2) * 68 * 8 + NP * 64 * 4);
-    static bool attr_set = false;
-    if (!attr_set) {
+    static PerDevice<bool> attr_set;
+    if (!attr_set.get()) {
         if (cudaFuncSetAttribute(spmv_pattern_box7_kernel<R, WC, Q, DEPTH, MINB, true, 1>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return -1;
-        attr_set = true;
+        attr_set.get() = true;
     }
     dim3 grid((p.sy + 63) / 64, (p.plane_lines + R - 1) / R, (n_planes + NP - 1) / NP);
     spmv_pattern_box7_kernel<R, WC, Q, DEPTH, MINB, true, 1><<<grid, WC * 32, smem, st>>>(p, n_planes);
@@ -949,11 +949,11 @@ static int launch_box8(const spmvb_matrix *a, PatternArgs &p, cudaStream_t st) {
     constexpr int NP = 2 * WZ;
     constexpr size_t stage = (size_t)(NP + 2) * 260 * 8 + NP * 256 * 4;
     const size_t smem = stage * DEPTH;
-    static bool attr_set = false;
-    if (!attr_set) {
+    static PerDevice<bool> attr_set;
+    if (!attr_set.get()) {
         if (cudaFuncSetAttribute(spmv_pattern_box8_kernel<R, DEPTH, WZ, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem) != cudaSuccess) return -1;
-        attr_set = true;
+        attr_set.get() = true;
     }
     const int tx = (p.sy + 255) / 256, ty = (p.plane_lines + R - 1) / R, tz = (n_planes + NP - 1) / NP;
     const int grid = std::min(tx * ty * tz, 148);

@@ -541,7 +541,8 @@ static int launch_ringp_t(const spmvb_matrix *a, PatternArgs &p_in, int chunk, c
     const int64_t total64 = (int64_t)n_cols * ((c_hi - c_lo + Q) / Q) * p.plane_lines;
     if (total64 >= INT32_MAX) return 1;
     const int total = (int)total64;
-    static int n_sm = 0;
+    static PerDevice<int> n_sm_dev;
+    int &n_sm = n_sm_dev.get();
     if (n_sm == 0) {
         int dev = 0;
         if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
@@ -551,7 +552,8 @@ static int launch_ringp_t(const spmvb_matrix *a, PatternArgs &p_in, int chunk, c
     const int min_steps = 8;
 #define LAUNCH_RINGP(NEG, CP)                                                                                                   \
     do {                                                                                                                         \
-        static int per_sm = 0;                                                                                                   \
+        static PerDevice<int> per_sm_dev;                                                                                        \
+        int &per_sm = per_sm_dev.get();                                                                                          \
         if (per_sm == 0) {                                                                                                       \
             if (cudaFuncSetAttribute(spmv_pattern_ringp_kernel<Q, S, MINB, NEG, CP, IDT, PFD, DBG, CTAC>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                      (int)L::kTotal) != cudaSuccess ||                                                           \
@@ -644,7 +646,8 @@ int launch_pattern_ring(int which, int lines, const spmvb_matrix *a, PatternArgs
             //    well inside L2);
             //  * larger x: tiles of 16 lines, columns fastest, dealt out round-robin, which keeps the planes being read few
             //    enough for their halo planes to be re-read from L2 (512^3: 530-575 us vs 686 us with contiguous chunks).
-            static int l2_bytes = 0;
+            static PerDevice<int> l2_dev;
+            int &l2_bytes = l2_dev.get();
             if (l2_bytes == 0) {
                 int dev = 0;
                 if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&l2_bytes, cudaDevAttrL2CacheSize, dev) != cudaSuccess) return -1;

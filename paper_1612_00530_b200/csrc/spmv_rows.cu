@@ -237,10 +237,10 @@ int launch_ell(const double *values, const int32_t *columns, int width, const do
         const size_t stage = smem;  // multiple of 16 for any width (128 rows)
         const size_t need = stage * NS;
         if (need <= 220 * 1024) {
-            static bool tma_attr = false;
-            if (!tma_attr) {
+            static PerDevice<bool> tma_attr;
+            if (!tma_attr.get()) {
                 SPMVB_CUDA(cudaFuncSetAttribute(spmv_rows_tma_kernel<kTileRows, NS, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-                tma_attr = true;
+                tma_attr.get() = true;
             }
             const int per_sm = std::max(1, (int)std::min<size_t>(8, (220 * 1024) / (need + 1024)));
             const int grid = std::min(tiles, 148 * per_sm);
@@ -249,10 +249,10 @@ int launch_ell(const double *values, const int32_t *columns, int width, const do
             return check_launch("spmv_ell_tma");
         }
     }
-    static bool attr_set = false;
-    if (!attr_set) {
+    static PerDevice<bool> attr_set;
+    if (!attr_set.get()) {
         SPMVB_CUDA(cudaFuncSetAttribute(spmv_ell_kernel<kTileRows>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr_set = true;
+        attr_set.get() = true;
     }
     spmv_ell_kernel<kTileRows><<<tiles, kTileRows, smem, st>>>(values, columns, width, x, x_col0, y, row_begin,
                                                                row_end, tile0, row_map);
@@ -271,10 +271,10 @@ int launch_vt(const spmvb_matrix *a, const double *x, int64_t x_col0, double *y,
         const size_t stage = (size_t)kTileRows * (a->width + a->m) * 4;
         const size_t need = stage * NS;
         if (need <= 200 * 1024) {
-            static bool tma_attr = false;
-            if (!tma_attr) {
+            static PerDevice<bool> tma_attr;
+            if (!tma_attr.get()) {
                 SPMVB_CUDA(cudaFuncSetAttribute(spmv_rows_tma_kernel<kTileRows, NS, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-                tma_attr = true;
+                tma_attr.get() = true;
             }
             const int per_sm = std::max(1, (int)std::min<size_t>(8, (200 * 1024) / (need + 4096)));
             const int grid = std::min(tiles, 148 * per_sm);
@@ -284,10 +284,10 @@ int launch_vt(const spmvb_matrix *a, const double *x, int64_t x_col0, double *y,
             return check_launch("spmv_vt_tma");
         }
     }
-    static bool attr_set = false;
-    if (!attr_set) {
+    static PerDevice<bool> attr_set;
+    if (!attr_set.get()) {
         SPMVB_CUDA(cudaFuncSetAttribute(spmv_vt_kernel<kTileRows>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr_set = true;
+        attr_set.get() = true;
     }
     spmv_vt_kernel<kTileRows><<<tiles, kTileRows, smem, st>>>(
         static_cast<const int32_t *>(a->s[SPMVB_S_SORTED_COLUMNS]), static_cast<const int32_t *>(a->s[SPMVB_S_ENDS]),
