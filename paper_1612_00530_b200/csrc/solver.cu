@@ -1,8 +1,11 @@
 // CG vector primitives and the unpreconditioned CG driver on the device
 // (inc/kernels.hpp:39-42 dot / waxpby, inc/solver.hpp:17-46 CgConfig / CgReport / cg_solve;
 // SPEC.md:238-256,308-321).  The caller of the SpMV hot path: 1 SpMV, 3 dots and 3 waxpbys
-// per iteration (inc/solver.hpp:43), everything device-resident; only the three dot results
-// per iteration cross to the host (they steer alpha, beta and the stopping test).
+// per iteration (inc/solver.hpp:43), everything device-resident.  Inside cg_solve the operations of an
+// iteration are fused where that saves passes over the vectors -- x and r are updated and r.r is
+// accumulated in one kernel, alpha and beta are formed on the device -- with exactly the arithmetic
+// and summation order of the stand-alone dot / waxpby; one pair of scalars (alpha, r.r) per iteration
+// crosses to the host for the history and the stopping test.
 //
 // waxpby is bit-identical to the reference expression alpha*x[i] + beta*y[i] (two products and
 // one sum, each rounded).  dot uses a fixed-shape two-level tree (deterministic run to run) and
@@ -50,15 +53,77 @@ __global__ void waxpby_kernel(double alpha, const double *__restrict__ x, double
         w[i] = __dadd_rn(__dmul_rn(alpha, x[i]), __dmul_rn(beta, y[i]));  // inc/kernels.hpp:41
 }
 
+// ---- fused forms used by cg_solve (same per-element expressions, same reduction tree as dot_partial_kernel) ----
+// scal: [0] p.Ap  [1] alpha  [2] r.z of the previous iteration  [3] r.r (= r.z, no preconditioner)  [4] beta
+//       [5] stop flag (set by the device when the iteration converged or produced a non-finite value; every later
+//           cg_* kernel is then a no-op, so the host may queue one iteration ahead)  [6] ||b||  [7] tolerance  [8] ||r||/||b||
+__global__ void cg_alpha_kernel(const double *__restrict__ partial, int count, double *__restrict__ scal) {
+    if (scal[5] != 0.0) return;
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < count; i += 32) acc = __dadd_rn(acc, partial[i]);
+    for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, o));
+    if (threadIdx.x == 0) {
+        scal[0] = acc;
+        scal[1] = scal[2] / acc;  // alpha = r.z / p.Ap
+    }
+}
+// x = 1*x + alpha*p (waxpby 1), r = 1*r + (-alpha)*Ap (waxpby 2), partial sums of r.r (dots 2 and 3) in one pass
+__global__ void __launch_bounds__(kDotThreads) cg_update_kernel(const double *__restrict__ scal, const double *__restrict__ p,
+                                                               const double *__restrict__ ap, double *__restrict__ x,
+                                                               double *__restrict__ r, int64_t n, double *__restrict__ partial) {
+    __shared__ double s[kDotThreads / 32];
+    if (scal[5] != 0.0) return;
+    const double alpha = scal[1], nalpha = -alpha;
+    double acc = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * kDotThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kDotThreads) {
+        x[i] = __dadd_rn(__dmul_rn(1.0, x[i]), __dmul_rn(alpha, p[i]));
+        const double rn = __dadd_rn(__dmul_rn(1.0, r[i]), __dmul_rn(nalpha, ap[i]));
+        r[i] = rn;
+        acc = __dadd_rn(acc, __dmul_rn(rn, rn));
+    }
+    for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, o));
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        acc = threadIdx.x < kDotThreads / 32 ? s[threadIdx.x] : 0.0;
+        for (int o = 4; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, o));
+        if (threadIdx.x == 0) partial[blockIdx.x] = acc;
+    }
+}
+__global__ void cg_beta_kernel(const double *__restrict__ partial, int count, double *__restrict__ scal) {
+    if (scal[5] != 0.0) return;
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < count; i += 32) acc = __dadd_rn(acc, partial[i]);
+    for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, o));
+    if (threadIdx.x == 0) {
+        const double rel = sqrt(acc) / scal[6];  // ||r||2 / ||b||2
+        scal[3] = acc;
+        scal[8] = rel;
+        scal[4] = acc / scal[2];  // beta = r.z_new / r.z
+        scal[2] = acc;
+        if (!isfinite(scal[1]) || !isfinite(rel) || rel <= scal[7]) scal[5] = 1.0;
+    }
+}
+// p = 1*r + beta*p (waxpby 3) with beta taken from the device
+__global__ void cg_direction_kernel(const double *__restrict__ scal, const double *__restrict__ r, double *__restrict__ p, int64_t n) {
+    if (scal[5] != 0.0) return;
+    const double beta = scal[4];
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        p[i] = __dadd_rn(__dmul_rn(1.0, r[i]), __dmul_rn(beta, p[i]));
+}
+
 struct DotScratch {
-    double *partial = nullptr, *out = nullptr;
+    double *partial = nullptr, *out = nullptr, *scal = nullptr;
     ~DotScratch() {
         if (partial) cudaFree(partial);
         if (out) cudaFree(out);
+        if (scal) cudaFree(scal);
     }
     int init() {
         SPMVB_CUDA(cudaMalloc(&partial, kDotBlocks * sizeof(double)));
         SPMVB_CUDA(cudaMalloc(&out, sizeof(double)));
+        SPMVB_CUDA(cudaMalloc(&scal, 16 * sizeof(double)));
         return SPMVB_OK;
     }
 };
@@ -136,35 +201,78 @@ int spmvb_cg_solve(const spmvb_matrix *a, const double *b_dev, double *x_dev, in
         *converged = 1;
         return done(SPMVB_OK);
     }
-    for (int it = 1; it <= max_iterations; it++) {
-        double pap = 0.0, rr = 0.0, rz_new = 0.0;
-        rc = spmvb_spmv(a, p, 0, n, ap, 0, (int32_t)n, stream);                       // 1 SpMV
-        if (rc == SPMVB_OK) rc = dot_device(p, ap, n, sc, &pap, st);                   // dot 1
-        if (rc != SPMVB_OK) return done(rc);
-        const double alpha = rz / pap;
-        rc = waxpby_device(1.0, x_dev, alpha, p, x_dev, n, st);                        // waxpby 1
-        if (rc == SPMVB_OK) rc = waxpby_device(1.0, r, -alpha, ap, r, n, st);          // waxpby 2
-        if (rc == SPMVB_OK) rc = dot_device(r, r, n, sc, &rr, st);                     // dot 2 (residual norm)
-        if (rc == SPMVB_OK) rc = dot_device(r, r, n, sc, &rz_new, st);                 // dot 3 (r.z with z = r)
-        if (rc != SPMVB_OK) return done(rc);
-        const double rel = std::sqrt(rr) / bnorm;
-        *iterations = it;
-        if (residual_history) residual_history[it] = rel;
-        if (!std::isfinite(alpha) || !std::isfinite(rel)) {
-            done(SPMVB_OK);
-            return fail(SPMVB_ERR_DIVERGENCE, "cg_solve: non-finite value in iteration %d", it);  // inc/solver.hpp:44
-        }
-        if (rel <= tolerance) {
-            *converged = 1;
-            break;
-        }
-        const double beta = rz_new / rz;
-        rz = rz_new;
-        rc = waxpby_device(1.0, r, beta, p, p, n, st);                                 // waxpby 3: p = z + beta p
-        if (rc != SPMVB_OK) return done(rc);
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + kDotThreads - 1) / kDotThreads, kDotBlocks));
+    const int wblocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+    {
+        const double init[16] = {0.0, 0.0, rz, 0.0, 0.0, 0.0, bnorm, tolerance, 0.0};
+        SPMVB_CUDA(cudaMemcpyAsync(sc.scal, init, sizeof(init), cudaMemcpyHostToDevice, st));
+        SPMVB_CUDA(cudaStreamSynchronize(st));
     }
-    SPMVB_CUDA(cudaStreamSynchronize(st));
-    return done(SPMVB_OK);
+    // The host queues iteration `it` before it looks at the scalars of iteration it-1 (pinned ring of two records, one
+    // event each): the stop decision is the device's (scal[5]); what was queued past it runs as no-ops.
+    // (the pinned ring and the events are allocated once per host thread: cudaMallocHost costs milliseconds)
+    struct HostRing {
+        double *ring = nullptr;
+        cudaEvent_t ev[2] = {nullptr, nullptr};
+        int init() {
+            if (ring) return SPMVB_OK;
+            if (cudaMallocHost(&ring, 2 * 16 * sizeof(double)) != cudaSuccess || cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming) != cudaSuccess ||
+                cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming) != cudaSuccess) {
+                ring = nullptr;
+                return fail(SPMVB_ERR_CUDA, "cg_solve: pinned scalar ring / events: %s", cudaGetErrorString(cudaGetLastError()));
+            }
+            return SPMVB_OK;
+        }
+    };
+    static thread_local HostRing hr;
+    if (hr.init() != SPMVB_OK) return done(SPMVB_ERR_CUDA);
+    double *ring = hr.ring;
+    cudaEvent_t *ev = hr.ev;
+    auto finish = [&](int code) {
+        cudaStreamSynchronize(st);
+        return done(code);
+    };
+    // looks at iteration k (already queued); returns 1 to stop, 0 to go on, < 0 on error
+    auto harvest = [&](int k) -> int {
+        if (cudaEventSynchronize(ev[k & 1]) != cudaSuccess) return -1;
+        const double *h = ring + (k & 1) * 16;
+        const double alpha = h[1], rel = h[8];
+        *iterations = k;
+        if (residual_history) residual_history[k] = rel;
+        if (!std::isfinite(alpha) || !std::isfinite(rel)) return 2;
+        if (h[5] != 0.0) {
+            *converged = 1;
+            return 1;
+        }
+        return 0;
+    };
+    int stop = 0;
+    for (int it = 1; it <= max_iterations && !stop; it++) {
+        rc = spmvb_spmv(a, p, 0, n, ap, 0, (int32_t)n, stream);                       // 1 SpMV
+        if (rc != SPMVB_OK) return finish(rc);
+        dot_partial_kernel<<<blocks, kDotThreads, 0, st>>>(p, ap, n, sc.partial);      // dot 1: p.Ap ...
+        cg_alpha_kernel<<<1, 32, 0, st>>>(sc.partial, blocks, sc.scal);                // ... and alpha = r.z / p.Ap
+        cg_update_kernel<<<blocks, kDotThreads, 0, st>>>(sc.scal, p, ap, x_dev, r, n, sc.partial);  // waxpby 1, 2, dots 2 = 3
+        cg_beta_kernel<<<1, 32, 0, st>>>(sc.partial, blocks, sc.scal);                 // r.r, beta, r.z, stop flag
+        if (cudaMemcpyAsync(ring + (it & 1) * 16, sc.scal, 16 * sizeof(double), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaEventRecord(ev[it & 1], st) != cudaSuccess) {
+            finish(SPMVB_OK);
+            return fail(SPMVB_ERR_CUDA, "cg_solve: %s", cudaGetErrorString(cudaGetLastError()));
+        }
+        if (it < max_iterations) cg_direction_kernel<<<wblocks, 256, 0, st>>>(sc.scal, r, p, n);  // waxpby 3: p = z + beta p
+        if (it > 1) stop = harvest(it - 1);
+        if (!stop && it == max_iterations) stop = harvest(it);
+    }
+    if (stop < 0 || cudaGetLastError() != cudaSuccess) {
+        finish(SPMVB_OK);
+        return fail(SPMVB_ERR_CUDA, "cg_solve: device error in the iteration");
+    }
+    if (stop == 2) {
+        const int at = *iterations;
+        finish(SPMVB_OK);
+        return fail(SPMVB_ERR_DIVERGENCE, "cg_solve: non-finite value in iteration %d", at);  // inc/solver.hpp:44
+    }
+    return finish(SPMVB_OK);
 }
 
 }  // extern "C"
