@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
             uint32_t sl[3];
 #pragma unroll
             for (int dy = 0; dy < 3; dy++) sl[dy] = ring + ((gs + j + dy) % S) * L::kSlotBytes + lane_off;
-            if (DBG >= 3) {  // measurement only: the data movement alone (ring fetches, waits, y stores)
+            if (DBG >= 3 && DBG <= 5) {  // measurement only: the data movement alone (ring fetches, waits, y stores)
                 if (DBG == 3) {
                     const double2 u = lds_f64x2(sl[1] + L::kLineBytes);
 #pragma unroll
@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
        // latency-bound gathers overlap with the marches of the others)
         const int n_left = sy - left_lo;
         const int total_left = n_left * pl * (c_hi - c_lo + 1);
-        for (int t = gw * 32 + lane; t < total_left && DBG != 5; t += n_warps * 32)
+        for (int t = gw * 32 + lane; t < total_left && DBG != 5 && DBG != 6; t += n_warps * 32)
             ring_leftover_row<OFF_NEG1, CENTER_POS>(p, s_masks, left_lo + t % n_left, (t / n_left) % pl, c_lo + t / (n_left * pl), np_x);
     }
 }
@@ -583,9 +583,12 @@ static int launch_ringp_t(const spmvb_matrix *a, PatternArgs &p_in, int chunk, c
 
 #ifdef SPMVB_RING_TU_Q6
 // Second translation unit (spmv_pattern_tma6.cu): the 6-planes-per-thread instantiations, so that the two halves build in parallel.
-// mode 0: chunk per CTA (with the ids-by-loads fallback); 1: per CTA, lab; 2: per warp, lab.
+// mode 0: chunk per CTA (with the ids-by-loads fallback); 1: per CTA, lab; 2: per warp, lab; 3-5: ablations.
 int launch_ring_q6(int mode, const spmvb_matrix *a, PatternArgs &p, int chunk, cudaStream_t st, int tile_lines) {
     if (mode == 2) return launch_ringp_t<6, 4, 2, true>(a, p, chunk, st, tile_lines);
+    if (mode == 3) return launch_ringp_t<6, 4, 2, true, 0, 6, true>(a, p, chunk, st, tile_lines);  // measurement only: no left-over columns
+    if (mode == 4) return launch_ringp_t<6, 4, 2, true, 0, 3, true>(a, p, chunk, st, tile_lines);  // measurement only: fetch + store
+    if (mode == 5) return launch_ringp_t<6, 4, 2, true, 0, 4, true>(a, p, chunk, st, tile_lines);  // measurement only: fetch
     const int rc = launch_ringp_t<6, 4, 2, true, 0, 0, true>(a, p, chunk, st, tile_lines);
     return rc == 1 && mode == 0 ? launch_ringp_t<6, 5, 2, false, 0, 0, true>(a, p, chunk, st, tile_lines) : rc;
 }
@@ -632,6 +635,9 @@ int launch_pattern_ring(int which, int lines, const spmvb_matrix *a, PatternArgs
         // (3 / 5 / 7 / 8 planes per thread, chunk per CTA: 80.6 / 76.2 / 74.0 / 84.1 us at 256^3, r01_probe_planes_per_thread.log)
         case 25: return launch_ring_q6(1, a, p, 0, st, tl);      // 6 planes/thread, round-robin tiles per CTA
         case 26: return launch_ring_q6(2, a, p, lines, st, 0);   // 6 planes/thread, chunk per warp
+        case 28: return launch_ring_q6(3, a, p, lines, st, 0);   // ablations of the default (6 planes/thread, chunk per CTA):
+        case 29: return launch_ring_q6(4, a, p, lines, st, 0);   //   no left-over columns / fetch + store only / fetch only
+        case 30: return launch_ring_q6(5, a, p, lines, st, 0);
         case 27: return launch_ring_q6(2, a, p, 0, st, tl);      // 6 planes/thread, round-robin tiles per warp
         case 19:  // ... a tile per warp
             rc = launch_ringp_t<4, 4, 3, true>(a, p, 0, st, tl);

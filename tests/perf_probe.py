@@ -73,7 +73,8 @@ if "pattern" in fmts or "generic" in fmts:
                             (105, "ring: st.cs stores"), (97, "ABLATION (chunk/warp) no FP chains"),
                             (98, "ABLATION (chunk/warp) one LDS quad/step"), (99, "ABLATION (chunk/warp) fetch+store only"),
                             (100, "ABLATION (chunk/warp) fetch only"), (103, "ABLATION fetch+store only"), (102, "ABLATION fetch only"),
-                            (106, "ABLATION fetch only, no left-over column")):
+                            (106, "ABLATION fetch only, no left-over column"), (118, "ABLATION default, no left-over column (wrong col)"),
+                            (119, "ABLATION default, fetch+store only"), (120, "ABLATION default, fetch only")):
             if march >= 90 and ring_lines:
                 for ln in ring_lines:
                     timeit(d, f"pattern {name} R={ln}", 20, pattern_kernel=2, box_march=march, box_prefetch=2, box_lines=ln)
