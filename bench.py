@@ -212,11 +212,11 @@ def run_b200(args):
         build_s = time.perf_counter() - t_build
 
         def kernel_of(a):
-            def k(xl, yl, b, e):
-                sp.spmv_rows(a, xl, yl, b, e, x_col0=L.x_col0, x_len=L.x_len, stream=main)
+            def k(xl, yl, b, e, stream=None):
+                sp.spmv_rows(a, xl, yl, b, e, x_col0=L.x_col0, x_len=L.x_len, stream=main if stream is None else stream)
             return k
 
-        slab = sp.SlabSpmv(L, kernel_of(pc), dist if world > 1 else None, comm, main, torch)
+        slab = sp.SlabSpmv(L, kernel_of(pc), dist if world > 1 else None, comm, main, torch, two_stream_boundaries=True)
 
         # ---- verification gate: no number for a kernel that failed parity
         slab.spmv(x, y)

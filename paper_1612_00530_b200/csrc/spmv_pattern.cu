@@ -99,7 +99,12 @@ static int launch_pattern(const spmvb_matrix *a, const double *x, int64_t x_col0
             }
             if (!ring && o.pattern_kernel != 3 && box3_ok(a, p)) {
                 const int64_t n_planes = ((int64_t)row_end - row_begin + (int64_t)p.sy * p.plane_lines - 1) / ((int64_t)p.sy * p.plane_lines);
-                if (n_planes == 1) rc3 = launch_box3<16, 4, 1, 2, 3, false>(a, p, st);  // single-plane ranges (slab boundary planes)
+                if (n_planes == 1) {  // single-plane ranges (slab boundary planes): short marches, so that the plane fills the GPU
+                    if (o.box_lines == 16) rc3 = launch_box3<16, 4, 1, 2, 3, false>(a, p, st);
+                    else if (o.box_lines == 8) rc3 = launch_box3<8, 4, 1, 2, 3, false>(a, p, st);
+                    else if (o.box_lines == 2) rc3 = launch_box3<2, 4, 1, 2, 3, false>(a, p, st);
+                    else rc3 = launch_box3<4, 4, 1, 2, 3, false>(a, p, st);
+                }
                 else switch (o.box_march) {
                     // measured alternatives kept selectable for A/B (profiles/r01_probe256_*.log, 256^3):
                     case 1: rc3 = launch_box3<16, 4, 2, 1, 3, false>(a, p, st); break;      // R=16 tiles            124 us

@@ -92,9 +92,12 @@ class SlabSpmv:
     passes the CUDA spmv_rows, the CPU tests inject the oracle's.  `dist` is
     torch.distributed (or None for a single slab)."""
 
-    def __init__(self, layout: SlabLayout, kernel, dist=None, comm_stream=None, main_stream=None, torch=None):
+    def __init__(self, layout: SlabLayout, kernel, dist=None, comm_stream=None, main_stream=None, torch=None,
+                 two_stream_boundaries=False):
+        """two_stream_boundaries: kernel accepts a `stream=` keyword; the lower boundary plane then runs on the side stream."""
         self.L, self.kernel, self.dist = layout, kernel, dist
         self.comm_stream, self.main_stream, self.torch = comm_stream, main_stream, torch
+        self.two_stream_boundaries = two_stream_boundaries and comm_stream is not None
 
     def _exchange_ops(self, x_local):
         L, d = self.L, self.dist
@@ -134,6 +137,14 @@ class SlabSpmv:
             with t.cuda.stream(self.comm_stream):
                 for r in reqs:
                     r.wait()
+            if self.two_stream_boundaries and lo > 0 and hi < n:
+                # the two boundary planes are independent: one goes on the side stream right behind the receive, the
+                # other on the main stream, so that they share the GPU once the interior kernel has drained
+                self.kernel(x_local, y_local, 0, lo, stream=self.comm_stream)
+                self.main_stream.wait_stream(self.comm_stream)  # (the receive; the lower plane is ordered by the final wait)
+                self.kernel(x_local, y_local, hi, n)
+                self.main_stream.wait_stream(self.comm_stream)
+                return
             self.main_stream.wait_stream(self.comm_stream)
         else:
             reqs = self.dist.batch_isend_irecv(self._exchange_ops(x_local))

@@ -101,3 +101,18 @@ def test_two_and_three_slabs_equal_the_whole_matrix(orc):
             r0, r1 = L.row_range
             assert np.array_equal(y.cpu().numpy().view(np.uint64), ref[r0:r1].view(np.uint64)), (nx, ny, nz, world, r)
             assert len(calls) == (1 if world == 1 else 1 + int(L.has_lower) + int(L.has_upper))
+            # the streamed form bench.py uses: exchange on a side stream, the two boundary planes on two streams
+            main, comm = torch.cuda.Stream(), torch.cuda.Stream()
+            y2 = torch.full((L.n_local,), float("nan"), dtype=torch.float64, device="cuda")
+            streams_used = []
+
+            def kernel_s(xl, yl, b, e, stream=None, pc=pc, L=L):
+                streams_used.append(comm if stream is comm else main)
+                sp.spmv_rows(pc, xl, yl, b, e, x_col0=L.x_col0, x_len=L.x_len, stream=main if stream is None else stream)
+
+            main.wait_stream(torch.cuda.current_stream())
+            sp.SlabSpmv(L, kernel_s, _NoComm(), comm, main, torch, two_stream_boundaries=True).spmv(xs[r], y2)
+            main.synchronize()
+            assert np.array_equal(y2.cpu().numpy().view(np.uint64), ref[r0:r1].view(np.uint64)), (nx, ny, nz, world, r)
+            if L.has_lower and L.has_upper:
+                assert comm in streams_used and main in streams_used
