@@ -171,7 +171,7 @@ __device__ __forceinline__ void ring_leftover_row(const PatternArgs &p, uint32_t
 template <int Q, int S, int MINB, bool OFF_NEG1, int CENTER_POS, bool IDT, int PFD = 0, int DBG = 0, bool CTAC = false>
 __global__ void __launch_bounds__(kRingWarps * 32, MINB)
     spmv_pattern_ringp_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm_ids, PatternArgs p, int c_lo,
-                              int c_hi, int np_x, int n_strips, int left_lo, int id_plane0, int total_steps, int steps_per_warp, int tile_lines) {
+                              int c_hi, int np_x, int n_strips, int left_lo, int id_plane0, int total_steps, int steps_per_warp, int tile_lines, int rot) {
     using L = RingLayout<Q, S, IDT>;
     constexpr int P = L::P;
     extern __shared__ unsigned char smem_raw[];
@@ -222,8 +222,12 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
         } else {
             if (s_pos >= s_end) break;
             col_idx = s_pos / pl;
-            b0 = s_pos - col_idx * pl;
-            nb = min(pl - b0, s_end - s_pos);
+            const int u = s_pos - col_idx * pl;  // position in the column's line sequence
+            // The line sequence of plane group g starts at line g*rot (cyclically).  rot = (steps per plane group) - k * (chunk
+            // length) for the nearest k: the CTA k chunks further on works on the next plane group and is then on the same lines
+            // at the same time, so the halo planes the two groups share are read from DRAM once.
+            b0 = (int)((u + (int64_t)(col_idx / (CTAC ? n_sg : n_strips)) * rot) % pl);
+            nb = min(min(pl - u, pl - b0), s_end - s_pos);
             s_pos += nb;
         }
         const int strip = CTAC ? (col_idx % n_sg) * kRingWarps + warp : col_idx % n_strips;
@@ -569,8 +573,11 @@ static int launch_ringp_t(const spmvb_matrix *a, PatternArgs &p_in, int chunk, c
             grid = std::max(1, std::min(grid, (total + min_steps * units - 1) / (min_steps * units)));                          \
         const int spw = chunk > 0 ? chunk : (total + grid * units - 1) / (grid * units);                                         \
         if (chunk > 0) grid = (total + spw * units - 1) / (spw * units);                                                         \
+        const int cols_per_group = CTAC ? n_cols : n_strips;                                                                    \
+        const int64_t wgrp = (int64_t)cols_per_group * p.plane_lines, kgrp = (wgrp + spw / 2) / spw;                              \
+        const int rot = options().debug_nochain == 7 ? 0 : (int)(((wgrp - kgrp * spw) % p.plane_lines + p.plane_lines) % p.plane_lines); \
         spmv_pattern_ringp_kernel<Q, S, MINB, NEG, CP, IDT, PFD, DBG, CTAC><<<grid, kRingWarps * 32, L::kTotal, st>>>(                          \
-            tm, tm_ids, p, c_lo, c_hi, np_x, n_strips, left_lo, id_plane0, total, spw, tile_lines);                                          \
+            tm, tm_ids, p, c_lo, c_hi, np_x, n_strips, left_lo, id_plane0, total, spw, tile_lines, rot);                                          \
     } while (0)
     if (neg1) {
         if (cp == 0) LAUNCH_RINGP(true, 0); else if (cp == 1) LAUNCH_RINGP(true, 1); else LAUNCH_RINGP(true, 2);
