@@ -123,12 +123,12 @@ __device__ __noinline__ void ring_masked_step(uint32_t sl0, uint32_t sl1, uint32
 }
 
 // -----------------------------------------------------------------------------------------
-// Persistent form of the direct variant (the default).  The (strip, plane group) columns of the
-// view, pl lines each, form one sequence of line steps; it is cut into equal contiguous chunks,
-// one per resident warp (a single wave of CTAs), so that every warp does the same amount of work
-// and nothing is left for a tail.  A chunk that crosses a column end is two marches.  The rows of
-// the left-over columns are dealt out to the warps and summed while the first line sets are in
-// flight.  The ring (slot = set number mod S, parity from the set number) runs on across marches.
+// The kernel.  One wave of persistent CTAs; the (strip or strip group, plane group) columns of the view, pl lines each,
+// form one sequence of line steps.  Two schedules (see launch_pattern_ring): equal contiguous chunks of that sequence,
+// one per CTA (its four warps on the four strips of the same lines) or per warp; or tiles of a few lines dealt out
+// round-robin.  A chunk that crosses a column end (or the rotation point of its column) is two marches.  The ring
+// (slot = set number mod S, parity from the set number) runs on across marches.  The rows of the left-over columns are
+// dealt out to the warps and summed after their marches.
 // -----------------------------------------------------------------------------------------
 // One row of a left-over column.  The id and all in-view box operands are requested together (one memory latency);
 // the row's mask then decides whether the plain sum is exact (same rule as the strips) or List 1 runs as written.
