@@ -118,6 +118,8 @@ int spmvb_set_device(int device);
  *   "host_chunks":    row chunks of the pipelined spmvb_spmv_host (0 = default 8)
  *   "ell_kernel":     0 auto (ELL: TMA bulk pipeline, vt: staged), 1 naive, 2 staged vector loads, 3 TMA for vt too
  *   "box_prefetch", "box_prefetch_l1": L2 / L1 prefetch distance of the sliding-window kernels
+ *   "debug_nochain":  measurement only (1: sliding-window kernels skip their FP64 chains -- wrong results; 7: tensor ring
+ *                     without the per-plane-group line rotation -- same results)
  *   "last_pattern_kernel" (read): family of the last pattern launch: 1 List 1, 2 one-column box, 3 sliding window,
  *                     4 lab variant, 9 tensor ring */
 int spmvb_set_option(const char *key, int value);
