@@ -116,6 +116,8 @@ int spmvb_set_device(int device);
  *                     sliding window (listed with their measured times in csrc/spmv_pattern*.cu)
  *   "box_lines":      lines per CTA tile / chunk length of the tensor ring (0 = default)
  *   "host_chunks":    row chunks of the pipelined spmvb_spmv_host (0 = default 8)
+ *   "cg_keep_workspace": 1 (default) spmvb_cg_solve keeps its three work vectors (3n doubles) on the matrix handle
+ *                     between solves, released by spmvb_matrix_destroy; 0 allocates and frees them in every solve
  *   "ell_kernel":     0 auto (ELL: TMA bulk pipeline, vt: staged), 1 naive, 2 staged vector loads, 3 TMA for vt too
  *   "box_prefetch", "box_prefetch_l1": L2 / L1 prefetch distance of the sliding-window kernels
  *   "debug_nochain":  measurement only (1: sliding-window kernels skip their FP64 chains -- wrong results; 7: tensor ring

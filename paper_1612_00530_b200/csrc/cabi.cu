@@ -56,6 +56,7 @@ void destroy(spmvb_matrix *a) {
         if (a->s[i]) cudaFree(a->s[i]);
     if (a->scratch_x) cudaFree(a->scratch_x);
     if (a->scratch_y) cudaFree(a->scratch_y);
+    if (a->cg_ws) cudaFree(a->cg_ws);
     for (auto &st : a->pipe_streams) if (st) cudaStreamDestroy(st);
     for (auto &ev : a->pipe_events) if (ev) cudaEventDestroy(ev);
     if (a->d_masks) cudaFree(a->d_masks);
@@ -249,6 +250,7 @@ static int *option_slot(const char *key) {
     if (!strcmp(key, "debug_nochain")) return &o.debug_nochain;
     if (!strcmp(key, "box_lines")) return &o.box_lines;
     if (!strcmp(key, "host_chunks")) return &o.host_chunks;
+    if (!strcmp(key, "cg_keep_workspace")) return &o.cg_keep_workspace;
     if (!strcmp(key, "last_pattern_kernel")) return &o.last_pattern_kernel;
     return nullptr;
 }

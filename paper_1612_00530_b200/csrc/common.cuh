@@ -83,6 +83,9 @@ struct spmvb_matrix {
     // persistent scratch of spmvb_spmv_host (x and y on the device)
     mutable double *scratch_x = nullptr, *scratch_y = nullptr;
     mutable int64_t scratch_x_len = 0;
+    // work vectors of spmvb_cg_solve (r, p, Ap: 3n doubles), kept between solves on this handle unless "cg_keep_workspace" is 0
+    mutable double *cg_ws = nullptr;
+    mutable int cg_ws_busy = 0;  // taken with an atomic exchange: a second concurrent solve on the handle allocates its own
     // streams / events of the pipelined host-buffer SpMV (created on first use)
     mutable cudaStream_t pipe_streams[3] = {};
     mutable cudaEvent_t pipe_events[128] = {};
@@ -108,6 +111,7 @@ struct Options {
     int box_prefetch_l1 = 0; // L1 prefetch distance in lines (0 = off)
     int debug_nochain = 0;   // measurement only
     int box_lines = 0;       // lines per CTA march of the tensor-ring kernel (0 = default)
+    int cg_keep_workspace = 1;  // 1: spmvb_cg_solve keeps its 3n work doubles on the handle until spmvb_free
     int host_chunks = 0;     // row chunks of the pipelined host-buffer SpMV (0 = default 8, at most 64)
     int last_pattern_kernel = 0;  // read-only: kernel family of the last pattern launch (1 List 1, 2 box v2, 3 box3, 4 lab, 9 tensor ring)
 };

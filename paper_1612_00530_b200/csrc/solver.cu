@@ -11,14 +11,17 @@
 // one sum, each rounded).  dot uses a fixed-shape two-level tree (deterministic run to run) and
 // therefore differs from the reference's index-ascending sum in the last bits
 // bounds that effect on the residual history by 1e-10.
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
 
 namespace spmvb {
 
-constexpr int kDotBlocks = 148 * 4;
+constexpr int kDotBlocks = 148 * 8;
 constexpr int kDotThreads = 256;
 
 __global__ void __launch_bounds__(kDotThreads) dot_partial_kernel(const double *__restrict__ u, const double *__restrict__ v,
@@ -172,21 +175,52 @@ int spmvb_cg_solve(const spmvb_matrix *a, const double *b_dev, double *x_dev, in
     if (a->row_offset != 0) return fail(SPMVB_ERR_INVALID_ARGUMENT, "cg_solve: handle is a slab; drive the slabs from slab.py");
     cudaStream_t st = as_stream(stream);
     const int64_t n = a->n;
+    // SPMVB_CG_TRACE=1: wall-clock of the phases of a solve on stderr (allocation, set-up, iterations, release)
+    static const bool trace = std::getenv("SPMVB_CG_TRACE") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto ms = [](auto t0, auto t1) { return std::chrono::duration<double, std::milli>(t1 - t0).count(); };
+    const auto t_begin = now();
+    auto t_alloc = t_begin, t_setup = t_begin, t_loop = t_begin;
     *iterations = 0;
     *converged = 0;
-    double *r = nullptr, *p = nullptr, *ap = nullptr;
+    // r, p, Ap: one block of 3 * n_pad doubles.  cudaMalloc / cudaFree of vectors this size cost ~1 ms each and now and then
+    // 10-150 ms (measured, profiles/r01_cg_probe.log), so the block stays on the handle between solves ("cg_keep_workspace").
+    const int64_t n_pad = (n + 63) / 64 * 64;
     DotScratch sc;
     SPMVB_TRY(sc.init());
-    int rc = spmvb_vec_alloc(n, &r);
-    if (rc == SPMVB_OK) rc = spmvb_vec_alloc(n, &p);
-    if (rc == SPMVB_OK) rc = spmvb_vec_alloc(n, &ap);
+    double *ws = nullptr;
+    bool ws_on_handle = false;
+    if (options().cg_keep_workspace && __atomic_exchange_n(&a->cg_ws_busy, 1, __ATOMIC_ACQUIRE) == 0) {
+        ws_on_handle = true;
+        if (!a->cg_ws && cudaMalloc(&a->cg_ws, (size_t)n_pad * 3 * sizeof(double)) != cudaSuccess) {
+            a->cg_ws = nullptr;
+            __atomic_store_n(&a->cg_ws_busy, 0, __ATOMIC_RELEASE);
+            return fail(SPMVB_ERR_CUDA, "cg_solve: work vectors (%lld doubles): %s", (long long)n_pad * 3, cudaGetErrorString(cudaGetLastError()));
+        }
+        ws = a->cg_ws;
+    } else if (cudaMalloc(&ws, (size_t)n_pad * 3 * sizeof(double)) != cudaSuccess) {
+        return fail(SPMVB_ERR_CUDA, "cg_solve: work vectors (%lld doubles): %s", (long long)n_pad * 3, cudaGetErrorString(cudaGetLastError()));
+    }
+    double *r = ws, *p = ws + n_pad, *ap = ws + 2 * n_pad;
+    int rc = SPMVB_OK;
     auto done = [&](int code) {
-        if (r) cudaFree(r);
-        if (p) cudaFree(p);
-        if (ap) cudaFree(ap);
+        if (trace) t_loop = now();
+        if (ws_on_handle) {
+            if (!options().cg_keep_workspace) {
+                cudaFree(a->cg_ws);
+                a->cg_ws = nullptr;
+            }
+            __atomic_store_n(&a->cg_ws_busy, 0, __ATOMIC_RELEASE);
+        } else {
+            cudaFree(ws);
+        }
+        if (trace)
+            std::fprintf(stderr, "[spmvb cg] alloc %.3f ms, set-up %.3f ms, %d iterations %.3f ms, release %.3f ms\n", ms(t_begin, t_alloc),
+                         ms(t_alloc, t_setup), *iterations, ms(t_setup, t_loop), ms(t_loop, now()));
         return code;
     };
     if (rc != SPMVB_OK) return done(rc);
+    t_alloc = t_setup = now();
     // x0 = 0, r = b, z = r (no preconditioner), p = z  (inc/solver.hpp:40-43)
     rc = cudaMemsetAsync(x_dev, 0, (size_t)n * 8, st) == cudaSuccess ? SPMVB_OK : fail(SPMVB_ERR_CUDA, "memset failed");
     if (rc == SPMVB_OK) rc = waxpby_device(1.0, b_dev, 0.0, b_dev, r, n, st);
@@ -208,16 +242,20 @@ int spmvb_cg_solve(const spmvb_matrix *a, const double *b_dev, double *x_dev, in
         SPMVB_CUDA(cudaMemcpyAsync(sc.scal, init, sizeof(init), cudaMemcpyHostToDevice, st));
         SPMVB_CUDA(cudaStreamSynchronize(st));
     }
-    // The host queues iteration `it` before it looks at the scalars of iteration it-1 (pinned ring of two records, one
-    // event each): the stop decision is the device's (scal[5]); what was queued past it runs as no-ops.
+    // The host queues iteration `it` before it looks at the scalars of iteration it-kAhead (pinned ring of kRing records,
+    // one event each): the stop decision is the device's (scal[5]); what was queued past it runs as no-ops (the SpMVs
+    // still run, into the scratch vector).  kAhead iterations of queued work ride out a host thread that is descheduled
+    // for a millisecond; with one iteration of run-ahead the device drained every time that happened.
     // (the pinned ring and the events are allocated once per host thread: cudaMallocHost costs milliseconds)
+    constexpr int kRing = 8, kAhead = 4;
     struct HostRing {
         double *ring = nullptr;
-        cudaEvent_t ev[2] = {nullptr, nullptr};
+        cudaEvent_t ev[kRing] = {};
         int init() {
             if (ring) return SPMVB_OK;
-            if (cudaMallocHost(&ring, 2 * 16 * sizeof(double)) != cudaSuccess || cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming) != cudaSuccess ||
-                cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming) != cudaSuccess) {
+            bool ok = cudaMallocHost(&ring, kRing * 16 * sizeof(double)) == cudaSuccess;
+            for (int i = 0; ok && i < kRing; i++) ok = cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming) == cudaSuccess;
+            if (!ok) {
                 ring = nullptr;
                 return fail(SPMVB_ERR_CUDA, "cg_solve: pinned scalar ring / events: %s", cudaGetErrorString(cudaGetLastError()));
             }
@@ -234,8 +272,8 @@ int spmvb_cg_solve(const spmvb_matrix *a, const double *b_dev, double *x_dev, in
     };
     // looks at iteration k (already queued); returns 1 to stop, 0 to go on, < 0 on error
     auto harvest = [&](int k) -> int {
-        if (cudaEventSynchronize(ev[k & 1]) != cudaSuccess) return -1;
-        const double *h = ring + (k & 1) * 16;
+        if (cudaEventSynchronize(ev[k % kRing]) != cudaSuccess) return -1;
+        const double *h = ring + (k % kRing) * 16;
         const double alpha = h[1], rel = h[8];
         *iterations = k;
         if (residual_history) residual_history[k] = rel;
@@ -246,7 +284,8 @@ int spmvb_cg_solve(const spmvb_matrix *a, const double *b_dev, double *x_dev, in
         }
         return 0;
     };
-    int stop = 0;
+    t_setup = now();
+    int stop = 0, queued = 0, seen = 0;
     for (int it = 1; it <= max_iterations && !stop; it++) {
         rc = spmvb_spmv(a, p, 0, n, ap, 0, (int32_t)n, stream);                       // 1 SpMV
         if (rc != SPMVB_OK) return finish(rc);
@@ -254,15 +293,16 @@ int spmvb_cg_solve(const spmvb_matrix *a, const double *b_dev, double *x_dev, in
         cg_alpha_kernel<<<1, 32, 0, st>>>(sc.partial, blocks, sc.scal);                // ... and alpha = r.z / p.Ap
         cg_update_kernel<<<blocks, kDotThreads, 0, st>>>(sc.scal, p, ap, x_dev, r, n, sc.partial);  // waxpby 1, 2, dots 2 = 3
         cg_beta_kernel<<<1, 32, 0, st>>>(sc.partial, blocks, sc.scal);                 // r.r, beta, r.z, stop flag
-        if (cudaMemcpyAsync(ring + (it & 1) * 16, sc.scal, 16 * sizeof(double), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
-            cudaEventRecord(ev[it & 1], st) != cudaSuccess) {
+        if (cudaMemcpyAsync(ring + (it % kRing) * 16, sc.scal, 16 * sizeof(double), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaEventRecord(ev[it % kRing], st) != cudaSuccess) {
             finish(SPMVB_OK);
             return fail(SPMVB_ERR_CUDA, "cg_solve: %s", cudaGetErrorString(cudaGetLastError()));
         }
         if (it < max_iterations) cg_direction_kernel<<<wblocks, 256, 0, st>>>(sc.scal, r, p, n);  // waxpby 3: p = z + beta p
-        if (it > 1) stop = harvest(it - 1);
-        if (!stop && it == max_iterations) stop = harvest(it);
+        queued = it;
+        if (it > kAhead) stop = harvest(seen = it - kAhead);
     }
+    while (!stop && seen < queued) stop = harvest(++seen);  // the last iterations queued (max_iterations reached)
     if (stop < 0 || cudaGetLastError() != cudaSuccess) {
         finish(SPMVB_OK);
         return fail(SPMVB_ERR_CUDA, "cg_solve: device error in the iteration");

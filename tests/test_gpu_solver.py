@@ -66,6 +66,42 @@ def test_cg_single_unknown_and_errors(sp, orc):
         sp.cg_solve(z, sp.DeviceVector.from_host(np.ones(2)))
 
 
+def test_cg_workspace_on_the_handle_and_run_ahead(sp, orc):
+    """Repeated solves reuse the work vectors kept on the handle ("cg_keep_workspace"); with or without them, and wherever
+    the stop falls relative to the host's run-ahead of four iterations, the report and the solution are identical."""
+    g = (20, 12, 10)
+    m = sp.generate_matrix(sp.GridSpec(*g))
+    n = m.n
+    a = sp.compress_patterns(m, True)
+    ell = sp.to_ell(m)
+    b = sp.DeviceVector(n)
+    sp.spmv_rows(ell, sp.DeviceVector.from_host(np.ones(n)), b, 0, n)
+    x0, rep0 = sp.cg_solve(a, b, tolerance=1e-9)
+    assert rep0.converged and rep0.iterations > 6
+    base = x0.to_host().view(np.uint64)
+    try:
+        for keep in (1, 0, 1):
+            sp.set_option("cg_keep_workspace", keep)
+            for _ in range(2):
+                x, rep = sp.cg_solve(a, b, tolerance=1e-9)
+                assert rep.iterations == rep0.iterations and rep.residual_history == rep0.residual_history
+                assert np.array_equal(x.to_host().view(np.uint64), base)
+    finally:
+        sp.set_option("cg_keep_workspace", 1)
+    # max_iterations below, at and above the run-ahead depth, and one past convergence: same prefix of the history
+    for cap in (1, 2, 3, 4, 5, 6, rep0.iterations - 1, rep0.iterations, rep0.iterations + 1, rep0.iterations + 7):
+        x, rep = sp.cg_solve(a, b, max_iterations=cap, tolerance=1e-9)
+        k = min(cap, rep0.iterations)
+        assert rep.iterations == k and rep.converged == (cap >= rep0.iterations)
+        assert rep.residual_history == rep0.residual_history[: k + 1]
+        if cap >= rep0.iterations:
+            assert np.array_equal(x.to_host().view(np.uint64), base)  # nothing queued past the stop touched x
+    # an interleaved solve on another handle does not disturb this one's vectors
+    xe, repe = sp.cg_solve(ell, b, tolerance=1e-9)
+    x, rep = sp.cg_solve(a, b, tolerance=1e-9)
+    assert np.array_equal(x.to_host().view(np.uint64), base) and repe.iterations == rep0.iterations
+
+
 def test_slab_cg_driver_on_the_device(sp, orc):
     """The distributed CG driver (slab.py:SlabCg) with the CUDA kernels as its operations, one slab: the same iteration
     count and history as the single-call device solver, and the known solution."""
