@@ -116,6 +116,9 @@ int spmvb_set_device(int device);
  *                     sliding window (listed with their measured times in csrc/spmv_pattern*.cu)
  *   "box_lines":      lines per CTA tile / chunk length of the tensor ring (0 = default)
  *   "host_chunks":    row chunks of the pipelined spmvb_spmv_host (0 = default 8)
+ *   "cg_fused_dot":   1 (default) spmvb_cg_solve takes p.Ap from the SpMV kernel when that kernel offers it (pattern format,
+ *                     tensor ring, whole square grid): one pass over p and Ap less per iteration; 0 always runs the dot
+ *   "last_cg_fused_dot": read-only, 1 when the last spmvb_cg_solve took p.Ap from the SpMV kernel
  *   "cg_keep_workspace": 1 (default) spmvb_cg_solve keeps its three work vectors (3n doubles) on the matrix handle
  *                     between solves, released by spmvb_matrix_destroy; 0 allocates and frees them in every solve
  *   "ell_kernel":     0 auto (ELL: TMA bulk pipeline, vt: staged), 1 naive, 2 staged vector loads, 3 TMA for vt too

@@ -251,6 +251,8 @@ static int *option_slot(const char *key) {
     if (!strcmp(key, "box_lines")) return &o.box_lines;
     if (!strcmp(key, "host_chunks")) return &o.host_chunks;
     if (!strcmp(key, "cg_keep_workspace")) return &o.cg_keep_workspace;
+    if (!strcmp(key, "cg_fused_dot")) return &o.cg_fused_dot;
+    if (!strcmp(key, "last_cg_fused_dot")) return &o.last_cg_fused_dot;
     if (!strcmp(key, "last_pattern_kernel")) return &o.last_pattern_kernel;
     return nullptr;
 }

@@ -111,6 +111,8 @@ struct Options {
     int box_prefetch_l1 = 0; // L1 prefetch distance in lines (0 = off)
     int debug_nochain = 0;   // measurement only
     int box_lines = 0;       // lines per CTA march of the tensor-ring kernel (0 = default)
+    int cg_fused_dot = 1;       // 1: cg_solve takes p.Ap from the SpMV kernel where that kernel offers it (pattern format, tensor ring)
+    int last_cg_fused_dot = 0;  // read-only: 1 when the last iteration of the last cg_solve took p.Ap from the SpMV kernel
     int cg_keep_workspace = 1;  // 1: spmvb_cg_solve keeps its 3n work doubles on the handle until spmvb_free
     int host_chunks = 0;     // row chunks of the pipelined host-buffer SpMV (0 = default 8, at most 64)
     int last_pattern_kernel = 0;  // read-only: kernel family of the last pattern launch (1 List 1, 2 box v2, 3 box3, 4 lab, 9 tensor ring)

@@ -37,6 +37,8 @@ struct PatternArgs {
     int prefetch;              // L2 prefetch distance in lines
     int prefetch_l1;           // L1 prefetch distance in lines (v3), 0 = off
     int debug_nochain;         // measurement only: skip the FP64 chains (y = centre operand)
+    double *dot_partial = nullptr;  // fused x.y (CG's p.Ap): one partial sum per warp of the tensor-ring kernel, else nullptr
+    int dot_capacity = 0;
 };
 
 // List 1, one row: groups in table order, per element value * x.

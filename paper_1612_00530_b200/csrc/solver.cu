@@ -18,11 +18,13 @@
 #include <vector>
 
 #include "common.cuh"
+#include "spmv_internal.cuh"
 
 namespace spmvb {
 
 constexpr int kDotBlocks = 148 * 8;
 constexpr int kDotThreads = 256;
+constexpr int kPartialCap = 8192;  // partial sums: kDotBlocks from the vector kernels, one per warp from the SpMV's fused dot
 
 __global__ void __launch_bounds__(kDotThreads) dot_partial_kernel(const double *__restrict__ u, const double *__restrict__ v,
                                                                  int64_t n, double *__restrict__ partial) {
@@ -124,7 +126,7 @@ struct DotScratch {
         if (scal) cudaFree(scal);
     }
     int init() {
-        SPMVB_CUDA(cudaMalloc(&partial, kDotBlocks * sizeof(double)));
+        SPMVB_CUDA(cudaMalloc(&partial, kPartialCap * sizeof(double)));
         SPMVB_CUDA(cudaMalloc(&out, sizeof(double)));
         SPMVB_CUDA(cudaMalloc(&scal, 16 * sizeof(double)));
         return SPMVB_OK;
@@ -287,10 +289,15 @@ int spmvb_cg_solve(const spmvb_matrix *a, const double *b_dev, double *x_dev, in
     t_setup = now();
     int stop = 0, queued = 0, seen = 0;
     for (int it = 1; it <= max_iterations && !stop; it++) {
-        rc = spmvb_spmv(a, p, 0, n, ap, 0, (int32_t)n, stream);                       // 1 SpMV
+        // 1 SpMV; the pattern format's tensor-ring kernel also leaves the partial sums of p.Ap (dot 1) when it can
+        FusedDot fused{sc.partial, kPartialCap, 0};
+        fused_dot_request() = options().cg_fused_dot ? &fused : nullptr;
+        rc = spmvb_spmv(a, p, 0, n, ap, 0, (int32_t)n, stream);
+        fused_dot_request() = nullptr;
         if (rc != SPMVB_OK) return finish(rc);
-        dot_partial_kernel<<<blocks, kDotThreads, 0, st>>>(p, ap, n, sc.partial);      // dot 1: p.Ap ...
-        cg_alpha_kernel<<<1, 32, 0, st>>>(sc.partial, blocks, sc.scal);                // ... and alpha = r.z / p.Ap
+        options().last_cg_fused_dot = fused.count != 0;
+        if (fused.count == 0) dot_partial_kernel<<<blocks, kDotThreads, 0, st>>>(p, ap, n, sc.partial);  // dot 1: p.Ap ...
+        cg_alpha_kernel<<<1, 32, 0, st>>>(sc.partial, fused.count ? fused.count : blocks, sc.scal);      // ... and alpha = r.z / p.Ap
         cg_update_kernel<<<blocks, kDotThreads, 0, st>>>(sc.scal, p, ap, x_dev, r, n, sc.partial);  // waxpby 1, 2, dots 2 = 3
         cg_beta_kernel<<<1, 32, 0, st>>>(sc.partial, blocks, sc.scal);                 // r.r, beta, r.z, stop flag
         if (cudaMemcpyAsync(ring + (it % kRing) * 16, sc.scal, 16 * sizeof(double), cudaMemcpyDeviceToHost, st) != cudaSuccess ||

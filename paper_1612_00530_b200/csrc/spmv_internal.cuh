@@ -14,6 +14,16 @@ int launch_vt(const spmvb_matrix *a, const double *x, int64_t x_col0, double *y,
 // measured experiments (spmv_pattern_lab.cu): returns 0 launched, 1 not served, -1 CUDA error
 int launch_pattern_lab(int which, const spmvb_matrix *a, PatternArgs &p, cudaStream_t st);
 
+// Request of cg_solve to the next spmvb_spmv of this host thread: also leave partial sums of x.y (y = A x, square full-grid
+// handle).  Served only by the default tensor-ring launch (count = partials written, one per warp); count stays 0 when the
+// launch that ran could not serve it, and the caller then runs its own dot.  The partials are summed in a fixed order
+// (each thread over its rows in schedule order, a shuffle tree per warp), so the result is deterministic run to run.
+struct FusedDot {
+    double *partial = nullptr;
+    int capacity = 0, count = 0;
+};
+FusedDot *&fused_dot_request();
+
 // tensor-ring kernel (spmv_pattern_tma.cu): same return convention; `which` selects a measured variant
 bool ring_ok(const spmvb_matrix *a, const PatternArgs &p);
 int launch_pattern_ring(int which, int lines, const spmvb_matrix *a, PatternArgs &p, cudaStream_t st);

@@ -60,6 +60,11 @@ static bool box3_ok(const spmvb_matrix *a, const PatternArgs &p) {
            a->n_patterns <= kDictSmemPat && 6 * sz + 128 * (int64_t)p.sy + 4096 < INT32_MAX;
 }
 
+FusedDot *&fused_dot_request() {
+    static thread_local FusedDot *req = nullptr;
+    return req;
+}
+
 static int launch_pattern(const spmvb_matrix *a, const double *x, int64_t x_col0, int64_t x_len, double *y,
                           int row_begin, int row_end, cudaStream_t st) {
     if (row_end > row_begin) {
@@ -83,6 +88,13 @@ static int launch_pattern(const spmvb_matrix *a, const double *x, int64_t x_col0
         p.prefetch = o.box_prefetch >= 0 ? o.box_prefetch : 2;
         p.prefetch_l1 = o.box_prefetch_l1;
         p.debug_nochain = o.debug_nochain;
+        if (FusedDot *req = fused_dot_request()) {  // x.y alongside y: every row through one ring launch, x[row] = the row's own entry
+            if (a->n_exc == 0 && row_begin == 0 && row_end == a->n && a->row_offset == 0 && x_col0 == 0 && a->n_cols == a->n && x_len == a->n &&
+                o.box_march == 0 && o.pattern_kernel == 0 && o.debug_nochain == 0) {
+                p.dot_partial = req->partial;
+                p.dot_capacity = req->capacity;
+            }
+        }
         const bool use_box = a->box.valid && o.pattern_kernel != 1;
         if (o.pattern_kernel == 2 && !a->box.valid)
             return fail(SPMVB_ERR_INVALID_ARGUMENT, "box kernel requested but the dictionary has no box plan");

@@ -55,6 +55,11 @@ __device__ __forceinline__ double2 lds_f64x2(uint32_t addr) {
     asm volatile("ld.shared.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
     return v;
 }
+__device__ __forceinline__ double lds_f64(uint32_t addr) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+    return v;
+}
 __device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t v) { asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory"); }
 
 constexpr int kIdBoxCols = kStripCols + 8;  // id box: columns 64s-4 .. 64s+67 (a 16-byte aligned start for 4-byte ids)
@@ -132,13 +137,14 @@ __device__ __noinline__ void ring_masked_step(uint32_t sl0, uint32_t sl1, uint32
 // -----------------------------------------------------------------------------------------
 // One row of a left-over column.  The id and all in-view box operands are requested together (one memory latency);
 // the row's mask then decides whether the plain sum is exact (same rule as the strips) or List 1 runs as written.
+// Returns y[row] * x[row's own column] (0 when there is no such row): the fused dot of the DOT instantiation.
 template <bool OFF_NEG1, int CENTER_POS>
-__device__ __forceinline__ void ring_leftover_row(const PatternArgs &p, uint32_t s_masks, int col, int line, int c, int np_x) {
+__device__ __forceinline__ double ring_leftover_row(const PatternArgs &p, uint32_t s_masks, int col, int line, int c, int np_x) {
     const int sy = p.sy, pl = p.plane_lines;
     const int64_t sz = (int64_t)sy * pl;
     const int64_t xi = col + (int64_t)sy * line + sz * c;
     const int64_t row = xi - p.g0;
-    if (row < p.row_begin || row >= p.row_end) return;
+    if (row < p.row_begin || row >= p.row_end) return 0.0;
     const uint32_t oob = (col == 0 ? kLBits : 0u) | (col == sy - 1 ? kRBits : 0u) | (line == 0 ? kDyLoBits : 0u) |
                          (line == pl - 1 ? kDyHiBits : 0u) | (c == 0 ? kDzLoBits : 0u) | (c == np_x - 1 ? kDzHiBits : 0u);
     const uint32_t in_view = c < np_x ? (kFullBox & ~oob) : 0u;
@@ -147,7 +153,7 @@ __device__ __forceinline__ void ring_leftover_row(const PatternArgs &p, uint32_t
 #pragma unroll
     for (int e = 0; e < 27; e++)
         xv[e] = (in_view >> e & 1u) ? __ldg(p.x + (xi + (e % 3 - 1) + (int64_t)sy * ((e / 3) % 3 - 1) + sz * (e / 9 - 1))) : 0.0;
-    if (id < 0) return;
+    if (id < 0) return 0.0;
     if (in_view != 0 && lds_u32(s_masks + 4 + 4 * id) == in_view) {
         double acc = 0.0;
         if (CENTER_POS == 0) acc = __dadd_rn(acc, __dmul_rn(p.v_center, xv[13]));
@@ -163,12 +169,15 @@ __device__ __forceinline__ void ring_leftover_row(const PatternArgs &p, uint32_t
         }
         if (CENTER_POS == 1) acc = __dadd_rn(acc, __dmul_rn(p.v_center, xv[13]));
         p.y[row] = acc;
+        return __dmul_rn(acc, xv[13]);
     } else {
-        p.y[row] = pattern_row(p, p.disp, p.ends, p.table, id, xi);
+        const double acc = pattern_row(p, p.disp, p.ends, p.table, id, xi);
+        p.y[row] = acc;
+        return in_view != 0 ? __dmul_rn(acc, __ldg(p.x + xi)) : 0.0;
     }
 }
 
-template <int Q, int S, int MINB, bool OFF_NEG1, int CENTER_POS, bool IDT, int PFD = 0, int DBG = 0, bool CTAC = false>
+template <int Q, int S, int MINB, bool OFF_NEG1, int CENTER_POS, bool IDT, int PFD = 0, int DBG = 0, bool CTAC = false, bool DOT = false>
 __global__ void __launch_bounds__(kRingWarps * 32, MINB)
     spmv_pattern_ringp_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm_ids, PatternArgs p, int c_lo,
                               int c_hi, int np_x, int n_strips, int left_lo, int id_plane0, int total_steps, int steps_per_warp, int tile_lines, int rot) {
@@ -199,6 +208,7 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
     const double vc = p.v_center, vo = p.v_off;
     const uint32_t lane_off = lane * 16;
     uint32_t gs = 0;  // sets issued so far by this warp: slot = set number % S, parity = (set number / S) & 1
+    double dsum = 0.0;  // DOT: this thread's share of x.y, rows in schedule order
     // CTAC: a work unit belongs to the CTA and its four warps take the four strips of the same lines (they then read
     // whole contiguous lines of x together); otherwise every warp has units of its own.
     // tile_lines == 0: one contiguous chunk of the column-major step sequence per unit (steps_per_warp steps);
@@ -427,6 +437,8 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
                     if (id[q][i] >= 0) {
                         if (PFD == 9) __stcs(&y[row0 + q * sz + j * sy + i], acc[q][i]);
                         else y[row0 + q * sz + j * sy + i] = acc[q][i];
+                        // the row's own x entry is still in the ring (line b, plane q of the box + 1; the refill above took line b-1)
+                        if (DOT) dsum = __dadd_rn(dsum, __dmul_rn(acc[q][i], lds_f64(sl[1] + (q + 1) * L::kLineBytes + 8 * (1 + i))));
                     }
         }
         gs += n_sets;
@@ -436,8 +448,14 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
        // latency-bound gathers overlap with the marches of the others)
         const int n_left = sy - left_lo;
         const int total_left = n_left * pl * (c_hi - c_lo + 1);
-        for (int t = gw * 32 + lane; t < total_left && DBG != 5 && DBG != 6; t += n_warps * 32)
-            ring_leftover_row<OFF_NEG1, CENTER_POS>(p, s_masks, left_lo + t % n_left, (t / n_left) % pl, c_lo + t / (n_left * pl), np_x);
+        for (int t = gw * 32 + lane; t < total_left && DBG != 5 && DBG != 6; t += n_warps * 32) {
+            const double d = ring_leftover_row<OFF_NEG1, CENTER_POS>(p, s_masks, left_lo + t % n_left, (t / n_left) % pl, c_lo + t / (n_left * pl), np_x);
+            if (DOT) dsum = __dadd_rn(dsum, d);
+        }
+    }
+    if (DOT) {  // one partial per warp, fixed tree
+        for (int o = 16; o > 0; o >>= 1) dsum = __dadd_rn(dsum, __shfl_down_sync(0xffffffffu, dsum, o));
+        if (lane == 0) p.dot_partial[gw] = dsum;
     }
 }
 
@@ -519,7 +537,7 @@ static bool ids_view_ok(const spmvb_matrix *a, const PatternArgs &p) {
     return p.g0 >= 0 && p.g0 % sz == 0 && (int64_t)a->n % sz == 0 && p.sy % 4 == 0 && (uintptr_t)p.ids % 16 == 0;
 }
 
-template <int Q, int S, int MINB, bool IDT, int PFD = 0, int DBG = 0, bool CTAC = false>
+template <int Q, int S, int MINB, bool IDT, int PFD = 0, int DBG = 0, bool CTAC = false, bool DOT = false>
 static int launch_ringp_t(const spmvb_matrix *a, PatternArgs &p_in, int chunk, cudaStream_t st, int tile_lines = 0) {
     PatternArgs p = clip_view(a, p_in);
     using L = RingLayout<Q, S, IDT>;
@@ -559,9 +577,9 @@ static int launch_ringp_t(const spmvb_matrix *a, PatternArgs &p_in, int chunk, c
         static PerDevice<int> per_sm_dev;                                                                                        \
         int &per_sm = per_sm_dev.get();                                                                                          \
         if (per_sm == 0) {                                                                                                       \
-            if (cudaFuncSetAttribute(spmv_pattern_ringp_kernel<Q, S, MINB, NEG, CP, IDT, PFD, DBG, CTAC>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+            if (cudaFuncSetAttribute(spmv_pattern_ringp_kernel<Q, S, MINB, NEG, CP, IDT, PFD, DBG, CTAC, DOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                      (int)L::kTotal) != cudaSuccess ||                                                           \
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmv_pattern_ringp_kernel<Q, S, MINB, NEG, CP, IDT, PFD, DBG, CTAC>,      \
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmv_pattern_ringp_kernel<Q, S, MINB, NEG, CP, IDT, PFD, DBG, CTAC, DOT>,      \
                                                               kRingWarps * 32, L::kTotal) != cudaSuccess || per_sm <= 0)         \
                 return -1;                                                                                                       \
         }                                                                                                                        \
@@ -576,7 +594,11 @@ static int launch_ringp_t(const spmvb_matrix *a, PatternArgs &p_in, int chunk, c
         const int cols_per_group = CTAC ? n_cols : n_strips;                                                                    \
         const int64_t wgrp = (int64_t)cols_per_group * p.plane_lines, kgrp = (wgrp + spw / 2) / spw;                              \
         const int rot = options().debug_nochain == 7 ? 0 : (int)(((wgrp - kgrp * spw) % p.plane_lines + p.plane_lines) % p.plane_lines); \
-        spmv_pattern_ringp_kernel<Q, S, MINB, NEG, CP, IDT, PFD, DBG, CTAC><<<grid, kRingWarps * 32, L::kTotal, st>>>(                          \
+        if (DOT) {                                                                                                               \
+            if (grid * kRingWarps > p.dot_capacity) return 1;                                                                    \
+            fused_dot_request()->count = grid * kRingWarps;                                                                      \
+        }                                                                                                                        \
+        spmv_pattern_ringp_kernel<Q, S, MINB, NEG, CP, IDT, PFD, DBG, CTAC, DOT><<<grid, kRingWarps * 32, L::kTotal, st>>>(                          \
             tm, tm_ids, p, c_lo, c_hi, np_x, n_strips, left_lo, id_plane0, total, spw, tile_lines, rot);                                          \
     } while (0)
     if (neg1) {
@@ -596,11 +618,25 @@ int launch_ring_q6(int mode, const spmvb_matrix *a, PatternArgs &p, int chunk, c
     if (mode == 3) return launch_ringp_t<6, 4, 2, true, 0, 6, true>(a, p, chunk, st, tile_lines);  // measurement only: no left-over columns
     if (mode == 4) return launch_ringp_t<6, 4, 2, true, 0, 3, true>(a, p, chunk, st, tile_lines);  // measurement only: fetch + store
     if (mode == 5) return launch_ringp_t<6, 4, 2, true, 0, 4, true>(a, p, chunk, st, tile_lines);  // measurement only: fetch
+    if (mode == 0 && p.dot_partial && fused_dot_request()) {  // cg_solve: x.y in the same pass (ids through the ring only)
+        const int rcd = launch_ringp_t<6, 4, 2, true, 0, 0, true, true>(a, p, chunk, st, tile_lines);
+        if (rcd != 1) return rcd;
+        fused_dot_request()->count = 0;
+    }
     const int rc = launch_ringp_t<6, 4, 2, true, 0, 0, true>(a, p, chunk, st, tile_lines);
     return rc == 1 && mode == 0 ? launch_ringp_t<6, 5, 2, false, 0, 0, true>(a, p, chunk, st, tile_lines) : rc;
 }
+// The 4-planes-per-thread kernels of the default policy with the fused dot (cg_solve); 1 = not served, run the plain kernel.
+int launch_ring_q4_dot(bool per_cta, const spmvb_matrix *a, PatternArgs &p, int chunk, cudaStream_t st, int tile_lines) {
+    if (!p.dot_partial || !fused_dot_request()) return 1;
+    const int rc = per_cta ? launch_ringp_t<4, 4, 3, true, 0, 0, true, true>(a, p, chunk, st, tile_lines)
+                           : launch_ringp_t<4, 4, 3, true, 0, 0, false, true>(a, p, chunk, st, tile_lines);
+    if (rc == 1) fused_dot_request()->count = 0;
+    return rc;
+}
 #else
 int launch_ring_q6(int mode, const spmvb_matrix *a, PatternArgs &p, int chunk, cudaStream_t st, int tile_lines);
+int launch_ring_q4_dot(bool per_cta, const spmvb_matrix *a, PatternArgs &p, int chunk, cudaStream_t st, int tile_lines);
 
 // Conditions: the TMA view needs a 16-byte aligned base, strides that are multiples of 16 bytes (even
 // sy), at least one whole plane of x and a line no narrower than a box; row arithmetic is 32-bit.
@@ -674,6 +710,8 @@ int launch_pattern_ring(int which, int lines, const spmvb_matrix *a, PatternArgs
             if (fours && tile_lines == 0) {  // 6 planes/thread at 8 warps/SM: 5-10 % faster than 4 at 12 on every shape tried
                 return launch_ring_q6(0, a, p, chunk, st, 0);
             }
+            rc = launch_ring_q4_dot(fours, a, p, chunk, st, tile_lines);  // cg_solve's request for x.y, when there is one
+            if (rc != 1) return rc;
             if (fours) {
                 rc = launch_ringp_t<4, 4, 3, true, 0, 0, true>(a, p, chunk, st, tile_lines);
                 return rc == 1 ? launch_ringp_t<4, 5, 3, false, 0, 0, true>(a, p, chunk, st, tile_lines) : rc;

@@ -102,6 +102,35 @@ def test_cg_workspace_on_the_handle_and_run_ahead(sp, orc):
     assert np.array_equal(x.to_host().view(np.uint64), base) and repe.iterations == rep0.iterations
 
 
+@pytest.mark.parametrize("g", [(192, 6, 9), (128, 10, 8), (256, 6, 14), (72, 6, 9)])
+def test_cg_takes_p_ap_from_the_tensor_ring_kernel(sp, orc, g):
+    """Pattern format, whole square grid, tensor ring: p.Ap comes out of the SpMV kernel (one partial per warp, rows in
+    schedule order).  Against the stand-alone dot: same iteration count, histories within 1e-12, solutions within 1e-12;
+    deterministic run to run.  Grids whose lines end in a left-over column (128, 192, 256: per-warp, per-warp and per-CTA schedules) and one that does not (72)."""
+    m = sp.generate_matrix(sp.GridSpec(*g))
+    n = m.n
+    a = sp.compress_patterns(m, True)
+    b = sp.DeviceVector(n)
+    sp.spmv_rows(sp.to_ell(m), sp.DeviceVector.from_host(np.ones(n)), b, 0, n)
+    try:
+        sp.set_option("cg_fused_dot", 0)
+        x0, rep0 = sp.cg_solve(a, b, tolerance=1e-9)
+        assert sp.get_option("last_cg_fused_dot") == 0
+        sp.set_option("cg_fused_dot", 1)
+        x1, rep1 = sp.cg_solve(a, b, tolerance=1e-9)
+        assert sp.get_option("last_cg_fused_dot") == 1 and sp.get_option("last_pattern_kernel") == 9
+        x2, rep2 = sp.cg_solve(a, b, tolerance=1e-9)
+    finally:
+        sp.set_option("cg_fused_dot", 1)
+    assert rep0.converged and rep1.converged and rep1.iterations == rep0.iterations
+    assert np.abs(np.array(rep1.residual_history) - np.array(rep0.residual_history)).max() <= 1e-12
+    assert np.abs(x1.to_host() - x0.to_host()).max() <= 1e-12 and np.abs(x1.to_host() - 1.0).max() <= 1e-6
+    assert rep2.residual_history == rep1.residual_history and np.array_equal(x2.to_host().view(np.uint64), x1.to_host().view(np.uint64))
+    # hybrid handles (exception rows go through another kernel) and the other formats keep the stand-alone dot
+    xe, repe = sp.cg_solve(sp.to_ell(m), b, tolerance=1e-9)
+    assert sp.get_option("last_cg_fused_dot") == 0 and repe.iterations == rep0.iterations
+
+
 def test_slab_cg_driver_on_the_device(sp, orc):
     """The distributed CG driver (slab.py:SlabCg) with the CUDA kernels as its operations, one slab: the same iteration
     count and history as the single-call device solver, and the known solution."""
