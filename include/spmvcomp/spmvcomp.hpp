@@ -15,6 +15,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <map>
+#include <filesystem>
 #include <optional>
 #include <span>
 #include <stdexcept>
@@ -92,6 +93,9 @@ StencilMatrix generate_matrix(const GridSpec& spec, double diagonal = 26.0, doub
 // inc/stencil.hpp:47-50: explicit rows; columns strictly ascending and in [0, n)
 StencilMatrix stencil_from_rows(std::int32_t n, const std::vector<std::vector<std::pair<std::int32_t, double>>>& rows);
 bool is_symmetric(const StencilMatrix& m);  // inc/stencil.hpp:52
+
+// inc/stencil.hpp:61-64: coordinate format, 1-based, lower triangle only; the matrix must be symmetric (spmvcomp/io.hpp)
+void write_matrix_market(const StencilMatrix& m, const std::filesystem::path& path);
 
 enum class VectorKind { ones, linear, random };  // inc/stencil.hpp:54
 // inc/stencil.hpp:56-59: random is deterministic in [0,1) per seed; the seed is required for it

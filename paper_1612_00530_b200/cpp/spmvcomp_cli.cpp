@@ -1,12 +1,15 @@
 // spmvcomp command-line harness (SPEC.md:425-500 [MODULE] bench_cli) on the device path.
-//   spmvcomp_cli generate  --grid NX NY NZ
-//   spmvcomp_cli bench     --grid NX NY NZ --format ell|vt|pattern|pattern-values [--reps R] [--out json|csv] [--seed S]
-//   spmvcomp_cli solve     --grid NX NY NZ [--backend ell|vt|pattern] [--tol T] [--max-iter K]
+//   spmvcomp_cli generate  --grid NX NY NZ [--out m.bin] [--mm m.mtx]
+//   spmvcomp_cli bench     (--grid NX NY NZ | --matrix m.bin) --format ell|vt|pattern|pattern-values [--reps R] [--out json|csv]
+//                          [--seed S] [--save format.bin]
+//   spmvcomp_cli solve     (--grid NX NY NZ | --matrix m.bin) [--backend ell|vt|pattern] [--tol T] [--max-iter K]
 //   spmvcomp_cli model     --bandwidth GB/s [--formats ell,vt,pattern,pattern-values]
 //   spmvcomp_cli calibrate
 // Exit codes: 0 success, 1 verification / convergence failure, 2 usage error.
-// The matrix file arguments of the reference CLI are replaced by --grid: the serialized formats are
-// not part of this build, the generator runs on the device instead.  `generate` therefore only sizes the matrix.
+// Matrix files (layout in include/spmvcomp/io.hpp): `generate --out` writes the serialized
+// StencilMatrix (and `--mm` the Matrix Market export), `bench` / `solve` take it with --matrix; --grid runs the
+// generator on the device instead and touches no file.  `bench --save` writes the serialized format that was timed.
+// A file that cannot be read or written is a failure (exit 1), not a usage error.
 // Verification before timing: bench prints nothing but an error when the compressed kernel's y
 // differs from the ELL backend's by more than 1e-12 relative per row (scale = sum |a_ik x_k|).
 #include <chrono>
@@ -17,6 +20,7 @@
 #include <string>
 #include <vector>
 
+#include "spmvcomp/io.hpp"
 #include "spmvcomp/spmvcomp.hpp"
 #include "spmvcomp_b200.h"
 
@@ -37,6 +41,8 @@ struct Args {
     int nx = 0, ny = 0, nz = 0, reps = 100, max_iter = 500;
     bool have_grid = false;
     std::string format = "pattern-values", backend = "pattern", out = "json", formats = "ell,vt,pattern,pattern-values";
+    std::string matrix, mm, save;
+    bool out_given = false;
     double tol = 1e-8, bandwidth = 0.0;
     unsigned long long seed = 7;
 };
@@ -56,7 +62,10 @@ Args parse(int argc, char **argv) {
         } else if (k == "--format") { need(1); a.format = argv[++i];
         } else if (k == "--backend") { need(1); a.backend = argv[++i];
         } else if (k == "--reps") { need(1); a.reps = std::atoi(argv[++i]);
-        } else if (k == "--out") { need(1); a.out = argv[++i];
+        } else if (k == "--out") { need(1); a.out = argv[++i]; a.out_given = true;
+        } else if (k == "--matrix") { need(1); a.matrix = argv[++i];
+        } else if (k == "--mm") { need(1); a.mm = argv[++i];
+        } else if (k == "--save") { need(1); a.save = argv[++i];
         } else if (k == "--seed") { need(1); a.seed = std::strtoull(argv[++i], nullptr, 10);
         } else if (k == "--tol") { need(1); a.tol = std::atof(argv[++i]);
         } else if (k == "--max-iter") { need(1); a.max_iter = std::atoi(argv[++i]);
@@ -86,6 +95,30 @@ struct DVec {
     DVec(const DVec &) = delete;
     ~DVec() { if (p) spmvb_vec_free(p); }
 };
+
+// The matrix of a run: generated on the device from --grid, or read from --matrix (then also kept on the host).
+struct Source {
+    spmvcomp::GridSpec grid{0, 0, 0};
+    spmvcomp::StencilMatrix host;  // --matrix only
+    bool from_file = false;
+};
+
+void generate_csr(const spmvcomp::GridSpec &g, Handle &csr);
+
+Source open_matrix(const Args &a, Handle &csr) {
+    Source s;
+    if (a.have_grid == !a.matrix.empty()) throw Usage{"exactly one of --grid NX NY NZ and --matrix FILE is required"};
+    if (a.have_grid) {
+        s.grid = grid_of(a);
+        generate_csr(s.grid, csr);
+        return s;
+    }
+    s.host = spmvcomp::load_stencil(a.matrix);  // IoError -> exit 1
+    s.grid = s.host.grid;
+    s.from_file = true;
+    ck(spmvb_csr_upload(s.host.n, s.host.n, 0, s.host.row_start.data(), s.host.cols.data(), s.host.vals.data(), &csr.h), "csr_upload");
+    return s;
+}
 
 void generate_csr(const spmvcomp::GridSpec &g, Handle &csr) {
     spmvb_grid sg{};
@@ -121,20 +154,31 @@ double model_bytes_per_row(const std::string &fmt, const spmvb_matrix_info &inf)
 int cmd_generate(const Args &a) {
     const spmvcomp::GridSpec g = grid_of(a);
     const long long nnz = (3LL * g.nx - 2) * (3LL * g.ny - 2) * (3LL * g.nz - 2);
-    std::printf("{\"grid\": [%d, %d, %d], \"rows\": %lld, \"nnz\": %lld, \"csr_bytes\": %lld}\n", g.nx, g.ny, g.nz, (long long)g.rows(),
-                nnz, 8LL * (g.rows() + 1) + 12LL * nnz);
+    long long file_bytes = 0;
+    if (a.out_given || !a.mm.empty()) {  // the device generator's matrix, brought to the host and written out
+        const spmvcomp::StencilMatrix m = spmvcomp::generate_matrix(g);
+        if (a.out_given) {
+            spmvcomp::save(m, a.out);
+            file_bytes = (long long)spmvcomp::serialized_size(m);
+        }
+        if (!a.mm.empty()) spmvcomp::write_matrix_market(m, a.mm);
+    }
+    std::printf("{\"grid\": [%d, %d, %d], \"rows\": %lld, \"nnz\": %lld, \"csr_bytes\": %lld, \"file_bytes\": %lld}\n", g.nx, g.ny, g.nz,
+                (long long)g.rows(), nnz, 8LL * (g.rows() + 1) + 12LL * nnz, file_bytes);
     return 0;
 }
 
 int cmd_bench(const Args &a) {
-    const spmvcomp::GridSpec g = grid_of(a);
     if (a.reps < 1) throw Usage{"--reps must be >= 1"};
     if (a.out != "json" && a.out != "csv") throw Usage{"--out must be json or csv"};
     if (a.format != "ell" && a.format != "vt" && a.format != "pattern" && a.format != "pattern-values")
         throw Usage{"unknown format " + a.format};
-    const int64_t n = g.rows();
     Handle csr, ell, fmt;
-    generate_csr(g, csr);
+    const Source src = open_matrix(a, csr);
+    const spmvcomp::GridSpec g = src.grid;
+    spmvb_matrix_info cinf{};
+    ck(spmvb_matrix_get_info(csr.h, &cinf), "info");
+    const int64_t n = cinf.n;
     build_format(csr, "ell", ell);
     const bool is_ell = a.format == "ell";
     if (!is_ell) build_format(csr, a.format, fmt);
@@ -170,12 +214,26 @@ int cmd_bench(const Args &a) {
     const double bpr = model_bytes_per_row(a.format, inf);
     const double eff_bw = bpr * (double)n * a.reps / sec / 1e9;
     const double ratio = 12.0 * einf.width / bpr;
+    long long file_bytes = 0;
+    if (!a.save.empty()) {  // the serialized format (host structs through the C++ API: built on the device, copied back)
+        const spmvcomp::StencilMatrix m = src.from_file ? src.host : spmvcomp::generate_matrix(g);
+        if (a.format == "ell") {
+            const auto f = spmvcomp::to_ell(m);
+            spmvcomp::save(f, a.save), file_bytes = (long long)spmvcomp::serialized_size(f);
+        } else if (a.format == "vt") {
+            const auto f = spmvcomp::compress_values(m);
+            spmvcomp::save(f, a.save), file_bytes = (long long)spmvcomp::serialized_size(f);
+        } else {
+            const auto f = spmvcomp::compress_patterns(m, a.format == "pattern-values");
+            spmvcomp::save(f, a.save), file_bytes = (long long)spmvcomp::serialized_size(f);
+        }
+    }
     if (a.out == "json")
         std::printf("{\"format\": \"%s\", \"grid\": [%d, %d, %d], \"repetitions\": %d, \"wall_time\": %.9g, \"achieved_gflops\": %.6g, "
                     "\"effective_bandwidth_gbs\": %.6g, \"compression_ratio\": %.6g, \"bytes_per_row\": %.6g, \"checksum\": %.17g, "
-                    "\"checksum_ell\": %.17g, \"max_scaled_deviation_vs_ell\": %.3g, \"rows\": %lld, \"nnz\": %lld}\n",
+                    "\"checksum_ell\": %.17g, \"max_scaled_deviation_vs_ell\": %.3g, \"rows\": %lld, \"nnz\": %lld, \"file_bytes\": %lld}\n",
                     a.format.c_str(), g.nx, g.ny, g.nz, a.reps, sec, gflops, eff_bw, ratio, bpr, checksum, checksum_ell, worst, (long long)n,
-                    (long long)inf.nnz);
+                    (long long)inf.nnz, file_bytes);
     else {
         std::printf("format,nx,ny,nz,repetitions,wall_time,achieved_gflops,effective_bandwidth_gbs,compression_ratio,bytes_per_row,checksum\n");
         std::printf("%s,%d,%d,%d,%d,%.9g,%.6g,%.6g,%.6g,%.6g,%.17g\n", a.format.c_str(), g.nx, g.ny, g.nz, a.reps, sec, gflops, eff_bw, ratio, bpr,
@@ -185,12 +243,14 @@ int cmd_bench(const Args &a) {
 }
 
 int cmd_solve(const Args &a) {
-    const spmvcomp::GridSpec g = grid_of(a);
     if (a.max_iter < 1 || !(a.tol > 0.0)) throw Usage{"--max-iter >= 1 and --tol > 0 are required"};
     if (a.backend != "ell" && a.backend != "vt" && a.backend != "pattern") throw Usage{"unknown backend " + a.backend};
-    const int64_t n = g.rows();
     Handle csr, ell, fmt;
-    generate_csr(g, csr);
+    const Source src = open_matrix(a, csr);
+    const spmvcomp::GridSpec g = src.grid;
+    spmvb_matrix_info cinf{};
+    ck(spmvb_matrix_get_info(csr.h, &cinf), "info");
+    const int64_t n = cinf.n;
     build_format(csr, "ell", ell);
     if (a.backend != "ell") build_format(csr, a.backend == "pattern" ? "pattern-values" : a.backend, fmt);
     const spmvb_matrix *run = a.backend == "ell" ? ell.h : fmt.h;

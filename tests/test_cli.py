@@ -45,13 +45,14 @@ def test_generate_sizes_and_overflow_guard():
     rc, out, _ = run("generate", "--grid", 4, 4, 4)
     assert rc == 0 and json.loads(out)["rows"] == 64 and json.loads(out)["nnz"] == 1000
     rc, out, _ = run("generate", "--grid", 1, 1, 1)
-    assert rc == 0 and json.loads(out) == {"grid": [1, 1, 1], "rows": 1, "nnz": 1, "csr_bytes": 28}
+    assert rc == 0 and json.loads(out) == {"grid": [1, 1, 1], "rows": 1, "nnz": 1, "csr_bytes": 28, "file_bytes": 0}
     rc, _, err = run("generate", "--grid", 100000, 100000, 100000)
     assert rc != 0 and "rows" in err  # SPEC.md:442 sizing error, nonzero exit
 
 
 def test_usage_errors_exit_2():
     for args in (("frobnicate",), (), ("bench", "--grid", 4, 4), ("model",), ("bench", "--grid", 4, 4, 4, "--format", "csr5"),
+                 ("bench", "--format", "ell"), ("bench", "--grid", 4, 4, 4, "--matrix", "m.bin", "--format", "ell"),
                  ("solve", "--grid", 4, 4, 4, "--max-iter", 0)):
         rc, _, err = run(*args)
         assert rc == 2 and err, args

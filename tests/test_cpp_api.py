@@ -15,7 +15,8 @@ def test_shim_is_signature_compatible_with_the_reference_headers():
     (Only where /root/reference is mounted; nothing is copied from it.)"""
     if not os.path.isdir(REF_INC):
         pytest.skip("reference headers not present on this machine")
-    for src in (os.path.join(PKG, "cpp", "spmvcomp_host.cpp"), os.path.join(ROOT, "tests", "cpp", "test_api.cpp")):
+    for src in (os.path.join(PKG, "cpp", "spmvcomp_host.cpp"), os.path.join(PKG, "cpp", "spmvcomp_io.cpp"),
+                os.path.join(ROOT, "tests", "cpp", "test_api.cpp"), os.path.join(ROOT, "tests", "cpp", "test_io.cpp")):
         r = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-I", REF_INC, "-I", os.path.join(ROOT, "include"), src],
                            capture_output=True, text=True)
         assert r.returncode == 0, r.stderr[-2000:]
