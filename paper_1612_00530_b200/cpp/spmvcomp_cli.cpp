@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <filesystem>
 #include <string>
 #include <vector>
 
@@ -81,6 +82,25 @@ spmvcomp::GridSpec grid_of(const Args &a) {
     spmvcomp::GridSpec g{a.nx, a.ny, a.nz};
     spmvcomp::validate(g);  // std::invalid_argument on dims < 1 or more than 2^31-1 rows (grid.hpp:35-47)
     return g;
+}
+
+// A report goes to stdout and, when SPMVCOMP_REPORT_DIR is set, also into that directory as `name` (SPEC.md:500
+// "env var to override report directory"; the reference does not name the variable -- this name is this repository's).
+void emit(const std::string &name, const std::string &text) {
+    std::fputs(text.c_str(), stdout);
+    if (const char *dir = std::getenv("SPMVCOMP_REPORT_DIR"); dir && *dir) {
+        const std::filesystem::path path = std::filesystem::path(dir) / name;
+        std::FILE *f = std::fopen(path.string().c_str(), "w");
+        if (!f || std::fputs(text.c_str(), f) < 0 || std::fclose(f) != 0) throw Failure{"cannot write the report to " + path.string()};
+    }
+}
+template <class... A>
+std::string fmt_str(const char *f, A... a) {
+    const int len = std::snprintf(nullptr, 0, f, a...);
+    std::string out((size_t)len + 1, '\0');
+    std::snprintf(out.data(), out.size(), f, a...);
+    out.resize((size_t)len);
+    return out;
 }
 
 struct Handle {  // device handle with scope-bound lifetime
@@ -228,17 +248,23 @@ int cmd_bench(const Args &a) {
             spmvcomp::save(f, a.save), file_bytes = (long long)spmvcomp::serialized_size(f);
         }
     }
+    // roofline prediction for the configured MachineSpec (perf_model.hpp:59-72): --bandwidth GB/s, else the reference's default 75
+    const double mach_bw = a.bandwidth > 0.0 ? a.bandwidth : 75.0;
+    const double roofline_gflops = mach_bw * (2.0 * (double)inf.nnz / (double)n) / bpr;
+    const std::string stem = "bench_" + a.format + "_" + std::to_string(g.nx) + "x" + std::to_string(g.ny) + "x" + std::to_string(g.nz);
     if (a.out == "json")
-        std::printf("{\"format\": \"%s\", \"grid\": [%d, %d, %d], \"repetitions\": %d, \"wall_time\": %.9g, \"achieved_gflops\": %.6g, "
-                    "\"effective_bandwidth_gbs\": %.6g, \"compression_ratio\": %.6g, \"bytes_per_row\": %.6g, \"checksum\": %.17g, "
-                    "\"checksum_ell\": %.17g, \"max_scaled_deviation_vs_ell\": %.3g, \"rows\": %lld, \"nnz\": %lld, \"file_bytes\": %lld}\n",
-                    a.format.c_str(), g.nx, g.ny, g.nz, a.reps, sec, gflops, eff_bw, ratio, bpr, checksum, checksum_ell, worst, (long long)n,
-                    (long long)inf.nnz, file_bytes);
-    else {
-        std::printf("format,nx,ny,nz,repetitions,wall_time,achieved_gflops,effective_bandwidth_gbs,compression_ratio,bytes_per_row,checksum\n");
-        std::printf("%s,%d,%d,%d,%d,%.9g,%.6g,%.6g,%.6g,%.6g,%.17g\n", a.format.c_str(), g.nx, g.ny, g.nz, a.reps, sec, gflops, eff_bw, ratio, bpr,
-                    checksum);
-    }
+        emit(stem + ".json",
+             fmt_str("{\"format\": \"%s\", \"grid\": [%d, %d, %d], \"repetitions\": %d, \"wall_time\": %.9g, \"achieved_gflops\": %.6g, "
+                     "\"effective_bandwidth_gbs\": %.6g, \"compression_ratio\": %.6g, \"bytes_per_row\": %.6g, \"machine_bandwidth_gbs\": %.6g, "
+                     "\"roofline_gflops\": %.6g, \"checksum\": %.17g, \"checksum_ell\": %.17g, \"max_scaled_deviation_vs_ell\": %.3g, "
+                     "\"rows\": %lld, \"nnz\": %lld, \"file_bytes\": %lld}\n",
+                     a.format.c_str(), g.nx, g.ny, g.nz, a.reps, sec, gflops, eff_bw, ratio, bpr, mach_bw, roofline_gflops, checksum, checksum_ell, worst,
+                     (long long)n, (long long)inf.nnz, file_bytes));
+    else  // fixed column order
+        emit(stem + ".csv",
+             "format,nx,ny,nz,repetitions,wall_time,achieved_gflops,effective_bandwidth_gbs,compression_ratio,bytes_per_row,checksum\n" +
+                 fmt_str("%s,%d,%d,%d,%d,%.9g,%.6g,%.6g,%.6g,%.6g,%.17g\n", a.format.c_str(), g.nx, g.ny, g.nz, a.reps, sec, gflops, eff_bw, ratio, bpr,
+                         checksum));
     return 0;
 }
 
@@ -267,10 +293,10 @@ int cmd_solve(const Args &a) {
     ck(rc, "cg_solve");
     spmvb_matrix_info inf{};
     ck(spmvb_matrix_get_info(run, &inf), "info");
-    std::printf("{\"backend\": \"%s\", \"grid\": [%d, %d, %d], \"iterations\": %d, \"converged\": %s, \"final_residual\": %.6g, "
-                "\"flops_total\": %lld}\n",
-                a.backend.c_str(), g.nx, g.ny, g.nz, it, conv ? "true" : "false", hist[(size_t)it],
-                (long long)it * (2LL * inf.nnz + 12LL * n));
+    emit("solve_" + a.backend + "_" + std::to_string(g.nx) + "x" + std::to_string(g.ny) + "x" + std::to_string(g.nz) + ".json",
+         fmt_str("{\"backend\": \"%s\", \"grid\": [%d, %d, %d], \"iterations\": %d, \"converged\": %s, \"final_residual\": %.6g, "
+                 "\"flops_total\": %lld}\n",
+                 a.backend.c_str(), g.nx, g.ny, g.nz, it, conv ? "true" : "false", hist[(size_t)it], (long long)it * (2LL * inf.nnz + 12LL * n)));
     return conv ? 0 : 1;
 }
 

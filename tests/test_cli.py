@@ -50,6 +50,57 @@ def test_generate_sizes_and_overflow_guard():
     assert rc != 0 and "rows" in err  # SPEC.md:442 sizing error, nonzero exit
 
 
+SCHEMA = os.path.join(ROOT, "paper_1612_00530_b200", "cpp", "report.schema.json")
+
+
+def validate_report(text):
+    """JSON reports validate against the schema shipped in the repo."""
+    import jsonschema
+    with open(SCHEMA) as f:
+        schema = json.load(f)
+    jsonschema.Draft202012Validator.check_schema(schema)
+    obj = json.loads(text)
+    jsonschema.validate(obj, schema)
+    return obj
+
+
+def test_generate_report_validates_against_the_schema():
+    import jsonschema
+    rc, out, _ = run("generate", "--grid", 4, 4, 4)
+    assert rc == 0 and validate_report(out)["rows"] == 64
+    with pytest.raises(jsonschema.ValidationError):
+        validate_report('{"grid": [4, 4, 4], "rows": 64}')
+    with pytest.raises(jsonschema.ValidationError):
+        validate_report('{"backend": "csr", "grid": [4, 4, 4], "iterations": 1, "converged": true, "final_residual": 0, "flops_total": 1}')
+
+
+@pytest.mark.gpu
+def test_reports_validate_and_land_in_the_report_directory(tmp_path):
+    """bench / solve reports validate against the schema; the roofline column follows the configured bandwidth;
+    SPMVCOMP_REPORT_DIR receives a copy of every report."""
+    env = dict(os.environ, SPMVCOMP_REPORT_DIR=str(tmp_path))
+    r = subprocess.run([CLI, "bench", "--grid", "32", "32", "32", "--format", "vt", "--reps", "3", "--bandwidth", "150"],
+                       capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stderr
+    rep = validate_report(r.stdout)
+    assert rep["machine_bandwidth_gbs"] == 150.0
+    assert rep["roofline_gflops"] == pytest.approx(150.0 * (2 * rep["nnz"] / rep["rows"]) / rep["bytes_per_row"], rel=1e-5)
+    assert (tmp_path / "bench_vt_32x32x32.json").read_text() == r.stdout
+    rc, out, _ = run("bench", "--grid", 32, 32, 32, "--format", "pattern", "--reps", 2)
+    assert validate_report(out)["machine_bandwidth_gbs"] == 75.0  # the reference's default MachineSpec (perf_model.hpp)
+    r = subprocess.run([CLI, "bench", "--grid", "16", "16", "16", "--format", "ell", "--reps", "2", "--out", "csv"],
+                       capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0 and (tmp_path / "bench_ell_16x16x16.csv").read_text() == r.stdout
+    assert r.stdout.splitlines()[0] == ("format,nx,ny,nz,repetitions,wall_time,achieved_gflops,effective_bandwidth_gbs,"
+                                        "compression_ratio,bytes_per_row,checksum")
+    r = subprocess.run([CLI, "solve", "--grid", "16", "16", "16", "--backend", "vt"], capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0 and validate_report(r.stdout)["converged"] is True
+    assert (tmp_path / "solve_vt_16x16x16.json").read_text() == r.stdout
+    env["SPMVCOMP_REPORT_DIR"] = str(tmp_path / "missing")
+    r = subprocess.run([CLI, "solve", "--grid", "8", "8", "8"], capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 1 and "cannot write the report" in r.stderr
+
+
 def test_usage_errors_exit_2():
     for args in (("frobnicate",), (), ("bench", "--grid", 4, 4), ("model",), ("bench", "--grid", 4, 4, 4, "--format", "csr5"),
                  ("bench", "--format", "ell"), ("bench", "--grid", 4, 4, 4, "--matrix", "m.bin", "--format", "ell"),
