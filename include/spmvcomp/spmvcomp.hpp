@@ -7,9 +7,8 @@
 // through the C-ABI in spmvcomp_b200.h -- there is no CPU implementation.
 //
 // Declared here: everything on the SpMV path and its first
-// caller, the CG driver with dot / waxpby (section 8f row N1; unpreconditioned only).
-// Not declared: symgs_sweep, model_table*, Matrix Market export (tooling / sequential
-// smoother outside the path, section 8f rows N2-N4).
+// caller, the CG driver with dot / waxpby / symgs_sweep (section 8f rows N1, N4).
+// Not declared: the model_table* emitters (tooling outside the path).  File formats: spmvcomp/io.hpp.
 #pragma once
 
 #include <cstddef>
@@ -181,6 +180,10 @@ void spmv_rows(const PatternCompressedMatrix& a, std::span<const double> x, std:
 double dot(const Vector& u, const Vector& v);                                               // length mismatch -> invalid_argument
 Vector waxpby(double alpha, const Vector& x, double beta, const Vector& y);                 // w = alpha*x + beta*y
 void waxpby_into(double alpha, const Vector& x, double beta, const Vector& y, Vector& w);
+// inc/kernels.hpp:44-48: forward then backward Gauss-Seidel sweep in natural order, in place.  On the device the rows run by
+// hyperplanes of the matrix's grid (m.grid; results bit-identical to the sequential loop); std::invalid_argument for a zero
+// diagonal, a length mismatch, or a matrix without grid provenance / with couplings outside the 27-point neighbourhood.
+void symgs_sweep(const StencilMatrix& m, Vector& x, const Vector& b);
 
 enum class SpmvBackend { ell, vt, pattern };
 const char* backend_name(SpmvBackend b);
@@ -188,7 +191,7 @@ const char* backend_name(SpmvBackend b);
 struct CgConfig {
     int max_iterations = 500;
     double tolerance = 1e-8;  // relative residual ||r||2 / ||b||2
-    int symgs_sweeps = 0;     // 0 = unpreconditioned; >= 1 is not available on the device path (std::invalid_argument)
+    int symgs_sweeps = 0;     // 0 = unpreconditioned; >= 1: SymGS sweeps from a zero guess (needs m.grid, see symgs_sweep)
     SpmvBackend backend = SpmvBackend::ell;
 };
 struct OpStats {

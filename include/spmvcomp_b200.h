@@ -116,6 +116,7 @@ int spmvb_set_device(int device);
  *                     sliding window (listed with their measured times in csrc/spmv_pattern*.cu)
  *   "box_lines":      lines per CTA tile / chunk length of the tensor ring (0 = default)
  *   "host_chunks":    row chunks of the pipelined spmvb_spmv_host (0 = default 8)
+ *   "symgs_graph":    1 (default) the launches of a symgs sweep are recorded into a CUDA graph and replayed; 0 launches directly
  *   "cg_fused_dot":   1 (default) spmvb_cg_solve takes p.Ap from the SpMV kernel when that kernel offers it (pattern format,
  *                     tensor ring, whole square grid): one pass over p and Ap less per iteration; 0 always runs the dot
  *   "last_cg_fused_dot": read-only, 1 when the last spmvb_cg_solve took p.Ap from the SpMV kernel
@@ -226,6 +227,20 @@ int spmvb_waxpby(double alpha, const double *x_dev, double beta, const double *y
  * (iteration in the message and in *iterations). */
 int spmvb_cg_solve(const spmvb_matrix *a, const double *b_dev, double *x_dev, int32_t max_iterations, double tolerance,
                    int32_t *iterations, int32_t *converged, double *residual_history, void *stream);
+
+/* symgs_sweep (inc/kernels.hpp:44-48): one forward then one backward Gauss-Seidel sweep in natural
+ * order, in place, on the whole square matrix as a CSR handle whose rows are the nodes of `grid` (only nx, ny, nz are
+ * read).  Bit-identical to the sequential loop: the rows are processed by hyperplanes ix + 2 iy + 4 iz, which order every
+ * coupling of a 27-point (or sparser) stencil the way the row index does; the schedule is verified against the matrix
+ * first.  SPMVB_ERR_INVALID_ARGUMENT for a zero or missing diagonal (the reference's singularity error) and for a matrix
+ * with couplings the schedule does not order (nothing is written in either case). */
+int spmvb_symgs_sweep(const spmvb_matrix *csr, const spmvb_grid *grid, double *x_dev, const double *b_dev, void *stream);
+/* cg_solve (inc/solver.hpp:40-46) with the SymGS preconditioner: z = symgs_sweeps sweeps on A z = r from a zero guess
+ * (SPEC.md:311,327); `a` is the SpMV backend (any format), `csr` the same matrix for the sweeps.  Per iteration 1 SpMV,
+ * 3 dots (p.Ap, r.r, r.z), 3 waxpbys, 1 preconditioner application.  History and errors as spmvb_cg_solve. */
+int spmvb_pcg_solve(const spmvb_matrix *a, const spmvb_matrix *csr, const spmvb_grid *grid, int32_t symgs_sweeps, const double *b_dev,
+                    double *x_dev, int32_t max_iterations, double tolerance, int32_t *iterations, int32_t *converged,
+                    double *residual_history, void *stream);
 
 /* ---- verification helpers ----------------------------------------------------- */
 /* max_i |y[i]-ref[i]| / den[i] and the number of entries whose bit patterns

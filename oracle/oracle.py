@@ -427,9 +427,21 @@ class DivergenceError(OracleError):  # errors.hpp:22
     pass
 
 
-def cg_solve(a, b, max_iterations=500, tolerance=1e-8):
-    """cg_solve (solver.hpp:40-46), unpreconditioned; `a` is the SpMV backend (Ell, Vt or Pattern).
-    Returns (x, iterations, converged, residual_history)."""
+def symgs_sweep(m, x, b):
+    """symgs_sweep (kernels.hpp:44-48): forward then backward Gauss-Seidel sweep in natural order; returns the new x."""
+    x = np.array(x, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    if x.shape[0] != m.n or b.shape[0] != m.n:
+        raise InvalidArgument(INVALID_ARGUMENT, "length mismatch")
+    fn = lib().orc_symgs_sweep
+    fn.argtypes, fn.restype = [C.c_void_p, C.c_void_p, C.c_void_p], C.c_int
+    _check(fn(C.cast(m.p, C.c_void_p), _ptr(x), _ptr(b)))
+    return x
+
+
+def cg_solve(a, b, max_iterations=500, tolerance=1e-8, symgs_sweeps=0, matrix=None):
+    """cg_solve (solver.hpp:40-46); `a` is the SpMV backend (Ell, Vt or Pattern).  symgs_sweeps >= 1 preconditions with
+    that many SymGS sweeps from a zero guess on `matrix` (the Csr).  Returns (x, iterations, converged, residual_history)."""
     b = np.ascontiguousarray(b, dtype=np.float64)
     if b.shape[0] != a.n:
         raise InvalidArgument(INVALID_ARGUMENT, "length mismatch")
@@ -437,8 +449,16 @@ def cg_solve(a, b, max_iterations=500, tolerance=1e-8):
     x = np.empty(a.n)
     hist = np.zeros(max_iterations + 1)
     it, conv, div = C.c_int32(), C.c_int32(), C.c_int32()
-    _check(lib().orc_cg_solve(fmt, C.cast(a.p, C.c_void_p), a.n, _ptr(b), _ptr(x), max_iterations, tolerance,
-                              C.byref(it), C.byref(conv), _ptr(hist), C.byref(div)))
+    if symgs_sweeps:
+        fn = lib().orc_pcg_solve
+        fn.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int32, C.c_double, C.c_int32,
+                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        fn.restype = C.c_int
+        _check(fn(fmt, C.cast(a.p, C.c_void_p), C.cast(matrix.p, C.c_void_p), a.n, _ptr(b), _ptr(x), max_iterations, tolerance,
+                  symgs_sweeps, C.byref(it), C.byref(conv), _ptr(hist), C.byref(div)))
+    else:
+        _check(lib().orc_cg_solve(fmt, C.cast(a.p, C.c_void_p), a.n, _ptr(b), _ptr(x), max_iterations, tolerance,
+                                  C.byref(it), C.byref(conv), _ptr(hist), C.byref(div)))
     if div.value:
         raise DivergenceError(6, f"non-finite value in iteration {div.value}")
     return x, it.value, bool(conv.value), hist[:it.value + 1].copy()

@@ -1031,6 +1031,68 @@ int orc_cg_solve(int format, const void *a, int32_t n, const double *b, double *
     return ORC_OK;
 }
 
+int orc_symgs_sweep(const orc_csr *m, double *x, const double *b) {
+    /* kernels.hpp:44-48: one forward sweep (rows ascending) then one backward sweep (rows descending),
+     * x[i] <- (b[i] - sum_{j != i} a_ij x[j]) / a_ii with the latest values; the sum runs over the row's entries in
+     * ascending column order, every product and sum rounded separately. */
+    for (int32_t i = 0; i < m->n; i++) {
+        int found = 0;
+        for (int64_t t = m->row_start[i]; t < m->row_start[i + 1]; t++)
+            if (m->cols[t] == i && m->vals[t] != 0.0) found = 1;
+        if (!found) FAIL(ORC_INVALID_ARGUMENT, "symgs_sweep: zero or missing diagonal in row %d (singular)", i);
+    }
+    for (int dir = 0; dir < 2; dir++)
+        for (int32_t k = 0; k < m->n; k++) {
+            const int32_t i = dir == 0 ? k : m->n - 1 - k;
+            double sum = 0.0, diag = 0.0;
+            for (int64_t t = m->row_start[i]; t < m->row_start[i + 1]; t++) {
+                if (m->cols[t] == i) diag = m->vals[t];
+                else sum = sum + m->vals[t] * x[m->cols[t]];
+            }
+            x[i] = (b[i] - sum) / diag;
+        }
+    return ORC_OK;
+}
+
+int orc_pcg_solve(int format, const void *a, const orc_csr *m, int32_t n, const double *b, double *x, int32_t max_iterations,
+                  double tolerance, int32_t sweeps, int32_t *iterations, int32_t *converged, double *history, int32_t *diverged_at) {
+    /* solver.hpp:40-46, SPEC.md:308-311 with the SymGS preconditioner: z <- M^-1 r = `sweeps` symgs_sweep calls on A z = r
+     * from a zero initial guess; per iteration 1 SpMV, 3 dots (p.Ap, r.r, r.z), 3 waxpbys, 1 preconditioner application. */
+    if (max_iterations < 1 || !(tolerance > 0.0) || format < 0 || format > 2 || sweeps < 1 || m->n != n)
+        FAIL(ORC_INVALID_ARGUMENT, "pcg_solve: bad configuration");
+    double *r = malloc((size_t)n * 8), *z = malloc((size_t)n * 8), *p = malloc((size_t)n * 8), *ap = malloc((size_t)n * 8);
+    int rc = ORC_OK;
+    *iterations = 0; *converged = 0; *diverged_at = 0;
+    for (int32_t i = 0; i < n; i++) { x[i] = 0.0; r[i] = b[i]; z[i] = 0.0; }
+    for (int32_t s = 0; s < sweeps && rc == ORC_OK; s++) rc = orc_symgs_sweep(m, z, r);
+    if (rc != ORC_OK) { free(r); free(z); free(p); free(ap); return rc; }
+    for (int32_t i = 0; i < n; i++) p[i] = z[i];
+    double bnorm = sqrt(orc_dot(b, b, n));
+    double rz = orc_dot(r, z, n);
+    history[0] = 1.0;
+    if (bnorm == 0.0) { *converged = 1; free(r); free(z); free(p); free(ap); return ORC_OK; }
+    for (int32_t it = 1; it <= max_iterations; it++) {
+        cg_spmv(format, a, n, p, ap);
+        double alpha = rz / orc_dot(p, ap, n);
+        orc_waxpby(1.0, x, alpha, p, x, n);
+        orc_waxpby(1.0, r, -alpha, ap, r, n);
+        double rr = orc_dot(r, r, n);
+        double rel = sqrt(rr) / bnorm;
+        *iterations = it;
+        history[it] = rel;
+        if (!isfinite(alpha) || !isfinite(rel)) { *diverged_at = it; break; }
+        if (rel <= tolerance) { *converged = 1; break; }
+        for (int32_t i = 0; i < n; i++) z[i] = 0.0;
+        for (int32_t s = 0; s < sweeps; s++) orc_symgs_sweep(m, z, r);
+        double rz_new = orc_dot(r, z, n);
+        double beta = rz_new / rz;
+        rz = rz_new;
+        orc_waxpby(1.0, z, beta, p, p, n);
+    }
+    free(r); free(z); free(p); free(ap);
+    return ORC_OK;
+}
+
 /* ------------------------------------------------------------------------- */
 /* byte model                                                                 */
 /* ------------------------------------------------------------------------- */

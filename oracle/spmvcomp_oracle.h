@@ -173,6 +173,13 @@ void orc_waxpby(double alpha, const double *x, double beta, const double *y, dou
 int orc_cg_solve(int format, const void *a, int32_t n, const double *b, double *x, int32_t max_iterations,
                  double tolerance, int32_t *iterations, int32_t *converged, double *history, int32_t *diverged_at);
 
+/* symgs_sweep (kernels.hpp:44-48): forward then backward Gauss-Seidel in natural order, in place;
+ * ORC_INVALID_ARGUMENT for a zero or missing diagonal ("singularity error"). */
+int orc_symgs_sweep(const orc_csr *m, double *x, const double *b);
+/* CG with the SymGS preconditioner (z = `sweeps` sweeps from a zero guess); m = the matrix as CSR. */
+int orc_pcg_solve(int format, const void *a, const orc_csr *m, int32_t n, const double *b, double *x, int32_t max_iterations,
+                  double tolerance, int32_t sweeps, int32_t *iterations, int32_t *converged, double *history, int32_t *diverged_at);
+
 /* ---- byte model (perf_model.hpp:49-80) -------------------- */
 typedef struct orc_cost {
     double bytes_per_row, flops_per_row, bytes_per_flop;

@@ -88,7 +88,7 @@ SYMBOLS = [
     "spmvb_matrix_stream_bytes", "spmvb_matrix_download", "spmvb_matrix_stream_ptr", "spmvb_matrix_destroy",
     "spmvb_vec_alloc", "spmvb_vec_free", "spmvb_vec_upload", "spmvb_vec_download", "spmvb_vec_fill",
     "spmvb_spmv", "spmvb_spmv_host", "spmvb_compare", "spmvb_row_abs_scale", "spmvb_dot", "spmvb_waxpby",
-    "spmvb_cg_solve",
+    "spmvb_cg_solve", "spmvb_symgs_sweep", "spmvb_pcg_solve",
 ]
 
 if not os.path.exists(SO_PATH):
@@ -130,6 +130,8 @@ lib.spmvb_row_abs_scale.argtypes = [_vp, _vp, _i64, _vp, _vp]
 lib.spmvb_dot.argtypes = [_vp, _vp, _i64, C.POINTER(_f64), _vp]
 lib.spmvb_waxpby.argtypes = [_f64, _vp, _f64, _vp, _vp, _i64, _vp]
 lib.spmvb_cg_solve.argtypes = [_vp, _vp, _vp, _i32, _f64, C.POINTER(_i32), C.POINTER(_i32), _vp, _vp]
+lib.spmvb_symgs_sweep.argtypes = [_vp, C.POINTER(Grid), _vp, _vp, _vp]
+lib.spmvb_pcg_solve.argtypes = [_vp, _vp, C.POINTER(Grid), _i32, _vp, _vp, _i32, _f64, C.POINTER(_i32), C.POINTER(_i32), _vp, _vp]
 lib.spmvb_set_option.argtypes = [C.c_char_p, C.c_int]
 lib.spmvb_get_option.argtypes = [C.c_char_p, C.POINTER(C.c_int)]
 lib.spmvb_device_count.argtypes = [C.POINTER(C.c_int)]

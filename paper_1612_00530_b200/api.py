@@ -329,12 +329,28 @@ class CgReport:
         return self.residual_history[-1]
 
 
-def cg_solve(a: DeviceMatrix, b, max_iterations=500, tolerance=1e-8, stream=None):
-    """cg_solve (solver.hpp:40-46), unpreconditioned, on the device.  b: device vector; returns (x, CgReport)."""
+def symgs_sweep(csr: DeviceMatrix, grid: GridSpec, x, b, stream=None):
+    """symgs_sweep (kernels.hpp:44-48) in place on device vectors: the natural-order sweep by hyperplanes of `grid`."""
+    g = cabi.Grid(grid.nx, grid.ny, grid.nz, 0.0, 0.0, 0, 0, 0.0, 0.0)
+    check(lib.spmvb_symgs_sweep(csr.h, C.byref(g), _ptr(x), _ptr(b), _stream(stream)))
+
+
+def cg_solve(a: DeviceMatrix, b, max_iterations=500, tolerance=1e-8, stream=None, symgs_sweeps=0, csr=None, grid=None):
+    """cg_solve (solver.hpp:40-46) on the device.  b: device vector; returns (x, CgReport).  symgs_sweeps >= 1 preconditions
+    with that many SymGS sweeps from a zero guess (needs the matrix as `csr` and its `grid`)."""
     n = a.n
     x = DeviceVector(n)
     hist = np.zeros(max_iterations + 1, dtype=np.float64)
     it, conv = C.c_int32(), C.c_int32()
+    if symgs_sweeps:
+        if csr is None or grid is None:
+            raise InvalidArgument("cg_solve: the SymGS preconditioner needs csr= and grid=")
+        g = cabi.Grid(grid.nx, grid.ny, grid.nz, 0.0, 0.0, 0, 0, 0.0, 0.0)
+        check(lib.spmvb_pcg_solve(a.h, csr.h, C.byref(g), symgs_sweeps, _ptr(b), _ptr(x), max_iterations, tolerance, C.byref(it),
+                                  C.byref(conv), _ptr(hist), _stream(stream)))
+        k = it.value
+        applications = k + (0 if conv.value else 1)
+        return x, CgReport(k, bool(conv.value), hist[:k + 1].tolist(), k * (2 * a.nnz + 12 * n) + applications * symgs_sweeps * 4 * a.nnz)
     check(lib.spmvb_cg_solve(a.h, _ptr(b), _ptr(x), max_iterations, tolerance, C.byref(it), C.byref(conv), _ptr(hist),
                              _stream(stream)))
     k = it.value

@@ -3,6 +3,7 @@
 //   spmvcomp_cli bench     (--grid NX NY NZ | --matrix m.bin) --format ell|vt|pattern|pattern-values [--reps R] [--out json|csv]
 //                          [--seed S] [--save format.bin]
 //   spmvcomp_cli solve     (--grid NX NY NZ | --matrix m.bin) [--backend ell|vt|pattern] [--tol T] [--max-iter K]
+//                          [--precond none|symgs|symgs:SWEEPS]
 //   spmvcomp_cli model     --bandwidth GB/s [--formats ell,vt,pattern,pattern-values]
 //   spmvcomp_cli calibrate
 // Exit codes: 0 success, 1 verification / convergence failure, 2 usage error.
@@ -42,7 +43,7 @@ struct Args {
     int nx = 0, ny = 0, nz = 0, reps = 100, max_iter = 500;
     bool have_grid = false;
     std::string format = "pattern-values", backend = "pattern", out = "json", formats = "ell,vt,pattern,pattern-values";
-    std::string matrix, mm, save;
+    std::string matrix, mm, save, precond = "none";
     bool out_given = false;
     double tol = 1e-8, bandwidth = 0.0;
     unsigned long long seed = 7;
@@ -67,6 +68,7 @@ Args parse(int argc, char **argv) {
         } else if (k == "--matrix") { need(1); a.matrix = argv[++i];
         } else if (k == "--mm") { need(1); a.mm = argv[++i];
         } else if (k == "--save") { need(1); a.save = argv[++i];
+        } else if (k == "--precond") { need(1); a.precond = argv[++i];
         } else if (k == "--seed") { need(1); a.seed = std::strtoull(argv[++i], nullptr, 10);
         } else if (k == "--tol") { need(1); a.tol = std::atof(argv[++i]);
         } else if (k == "--max-iter") { need(1); a.max_iter = std::atoi(argv[++i]);
@@ -271,6 +273,10 @@ int cmd_bench(const Args &a) {
 int cmd_solve(const Args &a) {
     if (a.max_iter < 1 || !(a.tol > 0.0)) throw Usage{"--max-iter >= 1 and --tol > 0 are required"};
     if (a.backend != "ell" && a.backend != "vt" && a.backend != "pattern") throw Usage{"unknown backend " + a.backend};
+    int sweeps = 0;  // SPEC.md:456 precond: none | symgs(sweeps)
+    if (a.precond == "symgs") sweeps = 1;
+    else if (a.precond.rfind("symgs:", 0) == 0) sweeps = std::atoi(a.precond.c_str() + 6);
+    if (a.precond != "none" && sweeps < 1) throw Usage{"--precond must be none, symgs or symgs:SWEEPS with SWEEPS >= 1"};
     Handle csr, ell, fmt;
     const Source src = open_matrix(a, csr);
     const spmvcomp::GridSpec g = src.grid;
@@ -285,7 +291,10 @@ int cmd_solve(const Args &a) {
     ck(spmvb_spmv(ell.h, ones.p, 0, n, b.p, 0, (int32_t)n, nullptr), "spmv");  // b = A * ones
     std::vector<double> hist((size_t)a.max_iter + 1);
     int32_t it = 0, conv = 0;
-    const int rc = spmvb_cg_solve(run, b.p, x.p, a.max_iter, a.tol, &it, &conv, hist.data(), nullptr);
+    spmvb_grid sg{};
+    sg.nx = g.nx, sg.ny = g.ny, sg.nz = g.nz;
+    const int rc = sweeps > 0 ? spmvb_pcg_solve(run, csr.h, &sg, sweeps, b.p, x.p, a.max_iter, a.tol, &it, &conv, hist.data(), nullptr)
+                              : spmvb_cg_solve(run, b.p, x.p, a.max_iter, a.tol, &it, &conv, hist.data(), nullptr);
     if (rc == SPMVB_ERR_DIVERGENCE) {
         std::fprintf(stderr, "divergence: %s\n", spmvb_last_error());
         return 1;
@@ -294,9 +303,10 @@ int cmd_solve(const Args &a) {
     spmvb_matrix_info inf{};
     ck(spmvb_matrix_get_info(run, &inf), "info");
     emit("solve_" + a.backend + "_" + std::to_string(g.nx) + "x" + std::to_string(g.ny) + "x" + std::to_string(g.nz) + ".json",
-         fmt_str("{\"backend\": \"%s\", \"grid\": [%d, %d, %d], \"iterations\": %d, \"converged\": %s, \"final_residual\": %.6g, "
-                 "\"flops_total\": %lld}\n",
-                 a.backend.c_str(), g.nx, g.ny, g.nz, it, conv ? "true" : "false", hist[(size_t)it], (long long)it * (2LL * inf.nnz + 12LL * n)));
+         fmt_str("{\"backend\": \"%s\", \"preconditioner\": \"%s\", \"grid\": [%d, %d, %d], \"iterations\": %d, \"converged\": %s, "
+                 "\"final_residual\": %.6g, \"flops_total\": %lld}\n",
+                 a.backend.c_str(), a.precond.c_str(), g.nx, g.ny, g.nz, it, conv ? "true" : "false", hist[(size_t)it],
+                 (long long)it * (2LL * inf.nnz + 12LL * n) + (long long)(sweeps > 0 ? it + (conv ? 0 : 1) : 0) * sweeps * 4LL * inf.nnz));
     return conv ? 0 : 1;
 }
 

@@ -390,11 +390,23 @@ Vector waxpby(double alpha, const Vector& x, double beta, const Vector& y) {
 const char* backend_name(SpmvBackend b) {
     return b == SpmvBackend::ell ? "ell" : (b == SpmvBackend::vt ? "vt" : "pattern");
 }
+void symgs_sweep(const StencilMatrix& m, Vector& x, const Vector& b) {
+    if ((std::int64_t)x.size() != m.n || (std::int64_t)b.size() != m.n) throw std::invalid_argument("symgs_sweep: x or b has the wrong length");
+    if (m.grid.rows() != m.n) throw std::invalid_argument("symgs_sweep: the device sweep needs the matrix's grid (StencilMatrix::grid)");
+    DeviceMatrix csr(m);
+    b200::DeviceVector dx(x), db(b);
+    spmvb_grid sg{};
+    sg.nx = m.grid.nx, sg.ny = m.grid.ny, sg.nz = m.grid.nz;
+    throw_on_error(spmvb_symgs_sweep(csr.handle(), &sg, dx.data(), db.data(), nullptr));
+    x = dx.download();
+}
+
 std::pair<Vector, CgReport> cg_solve(const StencilMatrix& m, const Vector& b, const CgConfig& cfg) {
     if ((std::int64_t)b.size() != m.n) throw std::invalid_argument("cg_solve: b has the wrong length");
     if (cfg.max_iterations < 1 || !(cfg.tolerance > 0.0)) throw std::invalid_argument("cg_solve: need max_iterations >= 1 and tolerance > 0");
-    if (cfg.symgs_sweeps != 0)
-        throw std::invalid_argument("cg_solve: the SymGS preconditioner is sequential by definition and is not part of the device path");
+    if (cfg.symgs_sweeps < 0) throw std::invalid_argument("cg_solve: symgs_sweeps must be >= 0");
+    if (cfg.symgs_sweeps > 0 && m.grid.rows() != m.n)
+        throw std::invalid_argument("cg_solve: the SymGS preconditioner needs the matrix's grid (StencilMatrix::grid)");
     DeviceMatrix csr(m);
     DeviceMatrix a = cfg.backend == SpmvBackend::ell ? csr.to_ell()
                    : cfg.backend == SpmvBackend::vt ? csr.compress_values() : csr.compress_patterns(true);
@@ -403,8 +415,13 @@ std::pair<Vector, CgReport> cg_solve(const StencilMatrix& m, const Vector& b, co
     rep.residual_history.assign((std::size_t)cfg.max_iterations + 1, 0.0);
     std::int32_t it = 0, conv = 0;
     const auto t0 = std::chrono::steady_clock::now();
-    const int rc = spmvb_cg_solve(a.handle(), db.data(), dx.data(), cfg.max_iterations, cfg.tolerance, &it, &conv,
-                                  rep.residual_history.data(), nullptr);
+    spmvb_grid sg{};
+    sg.nx = m.grid.nx, sg.ny = m.grid.ny, sg.nz = m.grid.nz;
+    const int rc = cfg.symgs_sweeps > 0
+                       ? spmvb_pcg_solve(a.handle(), csr.handle(), &sg, cfg.symgs_sweeps, db.data(), dx.data(), cfg.max_iterations, cfg.tolerance,
+                                         &it, &conv, rep.residual_history.data(), nullptr)
+                       : spmvb_cg_solve(a.handle(), db.data(), dx.data(), cfg.max_iterations, cfg.tolerance, &it, &conv,
+                                        rep.residual_history.data(), nullptr);
     const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     if (rc == SPMVB_ERR_DIVERGENCE) throw DivergenceError(it, spmvb_last_error());
     throw_on_error(rc);
@@ -415,9 +432,11 @@ std::pair<Vector, CgReport> cg_solve(const StencilMatrix& m, const Vector& b, co
     rep.per_op["spmv"] = {it, it * spmv_flops(m.nnz()), 0.0};
     rep.per_op["dot"] = {3LL * it, 3LL * it * dot_flops(m.n), 0.0};
     rep.per_op["waxpby"] = {3LL * it, 3LL * it * waxpby_flops(m.n), 0.0};
-    rep.per_op["precond"] = {0, 0, 0.0};
+    // one application before the loop and one per iteration that goes on: symgs_flops per sweep (inc/kernels.hpp:17)
+    const std::int64_t applications = cfg.symgs_sweeps > 0 ? (std::int64_t)it + (conv ? 0 : 1) : 0;
+    rep.per_op["precond"] = {applications, applications * cfg.symgs_sweeps * symgs_flops(m.nnz()), 0.0};
     rep.per_op["spmv"].seconds = secs;  // the loop is timed as a whole on the device path
-    rep.flops_total = rep.per_op["spmv"].flops + rep.per_op["dot"].flops + rep.per_op["waxpby"].flops;
+    rep.flops_total = rep.per_op["spmv"].flops + rep.per_op["dot"].flops + rep.per_op["waxpby"].flops + rep.per_op["precond"].flops;
     return {dx.download(), rep};
 }
 

@@ -57,6 +57,8 @@ void destroy(spmvb_matrix *a) {
     if (a->scratch_x) cudaFree(a->scratch_x);
     if (a->scratch_y) cudaFree(a->scratch_y);
     if (a->cg_ws) cudaFree(a->cg_ws);
+    if (a->symgs_graph.exec) cudaGraphExecDestroy(a->symgs_graph.exec);
+    if (a->symgs_graph.capture_stream) cudaStreamDestroy(a->symgs_graph.capture_stream);
     for (auto &st : a->pipe_streams) if (st) cudaStreamDestroy(st);
     for (auto &ev : a->pipe_events) if (ev) cudaEventDestroy(ev);
     if (a->d_masks) cudaFree(a->d_masks);
@@ -252,6 +254,7 @@ static int *option_slot(const char *key) {
     if (!strcmp(key, "host_chunks")) return &o.host_chunks;
     if (!strcmp(key, "cg_keep_workspace")) return &o.cg_keep_workspace;
     if (!strcmp(key, "cg_fused_dot")) return &o.cg_fused_dot;
+    if (!strcmp(key, "symgs_graph")) return &o.symgs_graph;
     if (!strcmp(key, "last_cg_fused_dot")) return &o.last_cg_fused_dot;
     if (!strcmp(key, "last_pattern_kernel")) return &o.last_pattern_kernel;
     return nullptr;

@@ -67,6 +67,14 @@ constexpr uint32_t kGenericMask = 0xFFFFFFFFu;
 
 }  // namespace spmvb
 
+struct SymgsGraph {  // the recorded launches of one symgs sweep (symgs.cu)
+    cudaGraphExec_t exec = nullptr;
+    cudaStream_t capture_stream = nullptr;
+    const double *b = nullptr;
+    double *x = nullptr;
+    int nx = 0, ny = 0, nz = 0;
+};
+
 struct spmvb_matrix {
     int32_t format = 0;
     int32_t device = 0;
@@ -86,6 +94,8 @@ struct spmvb_matrix {
     // work vectors of spmvb_cg_solve (r, p, Ap: 3n doubles), kept between solves on this handle unless "cg_keep_workspace" is 0
     mutable double *cg_ws = nullptr;
     mutable int cg_ws_busy = 0;  // taken with an atomic exchange: a second concurrent solve on the handle allocates its own
+    mutable SymgsGraph symgs_graph;
+    mutable int symgs_checked[3] = {0, 0, 0};  // CSR handles: grid whose hyperplane schedule was verified against the matrix (symgs.cu)
     // streams / events of the pipelined host-buffer SpMV (created on first use)
     mutable cudaStream_t pipe_streams[3] = {};
     mutable cudaEvent_t pipe_events[128] = {};
@@ -111,6 +121,7 @@ struct Options {
     int box_prefetch_l1 = 0; // L1 prefetch distance in lines (0 = off)
     int debug_nochain = 0;   // measurement only
     int box_lines = 0;       // lines per CTA march of the tensor-ring kernel (0 = default)
+    int symgs_graph = 1;        // 1: a symgs sweep's launches are recorded into a CUDA graph and replayed
     int cg_fused_dot = 1;       // 1: cg_solve takes p.Ap from the SpMV kernel where that kernel offers it (pattern format, tensor ring)
     int last_cg_fused_dot = 0;  // read-only: 1 when the last iteration of the last cg_solve took p.Ap from the SpMV kernel
     int cg_keep_workspace = 1;  // 1: spmvb_cg_solve keeps its 3n work doubles on the handle until spmvb_free

@@ -1,0 +1,253 @@
+// symgs_sweep on the device (inc/kernels.hpp:44-48) and CG preconditioned with it
+// (inc/solver.hpp:40-46).
+//
+// The reference's sweep is sequential by definition: natural order, every row uses the latest values.  For the matrix
+// of a grid (27-point couplings or a subset of them) the same result comes out of a hyperplane schedule: the row of
+// node (ix, iy, iz) depends, in the forward sweep, on the rows with a smaller index among its neighbours, and every one
+// of those lies on a lower plane  level = ix + 2 iy + 4 iz  (the smallest integer weights with that property for
+// couplings dx, dy, dz in {-1, 0, 1}); the backward sweep walks the levels downwards.  Rows of one level do not read
+// one another, so a level is one kernel launch, and a sweep is 2 * ((nx-1) + 2 (ny-1) + 4 (nz-1) + 1) launches whose
+// results are bit-identical to the sequential loop (same per-row expression: entries in ascending column order,
+// products and sums rounded separately, one subtraction, one division).  The schedule is checked against the matrix on
+// the device before the first sweep (every off-diagonal column must lie on the side of the level order that its index
+// order says): a matrix that does not fit -- explicit rows with other couplings -- is refused, not swept wrongly.
+// It is launch-bound (256^3: 3570 launches per sweep), far from the SpMV's rate, and far ahead of a sequential sweep.
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+#include "spmv_internal.cuh"
+
+namespace spmvb {
+
+__device__ __forceinline__ int level_of(int64_t row, int nx, int ny) {
+    const int ix = (int)(row % nx), iy = (int)((row / nx) % ny), iz = (int)(row / ((int64_t)nx * ny));
+    return ix + 2 * iy + 4 * iz;
+}
+
+// flags[0]: a row without a non-zero diagonal; flags[1]: a coupling the hyperplane schedule does not order
+__global__ void symgs_check_kernel(const int64_t *__restrict__ row_start, const int32_t *__restrict__ cols, const double *__restrict__ vals,
+                                   int n, int nx, int ny, int *__restrict__ flags) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int li = level_of(i, nx, ny);
+    bool diag = false, fits = true;
+    for (int64_t t = row_start[i]; t < row_start[i + 1]; t++) {
+        const int j = cols[t];
+        if (j == i) {
+            diag = vals[t] != 0.0;
+            continue;
+        }
+        const int lj = level_of(j, nx, ny);
+        fits = fits && (j < i ? lj < li : lj > li);
+    }
+    if (!diag) atomicOr(&flags[0], 1);
+    if (!fits) atomicOr(&flags[1], 1);
+}
+
+// the rows of one level: a thread per (iy, iz) with iz in [iz_lo, iz_lo + n_iz)
+__global__ void symgs_level_kernel(const int64_t *__restrict__ row_start, const int32_t *__restrict__ cols, const double *__restrict__ vals,
+                                   double *x, const double *__restrict__ b, int nx, int ny, int level, int iz_lo, int n_iz) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ny * n_iz) return;
+    const int iy = t % ny, iz = iz_lo + t / ny;
+    const int ix = level - 2 * iy - 4 * iz;
+    if (ix < 0 || ix >= nx) return;
+    const int i = ix + nx * (iy + ny * iz);
+    // Entries in ascending column order; the loads of a batch (columns, values, then the gathers of x) are issued together
+    // before the ordered sums consume them: a row costs a few memory latencies instead of one per entry (the launch of a
+    // level lasts as long as its slowest row).
+    constexpr int B = 27;  // a 27-point row in one batch: row_start -> columns, values -> x -> sum, four dependent latencies
+    const int64_t k0 = row_start[i];
+    const int cnt = (int)(row_start[i + 1] - k0);
+    double sum = 0.0, diag = 0.0;
+    for (int base = 0; base < cnt; base += B) {
+        int c[B];
+        double v[B], xv[B];
+#pragma unroll
+        for (int j = 0; j < B; j++) {
+            const bool in = base + j < cnt;
+            c[j] = in ? cols[k0 + base + j] : i;
+            v[j] = in ? vals[k0 + base + j] : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < B; j++) xv[j] = c[j] != i ? x[c[j]] : 0.0;
+#pragma unroll
+        for (int j = 0; j < B; j++) {
+            if (base + j >= cnt) continue;
+            if (c[j] == i) diag = v[j];
+            else sum = __dadd_rn(sum, __dmul_rn(v[j], xv[j]));
+        }
+    }
+    x[i] = __ddiv_rn(__dsub_rn(b[i], sum), diag);  // inc/kernels.hpp:46
+}
+
+static int check_schedule(const spmvb_matrix *a, const spmvb_grid *g, cudaStream_t st) {
+    if (a->symgs_checked[0] == g->nx && a->symgs_checked[1] == g->ny && a->symgs_checked[2] == g->nz) return SPMVB_OK;
+    int *flags = nullptr;
+    SPMVB_CUDA(cudaMalloc(&flags, 2 * sizeof(int)));
+    int h[2] = {0, 0};
+    cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(h), st);
+    if (e == cudaSuccess) {
+        symgs_check_kernel<<<(a->n + 255) / 256, 256, 0, st>>>(static_cast<const int64_t *>(a->s[SPMVB_S_CSR_ROW_START]),
+                                                              static_cast<const int32_t *>(a->s[SPMVB_S_CSR_COLS]),
+                                                              static_cast<const double *>(a->s[SPMVB_S_CSR_VALS]), a->n, g->nx, g->ny, flags);
+        e = cudaMemcpyAsync(h, flags, sizeof(h), cudaMemcpyDeviceToHost, st);
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(flags);
+    if (e != cudaSuccess) return fail(SPMVB_ERR_CUDA, "symgs_sweep: schedule check failed: %s", cudaGetErrorString(e));
+    if (h[0]) return fail(SPMVB_ERR_INVALID_ARGUMENT, "symgs_sweep: a row has a zero or missing diagonal (singular)");
+    if (h[1])
+        return fail(SPMVB_ERR_INVALID_ARGUMENT,
+                    "symgs_sweep: the matrix has couplings the %dx%dx%d hyperplane schedule does not order; the sweep is sequential for it",
+                    g->nx, g->ny, g->nz);
+    a->symgs_checked[0] = g->nx, a->symgs_checked[1] = g->ny, a->symgs_checked[2] = g->nz;
+    return SPMVB_OK;
+}
+
+static void launch_levels(const spmvb_matrix *a, const spmvb_grid *g, double *x, const double *b, cudaStream_t st) {
+    const int nx = g->nx, ny = g->ny, nz = g->nz;
+    const int levels = (nx - 1) + 2 * (ny - 1) + 4 * (nz - 1) + 1;
+    const auto *rs = static_cast<const int64_t *>(a->s[SPMVB_S_CSR_ROW_START]);
+    const auto *cols = static_cast<const int32_t *>(a->s[SPMVB_S_CSR_COLS]);
+    const auto *vals = static_cast<const double *>(a->s[SPMVB_S_CSR_VALS]);
+    for (int dir = 0; dir < 2; dir++)
+        for (int k = 0; k < levels; k++) {
+            const int level = dir == 0 ? k : levels - 1 - k;
+            // planes that hold a node of this level: 0 <= level - 4 iz - 2 iy - ix with iy <= ny-1, ix <= nx-1
+            const int rest = level - (nx - 1) - 2 * (ny - 1);
+            const int iz_lo = rest > 0 ? (rest + 3) / 4 : 0;
+            const int iz_hi = std::min(nz - 1, level / 4);
+            if (iz_hi < iz_lo) continue;
+            const int n_iz = iz_hi - iz_lo + 1;
+            const int threads = 128;
+            symgs_level_kernel<<<(ny * n_iz + threads - 1) / threads, threads, 0, st>>>(rs, cols, vals, x, b, nx, ny, level, iz_lo, n_iz);
+        }
+}
+
+// A sweep is thousands of tiny dependent launches: they are recorded once into a CUDA graph (kept on the handle, keyed by
+// the vectors and the grid) and replayed, which takes the host's per-launch cost out of every sweep after the first
+// (the preconditioner applies the sweep to the same two vectors in every iteration).  "symgs_graph" = 0 launches directly.
+static int sweep_device(const spmvb_matrix *a, const spmvb_grid *g, double *x, const double *b, cudaStream_t st) {
+    SymgsGraph &c = a->symgs_graph;
+    const bool hit = c.exec && c.x == x && c.b == b && c.nx == g->nx && c.ny == g->ny && c.nz == g->nz;
+    if (options().symgs_graph && !hit) {
+        if (c.exec) cudaGraphExecDestroy(c.exec), c.exec = nullptr;
+        if (!c.capture_stream && cudaStreamCreateWithFlags(&c.capture_stream, cudaStreamNonBlocking) != cudaSuccess) c.capture_stream = nullptr;
+        cudaGraph_t graph = nullptr;
+        if (c.capture_stream && cudaStreamBeginCapture(c.capture_stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+            launch_levels(a, g, x, b, c.capture_stream);
+            if (cudaStreamEndCapture(c.capture_stream, &graph) == cudaSuccess && graph &&
+                cudaGraphInstantiate(&c.exec, graph, nullptr, nullptr, 0) == cudaSuccess) {
+                c.x = x, c.b = b, c.nx = g->nx, c.ny = g->ny, c.nz = g->nz;
+            } else {
+                c.exec = nullptr;
+            }
+            if (graph) cudaGraphDestroy(graph);
+        }
+        (void)cudaGetLastError();  // a failed capture falls back to direct launches below
+    }
+    if (options().symgs_graph && c.exec) {
+        SPMVB_CUDA(cudaGraphLaunch(c.exec, st));
+        return SPMVB_OK;
+    }
+    launch_levels(a, g, x, b, st);
+    return check_launch("symgs_level");
+}
+
+}  // namespace spmvb
+
+using namespace spmvb;
+
+extern "C" {
+
+int spmvb_symgs_sweep(const spmvb_matrix *csr, const spmvb_grid *grid, double *x_dev, const double *b_dev, void *stream) {
+    if (!csr || !grid || !x_dev || !b_dev) return fail(SPMVB_ERR_INVALID_ARGUMENT, "symgs_sweep: NULL argument");
+    if (csr->format != SPMVB_FMT_CSR || csr->row_offset != 0 || csr->n_cols != csr->n)
+        return fail(SPMVB_ERR_INVALID_ARGUMENT, "symgs_sweep: needs the whole square matrix as a CSR handle (inc/kernels.hpp:48)");
+    if (grid->nx < 1 || grid->ny < 1 || grid->nz < 1 || (int64_t)grid->nx * grid->ny * grid->nz != csr->n)
+        return fail(SPMVB_ERR_INVALID_ARGUMENT, "symgs_sweep: the grid does not have the matrix's %d rows", csr->n);
+    if ((int64_t)grid->nx + 2LL * grid->ny + 4LL * grid->nz > INT32_MAX / 2) return fail(SPMVB_ERR_INVALID_ARGUMENT, "symgs_sweep: grid too large");
+    if (csr->n == 0) return SPMVB_OK;
+    cudaStream_t st = as_stream(stream);
+    SPMVB_TRY(check_schedule(csr, grid, st));
+    return sweep_device(csr, grid, x_dev, b_dev, st);
+}
+
+int spmvb_pcg_solve(const spmvb_matrix *a, const spmvb_matrix *csr, const spmvb_grid *grid, int32_t symgs_sweeps, const double *b_dev,
+                    double *x_dev, int32_t max_iterations, double tolerance, int32_t *iterations, int32_t *converged,
+                    double *residual_history, void *stream) {
+    if (!a || !csr || !grid || !b_dev || !x_dev || !iterations || !converged) return fail(SPMVB_ERR_INVALID_ARGUMENT, "pcg_solve: NULL argument");
+    if (max_iterations < 1 || !(tolerance > 0.0) || symgs_sweeps < 1)
+        return fail(SPMVB_ERR_INVALID_ARGUMENT, "pcg_solve: need max_iterations >= 1, tolerance > 0 and symgs_sweeps >= 1");
+    if (a->row_offset != 0 || a->n != csr->n) return fail(SPMVB_ERR_INVALID_ARGUMENT, "pcg_solve: backend and matrix must be the same whole matrix");
+    cudaStream_t st = as_stream(stream);
+    const int64_t n = a->n;
+    *iterations = 0;
+    *converged = 0;
+    // the schedule check (and the singularity error) before anything is written
+    if (csr->format != SPMVB_FMT_CSR) return fail(SPMVB_ERR_INVALID_ARGUMENT, "pcg_solve: the preconditioner needs the CSR handle");
+    if ((int64_t)grid->nx * grid->ny * grid->nz != n) return fail(SPMVB_ERR_INVALID_ARGUMENT, "pcg_solve: the grid does not have the matrix's rows");
+    if (n > 0) SPMVB_TRY(check_schedule(csr, grid, st));
+    const int64_t n_pad = (n + 63) / 64 * 64;
+    double *ws = nullptr;
+    SPMVB_CUDA(cudaMalloc(&ws, (size_t)std::max<int64_t>(n_pad, 64) * 4 * sizeof(double)));
+    double *r = ws, *z = ws + n_pad, *p = ws + 2 * n_pad, *ap = ws + 3 * n_pad;
+    auto done = [&](int code) {
+        cudaStreamSynchronize(st);
+        cudaFree(ws);
+        return code;
+    };
+    auto precondition = [&]() -> int {  // z <- M^-1 r: sweeps from a zero initial guess
+        if (cudaMemsetAsync(z, 0, (size_t)n * 8, st) != cudaSuccess) return fail(SPMVB_ERR_CUDA, "pcg_solve: memset failed");
+        for (int s = 0; s < symgs_sweeps; s++) SPMVB_TRY(sweep_device(csr, grid, z, r, st));
+        return SPMVB_OK;
+    };
+    int rc = cudaMemsetAsync(x_dev, 0, (size_t)n * 8, st) == cudaSuccess ? SPMVB_OK : fail(SPMVB_ERR_CUDA, "pcg_solve: memset failed");
+    if (rc == SPMVB_OK) rc = spmvb_waxpby(1.0, b_dev, 0.0, b_dev, r, n, stream);
+    if (rc == SPMVB_OK) rc = precondition();
+    if (rc == SPMVB_OK) rc = spmvb_waxpby(1.0, z, 0.0, z, p, n, stream);
+    double bb = 0.0, rz = 0.0;
+    if (rc == SPMVB_OK) rc = spmvb_dot(b_dev, b_dev, n, &bb, stream);
+    if (rc == SPMVB_OK) rc = spmvb_dot(r, z, n, &rz, stream);
+    if (rc != SPMVB_OK) return done(rc);
+    const double bnorm = std::sqrt(bb);
+    if (residual_history) residual_history[0] = 1.0;
+    if (bnorm == 0.0) {
+        *converged = 1;
+        return done(SPMVB_OK);
+    }
+    for (int it = 1; it <= max_iterations; it++) {
+        double pap = 0.0, rr = 0.0, rz_new = 0.0;
+        rc = spmvb_spmv(a, p, 0, n, ap, 0, (int32_t)n, stream);                 // 1 SpMV
+        if (rc == SPMVB_OK) rc = spmvb_dot(p, ap, n, &pap, stream);              // dot 1
+        if (rc != SPMVB_OK) return done(rc);
+        const double alpha = rz / pap;
+        rc = spmvb_waxpby(1.0, x_dev, alpha, p, x_dev, n, stream);              // waxpby 1
+        if (rc == SPMVB_OK) rc = spmvb_waxpby(1.0, r, -alpha, ap, r, n, stream); // waxpby 2
+        if (rc == SPMVB_OK) rc = spmvb_dot(r, r, n, &rr, stream);                // dot 2
+        if (rc != SPMVB_OK) return done(rc);
+        const double rel = std::sqrt(rr) / bnorm;
+        *iterations = it;
+        if (residual_history) residual_history[it] = rel;
+        if (!std::isfinite(alpha) || !std::isfinite(rel)) {
+            done(SPMVB_OK);
+            return fail(SPMVB_ERR_DIVERGENCE, "pcg_solve: non-finite value in iteration %d", it);
+        }
+        if (rel <= tolerance) {
+            *converged = 1;
+            break;
+        }
+        rc = precondition();                                                    // z = M^-1 r
+        if (rc == SPMVB_OK) rc = spmvb_dot(r, z, n, &rz_new, stream);            // dot 3
+        if (rc != SPMVB_OK) return done(rc);
+        const double beta = rz_new / rz;
+        rz = rz_new;
+        rc = spmvb_waxpby(1.0, z, beta, p, p, n, stream);                       // waxpby 3
+        if (rc != SPMVB_OK) return done(rc);
+    }
+    return done(SPMVB_OK);
+}
+
+}  // extern "C"

@@ -227,9 +227,43 @@ int main() {
         CgConfig one_it;
         one_it.max_iterations = 1;
         CHECK(!cg_solve(m, b, one_it).second.converged);
+        // SymGS preconditioner (inc/solver.hpp:17-28): fewer iterations, same solution, analytic flop count
         CgConfig pre;
         pre.symgs_sweeps = 1;
+        auto [xp, rp] = cg_solve(m, b, pre);
+        double worst = 0;
+        for (double v : xp) worst = std::max(worst, std::fabs(v - 1.0));
+        CHECK(rp.converged && rp.iterations < its[0] && worst <= 1e-6);
+        CHECK(rp.per_op.at("precond").calls == rp.iterations && rp.per_op.at("precond").flops == rp.iterations * symgs_flops(m.nnz()));
+        CHECK(rp.flops_total == (std::int64_t)rp.iterations * (2 * m.nnz() + 12 * (std::int64_t)m.n) + rp.per_op.at("precond").flops);
+        StencilMatrix no_grid = m;  // without provenance the device sweep has no schedule
+        no_grid.grid = GridSpec{0, 0, 0};
+        CHECK(throws<std::invalid_argument>([&] { cg_solve(no_grid, b, pre); }));
+        pre.symgs_sweeps = -1;
         CHECK(throws<std::invalid_argument>([&] { cg_solve(m, b, pre); }));
+    }
+    // ---- symgs_sweep (inc/kernels.hpp:44-48)
+    {
+        const StencilMatrix one = generate_matrix(GridSpec{1, 1, 1});
+        Vector x{0.0};
+        symgs_sweep(one, x, Vector{52.0});
+        CHECK(x[0] == 2.0);  // exact solve of the 1x1 system
+        const StencilMatrix m = generate_matrix(GridSpec{3, 3, 3});
+        const Vector b = spmv(to_ell(m), Vector(m.n, 1.0));
+        Vector y(m.n, 0.0), y2(m.n, 0.0);
+        symgs_sweep(m, y, b);
+        symgs_sweep(m, y2, b);
+        CHECK(std::memcmp(y.data(), y2.data(), y.size() * sizeof(double)) == 0);  // deterministic
+        const Vector ay = spmv(to_ell(m), y);
+        double r0 = 0, r1 = 0;
+        for (int i = 0; i < m.n; i++) r0 += b[i] * b[i], r1 += (b[i] - ay[i]) * (b[i] - ay[i]);
+        CHECK(r1 < r0);  // the residual norm decreases
+        Vector shortx(3, 0.0);
+        CHECK(throws<std::invalid_argument>([&] { symgs_sweep(m, shortx, b); }));
+        StencilMatrix z = stencil_from_rows(2, {{{0, 1.0}}, {{0, 1.0}}});  // row 1 has no diagonal
+        z.grid = GridSpec{2, 1, 1};
+        Vector zx(2, 0.0);
+        CHECK(throws<std::invalid_argument>([&] { symgs_sweep(z, zx, Vector(2, 1.0)); }));
     }
     // ---- device-resident use: generate and compress on the GPU, many SpMVs, one download
     {

@@ -71,7 +71,8 @@ def test_generate_report_validates_against_the_schema():
     with pytest.raises(jsonschema.ValidationError):
         validate_report('{"grid": [4, 4, 4], "rows": 64}')
     with pytest.raises(jsonschema.ValidationError):
-        validate_report('{"backend": "csr", "grid": [4, 4, 4], "iterations": 1, "converged": true, "final_residual": 0, "flops_total": 1}')
+        validate_report('{"backend": "csr", "preconditioner": "none", "grid": [4, 4, 4], "iterations": 1, "converged": true, '
+                        '"final_residual": 0, "flops_total": 1}')
 
 
 @pytest.mark.gpu
@@ -96,6 +97,14 @@ def test_reports_validate_and_land_in_the_report_directory(tmp_path):
     r = subprocess.run([CLI, "solve", "--grid", "16", "16", "16", "--backend", "vt"], capture_output=True, text=True, timeout=600, env=env)
     assert r.returncode == 0 and validate_report(r.stdout)["converged"] is True
     assert (tmp_path / "solve_vt_16x16x16.json").read_text() == r.stdout
+    plain = validate_report(r.stdout)
+    rc, out, err = run("solve", "--grid", 16, 16, 16, "--backend", "vt", "--precond", "symgs")  # SPEC.md:456 precond
+    pre = validate_report(out)
+    assert rc == 0 and pre["converged"] and pre["preconditioner"] == "symgs" and pre["iterations"] < plain["iterations"]
+    rc, out, _ = run("solve", "--grid", 16, 16, 16, "--precond", "symgs:2")
+    assert rc == 0 and validate_report(out)["iterations"] <= pre["iterations"]
+    rc, _, err = run("solve", "--grid", 16, 16, 16, "--precond", "jacobi")
+    assert rc == 2 and err
     env["SPMVCOMP_REPORT_DIR"] = str(tmp_path / "missing")
     r = subprocess.run([CLI, "solve", "--grid", "8", "8", "8"], capture_output=True, text=True, timeout=600, env=env)
     assert r.returncode == 1 and "cannot write the report" in r.stderr

@@ -131,6 +131,100 @@ def test_cg_takes_p_ap_from_the_tensor_ring_kernel(sp, orc, g):
     assert sp.get_option("last_cg_fused_dot") == 0 and repe.iterations == rep0.iterations
 
 
+@pytest.mark.parametrize("g", [(1, 1, 1), (3, 3, 3), (5, 4, 3), (16, 7, 2), (1, 6, 4), (4, 1, 1), (33, 9, 5), (20, 20, 20)])
+def test_symgs_sweep_by_hyperplanes_is_the_sequential_sweep(sp, orc, g):
+    """symgs_sweep (kernels.hpp:44-48) on the device: rows by hyperplanes ix + 2 iy + 4 iz, bit-identical to the oracle's
+    sequential natural-order sweep, for a random start and right-hand side, twice in a row."""
+    m = orc.generate_matrix(*g)
+    n = m.n
+    dm = sp.generate_matrix(sp.GridSpec(*g))
+    x = orc.make_test_vector(n, orc.RANDOM, seed=3, lo=-1.0, hi=1.0)
+    b = orc.make_test_vector(n, orc.RANDOM, seed=4, lo=-1.0, hi=1.0)
+    dx, db = sp.DeviceVector.from_host(x), sp.DeviceVector.from_host(b)
+    for _ in range(2):
+        x = orc.symgs_sweep(m, x, b)
+        sp.symgs_sweep(dm, sp.GridSpec(*g), dx, db)
+        assert np.array_equal(dx.to_host().view(np.uint64), x.view(np.uint64))
+
+
+def test_symgs_examples_and_refusals(sp, orc):
+    one = sp.generate_matrix(sp.GridSpec(1, 1, 1))
+    dx = sp.DeviceVector.from_host(np.array([0.0]))
+    sp.symgs_sweep(one, sp.GridSpec(1, 1, 1), dx, sp.DeviceVector.from_host(np.array([52.0])))
+    assert dx.to_host().tolist() == [2.0]  # SPEC.md:264
+    # user-supplied values, explicit rows of a sparser stencil (7-point): still ordered by the hyperplanes
+    g = (6, 5, 4)
+    gs = sp.GridSpec(*g)
+    rows = []
+    for iz in range(g[2]):
+        for iy in range(g[1]):
+            for ix in range(g[0]):
+                r = [(gs.node(ix, iy, iz), 6.5)]
+                for dx_, dy_, dz_ in ((-1, 0, 0), (1, 0, 0), (0, -1, 0), (0, 1, 0), (0, 0, -1), (0, 0, 1)):
+                    jx, jy, jz = ix + dx_, iy + dy_, iz + dz_
+                    if 0 <= jx < g[0] and 0 <= jy < g[1] and 0 <= jz < g[2]:
+                        r.append((gs.node(jx, jy, jz), -1.0 - 0.01 * (jx + jy)))
+                rows.append(sorted(r))
+    m7 = orc.stencil_from_rows(gs.rows(), rows)
+    d7 = sp.stencil_from_rows(gs.rows(), rows)
+    x = np.linspace(-1.0, 1.0, gs.rows())
+    b = np.cos(np.arange(gs.rows()))
+    dx, db = sp.DeviceVector.from_host(x), sp.DeviceVector.from_host(b)
+    sp.symgs_sweep(d7, gs, dx, db)
+    assert np.array_equal(dx.to_host().view(np.uint64), orc.symgs_sweep(m7, x, b).view(np.uint64))
+    # refusals leave x untouched: zero diagonal (singularity, SPEC.md:262); a coupling the schedule does not order; wrong grid
+    before = dx.to_host().copy()
+    z = sp.upload_csr(2, [0, 1, 2], [0, 1], [1.0, 0.0])
+    two = sp.DeviceVector.from_host(np.zeros(2))
+    with pytest.raises(sp.InvalidArgument, match="diagonal"):
+        sp.symgs_sweep(z, sp.GridSpec(2, 1, 1), two, two)
+    # couplings outside the 27-point box are swept exactly as long as the hyperplanes order them the way the row index does
+    far = [list(r) for r in rows]
+    far[0] = sorted(far[0] + [(gs.rows() - 1, -0.5)])
+    far[-1] = sorted(far[-1] + [(0, -0.5)])
+    far[3] = sorted(far[3] + [(3 + 2 * g[0] - 1, -0.25)])  # node (3,0,0) -> (2,2,0): higher index, higher level
+    dfar, xf = sp.DeviceVector.from_host(x), orc.symgs_sweep(orc.stencil_from_rows(gs.rows(), far), x, b)
+    sp.symgs_sweep(sp.stencil_from_rows(gs.rows(), far), gs, dfar, db)
+    assert np.array_equal(dfar.to_host().view(np.uint64), xf.view(np.uint64))
+    bad = [list(r) for r in rows]
+    bad[5] = sorted(bad[5] + [(6, -0.25)])  # node (5,0,0), level 5 -> node (0,1,0): higher index but level 2
+    with pytest.raises(sp.InvalidArgument, match="hyperplane"):
+        sp.symgs_sweep(sp.stencil_from_rows(gs.rows(), bad), gs, dx, db)
+    with pytest.raises(sp.InvalidArgument):
+        sp.symgs_sweep(d7, sp.GridSpec(6, 5, 5), dx, db)
+    with pytest.raises(sp.InvalidArgument):
+        sp.symgs_sweep(sp.to_ell(d7), gs, dx, db)  # the sweep runs on the uncompressed matrix only (SPEC.md DESIGN DECISIONS)
+    assert np.array_equal(dx.to_host().view(np.uint64), before.view(np.uint64))
+
+
+@pytest.mark.parametrize("g", [(12, 10, 8), (16, 16, 16)])
+def test_symgs_preconditioned_cg_matches_the_oracle(sp, orc, g):
+    """cg_solve with the SymGS preconditioner (solver.hpp:40-46): iteration counts identical to the oracle's on
+    every backend, histories within 1e-10, solutions within 1e-9; fewer iterations than without it; analytic flop count."""
+    ref_m = orc.generate_matrix(*g)
+    gs = sp.GridSpec(*g)
+    m = sp.generate_matrix(gs)
+    n = ref_m.n
+    b = orc.spmv(orc.to_ell(ref_m), np.ones(n))
+    db = sp.DeviceVector.from_host(b)
+    for sweeps in (1, 2):
+        x_ref, it_ref, conv_ref, hist_ref = orc.cg_solve(orc.to_ell(ref_m), b, symgs_sweeps=sweeps, matrix=ref_m)
+        assert conv_ref
+        for a in (sp.to_ell(m), sp.compress_values(m), sp.compress_patterns(m, True)):
+            x, rep = sp.cg_solve(a, db, symgs_sweeps=sweeps, csr=m, grid=gs)
+            assert rep.converged and rep.iterations == it_ref
+            assert np.abs(np.array(rep.residual_history) - hist_ref).max() <= 1e-10
+            assert np.abs(x.to_host() - x_ref).max() <= 1e-9 and np.abs(x.to_host() - 1.0).max() <= 1e-6
+            assert rep.flops_total == it_ref * (2 * ref_m.nnz + 12 * n) + it_ref * sweeps * 4 * ref_m.nnz  # SPEC.md:321 + symgs_flops
+    _, plain = sp.cg_solve(sp.to_ell(m), db)
+    _, pre = sp.cg_solve(sp.to_ell(m), db, symgs_sweeps=1, csr=m, grid=gs)
+    assert pre.iterations < plain.iterations
+    _, one = sp.cg_solve(sp.to_ell(m), db, symgs_sweeps=1, csr=m, grid=gs, max_iterations=1)
+    assert one.iterations == 1 and not one.converged
+    with pytest.raises(sp.InvalidArgument):
+        sp.cg_solve(sp.to_ell(m), db, symgs_sweeps=1)
+
+
 def test_slab_cg_driver_on_the_device(sp, orc):
     """The distributed CG driver (slab.py:SlabCg) with the CUDA kernels as its operations, one slab: the same iteration
     count and history as the single-call device solver, and the known solution."""

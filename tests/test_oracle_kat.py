@@ -346,3 +346,45 @@ def test_cg_examples(orc):
         assert np.abs(hist - results[0][3]).max() <= 1e-10
     _, it, conv, _ = orc.cg_solve(orc.to_ell(m), b, max_iterations=1)
     assert it == 1 and not conv
+
+
+# ---- symgs_sweep and the SymGS-preconditioned solve: SPEC.md:258-266, 308-311 ----------
+def test_symgs_examples(orc):
+    one = orc.generate_matrix(1, 1, 1)
+    assert orc.symgs_sweep(one, [0.0], [52.0]).tolist() == [2.0]  # exact solve of the 1x1 system
+    m = orc.generate_matrix(3, 3, 3)
+    ell = orc.to_ell(m)
+    b = orc.spmv(ell, np.ones(m.n))
+    x = orc.symgs_sweep(m, np.zeros(m.n), b)
+    assert np.linalg.norm(b - orc.spmv(ell, x)) < np.linalg.norm(b)  # the residual norm decreases
+    assert np.array_equal(orc.symgs_sweep(m, np.zeros(m.n), b).view(np.uint64), x.view(np.uint64))  # deterministic
+    # the definition, restated with a dense matrix: forward rows ascending, backward rows descending, latest values
+    d, y = m.dense(), np.zeros(m.n)
+    for order in (range(m.n), range(m.n - 1, -1, -1)):
+        for i in order:
+            s = 0.0
+            for j in range(m.n):
+                if j != i and d[i, j] != 0.0:
+                    s = s + d[i, j] * y[j]
+            y[i] = (b[i] - s) / d[i, i]
+    assert np.array_equal(y.view(np.uint64), x.view(np.uint64))
+    z = orc.csr_from_arrays(2, [0, 1, 2], [0, 1], [1.0, 0.0])  # zero diagonal: the singularity error
+    with pytest.raises(orc.InvalidArgument):
+        orc.symgs_sweep(z, [0.0, 0.0], [1.0, 1.0])
+    with pytest.raises(orc.InvalidArgument):
+        orc.symgs_sweep(m, np.zeros(3), b)
+
+
+def test_symgs_preconditioned_cg(orc):
+    m = orc.generate_matrix(12, 10, 8)
+    ell = orc.to_ell(m)
+    b = orc.spmv(ell, np.ones(m.n))
+    x0, it0, conv0, _ = orc.cg_solve(ell, b)
+    x1, it1, conv1, h1 = orc.cg_solve(ell, b, symgs_sweeps=1, matrix=m)
+    assert conv0 and conv1 and it1 < it0  # the preconditioner pays
+    assert np.abs(x1 - 1.0).max() <= 1e-6 and h1[0] == 1.0 and len(h1) == it1 + 1 and h1[-1] <= 1e-8
+    for f in (orc.compress_values(m), orc.compress_patterns(m, True)):  # backend swap: same counts
+        x2, it2, conv2, h2 = orc.cg_solve(f, b, symgs_sweeps=1, matrix=m)
+        assert it2 == it1 and np.abs(x2 - x1).max() <= 1e-9 and np.abs(h2 - h1).max() <= 1e-10
+    _, it3, _, _ = orc.cg_solve(ell, b, symgs_sweeps=2, matrix=m)
+    assert it3 <= it1
