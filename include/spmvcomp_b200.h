@@ -122,7 +122,8 @@ int spmvb_set_device(int device);
  *   "last_cg_fused_dot": read-only, 1 when the last spmvb_cg_solve took p.Ap from the SpMV kernel
  *   "cg_keep_workspace": 1 (default) spmvb_cg_solve keeps its three work vectors (3n doubles) on the matrix handle
  *                     between solves, released by spmvb_matrix_destroy; 0 allocates and frees them in every solve
- *   "ell_kernel":     0 auto (ELL: TMA bulk pipeline, vt: staged), 1 naive, 2 staged vector loads, 3 TMA for vt too
+ *   "ell_kernel":     0 auto (one bulk-copied tile per CTA: 32 rows for ELL, 128 for vt), 1 naive (ELL), 2 tiles staged with
+ *                     vector loads, 3 the persistent two-stage TMA ring, 4-7 other tile heights (measured alternatives)
  *   "box_prefetch", "box_prefetch_l1": L2 / L1 prefetch distance of the sliding-window kernels
  *   "debug_nochain":  measurement only (1: sliding-window kernels skip their FP64 chains -- wrong results; 7: tensor ring
  *                     without the per-plane-group line rotation -- same results)

@@ -55,20 +55,32 @@ __device__ __forceinline__ double vt_row(const int32_t *c, const int32_t *e, con
 // free for odd widths such as 27).  row_map != nullptr serves the exception block
 // of the hybrid pattern format: tile rows are exception slots, y goes to row_map[e].
 // =============================================================================
-template <int ROWS>
+template <int ROWS, bool BULK = false>
 __global__ void __launch_bounds__(ROWS) spmv_ell_kernel(const double *__restrict__ values,
                                                        const int32_t *__restrict__ columns, int width,
                                                        const double *__restrict__ x, int64_t x_col0,
                                                        double *__restrict__ y, int row_begin, int row_end,
-                                                       int tile0, const int32_t *__restrict__ row_map) {
+                                                       int tile0, const int32_t *__restrict__ row_map, int n_rows) {
     extern __shared__ __align__(16) unsigned char smem[];
     double *sv = reinterpret_cast<double *>(smem);
     int32_t *sc = reinterpret_cast<int32_t *>(smem + (size_t)ROWS * width * 8);
+    __shared__ __align__(8) uint64_t bar;
     const int r0 = (tile0 + blockIdx.x) * ROWS;
     const int64_t base = (int64_t)r0 * width;
     const int rows_here = min(ROWS, row_end - r0);
     const int nelem = rows_here * width;
-    {
+    if (BULK && r0 + ROWS <= n_rows) {  // a whole tile by two bulk copies (see spmv_vt_kernel); co-resident CTAs overlap one another
+        if (threadIdx.x == 0) {
+            mbar_init(smem_u32(&bar), 1);
+            fence_mbar_init();
+            const uint32_t bytes_v = (uint32_t)ROWS * width * 8, bytes_c = (uint32_t)ROWS * width * 4;
+            mbar_expect_tx(smem_u32(&bar), bytes_v + bytes_c);
+            bulk_g2s(smem_u32(sv), values + base, bytes_v, smem_u32(&bar));
+            bulk_g2s(smem_u32(sc), columns + base, bytes_c, smem_u32(&bar));
+        }
+        __syncthreads();
+        mbar_wait(smem_u32(&bar), 0);
+    } else {
         const int4 *gv = reinterpret_cast<const int4 *>(values + base);
         const int nv = (nelem + 1) >> 1;
 #pragma unroll 4
@@ -77,11 +89,13 @@ __global__ void __launch_bounds__(ROWS) spmv_ell_kernel(const double *__restrict
         const int nc = (nelem + 3) >> 2;
 #pragma unroll 4
         for (int i = threadIdx.x; i < nc; i += ROWS) reinterpret_cast<int4 *>(sc)[i] = ld_stream(gc + i);
+        __syncthreads();
     }
-    __syncthreads();
     const int r = r0 + threadIdx.x;
     if (r < row_begin || r >= row_end) return;
-    y[row_map ? row_map[r] : r] = ell_row<9>(sv + threadIdx.x * width, sc + threadIdx.x * width, width, x, x_col0);
+    const double *v = sv + threadIdx.x * width;
+    const int32_t *c = sc + threadIdx.x * width;
+    y[row_map ? row_map[r] : r] = (BULK && width == 27) ? ell_row<27>(v, c, 27, x, x_col0) : ell_row<9>(v, c, width, x, x_col0);
 }
 
 // Naive thread-per-row form, kept as the A/B baseline ("ell_kernel" = 1).
@@ -102,20 +116,37 @@ __global__ void spmv_ell_naive_kernel(const double *__restrict__ values, const i
 // SPEC.md:218-221): per row, sum x within each value group in stored order, then
 // one product per group in table order.
 // =============================================================================
-template <int ROWS>
+template <int ROWS, bool BULK>
 __global__ void __launch_bounds__(ROWS) spmv_vt_kernel(const int32_t *__restrict__ sorted_columns,
                                                       const int32_t *__restrict__ ends,
                                                       const double *__restrict__ table, int width, int m,
                                                       const double *__restrict__ x, int64_t x_col0,
                                                       double *__restrict__ y, int row_begin, int row_end,
-                                                      int tile0) {
+                                                      int tile0, int n_rows) {
     extern __shared__ __align__(16) unsigned char smem[];
     int32_t *sc = reinterpret_cast<int32_t *>(smem);
     int32_t *se = sc + (size_t)ROWS * width;
     double *st = reinterpret_cast<double *>(se + (size_t)ROWS * m);
+    __shared__ __align__(8) uint64_t bar;
     const int r0 = (tile0 + blockIdx.x) * ROWS;
     const int rows_here = min(ROWS, row_end - r0);
-    {
+    // BULK: a whole tile is fetched by two bulk copies (cp.async.bulk, one elected thread) instead of 128-bit loads and
+    // stores by every thread: the load/store unit is this kernel's busiest pipe (27 index reads + 27 gathers per row),
+    // and the staging traffic was 40 % of its wavefronts.  Tiles that are not whole (the stream's last) keep the loads.
+    const bool bulk = BULK && r0 + ROWS <= n_rows;
+    if (bulk) {
+        if (threadIdx.x == 0) {
+            mbar_init(smem_u32(&bar), 1);
+            fence_mbar_init();
+            const uint32_t bytes_c = (uint32_t)ROWS * width * 4, bytes_e = (uint32_t)ROWS * m * 4;
+            mbar_expect_tx(smem_u32(&bar), bytes_c + bytes_e);
+            bulk_g2s(smem_u32(sc), sorted_columns + (int64_t)r0 * width, bytes_c, smem_u32(&bar));
+            bulk_g2s(smem_u32(se), ends + (int64_t)r0 * m, bytes_e, smem_u32(&bar));
+        }
+        for (int i = threadIdx.x; i < m; i += ROWS) st[i] = table[i];
+        __syncthreads();  // the barrier is initialised (and the table staged) before anyone waits on it
+        mbar_wait(smem_u32(&bar), 0);
+    } else {
         const int4 *gc = reinterpret_cast<const int4 *>(sorted_columns + (int64_t)r0 * width);
         const int nc = (rows_here * width + 3) >> 2;
 #pragma unroll 4
@@ -124,8 +155,8 @@ __global__ void __launch_bounds__(ROWS) spmv_vt_kernel(const int32_t *__restrict
         const int ne = (rows_here * m + 3) >> 2;
         for (int i = threadIdx.x; i < ne; i += ROWS) reinterpret_cast<int4 *>(se)[i] = ld_stream(ge + i);
         for (int i = threadIdx.x; i < m; i += ROWS) st[i] = table[i];
+        __syncthreads();
     }
-    __syncthreads();
     const int r = r0 + threadIdx.x;
     if (r < row_begin || r >= row_end) return;
     y[r] = vt_row<9>(sc + threadIdx.x * width, se + threadIdx.x * m, st, m, x, x_col0);
@@ -231,8 +262,32 @@ int launch_ell(const double *values, const int32_t *columns, int width, const do
     const int tiles = (row_end + kTileRows - 1) / kTileRows - tile0;
     const size_t smem = (size_t)kTileRows * width * 12;
     if (smem > 200 * 1024) return fail(SPMVB_ERR_INVALID_ARGUMENT, "ELL width %d too large for the staged kernel", width);
+    {
+        // One bulk-copied tile per CTA, many CTAs per SM.  Default: 32-row tiles (one warp per CTA, 10.4 KB at width 27, ~21
+        // CTAs/SM): 795 us at 256^3 = 7.17 TB/s of algorithmic traffic -- a read-dominated stream, above the copy kernel's 6.54
+        // TB/s (half reads, half writes).  64-row tiles 922 us, 128-row tiles 946 us (ell_kernel = 5, 4;
+        // profiles/r01_probe256_ell_vt_bulk_tiles.log).  The persistent two-stage ring below (ell_kernel = 3) holds 2 CTAs/SM: 1021-1038 us.
+        const int k = options().ell_kernel;
+        const int rows = k == 4 ? 128 : k == 5 ? 64 : 32;
+        if ((k == 0 || k == 4 || k == 5 || k == 6) && (size_t)rows * width * 12 <= 200 * 1024) {
+            static PerDevice<bool> attr;
+            if (!attr.get()) {
+                SPMVB_CUDA(cudaFuncSetAttribute(spmv_ell_kernel<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+                SPMVB_CUDA(cudaFuncSetAttribute(spmv_ell_kernel<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+                SPMVB_CUDA(cudaFuncSetAttribute(spmv_ell_kernel<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+                attr.get() = true;
+            }
+            const int t0 = row_begin / rows, nt = (row_end + rows - 1) / rows - t0;
+            const size_t bytes = (size_t)rows * width * 12;
+            // whole tiles below row_end are bulk-copied; the last, partial one is staged with loads
+            if (rows == 128) spmv_ell_kernel<128, true><<<nt, 128, bytes, st>>>(values, columns, width, x, x_col0, y, row_begin, row_end, t0, row_map, row_end);
+            else if (rows == 64) spmv_ell_kernel<64, true><<<nt, 64, bytes, st>>>(values, columns, width, x, x_col0, y, row_begin, row_end, t0, row_map, row_end);
+            else spmv_ell_kernel<32, true><<<nt, 32, bytes, st>>>(values, columns, width, x, x_col0, y, row_begin, row_end, t0, row_map, row_end);
+            return check_launch("spmv_ell_bulk");
+        }
+    }
     if (options().ell_kernel != 2) {
-        // TMA bulk pipeline (default): persistent CTAs, NS stages of one tile each
+        // persistent TMA bulk pipeline (ell_kernel = 3, and widths whose tile does not fit above): NS stages of one tile each
         constexpr int NS = 2;
         const size_t stage = smem;  // multiple of 16 for any width (128 rows)
         const size_t need = stage * NS;
@@ -255,7 +310,7 @@ int launch_ell(const double *values, const int32_t *columns, int width, const do
         attr_set.get() = true;
     }
     spmv_ell_kernel<kTileRows><<<tiles, kTileRows, smem, st>>>(values, columns, width, x, x_col0, y, row_begin,
-                                                               row_end, tile0, row_map);
+                                                               row_end, tile0, row_map, 0);
     return check_launch("spmv_ell");
 }
 
@@ -284,14 +339,30 @@ int launch_vt(const spmvb_matrix *a, const double *x, int64_t x_col0, double *y,
             return check_launch("spmv_vt_tma");
         }
     }
+    // bulk-copy staging needs 16-byte multiples per tile part: 128 rows x width (and x m) ints always are
+    const bool bulk = options().ell_kernel != 2;
     static PerDevice<bool> attr_set;
     if (!attr_set.get()) {
-        SPMVB_CUDA(cudaFuncSetAttribute(spmv_vt_kernel<kTileRows>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        SPMVB_CUDA(cudaFuncSetAttribute(spmv_vt_kernel<kTileRows, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        SPMVB_CUDA(cudaFuncSetAttribute(spmv_vt_kernel<kTileRows, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr_set.get() = true;
     }
-    spmv_vt_kernel<kTileRows><<<tiles, kTileRows, smem, st>>>(
-        static_cast<const int32_t *>(a->s[SPMVB_S_SORTED_COLUMNS]), static_cast<const int32_t *>(a->s[SPMVB_S_ENDS]),
-        static_cast<const double *>(a->s[SPMVB_S_TABLE]), a->width, a->m, x, x_col0, y, row_begin, row_end, tile0);
+    const auto *sc = static_cast<const int32_t *>(a->s[SPMVB_S_SORTED_COLUMNS]);
+    const auto *se = static_cast<const int32_t *>(a->s[SPMVB_S_ENDS]);
+    const auto *tab = static_cast<const double *>(a->s[SPMVB_S_TABLE]);
+    if (options().ell_kernel == 6) {  // 64-row tiles
+        const int t0 = row_begin / 64, nt = (row_end + 63) / 64 - t0;
+        static PerDevice<bool> a64;
+        if (!a64.get()) {
+            SPMVB_CUDA(cudaFuncSetAttribute(spmv_vt_kernel<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            a64.get() = true;
+        }
+        spmv_vt_kernel<64, true><<<nt, 64, (size_t)64 * (a->width + a->m) * 4 + (size_t)a->m * 8 + 16, st>>>(sc, se, tab, a->width, a->m, x, x_col0, y, row_begin, row_end, t0, a->n);
+    } else if (options().ell_kernel == 7) {  // 32-row tiles
+        const int t0 = row_begin / 32, nt = (row_end + 31) / 32 - t0;
+        spmv_vt_kernel<32, true><<<nt, 32, (size_t)32 * (a->width + a->m) * 4 + (size_t)a->m * 8 + 16, st>>>(sc, se, tab, a->width, a->m, x, x_col0, y, row_begin, row_end, t0, a->n);
+    } else if (bulk) spmv_vt_kernel<kTileRows, true><<<tiles, kTileRows, smem, st>>>(sc, se, tab, a->width, a->m, x, x_col0, y, row_begin, row_end, tile0, a->n);
+    else spmv_vt_kernel<kTileRows, false><<<tiles, kTileRows, smem, st>>>(sc, se, tab, a->width, a->m, x, x_col0, y, row_begin, row_end, tile0, a->n);
     return check_launch("spmv_vt");
 }
 
