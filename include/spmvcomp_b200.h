@@ -117,6 +117,8 @@ int spmvb_set_device(int device);
  *   "box_lines":      lines per CTA tile / chunk length of the tensor ring (0 = default)
  *   "host_chunks":    row chunks of the pipelined spmvb_spmv_host (0 = default 8)
  *   "symgs_graph":    1 (default) the launches of a symgs sweep are recorded into a CUDA graph and replayed; 0 launches directly
+ *   "cg_graph":       1 (default) spmvb_cg_solve records its iteration into a CUDA graph after the first one and replays it (one
+ *                     graph launch per iteration); 0 launches the kernels directly.  "last_cg_graph" (read-only) says which ran
  *   "cg_fused_dot":   1 (default) spmvb_cg_solve takes p.Ap from the SpMV kernel when that kernel offers it (pattern format,
  *                     tensor ring, whole square grid): one pass over p and Ap less per iteration; 0 always runs the dot
  *   "last_cg_fused_dot": read-only, 1 when the last spmvb_cg_solve took p.Ap from the SpMV kernel

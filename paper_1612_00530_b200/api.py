@@ -335,11 +335,12 @@ def symgs_sweep(csr: DeviceMatrix, grid: GridSpec, x, b, stream=None):
     check(lib.spmvb_symgs_sweep(csr.h, C.byref(g), _ptr(x), _ptr(b), _stream(stream)))
 
 
-def cg_solve(a: DeviceMatrix, b, max_iterations=500, tolerance=1e-8, stream=None, symgs_sweeps=0, csr=None, grid=None):
+def cg_solve(a: DeviceMatrix, b, max_iterations=500, tolerance=1e-8, stream=None, symgs_sweeps=0, csr=None, grid=None, x=None):
     """cg_solve (solver.hpp:40-46) on the device.  b: device vector; returns (x, CgReport).  symgs_sweeps >= 1 preconditions
-    with that many SymGS sweeps from a zero guess (needs the matrix as `csr` and its `grid`)."""
+    with that many SymGS sweeps from a zero guess (needs the matrix as `csr` and its `grid`).  `x`: a device vector to
+    receive the solution (repeated solves then allocate nothing: cudaMalloc / cudaFree of large vectors stall now and then)."""
     n = a.n
-    x = DeviceVector(n)
+    x = DeviceVector(n) if x is None else x
     hist = np.zeros(max_iterations + 1, dtype=np.float64)
     it, conv = C.c_int32(), C.c_int32()
     if symgs_sweeps:

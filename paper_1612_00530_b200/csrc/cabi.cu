@@ -254,6 +254,8 @@ static int *option_slot(const char *key) {
     if (!strcmp(key, "host_chunks")) return &o.host_chunks;
     if (!strcmp(key, "cg_keep_workspace")) return &o.cg_keep_workspace;
     if (!strcmp(key, "cg_fused_dot")) return &o.cg_fused_dot;
+    if (!strcmp(key, "cg_graph")) return &o.cg_graph;
+    if (!strcmp(key, "last_cg_graph")) return &o.last_cg_graph;
     if (!strcmp(key, "symgs_graph")) return &o.symgs_graph;
     if (!strcmp(key, "last_cg_fused_dot")) return &o.last_cg_fused_dot;
     if (!strcmp(key, "last_pattern_kernel")) return &o.last_pattern_kernel;

@@ -122,6 +122,8 @@ struct Options {
     int debug_nochain = 0;   // measurement only
     int box_lines = 0;       // lines per CTA march of the tensor-ring kernel (0 = default)
     int symgs_graph = 1;        // 1: a symgs sweep's launches are recorded into a CUDA graph and replayed
+    int cg_graph = 1;           // 1: cg_solve records its iteration into a CUDA graph after the first and replays it
+    int last_cg_graph = 0;      // read-only: 1 when the last cg_solve replayed a graph
     int cg_fused_dot = 1;       // 1: cg_solve takes p.Ap from the SpMV kernel where that kernel offers it (pattern format, tensor ring)
     int last_cg_fused_dot = 0;  // read-only: 1 when the last iteration of the last cg_solve took p.Ap from the SpMV kernel
     int cg_keep_workspace = 1;  // 1: spmvb_cg_solve keeps its 3n work doubles on the handle until spmvb_free

@@ -95,7 +95,9 @@ __global__ void __launch_bounds__(kDotThreads) cg_update_kernel(const double *__
         if (threadIdx.x == 0) partial[blockIdx.x] = acc;
     }
 }
-__global__ void cg_beta_kernel(const double *__restrict__ partial, int count, double *__restrict__ scal) {
+// ... and the iteration's record of scalars goes straight into the host's pinned ring (slot = iteration number mod ring size;
+// scal[9] counts the iterations), so that an iteration is kernels only and can be replayed as a CUDA graph
+__global__ void cg_beta_kernel(const double *__restrict__ partial, int count, double *__restrict__ scal, double *host_ring, int ring_slots) {
     if (scal[5] != 0.0) return;
     double acc = 0.0;
     for (int i = threadIdx.x; i < count; i += 32) acc = __dadd_rn(acc, partial[i]);
@@ -107,6 +109,11 @@ __global__ void cg_beta_kernel(const double *__restrict__ partial, int count, do
         scal[4] = acc / scal[2];  // beta = r.z_new / r.z
         scal[2] = acc;
         if (!isfinite(scal[1]) || !isfinite(rel) || rel <= scal[7]) scal[5] = 1.0;
+        const int it = (int)scal[9] + 1;
+        scal[9] = (double)it;
+        double *rec = host_ring + (size_t)(it % ring_slots) * 16;
+        for (int i = 0; i < 10; i++) rec[i] = scal[i];
+        __threadfence_system();
     }
 }
 // p = 1*r + beta*p (waxpby 3) with beta taken from the device
@@ -288,38 +295,74 @@ int spmvb_cg_solve(const spmvb_matrix *a, const double *b_dev, double *x_dev, in
     };
     t_setup = now();
     int stop = 0, queued = 0, seen = 0;
-    for (int it = 1; it <= max_iterations && !stop; it++) {
-        // 1 SpMV; the pattern format's tensor-ring kernel also leaves the partial sums of p.Ap (dot 1) when it can
+    // One iteration, queued on `qs`: 1 SpMV (the pattern format's tensor-ring kernel also leaves the partial sums of p.Ap
+    // when it can), dot 1 and alpha, waxpby 1 + 2 with dots 2 = 3, beta / stop flag / record, waxpby 3.
+    bool fused_dot = false;
+    auto queue_iteration = [&](cudaStream_t qs, bool direction) -> int {
         FusedDot fused{sc.partial, kPartialCap, 0};
         fused_dot_request() = options().cg_fused_dot ? &fused : nullptr;
-        rc = spmvb_spmv(a, p, 0, n, ap, 0, (int32_t)n, stream);
+        const int rc2 = spmvb_spmv(a, p, 0, n, ap, 0, (int32_t)n, qs);
         fused_dot_request() = nullptr;
-        if (rc != SPMVB_OK) return finish(rc);
-        options().last_cg_fused_dot = fused.count != 0;
-        if (fused.count == 0) dot_partial_kernel<<<blocks, kDotThreads, 0, st>>>(p, ap, n, sc.partial);  // dot 1: p.Ap ...
-        cg_alpha_kernel<<<1, 32, 0, st>>>(sc.partial, fused.count ? fused.count : blocks, sc.scal);      // ... and alpha = r.z / p.Ap
-        cg_update_kernel<<<blocks, kDotThreads, 0, st>>>(sc.scal, p, ap, x_dev, r, n, sc.partial);  // waxpby 1, 2, dots 2 = 3
-        cg_beta_kernel<<<1, 32, 0, st>>>(sc.partial, blocks, sc.scal);                 // r.r, beta, r.z, stop flag
-        if (cudaMemcpyAsync(ring + (it % kRing) * 16, sc.scal, 16 * sizeof(double), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
-            cudaEventRecord(ev[it % kRing], st) != cudaSuccess) {
-            finish(SPMVB_OK);
+        if (rc2 != SPMVB_OK) return rc2;
+        fused_dot = fused.count != 0;
+        if (!fused_dot) dot_partial_kernel<<<blocks, kDotThreads, 0, qs>>>(p, ap, n, sc.partial);
+        cg_alpha_kernel<<<1, 32, 0, qs>>>(sc.partial, fused_dot ? fused.count : blocks, sc.scal);
+        cg_update_kernel<<<blocks, kDotThreads, 0, qs>>>(sc.scal, p, ap, x_dev, r, n, sc.partial);
+        cg_beta_kernel<<<1, 32, 0, qs>>>(sc.partial, blocks, sc.scal, ring, kRing);
+        if (direction) cg_direction_kernel<<<wblocks, 256, 0, qs>>>(sc.scal, r, p, n);
+        return cudaGetLastError() == cudaSuccess ? SPMVB_OK : fail(SPMVB_ERR_CUDA, "cg_solve: launch failed");
+    };
+    // The first iteration is queued directly (it also completes every lazy set-up of the SpMV launch); the iteration is then
+    // recorded once into a CUDA graph and replayed: one graph launch and one event per iteration on the host instead of
+    // seven launches, which keeps a slow or busy host thread from starving the device ("cg_graph" = 0: direct launches).
+    cudaGraphExec_t gexec = nullptr;
+    auto finish_graph = [&](int code) {
+        if (gexec) cudaGraphExecDestroy(gexec);
+        return finish(code);
+    };
+    options().last_cg_graph = 0;
+    for (int it = 1; it <= max_iterations && !stop; it++) {
+        if (it == 2 && options().cg_graph && max_iterations > 2) {
+            static thread_local cudaStream_t cs = nullptr;
+            if (!cs && cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) cs = nullptr;
+            cudaGraph_t graph = nullptr;
+            if (cs && cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+                const int rcq = queue_iteration(cs, true);
+                const bool ended = cudaStreamEndCapture(cs, &graph) == cudaSuccess && graph;
+                if (rcq != SPMVB_OK || !ended || cudaGraphInstantiate(&gexec, graph, nullptr, nullptr, 0) != cudaSuccess) gexec = nullptr;
+                if (graph) cudaGraphDestroy(graph);
+            }
+            (void)cudaGetLastError();  // a failed capture leaves the direct launches
+            options().last_cg_graph = gexec != nullptr;
+        }
+        if (gexec) {
+            if (cudaGraphLaunch(gexec, st) != cudaSuccess) {
+                finish_graph(SPMVB_OK);
+                return fail(SPMVB_ERR_CUDA, "cg_solve: graph launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+            }
+        } else {
+            rc = queue_iteration(st, it < max_iterations);
+            if (rc != SPMVB_OK) return finish_graph(rc);
+        }
+        options().last_cg_fused_dot = fused_dot;
+        if (cudaEventRecord(ev[it % kRing], st) != cudaSuccess) {
+            finish_graph(SPMVB_OK);
             return fail(SPMVB_ERR_CUDA, "cg_solve: %s", cudaGetErrorString(cudaGetLastError()));
         }
-        if (it < max_iterations) cg_direction_kernel<<<wblocks, 256, 0, st>>>(sc.scal, r, p, n);  // waxpby 3: p = z + beta p
         queued = it;
         if (it > kAhead) stop = harvest(seen = it - kAhead);
     }
     while (!stop && seen < queued) stop = harvest(++seen);  // the last iterations queued (max_iterations reached)
     if (stop < 0 || cudaGetLastError() != cudaSuccess) {
-        finish(SPMVB_OK);
+        finish_graph(SPMVB_OK);
         return fail(SPMVB_ERR_CUDA, "cg_solve: device error in the iteration");
     }
     if (stop == 2) {
         const int at = *iterations;
-        finish(SPMVB_OK);
+        finish_graph(SPMVB_OK);
         return fail(SPMVB_ERR_DIVERGENCE, "cg_solve: non-finite value in iteration %d", at);  // inc/solver.hpp:44
     }
-    return finish(SPMVB_OK);
+    return finish_graph(SPMVB_OK);
 }
 
 }  // extern "C"

@@ -66,6 +66,41 @@ def test_cg_single_unknown_and_errors(sp, orc):
         sp.cg_solve(z, sp.DeviceVector.from_host(np.ones(2)))
 
 
+@pytest.mark.parametrize("fmt", ["ell", "vt", "pattern", "hybrid"])
+def test_cg_iteration_replayed_as_a_graph(sp, orc, fmt):
+    """After the first iteration cg_solve replays its iteration as a CUDA graph ("cg_graph"): the same kernels in the same
+    order, so the report and the solution are bit-identical to direct launches, on every backend."""
+    g = (72, 10, 9)
+    m = sp.generate_matrix(sp.GridSpec(*g), perturb=(11, 0.1, 0.1) if fmt == "hybrid" else None)
+    n = m.n
+    ell = sp.to_ell(m)
+    a = {"ell": lambda: ell, "vt": lambda: sp.compress_values(sp.generate_matrix(sp.GridSpec(*g))),
+         "pattern": lambda: sp.compress_patterns(m, True),
+         "hybrid": lambda: sp.compress_patterns(m, True, min_pattern_rows=2)}[fmt]()
+    b = sp.DeviceVector(n)
+    sp.spmv_rows(ell if fmt != "vt" else a, sp.DeviceVector.from_host(np.ones(n)), b, 0, n)
+    out = {}
+    try:
+        for graph in (0, 1, 1):
+            sp.set_option("cg_graph", graph)
+            x, rep = sp.cg_solve(a, b, max_iterations=40, tolerance=1e-9)  # (the perturbed matrix is not SPD: no convergence asked)
+            assert sp.get_option("last_cg_graph") == graph and rep.iterations > 8
+            out.setdefault(graph, []).append((x.to_host().view(np.uint64), rep))
+        for cap in (1, 2, 3, 7):  # around the point where the graph takes over
+            reps = []
+            for graph in (0, 1):
+                sp.set_option("cg_graph", graph)
+                x, rep = sp.cg_solve(a, b, max_iterations=cap, tolerance=1e-9)
+                reps.append((x.to_host().view(np.uint64), rep))
+            assert reps[0][1].residual_history == reps[1][1].residual_history and np.array_equal(reps[0][0], reps[1][0])
+            assert reps[1][1].iterations == cap
+    finally:
+        sp.set_option("cg_graph", 1)
+    (x0, r0), (x1, r1), (x2, r2) = out[0][0], out[1][0], out[1][1]
+    assert r0.iterations == r1.iterations == r2.iterations and r0.residual_history == r1.residual_history == r2.residual_history
+    assert np.array_equal(x0, x1) and np.array_equal(x1, x2)
+
+
 def test_cg_workspace_on_the_handle_and_run_ahead(sp, orc):
     """Repeated solves reuse the work vectors kept on the handle ("cg_keep_workspace"); with or without them, and wherever
     the stop falls relative to the host's run-ahead of four iterations, the report and the solution are identical."""
