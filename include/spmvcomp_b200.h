@@ -109,11 +109,16 @@ const char *spmvb_last_error(void);
 int spmvb_version(void);
 int spmvb_device_count(int *count);
 int spmvb_set_device(int device);
-/* Tuning knobs for A/B measurement; results never depend on them.  Unknown keys -> SPMVB_ERR_INVALID_ARGUMENT.
+/* Tuning knobs for A/B measurement, per host thread.  SpMV results never depend on them (every kernel keeps the format's
+ * summation order); the one knob that touches floating-point results is "cg_fused_dot", which changes the order in which
+ * p.Ap is summed inside spmvb_cg_solve (iterates then agree to rounding, iteration counts are unchanged in every test).
+ * Unknown keys -> SPMVB_ERR_INVALID_ARGUMENT; so are values that select measurement-only variants unless the library
+ * was built with -DSPMVB_LAB ("lab_build", read-only, says which; the default build holds none of them).
  *   "pattern_kernel": 0 auto, 1 List 1 as written (thread per row), 2 box plan required, 3 one-column box kernel only
  *   "box_march":      0 auto (tensor ring for ranges of >= 8 planes, else the register sliding window);
- *                     3 sliding window forced; 90..110 variants / ablations of the tensor ring, 1..72 of the
- *                     sliding window (listed with their measured times in csrc/spmv_pattern*.cu)
+ *                     3 sliding window forced; 90 tensor ring forced, 101 / 107 / 108 / 109 / 110 its other schedules
+ *                     (chunk per warp, ids by loads, round-robin tiles per CTA / per warp, 4 planes per thread);
+ *                     lab build only: further variants and ablations (csrc/spmv_pattern*.cu list them with their times)
  *   "box_lines":      lines per CTA tile / chunk length of the tensor ring (0 = default)
  *   "host_chunks":    row chunks of the pipelined spmvb_spmv_host (0 = default 8)
  *   "symgs_graph":    1 (default) the launches of a symgs sweep are recorded into a CUDA graph and replayed; 0 launches directly
@@ -125,10 +130,10 @@ int spmvb_set_device(int device);
  *   "cg_keep_workspace": 1 (default) spmvb_cg_solve keeps its three work vectors (3n doubles) on the matrix handle
  *                     between solves, released by spmvb_matrix_destroy; 0 allocates and frees them in every solve
  *   "ell_kernel":     0 auto (one bulk-copied tile per CTA: 32 rows for ELL, 128 for vt), 1 naive (ELL), 2 tiles staged with
- *                     vector loads, 3 the persistent two-stage TMA ring, 4-7 other tile heights (measured alternatives)
+ *                     vector loads, 3 the persistent two-stage TMA ring; lab build only: 4-7 other tile heights
  *   "box_prefetch", "box_prefetch_l1": L2 / L1 prefetch distance of the sliding-window kernels
- *   "debug_nochain":  measurement only (1: sliding-window kernels skip their FP64 chains -- wrong results; 7: tensor ring
- *                     without the per-plane-group line rotation -- same results)
+ *   "debug_nochain":  lab build only, measurement only (1: sliding-window kernels skip their FP64 chains -- wrong results;
+ *                     7: tensor ring without the per-plane-group line rotation -- same results)
  *   "last_pattern_kernel" (read): family of the last pattern launch: 1 List 1, 2 one-column box, 3 sliding window,
  *                     4 lab variant, 9 tensor ring */
 int spmvb_set_option(const char *key, int value);

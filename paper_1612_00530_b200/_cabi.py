@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_HERE, "libspmvcomp_b200.so")
+SO_PATH = os.environ.get("SPMVB_LIB") or os.path.join(_HERE, "libspmvcomp_b200.so")  # SPMVB_LIB: another build of the same C-ABI (e.g. the lab build)
 
 
 class SpmvcompError(RuntimeError):

@@ -296,8 +296,14 @@ def spmv_rows(a: DeviceMatrix, x, y, begin, end, x_col0=0, x_len=None, stream=No
 
 
 def spmv(a: DeviceMatrix, x) -> np.ndarray:
-    """spmv (kernels.hpp:23-25) with host vectors: validated, returns a fresh vector."""
+    """spmv (kernels.hpp:23-25) with host vectors: validated, returns a fresh vector.  The device arrays of a handle
+    are immutable, so the structural validation (spmvb_validate: column / id ranges, group ends) runs once per handle."""
     x = _np(x, np.float64)
+    if not getattr(a, "_validated", False):
+        info = a.info
+        if info.format in (FMT_ELL, FMT_VT, FMT_PATTERN) and info.row_offset == 0 and x.shape[0] == info.n:
+            check(lib.spmvb_validate(a.h, info.n, None))  # whole square matrix: columns in [0, n)
+            a._validated = True
     y = np.empty(a.n, dtype=np.float64)
     check(lib.spmvb_spmv_host(a.h, _ptr(x), x.shape[0], _ptr(y)))
     return y

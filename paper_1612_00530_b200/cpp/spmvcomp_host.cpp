@@ -355,7 +355,7 @@ void rows_impl(const Fmt& a, std::span<const double> x, std::span<double> y, std
 }
 }  // namespace
 
-Vector spmv(const EllMatrix& a, const Vector& x) { return spmv_checked(a, x, false); }
+Vector spmv(const EllMatrix& a, const Vector& x) { return spmv_checked(a, x, true); }  // inc/kernels.hpp:23: validated like the other two
 Vector spmv(const VtCompressedMatrix& a, const Vector& x) { return spmv_checked(a, x, true); }
 Vector spmv(const PatternCompressedMatrix& a, const Vector& x) { return spmv_checked(a, x, true); }
 

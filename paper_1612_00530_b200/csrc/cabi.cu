@@ -24,8 +24,8 @@ int fail(int code, const char *fmt, ...) {
     return code;
 }
 
-Options &options() {
-    static Options o;
+Options &options() {  // per host thread: distinct handles driven by distinct threads do not see each other's knobs
+    static thread_local Options o;
     return o;
 }
 
@@ -139,13 +139,13 @@ void analyse_box_plan(spmvb_matrix *a) {
 // Smallest and largest global column referenced by the rows of a pattern handle (ids + per-pattern displacement
 // extremes, plus the exception block).  out[0] = min, out[1] = max.
 __global__ void column_range_kernel(const int32_t *__restrict__ ids, int n, int64_t row_offset, const int32_t *__restrict__ pmin,
-                                    const int32_t *__restrict__ pmax, const int32_t *__restrict__ exc_cols, int64_t n_exc_entries,
-                                    long long *out) {
+                                    const int32_t *__restrict__ pmax, int n_patterns, const int32_t *__restrict__ exc_cols,
+                                    int64_t n_exc_entries, long long *out) {
     long long lo = INT64_MAX, hi = INT64_MIN;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x, t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     for (int64_t r = t0; r < n; r += stride) {
         const int id = ids[r];
-        if (id >= 0) {
+        if (id >= 0 && id < n_patterns) {  // (a malformed id is reported by validate; never an out-of-bounds read here)
             lo = min(lo, (long long)(row_offset + r + pmin[id]));
             hi = max(hi, (long long)(row_offset + r + pmax[id]));
         }
@@ -189,7 +189,7 @@ static int compute_column_range(spmvb_matrix *a) {
     cudaError_t e1 = cudaMemcpy(d_ext, ext.data(), ext.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
     cudaError_t e2 = cudaMemcpy(d_out, init, sizeof(init), cudaMemcpyHostToDevice);
     if (e1 == cudaSuccess && e2 == cudaSuccess) {
-        column_range_kernel<<<592, 256>>>(static_cast<const int32_t *>(a->s[SPMVB_S_ROW_PATTERN]), a->n, a->row_offset, d_ext, d_ext + P,
+        column_range_kernel<<<592, 256>>>(static_cast<const int32_t *>(a->s[SPMVB_S_ROW_PATTERN]), a->n, a->row_offset, d_ext, d_ext + P, P,
                                           static_cast<const int32_t *>(a->s[SPMVB_S_EXC_COLUMNS]), (int64_t)a->n_exc * a->w_exc, d_out);
         e1 = cudaGetLastError();
         e2 = cudaMemcpy(res, d_out, sizeof(res), cudaMemcpyDeviceToHost);
@@ -262,14 +262,35 @@ static int *option_slot(const char *key) {
     return nullptr;
 }
 
+// Values that select measured experiments / ablations exist only in the lab build (-DSPMVB_LAB); the default library
+// rejects them, so no option can make it return a wrong y.
+static bool lab_only_value(const char *key, int value) {
+    if (kLabBuild) return false;
+    if (!strcmp(key, "box_march")) {
+        for (int ok : {0, 3, 90, 101, 107, 108, 109, 110})
+            if (value == ok) return false;
+        return true;
+    }
+    if (!strcmp(key, "debug_nochain")) return value != 0;
+    if (!strcmp(key, "ell_kernel")) return value < 0 || value > 3;
+    if (!strcmp(key, "pattern_kernel")) return value < 0 || value > 3;
+    return false;
+}
+
 int spmvb_set_option(const char *key, int value) {
     int *s = option_slot(key);
     if (!s) return fail(SPMVB_ERR_INVALID_ARGUMENT, "unknown option '%s'", key ? key : "(null)");
+    if (lab_only_value(key, value))
+        return fail(SPMVB_ERR_INVALID_ARGUMENT, "option '%s' = %d selects a lab variant; this library was built without -DSPMVB_LAB", key, value);
     *s = value;
     return SPMVB_OK;
 }
 
 int spmvb_get_option(const char *key, int *value) {
+    if (key && value && !strcmp(key, "lab_build")) {
+        *value = kLabBuild ? 1 : 0;
+        return SPMVB_OK;
+    }
     int *s = option_slot(key);
     if (!s || !value) return fail(SPMVB_ERR_INVALID_ARGUMENT, "unknown option '%s'", key ? key : "(null)");
     *value = *s;
@@ -336,8 +357,9 @@ int spmvb_pattern_upload(int32_t n, int32_t m, int64_t row_offset, const double 
                          const int32_t *ends_flat, const int32_t *row_pattern, int32_t values_in_pattern,
                          int32_t n_exc, int32_t w_exc, const int32_t *exc_rows, const double *exc_values,
                          const int32_t *exc_columns, spmvb_matrix **out) {
-    if (n < 0 || m < 0 || n_patterns < 0 || n_exc < 0 || w_exc < 0 || !disp_offsets ||
-        (n > 0 && !row_pattern) || (n_exc > 0 && (!exc_rows || (w_exc > 0 && (!exc_values || !exc_columns)))))
+    if (n < 0 || m < 0 || n_patterns < 0 || n_exc < 0 || w_exc < 0 || !disp_offsets || (m > 0 && !table) ||
+        (n_patterns > 0 && m > 0 && !ends_flat) || (n > 0 && !row_pattern) ||
+        (n_exc > 0 && (!exc_rows || (w_exc > 0 && (!exc_values || !exc_columns)))))
         return fail(SPMVB_ERR_INVALID_ARGUMENT, "pattern_upload: bad arguments");
     // structural checks on the small tables (validate(), inc/compress.hpp:92-95)
     for (int k = 1; k < m; k++)
@@ -358,6 +380,24 @@ int spmvb_pattern_upload(int32_t n, int32_t m, int64_t row_offset, const double 
     }
     if (disp_offsets[n_patterns] > INT32_MAX)
         return fail(SPMVB_ERR_INVALID_ARGUMENT, "dictionary too large");
+    if (disp_offsets[n_patterns] > 0 && !disp_flat) return fail(SPMVB_ERR_INVALID_ARGUMENT, "pattern_upload: disp_flat is NULL");
+    // the row stream and the exception list, before anything reaches the device: ids in [-1, P), the exception rows
+    // ascending, in range, and exactly the rows whose id is -1
+    int64_t nnz = 0, n_minus1 = 0;
+    for (int64_t i = 0; i < n; i++) {
+        const int32_t id = row_pattern[i];
+        if (id >= 0 && id < n_patterns) nnz += disp_offsets[id + 1] - disp_offsets[id];
+        else if (id == -1) n_minus1++;
+        else return fail(SPMVB_ERR_INTEGRITY, "row %lld: pattern id %d out of range", (long long)i, id);
+    }
+    if (n_minus1 != n_exc) return fail(SPMVB_ERR_INTEGRITY, "%lld rows have id -1 but the exception block holds %d rows", (long long)n_minus1, n_exc);
+    for (int64_t e = 0; e < n_exc; e++) {
+        const int32_t r = exc_rows[e];
+        if (r < 0 || r >= n || (e > 0 && r <= exc_rows[e - 1]) || row_pattern[r] != -1)
+            return fail(SPMVB_ERR_INTEGRITY, "exception slot %lld: row %d is out of range, out of order or has a pattern id", (long long)e, r);
+        for (int32_t t = 0; t < w_exc; t++)
+            if (!(exc_values[e * w_exc + t] == 0.0 && exc_columns[e * w_exc + t] == row_offset + r)) nnz++;
+    }
     spmvb_matrix *a = nullptr;
     SPMVB_TRY(new_handle(out, &a));
     a->format = SPMVB_FMT_PATTERN;
@@ -380,20 +420,7 @@ int spmvb_pattern_upload(int32_t n, int32_t m, int64_t row_offset, const double 
     GUARD(upload_stream(a, SPMVB_S_EXC_COLUMNS, exc_columns, (uint64_t)n_exc * w_exc * 4,
                         (uint64_t)kTileRows * w_exc * 4));
     GUARD(finish_pattern_handle(a));
-    // nnz: pattern rows via the dictionary, exception rows via non-padding slots
-    int64_t nnz = 0;
-    for (int64_t i = 0; i < n; i++) {
-        const int32_t id = row_pattern[i];
-        if (id >= 0 && id < n_patterns) nnz += disp_offsets[id + 1] - disp_offsets[id];
-        else if (id != -1) { destroy(a); return fail(SPMVB_ERR_INTEGRITY, "row %lld: pattern id %d out of range", (long long)i, id); }
-    }
-    for (int64_t e = 0; e < n_exc; e++)
-        for (int32_t t = 0; t < w_exc; t++) {
-            const double v = exc_values[e * w_exc + t];
-            const int64_t own = row_offset + exc_rows[e];
-            if (!(v == 0.0 && exc_columns[e * w_exc + t] == own)) nnz++;
-        }
-    a->nnz = nnz;
+    a->nnz = nnz;  // pattern rows via the dictionary, exception rows via non-padding slots
     *out = a;
     return SPMVB_OK;
 }

@@ -48,6 +48,26 @@ struct PerDevice {
     T &get() { return v[current_device()]; }
 };
 
+// Measured experiments and ablations (spmv_pattern_lab.cu, the non-default instantiations selected by "box_march" /
+// "ell_kernel" / "debug_nochain") are compiled only with -DSPMVB_LAB (make LAB=1 -> libspmvcomp_b200_lab.so); some of
+// them skip work on purpose and return wrong y.  The default library cannot reach any of them.
+#ifdef SPMVB_LAB
+constexpr bool kLabBuild = true;
+#else
+constexpr bool kLabBuild = false;
+#endif
+
+// SMs of the current device (grids are sized in multiples of it).
+inline int sm_count() {
+    static PerDevice<int> n;
+    int &v = n.get();
+    if (v == 0) {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 1;
+    }
+    return v;
+}
+
 // Rows per CTA tile of the row-major ELL-like streams.  Device allocations of
 // those streams are padded to a whole number of tiles so a tile can always be
 // fetched with full 16-byte vector loads.
@@ -130,6 +150,6 @@ struct Options {
     int host_chunks = 0;     // row chunks of the pipelined host-buffer SpMV (0 = default 8, at most 64)
     int last_pattern_kernel = 0;  // read-only: kernel family of the last pattern launch (1 List 1, 2 box v2, 3 box3, 4 lab, 9 tensor ring)
 };
-Options &options();
+Options &options();  // per host thread
 
 }  // namespace spmvb

@@ -80,7 +80,7 @@ int max_row_len(const Csr &m, cudaStream_t st, int *out) {
     DevBuf d;
     SPMVB_TRY(d.alloc(4));
     SPMVB_CUDA(cudaMemsetAsync(d.p, 0, 4, st));
-    if (m.n > 0) max_row_len_kernel<<<std::min(blocks_for(m.n, 256), 148u * 8), 256, 0, st>>>(m, d.as<int>());
+    if (m.n > 0) max_row_len_kernel<<<std::min(blocks_for(m.n, 256), (unsigned)sm_count() * 8u), 256, 0, st>>>(m, d.as<int>());
     SPMVB_CUDA(cudaMemcpyAsync(out, d.p, 4, cudaMemcpyDeviceToHost, st));
     return sync(st, "max_row_len");
 }
@@ -180,7 +180,7 @@ int scan_value_table(const Csr &m, int64_t nnz, const uint8_t *row_keep, size_t 
             SPMVB_CUDA(cudaMemcpyAsync(d_tab.p, table->data(), table->size() * 8, cudaMemcpyHostToDevice, st));
         const int64_t work = row_keep ? m.n : nnz;
         if (work > 0)
-            table_miss_kernel<<<std::min(blocks_for(work, 256), 148u * 16), 256, 0, st>>>(
+            table_miss_kernel<<<std::min(blocks_for(work, 256), (unsigned)sm_count() * 16u), 256, 0, st>>>(
                 m.vals, nnz, row_keep, m.row_start, m.n, d_tab.as<double>(), (int)table->size(), d_miss.as<double>(),
                 d_cnt.as<unsigned long long>());
         unsigned long long n_miss = 0;

@@ -37,6 +37,7 @@ struct PatternArgs {
     int prefetch;              // L2 prefetch distance in lines
     int prefetch_l1;           // L1 prefetch distance in lines (v3), 0 = off
     int debug_nochain;         // measurement only: skip the FP64 chains (y = centre operand)
+    int center_pos = 1;        // where the centre term sits in the summation order: 0 first, 1 last, 2 in place (BoxPlan)
     double *dot_partial = nullptr;  // fused x.y (CG's p.Ap): one partial sum per warp of the tensor-ring kernel, else nullptr
     int dot_capacity = 0;
 };
@@ -121,6 +122,7 @@ __device__ __forceinline__ void box_march(const PatternArgs &p, const uint32_t *
                                           int64_t n_rows, int nq, bool lane_ok, bool pf_lo, bool pf_hi) {
     constexpr int S = 3 + LA;
     constexpr int P = Q + 2;
+    const int cpos = CENTER_POS >= 0 ? CENTER_POS : p.center_pos;  // CENTER_POS = -1: read at run time (the general variant)
     const int64_t sy = p.sy;
     const int64_t sz = sy * p.plane_lines;
     const double *__restrict__ x = p.x;
@@ -180,13 +182,13 @@ __device__ __forceinline__ void box_march(const PatternArgs &p, const uint32_t *
                 const int sl[3] = {(k + S - 1) % S, k, (k + 1) % S};
                 if (__all_sync(0xffffffffu, full)) {
                     // every row of this step has the full box: no selects on the chain
-                    if (CENTER_POS == 0) {
+                    if (cpos == 0) {
 #pragma unroll
                         for (int q = 0; q < Q; q++) acc[q] = __dadd_rn(acc[q], __dmul_rn(vc, w[sl[1]][q + 1][1]));
                     }
 #pragma unroll
                     for (int t = 0; t < 27; t++) {
-                        if (t == 13 && CENTER_POS != 2) continue;
+                        if (t == 13 && cpos != 2) continue;
                         const int dz = t / 9, dy = (t / 3) % 3, dx = t % 3;
 #pragma unroll
                         for (int q = 0; q < Q; q++) {
@@ -194,7 +196,7 @@ __device__ __forceinline__ void box_march(const PatternArgs &p, const uint32_t *
                             acc[q] = OFF_NEG1 ? __dsub_rn(acc[q], e) : __dadd_rn(acc[q], __dmul_rn(vo, e));
                         }
                     }
-                    if (CENTER_POS == 1) {
+                    if (cpos == 1) {
 #pragma unroll
                         for (int q = 0; q < Q; q++) acc[q] = __dadd_rn(acc[q], __dmul_rn(vc, w[sl[1]][q + 1][1]));
                     }
@@ -202,7 +204,7 @@ __device__ __forceinline__ void box_march(const PatternArgs &p, const uint32_t *
                     // Masked rows: an absent entry contributes +0.0.  acc starts at +0.0 and can
                     // never become -0.0 (round to nearest), so adding +-0.0 leaves it unchanged
                     // bit for bit: identical to skipping the term as the reference does.
-                    if (CENTER_POS == 0) {
+                    if (cpos == 0) {
 #pragma unroll
                         for (int q = 0; q < Q; q++) {
                             const double pr = __dmul_rn(vc, w[sl[1]][q + 1][1]);
@@ -211,7 +213,7 @@ __device__ __forceinline__ void box_march(const PatternArgs &p, const uint32_t *
                     }
 #pragma unroll
                     for (int t = 0; t < 27; t++) {
-                        if (t == 13 && CENTER_POS != 2) continue;
+                        if (t == 13 && cpos != 2) continue;
                         const int dz = t / 9, dy = (t / 3) % 3, dx = t % 3;
 #pragma unroll
                         for (int q = 0; q < Q; q++) {
@@ -221,7 +223,7 @@ __device__ __forceinline__ void box_march(const PatternArgs &p, const uint32_t *
                             else acc[q] = __dadd_rn(acc[q], on ? __dmul_rn(vo, e) : 0.0);
                         }
                     }
-                    if (CENTER_POS == 1) {
+                    if (cpos == 1) {
 #pragma unroll
                         for (int q = 0; q < Q; q++) {
                             const double pr = __dmul_rn(vc, w[sl[1]][q + 1][1]);
@@ -300,7 +302,8 @@ constexpr uint32_t kRBits = 0x4924924u;  // box entries with dx = +1
 template <int Q, int S, int LPS, bool OFF_NEG1, int CENTER_POS, int MODE, bool SELL, bool SELR>
 __device__ __forceinline__ void box3_chain(const double (&w)[S][Q + 2][4], int kb, const uint32_t (&mk)[LPS][Q][2],
                                            const bool (&zl)[LPS][Q], const bool (&zr)[LPS][Q], double vc, double vo,
-                                           double (&acc)[LPS][Q][2]) {
+                                           double (&acc)[LPS][Q][2], int cp_rt) {
+    const int cpos = CENTER_POS >= 0 ? CENTER_POS : cp_rt;
     // MODE 0: operands straight from the window (with SELL/SELR: halo operands zeroed per lane)
     // MODE 1: every operand selected by its mask bit
     // line l of the step reads slots (kb+l-1, kb+l, kb+l+1) mod S for dy = -1, 0, +1
@@ -319,10 +322,10 @@ __device__ __forceinline__ void box3_chain(const double (&w)[S][Q + 2][4], int k
                     acc[l][q][i] = __dadd_rn(acc[l][q][i], (MODE == 1 && !(mk[l][q][i] >> 13 & 1u)) ? 0.0 : pr);
                 }
     };
-    if (CENTER_POS == 0) centre();
+    if (cpos == 0) centre();
 #pragma unroll
     for (int t = 0; t < 27; t++) {
-        if (t == 13 && CENTER_POS != 2) continue;
+        if (t == 13 && cpos != 2) continue;
         const int dz = t / 9, dy = (t / 3) % 3, dx = t % 3;
 #pragma unroll
         for (int l = 0; l < LPS; l++)
@@ -343,7 +346,7 @@ __device__ __forceinline__ void box3_chain(const double (&w)[S][Q + 2][4], int k
                     }
                 }
     }
-    if (CENTER_POS == 1) centre();
+    if (cpos == 1) centre();
 }
 
 // Row classes (shared-memory tables indexed by pattern id + 1; entry 0 serves exception
@@ -450,7 +453,7 @@ __device__ __forceinline__ void box3_march(const PatternArgs &p, const Box3Smem 
 #pragma unroll
                             for (int i = 0; i < 2; i++) acc[l][q][i] = w[(kb + l) % S][q + 1][i + 1] + w[(kb + l + 1) % S][q + 2][i + 2];
                 } else if (vote == 0) {
-                    box3_chain<Q, S, LPS, OFF_NEG1, CENTER_POS, 0, false, false>(w, kb, mk, zl, zr, vc, vo, acc);
+                    box3_chain<Q, S, LPS, OFF_NEG1, CENTER_POS, 0, false, false>(w, kb, mk, zl, zr, vc, vo, acc, p.center_pos);
                 } else if (vote == 1 || vote == 2) {
 #pragma unroll
                     for (int l = 0; l < LPS; l++)
@@ -459,8 +462,8 @@ __device__ __forceinline__ void box3_march(const PatternArgs &p, const Box3Smem 
                             zl[l][q] = c0[l][q] != 0;
                             zr[l][q] = c1[l][q] != 0;
                         }
-                    if (vote == 1) box3_chain<Q, S, LPS, OFF_NEG1, CENTER_POS, 0, true, false>(w, kb, mk, zl, zr, vc, vo, acc);
-                    else box3_chain<Q, S, LPS, OFF_NEG1, CENTER_POS, 0, false, true>(w, kb, mk, zl, zr, vc, vo, acc);
+                    if (vote == 1) box3_chain<Q, S, LPS, OFF_NEG1, CENTER_POS, 0, true, false>(w, kb, mk, zl, zr, vc, vo, acc, p.center_pos);
+                    else box3_chain<Q, S, LPS, OFF_NEG1, CENTER_POS, 0, false, true>(w, kb, mk, zl, zr, vc, vo, acc, p.center_pos);
                 } else {
 #pragma unroll
                     for (int l = 0; l < LPS; l++)
@@ -468,7 +471,7 @@ __device__ __forceinline__ void box3_march(const PatternArgs &p, const Box3Smem 
                         for (int q = 0; q < Q; q++)
 #pragma unroll
                             for (int i = 0; i < 2; i++) mk[l][q][i] = lds_u32(sm.masks + 4 + 4 * id[l][q][i]);
-                    box3_chain<Q, S, LPS, OFF_NEG1, CENTER_POS, 1, false, false>(w, kb, mk, zl, zr, vc, vo, acc);
+                    box3_chain<Q, S, LPS, OFF_NEG1, CENTER_POS, 1, false, false>(w, kb, mk, zl, zr, vc, vo, acc, p.center_pos);
 #pragma unroll
                     for (int l = 0; l < LPS; l++)
 #pragma unroll

@@ -22,7 +22,8 @@
 
 namespace spmvb {
 
-constexpr int kDotBlocks = 148 * 8;
+// Shape of the reduction tree of dot (part of the result's bits, so a constant, not the device's SM count): 1184 partial sums.
+constexpr int kDotBlocks = 1184;
 constexpr int kDotThreads = 256;
 constexpr int kPartialCap = 8192;  // partial sums: kDotBlocks from the vector kernels, one per warp from the SpMV's fused dot
 
@@ -151,7 +152,7 @@ static int dot_device(const double *u, const double *v, int64_t n, DotScratch &s
 
 static int waxpby_device(double alpha, const double *x, double beta, const double *y, double *w, int64_t n, cudaStream_t st) {
     if (n <= 0) return SPMVB_OK;
-    const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, sm_count() * 16);
     waxpby_kernel<<<blocks, 256, 0, st>>>(alpha, x, beta, y, w, n);
     SPMVB_CUDA(cudaGetLastError());
     return SPMVB_OK;
@@ -245,17 +246,19 @@ int spmvb_cg_solve(const spmvb_matrix *a, const double *b_dev, double *x_dev, in
         return done(SPMVB_OK);
     }
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + kDotThreads - 1) / kDotThreads, kDotBlocks));
-    const int wblocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+    const int wblocks = (int)std::min<int64_t>((n + 255) / 256, sm_count() * 16);
     {
         const double init[16] = {0.0, 0.0, rz, 0.0, 0.0, 0.0, bnorm, tolerance, 0.0};
-        SPMVB_CUDA(cudaMemcpyAsync(sc.scal, init, sizeof(init), cudaMemcpyHostToDevice, st));
-        SPMVB_CUDA(cudaStreamSynchronize(st));
+        // (every exit after the workspace was taken goes through done(): it releases or frees the work vectors)
+        if (cudaMemcpyAsync(sc.scal, init, sizeof(init), cudaMemcpyHostToDevice, st) != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess)
+            return done(fail(SPMVB_ERR_CUDA, "cg_solve: scalar set-up failed: %s", cudaGetErrorString(cudaGetLastError())));
     }
     // The host queues iteration `it` before it looks at the scalars of iteration it-kAhead (pinned ring of kRing records,
     // one event each): the stop decision is the device's (scal[5]); what was queued past it runs as no-ops (the SpMVs
     // still run, into the scratch vector).  kAhead iterations of queued work ride out a host thread that is descheduled
     // for a millisecond; with one iteration of run-ahead the device drained every time that happened.
-    // (the pinned ring and the events are allocated once per host thread: cudaMallocHost costs milliseconds)
+    // (the pinned ring and the events are allocated once per host thread and device: cudaMallocHost costs milliseconds, and an
+    // event or stream belongs to the device that was current when it was created)
     constexpr int kRing = 8, kAhead = 4;
     struct HostRing {
         double *ring = nullptr;
@@ -271,7 +274,8 @@ int spmvb_cg_solve(const spmvb_matrix *a, const double *b_dev, double *x_dev, in
             return SPMVB_OK;
         }
     };
-    static thread_local HostRing hr;
+    static thread_local PerDevice<HostRing> hr_dev;
+    HostRing &hr = hr_dev.get();
     if (hr.init() != SPMVB_OK) return done(SPMVB_ERR_CUDA);
     double *ring = hr.ring;
     cudaEvent_t *ev = hr.ev;
@@ -323,7 +327,8 @@ int spmvb_cg_solve(const spmvb_matrix *a, const double *b_dev, double *x_dev, in
     options().last_cg_graph = 0;
     for (int it = 1; it <= max_iterations && !stop; it++) {
         if (it == 2 && options().cg_graph && max_iterations > 2) {
-            static thread_local cudaStream_t cs = nullptr;
+            static thread_local PerDevice<cudaStream_t> cs_dev;
+            cudaStream_t &cs = cs_dev.get();
             if (!cs && cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) cs = nullptr;
             cudaGraph_t graph = nullptr;
             if (cs && cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {

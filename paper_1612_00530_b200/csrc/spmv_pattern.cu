@@ -17,11 +17,7 @@ static int launch_box_rw(const spmvb_matrix *a, PatternArgs &p, cudaStream_t st)
     const bool neg1 = p.v_off == -1.0;
     const int cp = a->box.center_pos;
 #define LAUNCH(NEG, CP) spmv_pattern_box_kernel<R, WC, Q, LA, NEG, CP><<<grid, block, 0, st>>>(p, n_planes)
-    if (neg1) {
-        if (cp == 0) LAUNCH(true, 0); else if (cp == 1) LAUNCH(true, 1); else LAUNCH(true, 2);
-    } else {
-        if (cp == 0) LAUNCH(false, 0); else if (cp == 1) LAUNCH(false, 1); else LAUNCH(false, 2);
-    }
+    if (neg1 && cp == 1) LAUNCH(true, 1); else LAUNCH(false, -1);  // the HPCG value pattern specialised; anything else: general variant
 #undef LAUNCH
     return check_launch("spmv_pattern_box");
 }
@@ -39,11 +35,7 @@ static int launch_box3(const spmvb_matrix *a, PatternArgs &p, cudaStream_t st) {
     dim3 block(WC * 32);
 #define LAUNCH3(NEG, CP) spmv_pattern_box3_kernel<R, WC, Q, LPS, MINB, NEG, CP, WA, LA><<<grid, block, 0, st>>>(p, n_planes)
     if constexpr (ALLV) {
-        if (neg1) {
-            if (cp == 0) LAUNCH3(true, 0); else if (cp == 1) LAUNCH3(true, 1); else LAUNCH3(true, 2);
-        } else {
-            if (cp == 0) LAUNCH3(false, 0); else if (cp == 1) LAUNCH3(false, 1); else LAUNCH3(false, 2);
-        }
+        if (neg1 && cp == 1) LAUNCH3(true, 1); else LAUNCH3(false, -1);
     } else {
         LAUNCH3(true, 1);
     }
@@ -84,10 +76,11 @@ static int launch_pattern(const spmvb_matrix *a, const double *x, int64_t x_col0
         p.sy = a->box.sy; p.plane_lines = a->box.valid ? a->box.sz / a->box.sy : 0;
         p.v_off = a->box.valid ? a->h_table[a->box.k_off] : 0.0;
         p.v_center = a->box.valid ? a->h_table[a->box.k_center] : 0.0;
+        p.center_pos = a->box.center_pos;
         Options &o = options();
         p.prefetch = o.box_prefetch >= 0 ? o.box_prefetch : 2;
         p.prefetch_l1 = o.box_prefetch_l1;
-        p.debug_nochain = o.debug_nochain;
+        p.debug_nochain = kLabBuild ? o.debug_nochain : 0;
         if (FusedDot *req = fused_dot_request()) {  // x.y alongside y: every row through one ring launch, x[row] = the row's own entry
             if (a->n_exc == 0 && row_begin == 0 && row_end == a->n && a->row_offset == 0 && x_col0 == 0 && a->n_cols == a->n && x_len == a->n &&
                 o.box_march == 0 && o.pattern_kernel == 0 && o.debug_nochain == 0) {
@@ -112,12 +105,16 @@ static int launch_pattern(const spmvb_matrix *a, const double *x, int64_t x_col0
             if (!ring && o.pattern_kernel != 3 && box3_ok(a, p)) {
                 const int64_t n_planes = ((int64_t)row_end - row_begin + (int64_t)p.sy * p.plane_lines - 1) / ((int64_t)p.sy * p.plane_lines);
                 if (n_planes == 1) {  // single-plane ranges (slab boundary planes): short marches, so that the plane fills the GPU
+#ifdef SPMVB_LAB
                     if (o.box_lines == 16) rc3 = launch_box3<16, 4, 1, 2, 3, false>(a, p, st);
                     else if (o.box_lines == 8) rc3 = launch_box3<8, 4, 1, 2, 3, false>(a, p, st);
                     else if (o.box_lines == 2) rc3 = launch_box3<2, 4, 1, 2, 3, false>(a, p, st);
-                    else rc3 = launch_box3<4, 4, 1, 2, 3, false>(a, p, st);
+                    else
+#endif
+                    rc3 = launch_box3<4, 4, 1, 2, 3, false>(a, p, st);
                 }
                 else switch (o.box_march) {
+#ifdef SPMVB_LAB
                     // measured alternatives kept selectable for A/B (profiles/r01_probe256_*.log, 256^3):
                     case 1: rc3 = launch_box3<16, 4, 2, 1, 3, false>(a, p, st); break;      // R=16 tiles            124 us
                     case 5: rc3 = launch_box3<16, 4, 1, 2, 3, false>(a, p, st); break;      // 1 plane, 2 lines/step 116-121 us
@@ -127,6 +124,7 @@ static int launch_pattern(const spmvb_matrix *a, const double *x, int64_t x_col0
                     case 70: rc3 = launch_box3<8, 4, 2, 1, 2, false, 1, 1>(a, p, st); break;   // register look-ahead LA=1: 146 us (sweep: profiles/r01_probe256_lookahead_sweep.log)
                     case 20: case 30: case 35: case 47: case 62:                            // spmv_pattern_lab.cu
                         rc3 = launch_pattern_lab(o.box_march, a, p, st); break;
+#endif
                     case 3: rc3 = launch_box3<8, 4, 2, 1, 3, true>(a, p, st); break;           // box3 default, forced
                     // <R=8 lines, 4 warps, Q=2 planes/thread, 1 line/step, 3 CTAs/SM>: 118-123 us
                     default: rc3 = launch_box3<8, 4, 2, 1, 3, true>(a, p, st); break;
@@ -135,8 +133,11 @@ static int launch_pattern(const spmvb_matrix *a, const double *x, int64_t x_col0
             }
             o.last_pattern_kernel = rc3 == 1 ? 2 : (ring ? 9 : (o.box_march >= 20 && o.box_march < 70 ? 4 : 3));
             if (rc3 == 1) {  // v2: any stride / alignment / value pattern
+#ifdef SPMVB_LAB
                 if (o.box_march == 11) SPMVB_TRY((launch_box_rw<32, 8, 1, 1>(a, p, st)));
-                else SPMVB_TRY((launch_box_rw<16, 8, 2, 0>(a, p, st)));
+                else
+#endif
+                SPMVB_TRY((launch_box_rw<16, 8, 2, 0>(a, p, st)));
             }
         } else {
             const int threads = 256;

@@ -172,11 +172,11 @@ __global__ void __launch_bounds__(WC * 32, MINB) spmv_pattern_box5_kernel(Patter
                     double acc[1][Q][2];
                     const unsigned vote = __ballot_sync(0xffffffffu, other) ? 4u
                                           : ((__ballot_sync(0xffffffffu, anyl) ? 1u : 0u) | (__ballot_sync(0xffffffffu, anyr) ? 2u : 0u));
-                    if (vote == 0) box3_chain<Q, S, 1, OFF_NEG1, CENTER_POS, 0, false, false>(w, k, mk, zl, zr, vc, vo, acc);
-                    else if (vote == 1) box3_chain<Q, S, 1, OFF_NEG1, CENTER_POS, 0, true, false>(w, k, mk, zl, zr, vc, vo, acc);
-                    else if (vote == 2) box3_chain<Q, S, 1, OFF_NEG1, CENTER_POS, 0, false, true>(w, k, mk, zl, zr, vc, vo, acc);
+                    if (vote == 0) box3_chain<Q, S, 1, OFF_NEG1, CENTER_POS, 0, false, false>(w, k, mk, zl, zr, vc, vo, acc, CENTER_POS);
+                    else if (vote == 1) box3_chain<Q, S, 1, OFF_NEG1, CENTER_POS, 0, true, false>(w, k, mk, zl, zr, vc, vo, acc, CENTER_POS);
+                    else if (vote == 2) box3_chain<Q, S, 1, OFF_NEG1, CENTER_POS, 0, false, true>(w, k, mk, zl, zr, vc, vo, acc, CENTER_POS);
                     else {
-                        box3_chain<Q, S, 1, OFF_NEG1, CENTER_POS, 1, false, false>(w, k, mk, zl, zr, vc, vo, acc);
+                        box3_chain<Q, S, 1, OFF_NEG1, CENTER_POS, 1, false, false>(w, k, mk, zl, zr, vc, vo, acc, CENTER_POS);
 #pragma unroll
                         for (int q = 0; q < Q; q++)
 #pragma unroll
@@ -618,7 +618,7 @@ __global__ void __launch_bounds__(WC * 32, MINB) spmv_pattern_box7_kernel(Patter
                 } else if (!slow) {
                     load_line((k + 2) % S, j + 2);             // setup of step j+1 ...
                     other_n = classify(j + 1, idn, zln, zrn);
-                    box3_chain<Q, S, 1, OFF_NEG1, CENTER_POS, 0, true, true>(w, k, mk, zl1, zr1, vc, vo, acc);  // ... under chain j
+                    box3_chain<Q, S, 1, OFF_NEG1, CENTER_POS, 0, true, true>(w, k, mk, zl1, zr1, vc, vo, acc, CENTER_POS);  // ... under chain j
                 } else {
                     load_line((k + 2) % S, j + 2);
                     other_n = classify(j + 1, idn, zln, zrn);
@@ -626,7 +626,7 @@ __global__ void __launch_bounds__(WC * 32, MINB) spmv_pattern_box7_kernel(Patter
                     for (int q = 0; q < Q; q++)
 #pragma unroll
                         for (int i = 0; i < 2; i++) mk[0][q][i] = lds_u32(mask_a + 4 + 4 * id[q][i]);
-                    box3_chain<Q, S, 1, OFF_NEG1, CENTER_POS, 1, false, false>(w, k, mk, zl1, zr1, vc, vo, acc);
+                    box3_chain<Q, S, 1, OFF_NEG1, CENTER_POS, 1, false, false>(w, k, mk, zl1, zr1, vc, vo, acc, CENTER_POS);
 #pragma unroll
                     for (int q = 0; q < Q; q++)
 #pragma unroll
@@ -831,18 +831,18 @@ __global__ void __maxnreg__(WZ == 3 ? 128 : 168) spmv_pattern_box8_kernel(Patter
                         bool zl[1][Q], zr[1][Q];
                         const unsigned vote = __reduce_or_sync(0xffffffffu, wv);
                         if (vote == 0) {
-                            box3_chain<Q, S, 1, OFF_NEG1, CENTER_POS, 0, false, false>(w, k, mk, zl, zr, vc, vo, acc);
+                            box3_chain<Q, S, 1, OFF_NEG1, CENTER_POS, 0, false, false>(w, k, mk, zl, zr, vc, vo, acc, CENTER_POS);
                         } else if (vote == 1 || vote == 2) {
 #pragma unroll
                             for (int q = 0; q < Q; q++) { zl[0][q] = c0v[q] != 0; zr[0][q] = c1v[q] != 0; }
-                            if (vote == 1) box3_chain<Q, S, 1, OFF_NEG1, CENTER_POS, 0, true, false>(w, k, mk, zl, zr, vc, vo, acc);
-                            else box3_chain<Q, S, 1, OFF_NEG1, CENTER_POS, 0, false, true>(w, k, mk, zl, zr, vc, vo, acc);
+                            if (vote == 1) box3_chain<Q, S, 1, OFF_NEG1, CENTER_POS, 0, true, false>(w, k, mk, zl, zr, vc, vo, acc, CENTER_POS);
+                            else box3_chain<Q, S, 1, OFF_NEG1, CENTER_POS, 0, false, true>(w, k, mk, zl, zr, vc, vo, acc, CENTER_POS);
                         } else {
 #pragma unroll
                             for (int q = 0; q < Q; q++)
 #pragma unroll
                                 for (int i = 0; i < 2; i++) mk[0][q][i] = lds_u32(sm.masks + 4 + 4 * id[0][q][i]);
-                            box3_chain<Q, S, 1, OFF_NEG1, CENTER_POS, 1, false, false>(w, k, mk, zl, zr, vc, vo, acc);
+                            box3_chain<Q, S, 1, OFF_NEG1, CENTER_POS, 1, false, false>(w, k, mk, zl, zr, vc, vo, acc, CENTER_POS);
 #pragma unroll
                             for (int q = 0; q < Q; q++)
 #pragma unroll

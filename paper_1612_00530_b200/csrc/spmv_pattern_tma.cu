@@ -83,8 +83,9 @@ struct RingLayout {
 // re-read from the three line slots of the ring; the rows stay interleaved as in the main chain.
 template <int Q, bool OFF_NEG1, int CENTER_POS, uint32_t LINE_BYTES>
 __device__ __noinline__ void ring_masked_step(uint32_t sl0, uint32_t sl1, uint32_t sl2, const uint32_t *mk, double vc, double vo,
-                                              double *out) {
+                                              double *out, int cp_rt) {
     constexpr int P = Q + 2;
+    const int cpos = CENTER_POS >= 0 ? CENTER_POS : cp_rt;
     const uint32_t sl[3] = {sl0, sl1, sl2};
     double acc[Q][2], xc[Q][2];
 #pragma unroll
@@ -93,7 +94,7 @@ __device__ __noinline__ void ring_masked_step(uint32_t sl0, uint32_t sl1, uint32
         xc[q][0] = (mk[q * 2] >> 13 & 1u) ? __dmul_rn(vc, u.y) : 0.0;
         xc[q][1] = (mk[q * 2 + 1] >> 13 & 1u) ? __dmul_rn(vc, v.x) : 0.0;
         acc[q][0] = acc[q][1] = 0.0;
-        if (CENTER_POS == 0) acc[q][0] = __dadd_rn(acc[q][0], xc[q][0]), acc[q][1] = __dadd_rn(acc[q][1], xc[q][1]);
+        if (cpos == 0) acc[q][0] = __dadd_rn(acc[q][0], xc[q][0]), acc[q][1] = __dadd_rn(acc[q][1], xc[q][1]);
     }
 #pragma unroll
     for (int pz = 0; pz < P; pz++)
@@ -112,7 +113,7 @@ __device__ __noinline__ void ring_masked_step(uint32_t sl0, uint32_t sl1, uint32
                     for (int i = 0; i < 2; i++) {
                         const bool on = mk[q * 2 + i] >> t & 1u;
                         if (t == 13) {
-                            if (CENTER_POS == 2) acc[q][i] = __dadd_rn(acc[q][i], xc[q][i]);
+                            if (cpos == 2) acc[q][i] = __dadd_rn(acc[q][i], xc[q][i]);
                         } else if (OFF_NEG1) {
                             acc[q][i] = __dsub_rn(acc[q][i], on ? e[i + dx] : 0.0);
                         } else {
@@ -124,7 +125,7 @@ __device__ __noinline__ void ring_masked_step(uint32_t sl0, uint32_t sl1, uint32
 #pragma unroll
     for (int q = 0; q < Q; q++)
 #pragma unroll
-        for (int i = 0; i < 2; i++) out[q * 2 + i] = CENTER_POS == 1 ? __dadd_rn(acc[q][i], xc[q][i]) : acc[q][i];
+        for (int i = 0; i < 2; i++) out[q * 2 + i] = cpos == 1 ? __dadd_rn(acc[q][i], xc[q][i]) : acc[q][i];
 }
 
 // -----------------------------------------------------------------------------------------
@@ -141,6 +142,7 @@ __device__ __noinline__ void ring_masked_step(uint32_t sl0, uint32_t sl1, uint32
 template <bool OFF_NEG1, int CENTER_POS>
 __device__ __forceinline__ double ring_leftover_row(const PatternArgs &p, uint32_t s_masks, int col, int line, int c, int np_x) {
     const int sy = p.sy, pl = p.plane_lines;
+    const int cpos = CENTER_POS >= 0 ? CENTER_POS : p.center_pos;
     const int64_t sz = (int64_t)sy * pl;
     const int64_t xi = col + (int64_t)sy * line + sz * c;
     const int64_t row = xi - p.g0;
@@ -156,18 +158,18 @@ __device__ __forceinline__ double ring_leftover_row(const PatternArgs &p, uint32
     if (id < 0) return 0.0;
     if (in_view != 0 && lds_u32(s_masks + 4 + 4 * id) == in_view) {
         double acc = 0.0;
-        if (CENTER_POS == 0) acc = __dadd_rn(acc, __dmul_rn(p.v_center, xv[13]));
+        if (cpos == 0) acc = __dadd_rn(acc, __dmul_rn(p.v_center, xv[13]));
 #pragma unroll
         for (int e = 0; e < 27; e++) {
             if (e == 13) {
-                if (CENTER_POS == 2) acc = __dadd_rn(acc, __dmul_rn(p.v_center, xv[13]));
+                if (cpos == 2) acc = __dadd_rn(acc, __dmul_rn(p.v_center, xv[13]));
             } else if (OFF_NEG1) {
                 acc = __dsub_rn(acc, xv[e]);
             } else {
                 acc = __dadd_rn(acc, __dmul_rn(p.v_off, xv[e]));
             }
         }
-        if (CENTER_POS == 1) acc = __dadd_rn(acc, __dmul_rn(p.v_center, xv[13]));
+        if (cpos == 1) acc = __dadd_rn(acc, __dmul_rn(p.v_center, xv[13]));
         p.y[row] = acc;
         return __dmul_rn(acc, xv[13]);
     } else {
@@ -183,6 +185,7 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
                               int c_hi, int np_x, int n_strips, int left_lo, int id_plane0, int total_steps, int steps_per_warp, int tile_lines, int rot) {
     using L = RingLayout<Q, S, IDT>;
     constexpr int P = L::P;
+    const int cpos = CENTER_POS >= 0 ? CENTER_POS : p.center_pos;  // CENTER_POS = -1: the general variant reads it at run time
     extern __shared__ unsigned char smem_raw[];
     const uint32_t sbase = (smem_u32(smem_raw) + 127u) & ~127u;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -340,7 +343,7 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
                 double xc[Q][2];
 #pragma unroll
                 for (int q = 0; q < Q; q++) acc[q][0] = acc[q][1] = 0.0;
-                if (CENTER_POS == 0) {
+                if (cpos == 0) {
 #pragma unroll
                     for (int q = 0; q < Q; q++) {
                         const double2 u = lds_f64x2(sl[1] + (q + 1) * L::kLineBytes), v = lds_f64x2(sl[1] + (q + 1) * L::kLineBytes + 16);
@@ -377,7 +380,7 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
                                 for (int i = 0; i < 2; i++) {
                                     const double ev = e[pz & 1][dy][i + dx];
                                     if (t == 13) {
-                                        if (CENTER_POS == 2) acc[q][i] = __dadd_rn(acc[q][i], __dmul_rn(vc, ev));
+                                        if (cpos == 2) acc[q][i] = __dadd_rn(acc[q][i], __dmul_rn(vc, ev));
                                         else xc[q][i] = ev;
                                     } else if (DBG == 1) {  // measurement only: no dependent FP64 chain
                                         if (dx == 1 && dy == 1) acc[q][i] = __dsub_rn(acc[q][i], ev);
@@ -389,7 +392,7 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
                                 }
                             }
                 }
-                if (CENTER_POS == 1) {
+                if (cpos == 1) {
 #pragma unroll
                     for (int q = 0; q < Q; q++)
 #pragma unroll
@@ -411,7 +414,7 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
                     }
                 if (__any_sync(0xffffffffu, real)) {
                     double am[Q * 2];
-                    ring_masked_step<Q, OFF_NEG1, CENTER_POS, L::kLineBytes>(sl[0], sl[1], sl[2], mk, vc, vo, am);
+                    ring_masked_step<Q, OFF_NEG1, CENTER_POS, L::kLineBytes>(sl[0], sl[1], sl[2], mk, vc, vo, am, p.center_pos);
 #pragma unroll
                     for (int q = 0; q < Q; q++)
 #pragma unroll
@@ -593,7 +596,7 @@ static int launch_ringp_t(const spmvb_matrix *a, PatternArgs &p_in, int chunk, c
         if (chunk > 0) grid = (total + spw * units - 1) / (spw * units);                                                         \
         const int cols_per_group = CTAC ? n_cols : n_strips;                                                                    \
         const int64_t wgrp = (int64_t)cols_per_group * p.plane_lines, kgrp = (wgrp + spw / 2) / spw;                              \
-        const int rot = options().debug_nochain == 7 ? 0 : (int)(((wgrp - kgrp * spw) % p.plane_lines + p.plane_lines) % p.plane_lines); \
+        const int rot = (kLabBuild && options().debug_nochain == 7) ? 0 : (int)(((wgrp - kgrp * spw) % p.plane_lines + p.plane_lines) % p.plane_lines); \
         if (DOT) {                                                                                                               \
             if (grid * kRingWarps > p.dot_capacity) return 1;                                                                    \
             fused_dot_request()->count = grid * kRingWarps;                                                                      \
@@ -601,11 +604,9 @@ static int launch_ringp_t(const spmvb_matrix *a, PatternArgs &p_in, int chunk, c
         spmv_pattern_ringp_kernel<Q, S, MINB, NEG, CP, IDT, PFD, DBG, CTAC, DOT><<<grid, kRingWarps * 32, L::kTotal, st>>>(                          \
             tm, tm_ids, p, c_lo, c_hi, np_x, n_strips, left_lo, id_plane0, total, spw, tile_lines, rot);                                          \
     } while (0)
-    if (neg1) {
-        if (cp == 0) LAUNCH_RINGP(true, 0); else if (cp == 1) LAUNCH_RINGP(true, 1); else LAUNCH_RINGP(true, 2);
-    } else {
-        if (cp == 0) LAUNCH_RINGP(false, 0); else if (cp == 1) LAUNCH_RINGP(false, 1); else LAUNCH_RINGP(false, 2);
-    }
+    // two instantiations: the HPCG value pattern (off-diagonals -1, centre last) fully specialised, and a general one
+    // (any off-diagonal value -- a product by -1.0 is exact, so it serves that case too -- centre position read at run time)
+    if (neg1 && cp == 1) LAUNCH_RINGP(true, 1); else LAUNCH_RINGP(false, -1);
 #undef LAUNCH_RINGP
     return check_launch("spmv_pattern_ringp") == SPMVB_OK ? 0 : -1;
 }
@@ -614,10 +615,12 @@ static int launch_ringp_t(const spmvb_matrix *a, PatternArgs &p_in, int chunk, c
 // Second translation unit (spmv_pattern_tma6.cu): the 6-planes-per-thread instantiations, so that the two halves build in parallel.
 // mode 0: chunk per CTA (with the ids-by-loads fallback); 1: per CTA, lab; 2: per warp, lab; 3-5: ablations.
 int launch_ring_q6(int mode, const spmvb_matrix *a, PatternArgs &p, int chunk, cudaStream_t st, int tile_lines) {
+#ifdef SPMVB_LAB
     if (mode == 2) return launch_ringp_t<6, 4, 2, true>(a, p, chunk, st, tile_lines);
     if (mode == 3) return launch_ringp_t<6, 4, 2, true, 0, 6, true>(a, p, chunk, st, tile_lines);  // measurement only: no left-over columns
     if (mode == 4) return launch_ringp_t<6, 4, 2, true, 0, 3, true>(a, p, chunk, st, tile_lines);  // measurement only: fetch + store
     if (mode == 5) return launch_ringp_t<6, 4, 2, true, 0, 4, true>(a, p, chunk, st, tile_lines);  // measurement only: fetch
+#endif
     if (mode == 0 && p.dot_partial && fused_dot_request()) {  // cg_solve: x.y in the same pass (ids through the ring only)
         const int rcd = launch_ringp_t<6, 4, 2, true, 0, 0, true, true>(a, p, chunk, st, tile_lines);
         if (rcd != 1) return rcd;
@@ -653,14 +656,12 @@ int launch_pattern_ring(int which, int lines, const spmvb_matrix *a, PatternArgs
     int rc = 1;
     const int tl = lines > 0 ? lines : 16;
     switch (which) {
+#ifdef SPMVB_LAB
         case 6: return launch_ringp_t<4, 4, 3, true, 2>(a, p, lines, st);     // + TMA L2 prefetch 2 sets ahead: 95 us (4 ahead: 105 us)
         case 7: return launch_ringp_t<4, 4, 3, true, 0, 1>(a, p, lines, st);  // measurement only (wrong results): no FP64 chains
         case 8: return launch_ringp_t<4, 4, 3, true, 0, 2>(a, p, lines, st);  // measurement only (wrong results): one operand quad per step
         case 9: return launch_ringp_t<4, 4, 3, true, 0, 3>(a, p, lines, st);  // measurement only: ring fetches + y stores, nothing else
         case 10: return launch_ringp_t<4, 4, 3, true, 0, 4>(a, p, lines, st); // measurement only: ring fetches only
-        case 11:  // a chunk per warp instead of per CTA: 87 us
-            rc = launch_ringp_t<4, 4, 3, true>(a, p, lines, st);
-            return rc == 1 ? launch_ringp_t<4, 5, 3, false>(a, p, lines, st) : rc;
         case 12: return launch_ringp_t<4, 4, 3, true, 0, 4, true>(a, p, lines, st);  // CTA chunks, fetch only
         case 13: return launch_ringp_t<4, 4, 3, true, 0, 3, true>(a, p, lines, st);  // CTA chunks, fetch + store only
         case 14:  // CTA chunks, 2 planes/thread, 6 slots: 90 us
@@ -668,6 +669,17 @@ int launch_pattern_ring(int which, int lines, const spmvb_matrix *a, PatternArgs
             return rc == 1 ? launch_ringp_t<4, 5, 3, false, 0, 0, true>(a, p, lines, st) : rc;
         case 15: return launch_ringp_t<4, 4, 3, true, 9, 0, true>(a, p, lines, st);   // CTA chunks, streaming (evict-first) y stores: no change
         case 16: return launch_ringp_t<4, 4, 3, true, 0, 5, true>(a, p, lines, st);   // measurement only: fetch only, no left-over columns
+        case 25: return launch_ring_q6(1, a, p, 0, st, tl);      // 6 planes/thread, round-robin tiles per CTA
+        case 26: return launch_ring_q6(2, a, p, lines, st, 0);   // 6 planes/thread, chunk per warp
+        case 28: return launch_ring_q6(3, a, p, lines, st, 0);   // ablations of the default (6 planes/thread, chunk per CTA):
+        case 29: return launch_ring_q6(4, a, p, lines, st, 0);   //   no left-over columns / fetch + store only / fetch only
+        case 30: return launch_ring_q6(5, a, p, lines, st, 0);
+        case 27: return launch_ring_q6(2, a, p, 0, st, tl);      // 6 planes/thread, round-robin tiles per warp
+#endif
+        // the schedules the default policy chooses between, forced (tests cover each of them on every shape):
+        case 11:  // a chunk per warp instead of per CTA: 87 us
+            rc = launch_ringp_t<4, 4, 3, true>(a, p, lines, st);
+            return rc == 1 ? launch_ringp_t<4, 5, 3, false>(a, p, lines, st) : rc;
         case 17: return launch_ringp_t<4, 5, 3, false, 0, 0, true>(a, p, lines, st);  // CTA chunks, 5 slots, ids by per-thread loads: 81 us
         case 18:  // tiles of `lines` (default 16) lines dealt out round-robin, a tile per CTA: 85-87 us (512^3: 530-575 us)
             rc = launch_ringp_t<4, 4, 3, true, 0, 0, true>(a, p, 0, st, tl);
@@ -676,12 +688,6 @@ int launch_pattern_ring(int which, int lines, const spmvb_matrix *a, PatternArgs
             rc = launch_ringp_t<4, 4, 3, true, 0, 0, true>(a, p, lines, st);
             return rc == 1 ? launch_ringp_t<4, 5, 3, false, 0, 0, true>(a, p, lines, st) : rc;
         // (3 / 5 / 7 / 8 planes per thread, chunk per CTA: 80.6 / 76.2 / 74.0 / 84.1 us at 256^3, r01_probe_planes_per_thread.log)
-        case 25: return launch_ring_q6(1, a, p, 0, st, tl);      // 6 planes/thread, round-robin tiles per CTA
-        case 26: return launch_ring_q6(2, a, p, lines, st, 0);   // 6 planes/thread, chunk per warp
-        case 28: return launch_ring_q6(3, a, p, lines, st, 0);   // ablations of the default (6 planes/thread, chunk per CTA):
-        case 29: return launch_ring_q6(4, a, p, lines, st, 0);   //   no left-over columns / fetch + store only / fetch only
-        case 30: return launch_ring_q6(5, a, p, lines, st, 0);
-        case 27: return launch_ring_q6(2, a, p, 0, st, tl);      // 6 planes/thread, round-robin tiles per warp
         case 19:  // ... a tile per warp
             rc = launch_ringp_t<4, 4, 3, true>(a, p, 0, st, tl);
             return rc == 1 ? launch_ringp_t<4, 5, 3, false>(a, p, 0, st, tl) : rc;

@@ -268,21 +268,26 @@ int launch_ell(const double *values, const int32_t *columns, int width, const do
         // TB/s (half reads, half writes).  64-row tiles 922 us, 128-row tiles 946 us (ell_kernel = 5, 4;
         // profiles/r01_probe256_ell_vt_bulk_tiles.log).  The persistent two-stage ring below (ell_kernel = 3) holds 2 CTAs/SM: 1021-1038 us.
         const int k = options().ell_kernel;
-        const int rows = k == 4 ? 128 : k == 5 ? 64 : 32;
-        if ((k == 0 || k == 4 || k == 5 || k == 6) && (size_t)rows * width * 12 <= 200 * 1024) {
+        const int rows = !kLabBuild ? 32 : k == 4 ? 128 : k == 5 ? 64 : 32;
+        if ((k == 0 || (kLabBuild && (k == 4 || k == 5 || k == 6))) && (size_t)rows * width * 12 <= 200 * 1024) {
             static PerDevice<bool> attr;
             if (!attr.get()) {
+#ifdef SPMVB_LAB
                 SPMVB_CUDA(cudaFuncSetAttribute(spmv_ell_kernel<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
                 SPMVB_CUDA(cudaFuncSetAttribute(spmv_ell_kernel<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+#endif
                 SPMVB_CUDA(cudaFuncSetAttribute(spmv_ell_kernel<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
                 attr.get() = true;
             }
             const int t0 = row_begin / rows, nt = (row_end + rows - 1) / rows - t0;
             const size_t bytes = (size_t)rows * width * 12;
             // whole tiles below row_end are bulk-copied; the last, partial one is staged with loads
+#ifdef SPMVB_LAB
             if (rows == 128) spmv_ell_kernel<128, true><<<nt, 128, bytes, st>>>(values, columns, width, x, x_col0, y, row_begin, row_end, t0, row_map, row_end);
             else if (rows == 64) spmv_ell_kernel<64, true><<<nt, 64, bytes, st>>>(values, columns, width, x, x_col0, y, row_begin, row_end, t0, row_map, row_end);
-            else spmv_ell_kernel<32, true><<<nt, 32, bytes, st>>>(values, columns, width, x, x_col0, y, row_begin, row_end, t0, row_map, row_end);
+            else
+#endif
+            spmv_ell_kernel<32, true><<<nt, 32, bytes, st>>>(values, columns, width, x, x_col0, y, row_begin, row_end, t0, row_map, row_end);
             return check_launch("spmv_ell_bulk");
         }
     }
@@ -298,7 +303,7 @@ int launch_ell(const double *values, const int32_t *columns, int width, const do
                 tma_attr.get() = true;
             }
             const int per_sm = std::max(1, (int)std::min<size_t>(8, (220 * 1024) / (need + 1024)));
-            const int grid = std::min(tiles, 148 * per_sm);
+            const int grid = std::min(tiles, sm_count() * per_sm);
             spmv_rows_tma_kernel<kTileRows, NS, 0><<<grid, kTileRows, need, st>>>(values, columns, nullptr, nullptr, width, 0, x, x_col0, y,
                                                                                row_begin, row_end, tile0, tiles, row_map);
             return check_launch("spmv_ell_tma");
@@ -332,7 +337,7 @@ int launch_vt(const spmvb_matrix *a, const double *x, int64_t x_col0, double *y,
                 tma_attr.get() = true;
             }
             const int per_sm = std::max(1, (int)std::min<size_t>(8, (200 * 1024) / (need + 4096)));
-            const int grid = std::min(tiles, 148 * per_sm);
+            const int grid = std::min(tiles, sm_count() * per_sm);
             spmv_rows_tma_kernel<kTileRows, NS, 1><<<grid, kTileRows, need, st>>>(
                 nullptr, static_cast<const int32_t *>(a->s[SPMVB_S_SORTED_COLUMNS]), static_cast<const int32_t *>(a->s[SPMVB_S_ENDS]),
                 static_cast<const double *>(a->s[SPMVB_S_TABLE]), a->width, a->m, x, x_col0, y, row_begin, row_end, tile0, tiles, nullptr);
@@ -350,6 +355,7 @@ int launch_vt(const spmvb_matrix *a, const double *x, int64_t x_col0, double *y,
     const auto *sc = static_cast<const int32_t *>(a->s[SPMVB_S_SORTED_COLUMNS]);
     const auto *se = static_cast<const int32_t *>(a->s[SPMVB_S_ENDS]);
     const auto *tab = static_cast<const double *>(a->s[SPMVB_S_TABLE]);
+#ifdef SPMVB_LAB
     if (options().ell_kernel == 6) {  // 64-row tiles
         const int t0 = row_begin / 64, nt = (row_end + 63) / 64 - t0;
         static PerDevice<bool> a64;
@@ -361,7 +367,9 @@ int launch_vt(const spmvb_matrix *a, const double *x, int64_t x_col0, double *y,
     } else if (options().ell_kernel == 7) {  // 32-row tiles
         const int t0 = row_begin / 32, nt = (row_end + 31) / 32 - t0;
         spmv_vt_kernel<32, true><<<nt, 32, (size_t)32 * (a->width + a->m) * 4 + (size_t)a->m * 8 + 16, st>>>(sc, se, tab, a->width, a->m, x, x_col0, y, row_begin, row_end, t0, a->n);
-    } else if (bulk) spmv_vt_kernel<kTileRows, true><<<tiles, kTileRows, smem, st>>>(sc, se, tab, a->width, a->m, x, x_col0, y, row_begin, row_end, tile0, a->n);
+    } else
+#endif
+    if (bulk) spmv_vt_kernel<kTileRows, true><<<tiles, kTileRows, smem, st>>>(sc, se, tab, a->width, a->m, x, x_col0, y, row_begin, row_end, tile0, a->n);
     else spmv_vt_kernel<kTileRows, false><<<tiles, kTileRows, smem, st>>>(sc, se, tab, a->width, a->m, x, x_col0, y, row_begin, row_end, tile0, a->n);
     return check_launch("spmv_vt");
 }

@@ -71,7 +71,7 @@ int spmvb_vec_fill(double *dev, int64_t n, int32_t kind, uint64_t seed, double l
     if (!dev || n < 0 || kind < 0 || kind > 2) return fail(SPMVB_ERR_INVALID_ARGUMENT, "vec_fill: bad arguments");
     if (n == 0) return SPMVB_OK;
     const int threads = 256;
-    const int blocks = (int)std::min<int64_t>((n + threads - 1) / threads, 148 * 16);
+    const int blocks = (int)std::min<int64_t>((n + threads - 1) / threads, sm_count() * 16);
     vec_fill_kernel<<<blocks, threads, 0, as_stream(stream)>>>(dev, n, kind, seed, lo, hi, first_index);
     SPMVB_CUDA(cudaGetLastError());
     return SPMVB_OK;
@@ -85,7 +85,7 @@ int spmvb_compare(const double *y, const double *ref, const double *scale, int64
     SPMVB_CUDA(cudaMemsetAsync(d, 0, 16, as_stream(stream)));
     if (n > 0) {
         const int threads = 256;
-        const int blocks = (int)std::min<int64_t>((n + threads - 1) / threads, 148 * 16);
+        const int blocks = (int)std::min<int64_t>((n + threads - 1) / threads, sm_count() * 16);
         compare_kernel<<<blocks, threads, 0, as_stream(stream)>>>(y, ref, scale, n, d, d + 1);
     }
     unsigned long long h[2] = {0, 0};

@@ -50,6 +50,37 @@ def test_no_cpu_fallback_without_a_device():
         sp.generate_matrix(sp.GridSpec(0, 1, 1))
 
 
+def test_default_library_rejects_unknown_and_lab_options():
+    """Measurement-only kernel variants (some return wrong y on purpose) are compiled only into the lab build;
+    the default library must refuse the option values that select them, and unknown keys."""
+    import paper_1612_00530_b200 as sp
+    assert sp.get_option("lab_build") == 0
+    with pytest.raises(sp.InvalidArgument):
+        sp.set_option("no_such_option", 1)
+    for key, values in (("box_march", (1, 5, 20, 47, 62, 96, 97, 98, 99, 100, 104, 118, 119, 120)), ("debug_nochain", (1, 7)),
+                        ("ell_kernel", (4, 5, 6, 7)), ("pattern_kernel", (4, -1))):
+        for v in values:
+            with pytest.raises(sp.InvalidArgument):
+                sp.set_option(key, v)
+        assert sp.get_option(key) == 0
+    for key, values in (("box_march", (3, 90, 101, 107, 108, 109, 110, 0)), ("ell_kernel", (1, 2, 3, 0)), ("pattern_kernel", (1, 2, 3, 0))):
+        for v in values:
+            sp.set_option(key, v)
+            assert sp.get_option(key) == v
+
+
+def test_default_library_holds_no_lab_kernels():
+    import shutil
+    import subprocess
+    if not shutil.which("cuobjdump"):
+        pytest.skip("cuobjdump not available")
+    from paper_1612_00530_b200 import _cabi
+    out = subprocess.run(["cuobjdump", "-elf", _cabi.SO_PATH], capture_output=True, text=True).stdout
+    kernels = set(re.findall(r"^\.text\.(\S+)", out, flags=re.M))
+    assert 0 < len(kernels) < 80, len(kernels)
+    assert not [k for k in kernels if "box5" in k or "box6" in k or "box7" in k or "box8" in k]
+
+
 def test_product_never_imports_the_oracle():
     """The oracle is test infrastructure: nothing under the product package may import,
     load, link or include it."""

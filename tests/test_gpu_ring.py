@@ -7,7 +7,7 @@ pytestmark = pytest.mark.gpu
 
 from tests.test_gpu_parity import bits, run, sp, up_pat  # noqa: E402,F401
 
-RING = [90, 101, 104, 107, 108, 109, 110]  # default schedule, chunk per warp, 2 planes/thread, ids by loads, round-robin tiles
+RING = [90, 101, 107, 108, 109, 110]  # default schedule, chunk per warp, ids by loads, round-robin tiles (per CTA, per warp), 4 planes/thread
 
 
 def ring_run(sp, d, x, march, lines=0, must_ring=True, **kw):
