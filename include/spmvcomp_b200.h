@@ -121,6 +121,7 @@ int spmvb_set_device(int device);
  *                     lab build only: further variants and ablations (csrc/spmv_pattern*.cu list them with their times)
  *   "box_lines":      lines per CTA tile / chunk length of the tensor ring (0 = default)
  *   "host_chunks":    row chunks of the pipelined spmvb_spmv_host (0 = default 8)
+ *   "slab_graph":     1 (default) spmvb_slab_spmv replays its copies and launches as a CUDA graph; 0 launches directly
  *   "symgs_graph":    1 (default) the launches of a symgs sweep are recorded into a CUDA graph and replayed; 0 launches directly
  *   "cg_graph":       1 (default) spmvb_cg_solve records its iteration into a CUDA graph after the first one and replays it (one
  *                     graph launch per iteration); 0 launches the kernels directly.  "last_cg_graph" (read-only) says which ran
@@ -221,6 +222,56 @@ int spmvb_spmv(const spmvb_matrix *a, const double *x_dev, int64_t x_col0, int64
  * x_len == n (length mismatch -> SPMVB_ERR_INVALID_ARGUMENT), copies x to the
  * device, runs, copies y back, synchronises. */
 int spmvb_spmv_host(const spmvb_matrix *a, const double *x_host, int64_t x_len, double *y_host);
+
+/* ---- z-slab SpMV with halo exchange (SURVEY 8b "spmv_multi", 8e) ---------------- */
+/* The grid is cut into z-slabs; a slab's rows are a contiguous range, exactly the [begin,end) of
+ * unchecked::spmv_rows (inc/kernels.hpp:27-36; the paper's distribution: PAPER.md:473-477,505-531).  `a` holds the
+ * rows of whole planes (plane_rows = nx*ny each; row_offset a multiple of it; global columns).  The slab's vector is
+ *     x_ghosted = [ghost plane | owned planes | ghost plane],  n + 2*plane_rows entries,
+ * i.e. spmvb_spmv's x_col0 = row_offset - plane_rows.  has_lower / has_upper: a neighbour exists on that side. */
+typedef struct spmvb_slab spmvb_slab; /* opaque, caller-destroyed; not re-entrant */
+enum spmvb_slab_mode {
+    SPMVB_SLAB_SERIAL = 0, /* ghost copies, then one launch over all owned planes */
+    SPMVB_SLAB_OVERLAP = 1 /* ghost copies on a side stream || planes that need no ghost; then the first and last plane */
+};
+int spmvb_slab_create(const spmvb_matrix *a, int64_t plane_rows, int32_t has_lower, int32_t has_upper, spmvb_slab **out);
+int spmvb_slab_destroy(spmvb_slab *s);
+/* One SpMV of the slab including its halo exchange as copies: lower_src = the lower neighbour's LAST owned plane,
+ * upper_src = the upper neighbour's FIRST owned plane (device pointers: same device, peer-mapped, or from
+ * spmvb_ipc_open; NULL = that ghost plane is already in place).  The neighbours' planes must not be written while the
+ * call is in flight (the caller orders producers of x before it).  Asynchronous on `stream`.  From the second call
+ * with the same pointers on, the copies and launches are replayed as one CUDA graph ("slab_graph" = 0: never). */
+int spmvb_slab_spmv(spmvb_slab *s, double *x_ghosted, double *y, const double *lower_src, const double *upper_src,
+                    int32_t mode, void *stream);
+/* The two halves, for callers that run the exchange themselves (NCCL send/recv on their own stream): the rows that
+ * need no ghost plane (may overlap the exchange), then the first and last owned planes (after the receive). */
+int spmvb_slab_interior(spmvb_slab *s, const double *x_ghosted, double *y, void *stream);
+int spmvb_slab_boundary(spmvb_slab *s, const double *x_ghosted, double *y, void *stream);
+int spmvb_slab_last_was_graph(const spmvb_slab *s, int32_t *flag);
+/* Peer memory across processes (one process per GPU): CUDA IPC handle of a vector from spmvb_vec_alloc. */
+int spmvb_ipc_export(const void *dev_base, unsigned char handle[64]);
+int spmvb_ipc_open(const unsigned char handle[64], void **dev_ptr);
+int spmvb_ipc_close(void *dev_ptr);
+
+/* One host thread driving G slabs over a device list (context over a device list, spmv_multi, bench).
+ * Devices may repeat (logical slabs on one device).  Build is per slab on its device (generator -> format), the
+ * per-slab pattern dictionaries are merged so that ids equal a single-matrix compression; slab g owns planes
+ * [z0,z1) of grid->nz split as evenly as possible (low slabs take the remainder). */
+typedef struct spmvb_multi spmvb_multi;
+int spmvb_multi_create(const spmvb_grid *grid, int32_t format, const spmvb_compress_options *opts, const int32_t *devices,
+                       int32_t n_devices, spmvb_multi **out);
+int spmvb_multi_destroy(spmvb_multi *m);
+int spmvb_multi_parts(const spmvb_multi *m, int32_t *n_parts);
+/* any out pointer may be NULL */
+int spmvb_multi_part(const spmvb_multi *m, int32_t part, int32_t *device, int64_t *z0, int64_t *z1,
+                     const spmvb_matrix **matrix, double **x_ghosted, double **y);
+int spmvb_multi_fill_x(spmvb_multi *m, int32_t kind, uint64_t seed, double lo, double hi); /* make_test_vector, global */
+int spmvb_multi_upload_x(spmvb_multi *m, const double *x_host, int64_t n);
+int spmvb_multi_download_y(spmvb_multi *m, double *y_host, int64_t n);
+int spmvb_multi_spmv(spmvb_multi *m, int32_t mode); /* y = A x on every slab, exchange included; asynchronous */
+int spmvb_multi_sync(spmvb_multi *m);
+/* reps SpMVs after a warm-up: host wall clock between device-wide syncs and the slowest slab's device time */
+int spmvb_multi_bench(spmvb_multi *m, int32_t reps, int32_t mode, double *seconds, double *device_seconds);
 
 /* ---- the caller of the path: CG vector primitives and driver ---- */
 /* dot (inc/kernels.hpp:39): device vectors, result to the host; fixed-shape tree (deterministic). */

@@ -6,4 +6,4 @@ CPU fallback and the import fails loudly when the library has not been built.
 from . import _cabi  # noqa: F401  (raises ImportError when the .so is missing)
 from .api import *  # noqa: F401,F403
 from .api import DeviceMatrix, DeviceVector, GridSpec  # noqa: F401
-from .slab import SlabCg, SlabLayout, SlabSpmv, build_slab_pattern, merge_dictionaries  # noqa: F401,E402
+from .slab import DeviceSlabSpmv, SlabCg, SlabLayout, SlabSpmv, build_slab_pattern, merge_dictionaries  # noqa: F401,E402

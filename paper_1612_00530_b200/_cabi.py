@@ -89,7 +89,12 @@ SYMBOLS = [
     "spmvb_vec_alloc", "spmvb_vec_free", "spmvb_vec_upload", "spmvb_vec_download", "spmvb_vec_fill",
     "spmvb_spmv", "spmvb_spmv_host", "spmvb_compare", "spmvb_row_abs_scale", "spmvb_dot", "spmvb_waxpby",
     "spmvb_cg_solve", "spmvb_symgs_sweep", "spmvb_pcg_solve",
+    "spmvb_slab_create", "spmvb_slab_destroy", "spmvb_slab_spmv", "spmvb_slab_interior", "spmvb_slab_boundary",
+    "spmvb_slab_last_was_graph", "spmvb_ipc_export", "spmvb_ipc_open", "spmvb_ipc_close",
+    "spmvb_multi_create", "spmvb_multi_destroy", "spmvb_multi_parts", "spmvb_multi_part", "spmvb_multi_fill_x",
+    "spmvb_multi_upload_x", "spmvb_multi_download_y", "spmvb_multi_spmv", "spmvb_multi_sync", "spmvb_multi_bench",
 ]
+SLAB_SERIAL, SLAB_OVERLAP = 0, 1
 
 if not os.path.exists(SO_PATH):
     raise ImportError(
@@ -132,6 +137,25 @@ lib.spmvb_waxpby.argtypes = [_f64, _vp, _f64, _vp, _vp, _i64, _vp]
 lib.spmvb_cg_solve.argtypes = [_vp, _vp, _vp, _i32, _f64, C.POINTER(_i32), C.POINTER(_i32), _vp, _vp]
 lib.spmvb_symgs_sweep.argtypes = [_vp, C.POINTER(Grid), _vp, _vp, _vp]
 lib.spmvb_pcg_solve.argtypes = [_vp, _vp, C.POINTER(Grid), _i32, _vp, _vp, _i32, _f64, C.POINTER(_i32), C.POINTER(_i32), _vp, _vp]
+lib.spmvb_slab_create.argtypes = [_vp, _i64, _i32, _i32, _pp]
+lib.spmvb_slab_destroy.argtypes = [_vp]
+lib.spmvb_slab_spmv.argtypes = [_vp, _vp, _vp, _vp, _vp, _i32, _vp]
+lib.spmvb_slab_interior.argtypes = [_vp, _vp, _vp, _vp]
+lib.spmvb_slab_boundary.argtypes = [_vp, _vp, _vp, _vp]
+lib.spmvb_slab_last_was_graph.argtypes = [_vp, C.POINTER(_i32)]
+lib.spmvb_ipc_export.argtypes = [_vp, C.c_char_p]
+lib.spmvb_ipc_open.argtypes = [C.c_char_p, _pp]
+lib.spmvb_ipc_close.argtypes = [_vp]
+lib.spmvb_multi_create.argtypes = [C.POINTER(Grid), _i32, C.POINTER(CompressOptions), C.POINTER(_i32), _i32, _pp]
+lib.spmvb_multi_destroy.argtypes = [_vp]
+lib.spmvb_multi_parts.argtypes = [_vp, C.POINTER(_i32)]
+lib.spmvb_multi_part.argtypes = [_vp, _i32, C.POINTER(_i32), C.POINTER(_i64), C.POINTER(_i64), _pp, _pp, _pp]
+lib.spmvb_multi_fill_x.argtypes = [_vp, _i32, _u64, _f64, _f64]
+lib.spmvb_multi_upload_x.argtypes = [_vp, _vp, _i64]
+lib.spmvb_multi_download_y.argtypes = [_vp, _vp, _i64]
+lib.spmvb_multi_spmv.argtypes = [_vp, _i32]
+lib.spmvb_multi_sync.argtypes = [_vp]
+lib.spmvb_multi_bench.argtypes = [_vp, _i32, _i32, C.POINTER(_f64), C.POINTER(_f64)]
 lib.spmvb_set_option.argtypes = [C.c_char_p, C.c_int]
 lib.spmvb_get_option.argtypes = [C.c_char_p, C.POINTER(C.c_int)]
 lib.spmvb_device_count.argtypes = [C.POINTER(C.c_int)]

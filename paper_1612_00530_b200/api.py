@@ -95,6 +95,11 @@ class DeviceVector:
     def data_ptr(self):
         return self.ptr
 
+    @property
+    def __cuda_array_interface__(self):
+        """Zero-copy view for torch.as_tensor(v, device="cuda") and friends (the vector stays owned by this object)."""
+        return {"shape": (self.n,), "typestr": "<f8", "data": (self.ptr, False), "version": 2}
+
     @classmethod
     def from_host(cls, host, stream=None):
         host = _np(host, np.float64)
@@ -389,3 +394,136 @@ def device_count() -> int:
     c = C.c_int()
     check(lib.spmvb_device_count(C.byref(c)))
     return c.value
+
+
+# ---- z-slabs behind the C-ABI (SURVEY 8b "spmv_multi", 8e) -----------------------------------------------------------
+SLAB_SERIAL, SLAB_OVERLAP = cabi.SLAB_SERIAL, cabi.SLAB_OVERLAP
+
+
+class Slab:
+    """One rank's slab of whole planes: spmvb_slab_* (the row ranges of unchecked::spmv_rows, kernels.hpp:27-36).
+    x is the ghosted local vector [ghost plane | owned planes | ghost plane]."""
+
+    def __init__(self, a: DeviceMatrix, plane_rows: int, has_lower: bool, has_upper: bool):
+        h = C.c_void_p()
+        check(lib.spmvb_slab_create(a.h, plane_rows, int(has_lower), int(has_upper), C.byref(h)))
+        self.h, self.a = h, a  # keeps the matrix alive
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib.spmvb_slab_destroy(self.h)
+            self.h = None
+
+    def spmv(self, x_ghosted, y, lower_src=None, upper_src=None, mode=SLAB_SERIAL, stream=None):
+        """Exchange (copies from the neighbours' planes: device pointers or None) + SpMV; a CUDA graph from the second call on."""
+        lo = None if lower_src is None else C.c_void_p(int(lower_src))
+        hi = None if upper_src is None else C.c_void_p(int(upper_src))
+        check(lib.spmvb_slab_spmv(self.h, _ptr(x_ghosted), _ptr(y), lo, hi, mode, _stream(stream)))
+
+    def interior(self, x_ghosted, y, stream=None):
+        check(lib.spmvb_slab_interior(self.h, _ptr(x_ghosted), _ptr(y), _stream(stream)))
+
+    def boundary(self, x_ghosted, y, stream=None):
+        check(lib.spmvb_slab_boundary(self.h, _ptr(x_ghosted), _ptr(y), _stream(stream)))
+
+    @property
+    def last_was_graph(self) -> bool:
+        f = C.c_int32()
+        check(lib.spmvb_slab_last_was_graph(self.h, C.byref(f)))
+        return bool(f.value)
+
+
+def ipc_export(dev_base) -> bytes:
+    """CUDA IPC handle (64 bytes) of a vector from DeviceVector / spmvb_vec_alloc, for a neighbour process to map."""
+    buf = C.create_string_buffer(64)
+    check(lib.spmvb_ipc_export(_ptr(dev_base), buf))
+    return buf.raw
+
+
+def ipc_open(handle: bytes) -> int:
+    p = C.c_void_p()
+    check(lib.spmvb_ipc_open(C.create_string_buffer(handle, 64), C.byref(p)))
+    return p.value
+
+
+def ipc_close(ptr: int):
+    check(lib.spmvb_ipc_close(C.c_void_p(ptr)))
+
+
+class _Borrowed:
+    """A device pointer owned by someone else."""
+
+    def __init__(self, ptr, n):
+        self.ptr, self.n = ptr, n
+
+    def data_ptr(self):
+        return self.ptr
+
+
+class MultiSlab:
+    """spmvb_multi_*: one host thread driving the z-slabs of a grid over a device list (devices may repeat)."""
+
+    def __init__(self, spec: GridSpec, devices, fmt=FMT_PATTERN, diagonal=26.0, off_diagonal=-1.0, perturb=None,
+                 values_in_pattern=True, min_pattern_rows=1, dict_cap=0, value_table_limit=256):
+        validate_grid(spec)
+        g = cabi.Grid(spec.nx, spec.ny, spec.nz, diagonal, off_diagonal, 0, 0, 0.0, 0.0)
+        if perturb is not None:
+            g.perturb, g.perturb_seed, g.perturb_fraction, g.perturb_noise = 1, perturb[0], perturb[1], perturb[2]
+        o = _opts(value_table_limit, values_in_pattern, min_pattern_rows, dict_cap)
+        devs = (C.c_int32 * len(devices))(*devices)
+        h = C.c_void_p()
+        check(lib.spmvb_multi_create(C.byref(g), fmt, C.byref(o), devs, len(devices), C.byref(h)))
+        self.h, self.spec, self.n = h, spec, spec.rows()
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib.spmvb_multi_destroy(self.h)
+            self.h = None
+
+    @property
+    def n_parts(self) -> int:
+        c = C.c_int32()
+        check(lib.spmvb_multi_parts(self.h, C.byref(c)))
+        return c.value
+
+    def part(self, g):
+        """(device, z0, z1, matrix view, x_ghosted, y) of slab g; the views are owned by this object."""
+        dev, z0, z1 = C.c_int32(), C.c_int64(), C.c_int64()
+        a, x, y = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        check(lib.spmvb_multi_part(self.h, g, C.byref(dev), C.byref(z0), C.byref(z1), C.byref(a), C.byref(x), C.byref(y)))
+        plane = self.spec.nx * self.spec.ny
+        n = (z1.value - z0.value) * plane
+        view = DeviceMatrix(a)
+        view.__class__ = _BorrowedMatrix  # never destroyed from here
+        return dev.value, z0.value, z1.value, view, _Borrowed(x.value, n + 2 * plane), _Borrowed(y.value, n)
+
+    def fill_x(self, kind, seed=None, lo=0.0, hi=1.0):
+        if kind == RANDOM and seed is None:
+            raise InvalidArgument("seed is required for the random kind")
+        check(lib.spmvb_multi_fill_x(self.h, kind, seed or 0, lo, hi))
+
+    def upload_x(self, x):
+        x = _np(x, np.float64)
+        check(lib.spmvb_multi_upload_x(self.h, _ptr(x), x.shape[0]))
+
+    def spmv(self, mode=SLAB_SERIAL):
+        check(lib.spmvb_multi_spmv(self.h, mode))
+
+    def sync(self):
+        check(lib.spmvb_multi_sync(self.h))
+
+    def download_y(self) -> np.ndarray:
+        y = np.empty(self.n, dtype=np.float64)
+        check(lib.spmvb_multi_download_y(self.h, _ptr(y), self.n))
+        return y
+
+    def bench(self, reps, mode=SLAB_SERIAL):
+        """(host seconds between device-wide syncs, slowest slab's device seconds) for `reps` SpMVs incl. exchange."""
+        t, td = C.c_double(), C.c_double()
+        check(lib.spmvb_multi_bench(self.h, reps, mode, C.byref(t), C.byref(td)))
+        return t.value, td.value
+
+
+class _BorrowedMatrix(DeviceMatrix):
+    def __del__(self):
+        self.h = None

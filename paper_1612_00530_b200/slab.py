@@ -158,6 +158,105 @@ class SlabSpmv:
             self.kernel(x_local, y_local, hi, n)
 
 
+class DeviceSlabSpmv(SlabSpmv):
+    """The product's z-slab SpMV of one rank: the kernels and, where the neighbours' memory is mapped, the exchange run
+    behind the C-ABI (spmvb_slab_*, csrc/slab.cu); torch.distributed carries the exchange otherwise.
+
+    exchange = "nccl": the two boundary planes travel by batch_isend_irecv (NCCL send/recv over NVLink).
+               schedule "serial": exchange, then ONE launch over all owned planes; "overlap": exchange on the side stream
+               while the planes that need no ghost are computed, then the first and last owned plane.
+    exchange = "p2p":  every rank maps its neighbours' vectors (CUDA IPC) and spmvb_slab_spmv pulls their boundary planes
+               with two copies in front of the launch, all of it one CUDA graph per SpMV.  x must be quiescent on the
+               neighbours during the call (true for a fixed x; CG orders it with its all-reduces plus `fence()`).
+    `x_local` must come from spmvb_vec_alloc (DeviceVector) for "p2p"."""
+
+    def __init__(self, sp, layout: SlabLayout, matrix, dist, main_stream, comm_stream, torch, exchange="nccl", schedule="serial"):
+        super().__init__(layout, None, dist, comm_stream, main_stream, torch)
+        if exchange not in ("nccl", "p2p") or schedule not in ("serial", "overlap"):
+            raise ValueError(f"unknown exchange / schedule: {exchange} / {schedule}")
+        self.sp, self.exchange_kind, self.schedule = sp, exchange, schedule
+        self.slab = sp.Slab(matrix, layout.plane, layout.has_lower, layout.has_upper)
+        self.mode = sp.SLAB_SERIAL if schedule == "serial" else sp.SLAB_OVERLAP
+        self._peers = {}      # rank -> mapped base pointer of its x_local
+        self._graph = None    # a captured step of the "nccl" exchange (torch.cuda.CUDAGraph), when capture worked
+        self._graph_key = None
+        self.launches_per_spmv = 1 if (schedule == "serial" or layout.world == 1) else 1 + int(layout.has_lower) + int(layout.has_upper)
+
+    # -- "p2p": map the neighbours' x_local once
+    def map_neighbours(self, x_local):
+        L, d, sp = self.L, self.dist, self.sp
+        handles = [None] * L.world
+        d.all_gather_object(handles, sp.ipc_export(x_local))
+        for r in (L.rank - 1, L.rank + 1):
+            if 0 <= r < L.world:
+                self._peers[r] = sp.ipc_open(handles[r])
+        self._mapped_for = x_local.data_ptr()
+
+    def unmap_neighbours(self):
+        for ptr in self._peers.values():
+            self.sp.ipc_close(ptr)
+        self._peers = {}
+
+    def _sources(self):
+        L = self.L
+        z = [SlabLayout(L.nx, L.ny, L.nz_global, r, L.world) for r in (L.rank - 1, L.rank + 1)]
+        lo = self._peers[L.rank - 1] + 8 * z[0].n_local if L.has_lower else None     # its last owned plane (skip its lower ghost)
+        hi = self._peers[L.rank + 1] + 8 * L.plane if L.has_upper else None           # its first owned plane
+        return lo, hi
+
+    def _step_nccl(self, x_local, y_local):
+        L, t = self.L, self.torch
+        if self.schedule == "serial":
+            for r in self.dist.batch_isend_irecv(self._exchange_ops(x_local)):
+                r.wait()
+            self.slab.spmv(x_local, y_local, None, None, self.mode, stream=t.cuda.current_stream())
+            return
+        cur = t.cuda.current_stream()
+        self.comm_stream.wait_stream(cur)
+        with t.cuda.stream(self.comm_stream):
+            reqs = self.dist.batch_isend_irecv(self._exchange_ops(x_local))
+        self.slab.interior(x_local, y_local, stream=cur)
+        with t.cuda.stream(self.comm_stream):
+            for r in reqs:
+                r.wait()
+        cur.wait_stream(self.comm_stream)
+        self.slab.boundary(x_local, y_local, stream=cur)
+
+    def capture(self, x_local, y_local):
+        """Record one step of the "nccl" exchange + launches into a CUDA graph (NCCL operations are capturable); call
+        after at least one eager step (communicators and kernel attributes exist).  False when capture is not possible."""
+        t = self.torch
+        if self.exchange_kind != "nccl" or self.L.world == 1:
+            return False
+        try:
+            g = t.cuda.CUDAGraph()
+            with t.cuda.graph(g, stream=self.main_stream, capture_error_mode="thread_local"):
+                self._step_nccl(x_local, y_local)
+            self._graph, self._graph_key = g, (x_local.data_ptr(), y_local.data_ptr())
+            return True
+        except Exception:  # noqa: BLE001 -- any failure leaves the eager path
+            self._graph = None
+            return False
+
+    def spmv(self, x_local, y_local):
+        L, t = self.L, self.torch
+        if self.dist is None or L.world == 1:
+            self.slab.spmv(x_local, y_local, None, None, self.sp.SLAB_SERIAL, stream=self.main_stream)
+            return
+        if self.exchange_kind == "p2p":
+            if not self._peers or self._mapped_for != x_local.data_ptr():
+                self.map_neighbours(x_local)
+            lo, hi = self._sources()
+            self.slab.spmv(x_local, y_local, lo, hi, self.mode, stream=self.main_stream)
+            return
+        if self._graph is not None and self._graph_key == (x_local.data_ptr(), y_local.data_ptr()):
+            with t.cuda.stream(self.main_stream):
+                self._graph.replay()
+            return
+        with t.cuda.stream(self.main_stream):
+            self._step_nccl(x_local, y_local)
+
+
 class SlabCg:
     """Unpreconditioned CG (solver.hpp:40-46) over z-slabs: the SpMV is SlabSpmv (halo of the search
     direction exchanged every iteration, overlapped with the interior rows), the three dots of an iteration are local
@@ -174,11 +273,13 @@ class SlabCg:
     def _sum(self, v):
         if self.dist is None or self.L.world == 1:
             return v
-        t = self.torch.tensor([v], dtype=self.torch.float64)
+        # the scalar lives where the vectors live: NCCL reduces CUDA tensors only, gloo (the CPU tests) host tensors
+        t = self.torch.tensor([v], dtype=self.torch.float64, device=self._device)
         self.dist.all_reduce(t)  # SUM; the same value on every rank
         return float(t[0])
 
     def solve(self, b_local, x_local, p_ghosted, r_local, ap_local, max_iterations=500, tolerance=1e-8):
+        self._device = getattr(p_ghosted, "device", None)
         """b, x, r, ap: owned rows (n_local); p_ghosted: x_len entries with ghost planes.  Returns
         (iterations, converged, residual_history).  Raises ArithmeticError on a non-finite value (DivergenceError)."""
         if max_iterations < 1 or not tolerance > 0.0:

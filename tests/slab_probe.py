@@ -1,51 +1,51 @@
-"""Exploratory: the three kernel calls a middle rank makes per SpMV (interior, lower plane, upper plane) on one GPU."""
+"""Exploratory: what the z-slab decomposition costs on ONE device (spmvb_multi_*, logical slabs, same-device ghost copies).
+G slabs of nx x ny x nzl each run back to back; time per slab = total / G, against the undivided slab."""
 import sys
-import torch
 sys.path.insert(0, ".")
 import paper_1612_00530_b200 as sp
-nx = ny = 256; nzl = 256; world = 4; rank = 1
-L = sp.SlabLayout(nx, ny, nzl * world, rank, world)
-n, plane = L.n_local, L.plane
-pc = sp.build_slab_pattern(sp, L, None, keep_csr=False)
-x = torch.empty(L.x_len, dtype=torch.float64, device="cuda"); y = torch.empty(n, dtype=torch.float64, device="cuda")
-sp.check(sp.lib.spmvb_vec_fill(x.data_ptr(), L.x_len, sp.RANDOM, 7, -1.0, 1.0, L.x_col0, None))
-def k(b, e):
-    sp.spmv_rows(pc, x, y, b, e, x_col0=L.x_col0, x_len=L.x_len)
-def t(fn, reps=50):
-    for _ in range(3): fn()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(reps): fn()
-    e1.record(); torch.cuda.synchronize()
-    return e0.elapsed_time(e1) / reps * 1e3
-print("x_col0", L.x_col0, "x_len", L.x_len, "n", n)
-print(f"whole slab           {t(lambda: k(0, n)):8.1f} us  family {sp.get_option('last_pattern_kernel')}")
-print(f"interior planes      {t(lambda: k(plane, n - plane)):8.1f} us  family {sp.get_option('last_pattern_kernel')}")
-print(f"lower boundary plane {t(lambda: k(0, plane)):8.1f} us  family {sp.get_option('last_pattern_kernel')}")
-print(f"upper boundary plane {t(lambda: k(n - plane, n)):8.1f} us  family {sp.get_option('last_pattern_kernel')}")
-for bl in (16, 8, 4, 2):
-    sp.set_option("box_lines", bl)
-    print(f"lower boundary plane, marches of {bl:2d} lines {t(lambda: k(0, plane)):8.1f} us")
-sp.set_option("box_lines", 0)
-print(f"all three            {t(lambda: (k(plane, n - plane), k(0, plane), k(n - plane, n))):8.1f} us")
 
-# the streamed driver (no exchange: single process), as bench.py uses it for N > 1
-main, comm = torch.cuda.Stream(), torch.cuda.Stream()
-class _NoComm:
-    P2POp = staticmethod(lambda op, t, peer: None)
-    isend = irecv = None
-    @staticmethod
-    def batch_isend_irecv(ops):
-        return []
-def ks(xl, yl, b, e, stream=None):
-    sp.spmv_rows(pc, xl, yl, b, e, x_col0=L.x_col0, x_len=L.x_len, stream=main if stream is None else stream)
-for two in (False, True):
-    slab = sp.SlabSpmv(L, ks, _NoComm(), comm, main, torch, two_stream_boundaries=two)
-    main.wait_stream(torch.cuda.current_stream())
-    for _ in range(3): slab.spmv(x, y)
-    main.synchronize()
+nx = ny = int(sys.argv[1]) if len(sys.argv) > 1 else 256
+nzl = int(sys.argv[2]) if len(sys.argv) > 2 else 256
+reps = 100
+print(f"grid {nx}x{ny}, {nzl} planes per slab")
+for G in (1, 2, 4):
+    ms = sp.MultiSlab(sp.GridSpec(nx, ny, nzl * G), [0] * G)
+    ms.fill_x(sp.RANDOM, 7, -1.0, 1.0)
+    for mode, name in ((sp.SLAB_SERIAL, "serial (copies, one launch)"), (sp.SLAB_OVERLAP, "overlap (copies || interior, 2 planes)")):
+        for graph in (1, 0):
+            sp.set_option("slab_graph", graph)
+            wall, dev = ms.bench(reps, mode)
+            print(f"G={G} {name:40s} graph={graph}: device {dev / reps / G * 1e6:7.1f} us per slab-SpMV, host wall {wall / reps / G * 1e6:7.1f} us")
+    sp.set_option("slab_graph", 1)
+    del ms
+
+# One slab alone, as a GPU of a multi-GPU run sees it: the middle slab of three, ghost copies from its neighbours' planes
+# (same-device copies here, peer copies over NVLink there), everything on one stream.
+import ctypes as C
+ms = sp.MultiSlab(sp.GridSpec(nx, ny, nzl * 3), [0] * 3)
+ms.fill_x(sp.RANDOM, 7, -1.0, 1.0)
+parts = [ms.part(g) for g in range(3)]
+_, z0, z1, a, xg, yg = parts[1]
+plane = nx * ny
+n = (z1 - z0) * plane
+lo_src = parts[0][4].ptr + 8 * (parts[0][2] - parts[0][1]) * plane   # the lower neighbour's last owned plane
+hi_src = parts[2][4].ptr + 8 * plane                                # the upper neighbour's first owned plane
+slab = sp.Slab(a, plane, True, True)
+import torch
+st = torch.cuda.Stream()
+def timed(fn, reps=200):
+    for _ in range(5): fn()
+    st.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(main)
-    for _ in range(50): slab.spmv(x, y)
-    e1.record(main); main.synchronize()
-    print(f"SlabSpmv middle rank, boundaries on {'two streams' if two else 'one stream'}: {e0.elapsed_time(e1)/50*1e3:8.1f} us per SpMV (no exchange)")
+    e0.record(st)
+    for _ in range(reps): fn()
+    e1.record(st); st.synchronize()
+    return e0.elapsed_time(e1) / reps * 1e3
+t_whole = timed(lambda: sp.spmv_rows(a, xg, yg, 0, n, x_col0=(z0 - 1) * plane, x_len=n + 2 * plane, stream=st))
+print(f"middle slab, all rows in one launch, no exchange:        {t_whole:7.1f} us")
+for mode, name in ((sp.SLAB_SERIAL, "serial"), (sp.SLAB_OVERLAP, "overlap")):
+    for graph in (1, 0):
+        sp.set_option("slab_graph", graph)
+        t = timed(lambda: slab.spmv(xg, yg, lo_src, hi_src, mode, stream=st))
+        print(f"middle slab, spmvb_slab_spmv {name:8s} graph={graph} (2 ghost copies + launches): {t:7.1f} us  (+{t - t_whole:.1f})")
+sp.set_option("slab_graph", 1)
