@@ -279,10 +279,10 @@ def time_graph(torch, stream, fn, reps):
     with torch.cuda.graph(g, stream=stream):
         for _ in range(reps):
             fn()
-    g.replay()
-    stream.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with torch.cuda.stream(stream):
+    with torch.cuda.stream(stream):  # replay() launches on the current stream: both replays on `stream`, never side by side
+        g.replay()
+        stream.synchronize()
         e0.record(stream)
         g.replay()
         e1.record(stream)

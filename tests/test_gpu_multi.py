@@ -77,7 +77,13 @@ def test_slab_graph_replay_and_direct_launches_agree(sp, orc):
     z0, z1 = 8, 16
     csr = sp.generate_matrix(sp.GridSpec(nx, ny, nz), row_begin=z0 * plane, row_end=z1 * plane)
     a = sp.compress_patterns(csr, True)
-    assert np.array_equal(a.download("row_pattern"), whole.row_pattern[z0 * plane:z1 * plane])  # interior slab: same ids without a merge
+    # an interior slab numbers its 9 shapes by its own first occurrences: the same shapes row by row, other numbers (no merge here)
+    def shapes_of(off, flat):
+        return [tuple(flat[off[q]:off[q + 1]].tolist()) for q in range(len(off) - 1)]
+    mine = shapes_of(a.download("disp_offsets"), a.download("disp_flat"))
+    theirs = shapes_of(whole.disp_offsets, whole.disp_flat)
+    to_whole = np.array([theirs.index(s) for s in mine], dtype=np.int32)
+    assert np.array_equal(to_whole[a.download("row_pattern")], whole.row_pattern[z0 * plane:z1 * plane])
     slab = sp.Slab(a, plane, True, True)
     xfull = sp.DeviceVector.from_host(x)
     n = (z1 - z0) * plane
