@@ -120,6 +120,9 @@ int spmvb_set_device(int device);
  *                     (chunk per warp, ids by loads, round-robin tiles per CTA / per warp, 4 planes per thread);
  *                     lab build only: further variants and ablations (csrc/spmv_pattern*.cu list them with their times)
  *   "box_lines":      lines per CTA tile / chunk length of the tensor ring (0 = default)
+ *   "ring_leftover":  tensor ring, the one column past the last 64-column strip when 64 divides the line length: 0 (default)
+ *                     the last strip's warp sums it from its own shared-memory ring, 1 row by row from global memory after
+ *                     the marches (the round-1 scheme; 256^3: 72.5 vs 69.7 us)
  *   "host_chunks":    row chunks of the pipelined spmvb_spmv_host (0 = default 8)
  *   "slab_graph":     1 (default) spmvb_slab_spmv replays its copies and launches as a CUDA graph; 0 launches directly
  *   "symgs_graph":    1 (default) the launches of a symgs sweep are recorded into a CUDA graph and replayed; 0 launches directly

@@ -251,6 +251,7 @@ static int *option_slot(const char *key) {
     if (!strcmp(key, "box_prefetch_l1")) return &o.box_prefetch_l1;
     if (!strcmp(key, "debug_nochain")) return &o.debug_nochain;
     if (!strcmp(key, "box_lines")) return &o.box_lines;
+    if (!strcmp(key, "ring_leftover")) return &o.ring_leftover;
     if (!strcmp(key, "host_chunks")) return &o.host_chunks;
     if (!strcmp(key, "cg_keep_workspace")) return &o.cg_keep_workspace;
     if (!strcmp(key, "cg_fused_dot")) return &o.cg_fused_dot;

@@ -182,7 +182,8 @@ __device__ __forceinline__ double ring_leftover_row(const PatternArgs &p, uint32
 template <int Q, int S, int MINB, bool OFF_NEG1, int CENTER_POS, bool IDT, int PFD = 0, int DBG = 0, bool CTAC = false, bool DOT = false>
 __global__ void __launch_bounds__(kRingWarps * 32, MINB)
     spmv_pattern_ringp_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm_ids, PatternArgs p, int c_lo,
-                              int c_hi, int np_x, int n_strips, int left_lo, int id_plane0, int total_steps, int steps_per_warp, int tile_lines, int rot) {
+                              int c_hi, int np_x, int n_strips, int left_lo, int left_in_ring, int id_plane0, int total_steps, int steps_per_warp,
+                              int tile_lines, int rot) {
     using L = RingLayout<Q, S, IDT>;
     constexpr int P = L::P;
     const int cpos = CENTER_POS >= 0 ? CENTER_POS : p.center_pos;  // CENTER_POS = -1: the general variant reads it at run time
@@ -281,6 +282,15 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
                 expect[q][i] = (c >= np_x || !ok[q][i]) ? 0u : (kFullBox & ~(oob_a | oob_c));
             }
         }
+        // The left-over column sy-1 (64 | sy) rides with the last strip: its operands -- columns sy-2, sy-1 of the three lines,
+        // box elements 64 and 65; column sy is outside the view -- are in this warp's ring already, and so is its id (element
+        // 67 of the id box).  Lane q < Q sums the row of plane c0+q after the strip's own rows, one short chain per step.
+        const bool do_left = IDT && DBG == 0 && left_in_ring && strip == n_strips - 1;
+        const int ql = min(lane, Q - 1);
+        const int rowl0 = (int)((int64_t)(sy - 1) + (int64_t)sy * b0 + (int64_t)sz * (c0 + ql) - p.g0);
+        const bool okl = do_left && lane < Q && c0 + ql <= c_hi;
+        const uint32_t expect_l = (!okl || c0 + ql >= np_x) ? 0u
+                                  : (kFullBox & ~(kRBits | (c0 + ql == 0 ? kDzLoBits : 0u) | (c0 + ql == np_x - 1 ? kDzHiBits : 0u)));
         // -1: no such row here (computed on whatever the ring holds, never stored)
         auto load_id = [&](int q, int i, int j) {
             const int r = row0 + q * sz + j * sy + i;
@@ -426,11 +436,42 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
                         }
                 }
             }
+            double accl = 0.0, xcl = 0.0;
+            int idl = -1;
+            if (do_left) {  // warp-uniform
+                const int rl = rowl0 + j * sy;
+                const int v = (int)lds_u32(sl[1] - lane_off + L::kXBytes + ql * L::kIdLineBytes + 67 * 4);
+                idl = (okl && (unsigned)(rl - rb) < n_range) ? v : -1;
+                const uint32_t lb = sl[0] - lane_off + ql * L::kLineBytes + 64 * 8, lc = sl[1] - lane_off + ql * L::kLineBytes + 64 * 8,
+                               lt = sl[2] - lane_off + ql * L::kLineBytes + 64 * 8;
+                xcl = lds_f64(lc + L::kLineBytes + 8);
+                if (cpos == 0) accl = __dadd_rn(accl, __dmul_rn(vc, xcl));
+#pragma unroll
+                for (int dz = 0; dz < 3; dz++)
+#pragma unroll
+                    for (int dy = 0; dy < 3; dy++) {
+                        const double2 u = lds_f64x2((dy == 0 ? lb : dy == 1 ? lc : lt) + dz * L::kLineBytes);
+                        accl = OFF_NEG1 ? __dsub_rn(accl, u.x) : __dadd_rn(accl, __dmul_rn(vo, u.x));
+                        if (dz == 1 && dy == 1) {
+                            if (cpos == 2) accl = __dadd_rn(accl, __dmul_rn(vc, u.y));
+                        } else {
+                            accl = OFF_NEG1 ? __dsub_rn(accl, u.y) : __dadd_rn(accl, __dmul_rn(vo, u.y));
+                        }
+                    }
+                if (cpos == 1) accl = __dadd_rn(accl, __dmul_rn(vc, xcl));
+                // any other row shape (or entries outside the view): List 1 as written
+                if (idl >= 0 && lds_u32(s_masks + 4 + 4 * idl) != (expect_l & in_b))
+                    accl = pattern_row_cold(p, idl, (int64_t)rl + p.g0);
+            }
             __syncwarp();  // every lane is done with the slot of line b-1
             if (lane == 0 && j + S < n_sets) {
                 fence_proxy_async();  // generic-proxy reads before the async-proxy refill
                 issue(j + S);
                 if (PFD > 0 && PFD < 9 && j + S + PFD < n_sets) prefetch(j + S + PFD);
+            }
+            if (idl >= 0) {
+                y[rowl0 + j * sy] = accl;
+                if (DOT) dsum = __dadd_rn(dsum, __dmul_rn(accl, xcl));
             }
             // (16-byte stores of the aligned pairs (a+1, a+2) through a lane shuffle were measured slower: 81 vs 78 us)
 #pragma unroll
@@ -560,7 +601,10 @@ static int launch_ringp_t(const spmvb_matrix *a, PatternArgs &p_in, int chunk, c
     }
     int n_strips = (p.sy + 1) / kStripCols;
     if (p.sy - (n_strips * kStripCols - 1) > 2) n_strips++;
-    const int left_lo = std::min(p.sy, n_strips * kStripCols - 1);
+    int left_lo = std::min(p.sy, n_strips * kStripCols - 1);
+    // one left-over column (64 | sy) and ids through the ring: the last strip's warp sums it from its own ring
+    const int left_in_ring = (IDT && DBG == 0 && p.sy - left_lo == 1 && options().ring_leftover != 1) ? 1 : 0;
+    if (left_in_ring) left_lo = p.sy;
     const int n_cols = CTAC ? (n_strips + kRingWarps - 1) / kRingWarps : n_strips;
     const int units = CTAC ? 1 : kRingWarps;  // chunks per CTA
     const int64_t total64 = (int64_t)n_cols * ((c_hi - c_lo + Q) / Q) * p.plane_lines;
@@ -602,7 +646,7 @@ static int launch_ringp_t(const spmvb_matrix *a, PatternArgs &p_in, int chunk, c
             fused_dot_request()->count = grid * kRingWarps;                                                                      \
         }                                                                                                                        \
         spmv_pattern_ringp_kernel<Q, S, MINB, NEG, CP, IDT, PFD, DBG, CTAC, DOT><<<grid, kRingWarps * 32, L::kTotal, st>>>(                          \
-            tm, tm_ids, p, c_lo, c_hi, np_x, n_strips, left_lo, id_plane0, total, spw, tile_lines, rot);                                          \
+            tm, tm_ids, p, c_lo, c_hi, np_x, n_strips, left_lo, left_in_ring, id_plane0, total, spw, tile_lines, rot);                                          \
     } while (0)
     // two instantiations: the HPCG value pattern (off-diagonals -1, centre last) fully specialised, and a general one
     // (any off-diagonal value -- a product by -1.0 is exact, so it serves that case too -- centre position read at run time)
