@@ -120,6 +120,9 @@ int spmvb_set_device(int device);
  *                     (chunk per warp, ids by loads, round-robin tiles per CTA / per warp, 4 planes per thread);
  *                     lab build only: further variants and ablations (csrc/spmv_pattern*.cu list them with their times)
  *   "box_lines":      lines per CTA tile / chunk length of the tensor ring (0 = default)
+ *   "ring_pdl":       1 (default) the tensor-ring kernel is launched with programmatic stream serialization: its CTAs take the
+ *                     places of the previous kernel's CTAs as those exit and wait (griddepcontrol.wait) for that kernel to
+ *                     complete before touching global memory; 0 plain stream order
  *   "ring_leftover":  tensor ring, the one column past the last 64-column strip when 64 divides the line length: 0 (default)
  *                     the last strip's warp sums it from its own shared-memory ring, 1 row by row from global memory after
  *                     the marches (the round-1 scheme; 256^3: 72.5 vs 69.7 us)

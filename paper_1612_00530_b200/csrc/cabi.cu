@@ -252,6 +252,7 @@ static int *option_slot(const char *key) {
     if (!strcmp(key, "debug_nochain")) return &o.debug_nochain;
     if (!strcmp(key, "box_lines")) return &o.box_lines;
     if (!strcmp(key, "ring_leftover")) return &o.ring_leftover;
+    if (!strcmp(key, "ring_pdl")) return &o.ring_pdl;
     if (!strcmp(key, "host_chunks")) return &o.host_chunks;
     if (!strcmp(key, "cg_keep_workspace")) return &o.cg_keep_workspace;
     if (!strcmp(key, "cg_fused_dot")) return &o.cg_fused_dot;
@@ -269,7 +270,7 @@ static int *option_slot(const char *key) {
 static bool lab_only_value(const char *key, int value) {
     if (kLabBuild) return false;
     if (!strcmp(key, "box_march")) {
-        for (int ok : {0, 3, 90, 101, 107, 108, 109, 110})
+        for (int ok : {0, 3, 90, 101, 107, 108, 109, 110, 111, 112, 113})
             if (value == ok) return false;
         return true;
     }

@@ -141,6 +141,7 @@ struct Options {
     int box_prefetch_l1 = 0; // L1 prefetch distance in lines (0 = off)
     int debug_nochain = 0;   // measurement only
     int box_lines = 0;       // lines per CTA march of the tensor-ring kernel (0 = default)
+    int ring_pdl = 1;        // tensor ring launched with programmatic stream serialization (its preamble overlaps the previous kernel's tail)
     int ring_leftover = 0;   // tensor ring, left-over column (64 | sy): 0 summed by the last strip's warp from its ring, 1 row by row after the marches
     int slab_graph = 1;         // 1: spmvb_slab_spmv records its exchange copies and launches into a CUDA graph and replays it
     int symgs_graph = 1;        // 1: a symgs sweep's launches are recorded into a CUDA graph and replayed

@@ -58,6 +58,12 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t
                  "l"(src), "r"(bytes), "r"(bar)
                  : "memory");
 }
+// Programmatic dependent launch (PDL).  launch_dependents: the next kernel of the stream, when it was launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization, may start occupying SMs as this grid's CTAs exit (instead of after the
+// whole grid has drained and the launch latency has passed).  grid_dependency_wait: returns once every prerequisite grid has
+// completed and its writes are visible -- nothing that reads or writes global memory may precede it.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_grid_dependency_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 

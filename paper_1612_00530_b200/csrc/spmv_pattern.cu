@@ -91,6 +91,16 @@ static int launch_pattern(const spmvb_matrix *a, const double *x, int64_t x_col0
         const bool use_box = a->box.valid && o.pattern_kernel != 1;
         if (o.pattern_kernel == 2 && !a->box.valid)
             return fail(SPMVB_ERR_INVALID_ARGUMENT, "box kernel requested but the dictionary has no box plan");
+        auto launch_list1 = [&]() -> int {  // List 1 as written: a thread per row, one round of gathers
+            const int threads = 256;
+            const int blocks = (row_end - row_begin + threads - 1) / threads;
+            o.last_pattern_kernel = 1;
+            const bool dict_smem = a->disp_total <= kDictSmemDisp && a->n_patterns <= kDictSmemPat && a->m <= kDictSmemTab;
+            if (dict_smem) spmv_pattern_generic_kernel<true><<<blocks, threads, 0, st>>>(p);
+            else spmv_pattern_generic_kernel<false><<<blocks, threads, 0, st>>>(p);
+            return check_launch("spmv_pattern_generic");
+        };
+        bool done = false;
         if (use_box) {
             int rc3 = 1;  // 1 = not served by v3
             bool ring = false;
@@ -102,7 +112,15 @@ static int launch_pattern(const spmvb_matrix *a, const double *x, int64_t x_col0
                 if (rc3 < 0) return SPMVB_ERR_CUDA;
                 ring = rc3 == 0;
             }
-            if (!ring && o.pattern_kernel != 3 && box3_ok(a, p)) {
+            // Short ranges the ring does not serve (lines narrower than a box, fewer than 8 planes -- a slab's boundary plane, a
+            // 32^3 or 64^3 grid): the sliding-window kernels march a handful of long serial chains (15.7 us per SpMV at 32^3 and
+            // 64^3 alike, graph-replayed); List 1 with a thread per row is one round of gathers: 4.0 / 6.7 us.  Above ~1 M rows the
+            // windows win (7 vs 15.7 ns per 1000 rows).
+            if (!ring && o.pattern_kernel == 0 && o.box_march == 0 && (int64_t)row_end - row_begin < (1 << 20)) {
+                SPMVB_TRY(launch_list1());
+                done = true;
+            }
+            if (!done && !ring && o.pattern_kernel != 3 && box3_ok(a, p)) {
                 const int64_t n_planes = ((int64_t)row_end - row_begin + (int64_t)p.sy * p.plane_lines - 1) / ((int64_t)p.sy * p.plane_lines);
                 if (n_planes == 1) {  // single-plane ranges (slab boundary planes): short marches, so that the plane fills the GPU
 #ifdef SPMVB_LAB
@@ -131,8 +149,8 @@ static int launch_pattern(const spmvb_matrix *a, const double *x, int64_t x_col0
                 }
                 if (rc3 < 0) return SPMVB_ERR_CUDA;
             }
-            o.last_pattern_kernel = rc3 == 1 ? 2 : (ring ? 9 : (o.box_march >= 20 && o.box_march < 70 ? 4 : 3));
-            if (rc3 == 1) {  // v2: any stride / alignment / value pattern
+            if (!done) o.last_pattern_kernel = rc3 == 1 ? 2 : (ring ? 9 : (o.box_march >= 20 && o.box_march < 70 ? 4 : 3));
+            if (!done && rc3 == 1) {  // v2: any stride / alignment / value pattern
 #ifdef SPMVB_LAB
                 if (o.box_march == 11) SPMVB_TRY((launch_box_rw<32, 8, 1, 1>(a, p, st)));
                 else
@@ -140,13 +158,7 @@ static int launch_pattern(const spmvb_matrix *a, const double *x, int64_t x_col0
                 SPMVB_TRY((launch_box_rw<16, 8, 2, 0>(a, p, st)));
             }
         } else {
-            const int threads = 256;
-            const int blocks = (row_end - row_begin + threads - 1) / threads;
-            o.last_pattern_kernel = 1;
-            const bool dict_smem = a->disp_total <= kDictSmemDisp && a->n_patterns <= kDictSmemPat && a->m <= kDictSmemTab;
-            if (dict_smem) spmv_pattern_generic_kernel<true><<<blocks, threads, 0, st>>>(p);
-            else spmv_pattern_generic_kernel<false><<<blocks, threads, 0, st>>>(p);
-            SPMVB_TRY(check_launch("spmv_pattern_generic"));
+            SPMVB_TRY(launch_list1());
         }
     }
     if (a->n_exc > 0 && row_end > row_begin) {

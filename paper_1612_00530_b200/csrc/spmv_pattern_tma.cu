@@ -75,7 +75,8 @@ struct RingLayout {
     static constexpr uint32_t kSlotBytes = kXBytes + (kIdBytes + 127u) / 128u * 128u;
     static constexpr uint32_t kRingBytes = kRingWarps * S * kSlotBytes;
     static constexpr uint32_t kBarBytes = kRingWarps * S * 8;
-    static constexpr uint32_t kTotal = kRingBytes + kBarBytes + (kDictSmemPat + 1) * 4 + 128;  // + alignment slack
+    static constexpr uint32_t kMaskBytes = ((kDictSmemPat + 1) * 4 + 15u) / 16u * 16u;  // one private copy of the mask table per warp
+    static constexpr uint32_t kTotal = kRingBytes + kBarBytes + kRingWarps * kMaskBytes + 128;  // + alignment slack
 };
 
 // Rare path of the direct variant, kept out of line so that its registers do not weigh on the main loop: the sums
@@ -196,14 +197,22 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
     const unsigned n_range = (unsigned)(p.row_end - p.row_begin);
     const uint32_t ring = sbase + warp * (S * L::kSlotBytes);
     const uint32_t bars = sbase + L::kRingBytes + warp * (S * 8);
-    const uint32_t s_masks = sbase + L::kRingBytes + L::kBarBytes;  // entry 0 serves id = -1
-    for (int i = threadIdx.x; i <= p.n_patterns; i += kRingWarps * 32) sts_u32(s_masks + 4 * i, i == 0 ? 0u : p.masks[i - 1]);
+    const uint32_t s_masks = sbase + L::kRingBytes + L::kBarBytes + warp * L::kMaskBytes;  // this warp's copy; entry 0 serves id = -1
+    // PDL: the next launch of the stream may take this CTA's place as soon as it exits; this launch, in turn, may have been
+    // started while the kernel before it was still draining -- no global memory is touched before the wait below.
+    pdl_launch_dependents();
     if (lane == 0) {
 #pragma unroll
         for (int s = 0; s < S; s++) mbar_init(bars + 8 * s, 1);
         fence_mbar_init();
     }
-    __syncthreads();  // the only CTA barrier: the warps are independent from here on
+    if (threadIdx.x == 0) {  // the descriptors live in the kernel parameters: fetched ahead of their first use
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tm) : "memory");
+        if (IDT) asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_ids) : "memory");
+    }
+    __syncwarp();  // this warp's barriers are initialised; no other warp ever touches them
+    pdl_grid_dependency_wait();
+    bool masks_staged = false;  // the mask table is staged behind the first line sets' fetches; no CTA barrier anywhere
 
     const int gw = blockIdx.x * kRingWarps + warp, n_warps = gridDim.x * kRingWarps;
     const int n_sg = (n_strips + kRingWarps - 1) / kRingWarps;  // CTAC: columns are (group of 4 strips, plane group)
@@ -263,6 +272,11 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
             for (int k = 0; k < S && k < n_sets; k++) issue(k);
             if (PFD > 0 && PFD < 9)
                 for (int k = S; k < S + PFD && k < n_sets; k++) prefetch(k);
+        }
+        if (!masks_staged) {
+            for (int i = lane; i <= p.n_patterns; i += 32) sts_u32(s_masks + 4 * i, i == 0 ? 0u : p.masks[i - 1]);
+            __syncwarp();
+            masks_staged = true;
         }
 
         // per-thread geometry: columns a, a+1 (a odd); the row of (column a, line b0 + j, plane c0 + q) is row0 + q*sz + j*sy
@@ -492,6 +506,10 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
        // latency-bound gathers overlap with the marches of the others)
         const int n_left = sy - left_lo;
         const int total_left = n_left * pl * (c_hi - c_lo + 1);
+        if (!masks_staged && n_left > 0) {  // a warp without a march
+            for (int i = lane; i <= p.n_patterns; i += 32) sts_u32(s_masks + 4 * i, i == 0 ? 0u : p.masks[i - 1]);
+            __syncwarp();
+        }
         for (int t = gw * 32 + lane; t < total_left && DBG != 5 && DBG != 6; t += n_warps * 32) {
             const double d = ring_leftover_row<OFF_NEG1, CENTER_POS>(p, s_masks, left_lo + t % n_left, (t / n_left) % pl, c_lo + t / (n_left * pl), np_x);
             if (DOT) dsum = __dadd_rn(dsum, d);
@@ -645,8 +663,19 @@ static int launch_ringp_t(const spmvb_matrix *a, PatternArgs &p_in, int chunk, c
             if (grid * kRingWarps > p.dot_capacity) return 1;                                                                    \
             fused_dot_request()->count = grid * kRingWarps;                                                                      \
         }                                                                                                                        \
-        spmv_pattern_ringp_kernel<Q, S, MINB, NEG, CP, IDT, PFD, DBG, CTAC, DOT><<<grid, kRingWarps * 32, L::kTotal, st>>>(                          \
-            tm, tm_ids, p, c_lo, c_hi, np_x, n_strips, left_lo, left_in_ring, id_plane0, total, spw, tile_lines, rot);                                          \
+        cudaLaunchConfig_t cfg = {};                                                                                             \
+        cfg.gridDim = dim3(grid);                                                                                                \
+        cfg.blockDim = dim3(kRingWarps * 32);                                                                                    \
+        cfg.dynamicSmemBytes = L::kTotal;                                                                                        \
+        cfg.stream = st;                                                                                                         \
+        cudaLaunchAttribute pdl[1];                                                                                              \
+        pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;                                                          \
+        pdl[0].val.programmaticStreamSerializationAllowed = 1;                                                                   \
+        cfg.attrs = pdl;                                                                                                         \
+        cfg.numAttrs = (options().ring_pdl && grid == n_sm * per_sm) ? 1 : 0; /* only a full wave: early CTAs of a partial grid crowd the SMs that free up first (128^3: 14.2 -> 17.9 us) */                                                                               \
+        if (cudaLaunchKernelEx(&cfg, spmv_pattern_ringp_kernel<Q, S, MINB, NEG, CP, IDT, PFD, DBG, CTAC, DOT>, tm, tm_ids, p, c_lo, c_hi, np_x,     \
+                               n_strips, left_lo, left_in_ring, id_plane0, total, spw, tile_lines, rot) != cudaSuccess)          \
+            return check_launch("spmv_pattern_ringp") == SPMVB_OK ? -1 : -1;                                                     \
     } while (0)
     // two instantiations: the HPCG value pattern (off-diagonals -1, centre last) fully specialised, and a general one
     // (any off-diagonal value -- a product by -1.0 is exact, so it serves that case too -- centre position read at run time)
@@ -732,6 +761,10 @@ int launch_pattern_ring(int which, int lines, const spmvb_matrix *a, PatternArgs
             rc = launch_ringp_t<4, 4, 3, true, 0, 0, true>(a, p, lines, st);
             return rc == 1 ? launch_ringp_t<4, 5, 3, false, 0, 0, true>(a, p, lines, st) : rc;
         // (3 / 5 / 7 / 8 planes per thread, chunk per CTA: 80.6 / 76.2 / 74.0 / 84.1 us at 256^3, r01_probe_planes_per_thread.log)
+        // small (L2-resident) grids: fewer rows per step and a deeper ring, a chunk per warp
+        case 21: rc = launch_ringp_t<2, 8, 2, true>(a, p, lines, st); return rc == 1 ? launch_ringp_t<4, 5, 3, false>(a, p, lines, st) : rc;
+        case 22: rc = launch_ringp_t<4, 6, 2, true>(a, p, lines, st); return rc == 1 ? launch_ringp_t<4, 5, 3, false>(a, p, lines, st) : rc;
+        case 23: rc = launch_ringp_t<2, 6, 3, true>(a, p, lines, st); return rc == 1 ? launch_ringp_t<4, 5, 3, false>(a, p, lines, st) : rc;
         case 19:  // ... a tile per warp
             rc = launch_ringp_t<4, 4, 3, true>(a, p, 0, st, tl);
             return rc == 1 ? launch_ringp_t<4, 5, 3, false>(a, p, 0, st, tl) : rc;

@@ -48,8 +48,27 @@ with torch.cuda.stream(st):
             st.synchronize()
             best = min(best, e0.elapsed_time(e1) / reps * 1e3)
         bad = int((y.view(torch.int64) != y2.view(torch.int64)).sum())
+        # the same launches replayed from a CUDA graph: host launch cost leaves the measurement (small grids)
+        gtime = float("nan")
+        try:
+            g_ = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g_, stream=st):
+                for _ in range(50):
+                    sp.spmv_rows(pc, x, y, 0, n, stream=st)
+            g_.replay()
+            st.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            for _ in range(4):
+                g_.replay()
+            e1.record(st)
+            st.synchronize()
+            gtime = e0.elapsed_time(e1) / 200 * 1e3
+            del g_
+        except Exception as ex:  # noqa: BLE001
+            print("graph capture failed:", ex)
         for k in opts:
             sp.set_option(k, 0)
-        print(f"grid {g}: {best:8.2f} us  {20.0 * n / best / 1e3:7.1f} GB/s ({20.0 * n / best / 1e3 / 6544:.3f} of 6544)  "
+        print(f"grid {g}: {best:8.2f} us (graph replay {gtime:7.2f} us)  {20.0 * n / best / 1e3:7.1f} GB/s ({20.0 * n / best / 1e3 / 6544:.3f} of 6544)  "
               f"{2 * nnz / best / 1e3:8.1f} GF/s  family {fam}  rows differing from List 1: {bad}  opts {opts}", flush=True)
         del pc, x, y, y2

@@ -148,8 +148,16 @@ def test_ring_is_the_default_for_large_ranges(sp, orc):
     assert sp.get_option("last_pattern_kernel") == 9
     assert np.array_equal(bits(y), bits(orc.spmv(pc, x)))
     dx, dy = sp.DeviceVector.from_host(x), sp.DeviceVector.from_host(np.zeros(m.n))
-    sp.spmv_rows(d, dx, dy, 0, 3 * 128 * 12)  # a few planes: sliding-window kernel
-    assert sp.get_option("last_pattern_kernel") == 3
+    sp.spmv_rows(d, dx, dy, 0, 3 * 128 * 12)  # a few planes, few rows: List 1 with a thread per row (one round of gathers)
+    assert sp.get_option("last_pattern_kernel") == 1
+    assert np.array_equal(bits(dy.to_host()[:3 * 128 * 12]), bits(orc.spmv(pc, x)[:3 * 128 * 12]))
+    sp.set_option("box_march", 3)  # the sliding-window kernel, forced
+    try:
+        sp.spmv_rows(d, dx, dy, 0, 3 * 128 * 12)
+        assert sp.get_option("last_pattern_kernel") == 3
+    finally:
+        sp.set_option("box_march", 0)
+    assert np.array_equal(bits(dy.to_host()[:3 * 128 * 12]), bits(orc.spmv(pc, x)[:3 * 128 * 12]))
 
 
 @pytest.mark.parametrize("march", [0, 101, 109])
