@@ -120,6 +120,12 @@ int spmvb_set_device(int device);
  *                     (chunk per warp, ids by loads, round-robin tiles per CTA / per warp, 4 planes per thread);
  *                     lab build only: further variants and ablations (csrc/spmv_pattern*.cu list them with their times)
  *   "box_lines":      lines per CTA tile / chunk length of the tensor ring (0 = default)
+ *   "exception_kernel": hybrid handles, the exception-row block: 0 / 1 (default) the ELL kernel with a row map, all gathers of a
+ *                     row requested in one batch; 64 / 32: the rows' operands come from three shared-memory windows of x per
+ *                     64- / 32-row tile (csrc/spmv_exception.cu; measured slower on BASELINE config 4: 43 vs 34 us)
+ *   "exception_overlap": hybrid handles: 1 (default) the exception block runs on a second stream beside the kernel of the dictionary
+ *                     rows (the two write disjoint rows of y; forked and joined by events, so the call still completes in
+ *                     stream order); 0 one after the other
  *   "ring_pdl":       1 (default) the tensor-ring kernel is launched with programmatic stream serialization: its CTAs take the
  *                     places of the previous kernel's CTAs as those exit and wait (griddepcontrol.wait) for that kernel to
  *                     complete before touching global memory; 0 plain stream order

@@ -61,6 +61,8 @@ void destroy(spmvb_matrix *a) {
     if (a->symgs_graph.capture_stream) cudaStreamDestroy(a->symgs_graph.capture_stream);
     for (auto &st : a->pipe_streams) if (st) cudaStreamDestroy(st);
     for (auto &ev : a->pipe_events) if (ev) cudaEventDestroy(ev);
+    if (a->exc_stream) cudaStreamDestroy(a->exc_stream);
+    for (auto &ev : a->exc_events) if (ev) cudaEventDestroy(ev);
     if (a->d_masks) cudaFree(a->d_masks);
     if (a->d_disp_off32) cudaFree(a->d_disp_off32);
     delete a;
@@ -253,6 +255,8 @@ static int *option_slot(const char *key) {
     if (!strcmp(key, "box_lines")) return &o.box_lines;
     if (!strcmp(key, "ring_leftover")) return &o.ring_leftover;
     if (!strcmp(key, "ring_pdl")) return &o.ring_pdl;
+    if (!strcmp(key, "exception_kernel")) return &o.exception_kernel;
+    if (!strcmp(key, "exception_overlap")) return &o.exception_overlap;
     if (!strcmp(key, "host_chunks")) return &o.host_chunks;
     if (!strcmp(key, "cg_keep_workspace")) return &o.cg_keep_workspace;
     if (!strcmp(key, "cg_fused_dot")) return &o.cg_fused_dot;

@@ -119,6 +119,8 @@ struct spmvb_matrix {
     // streams / events of the pipelined host-buffer SpMV (created on first use)
     mutable cudaStream_t pipe_streams[3] = {};
     mutable cudaEvent_t pipe_events[128] = {};
+    mutable cudaStream_t exc_stream = nullptr;  // hybrid handles: the exception block runs beside the dictionary rows (spmv_pattern.cu)
+    mutable cudaEvent_t exc_events[2] = {};
     spmvb::BoxPlan box;
     uint32_t *d_masks = nullptr;      // device copy of box.masks
     int32_t *d_disp_off32 = nullptr;  // 32-bit copy of disp_offsets for the kernels
@@ -141,6 +143,8 @@ struct Options {
     int box_prefetch_l1 = 0; // L1 prefetch distance in lines (0 = off)
     int debug_nochain = 0;   // measurement only
     int box_lines = 0;       // lines per CTA march of the tensor-ring kernel (0 = default)
+    int exception_overlap = 1; // hybrid format: 1 the exception block on a second stream beside the dictionary rows (fork / join by events), 0 one after the other
+    int exception_kernel = 0; // hybrid format, exception rows: 0 / 1 the ELL kernel with a row map (all gathers of a row in one batch), 64 / 32 shared-memory windows of x with that tile height
     int ring_pdl = 1;        // tensor ring launched with programmatic stream serialization (its preamble overlaps the previous kernel's tail)
     int ring_leftover = 0;   // tensor ring, left-over column (64 | sy): 0 summed by the last strip's warp from its ring, 1 row by row after the marches
     int slab_graph = 1;         // 1: spmvb_slab_spmv records its exchange copies and launches into a CUDA graph and replays it

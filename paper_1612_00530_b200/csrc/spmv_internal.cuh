@@ -10,6 +10,10 @@ int check_launch(const char *what);
 // ELL rows [row_begin,row_end); row_map != nullptr serves the exception block (rows = exception slots)
 int launch_ell(const double *values, const int32_t *columns, int width, const double *x, int64_t x_col0, double *y,
                int row_begin, int row_end, const int32_t *row_map, cudaStream_t st);
+// exception rows [e_begin,e_end) of a hybrid pattern handle from shared-memory windows of x (spmv_exception.cu):
+// 0 launched, 1 not served (run launch_ell with the row map), < 0 error
+int launch_exception_window(const spmvb_matrix *a, const double *x, int64_t x_col0, int64_t x_len, double *y, int e_begin, int e_end,
+                            cudaStream_t st);
 int launch_vt(const spmvb_matrix *a, const double *x, int64_t x_col0, double *y, int row_begin, int row_end, cudaStream_t st);
 // measured experiments (spmv_pattern_lab.cu): returns 0 launched, 1 not served, -1 CUDA error
 int launch_pattern_lab(int which, const spmvb_matrix *a, PatternArgs &p, cudaStream_t st);

@@ -59,6 +59,23 @@ FusedDot *&fused_dot_request() {
 
 static int launch_pattern(const spmvb_matrix *a, const double *x, int64_t x_col0, int64_t x_len, double *y,
                           int row_begin, int row_end, cudaStream_t st) {
+    // Hybrid handles: the exception block (below) shares nothing with the dictionary rows but x, and writes other rows of y;
+    // it runs on the handle's second stream, forked here and joined at the end, so that the two kernels share the GPU.
+    int e0 = 0, e1 = 0;
+    if (a->n_exc > 0 && row_end > row_begin) {
+        const auto &er = a->h_exc_rows;  // exception slots whose rows fall in [row_begin,row_end)
+        e0 = (int)(std::lower_bound(er.begin(), er.end(), row_begin) - er.begin());
+        e1 = (int)(std::lower_bound(er.begin(), er.end(), row_end) - er.begin());
+    }
+    const bool forked = e1 > e0 && options().exception_overlap != 0;
+    if (forked) {
+        if (!a->exc_stream) {
+            SPMVB_CUDA(cudaStreamCreateWithFlags(&a->exc_stream, cudaStreamNonBlocking));
+            for (auto &ev : a->exc_events) SPMVB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        }
+        SPMVB_CUDA(cudaEventRecord(a->exc_events[0], st));
+        SPMVB_CUDA(cudaStreamWaitEvent(a->exc_stream, a->exc_events[0], 0));
+    }
     if (row_end > row_begin) {
         PatternArgs p;
         p.ids = static_cast<const int32_t *>(a->s[SPMVB_S_ROW_PATTERN]);
@@ -161,14 +178,18 @@ static int launch_pattern(const spmvb_matrix *a, const double *x, int64_t x_col0
             SPMVB_TRY(launch_list1());
         }
     }
-    if (a->n_exc > 0 && row_end > row_begin) {
-        // exception slots whose rows fall in [row_begin,row_end)
-        const auto &er = a->h_exc_rows;
-        const int e0 = (int)(std::lower_bound(er.begin(), er.end(), row_begin) - er.begin());
-        const int e1 = (int)(std::lower_bound(er.begin(), er.end(), row_end) - er.begin());
-        SPMVB_TRY(launch_ell(static_cast<const double *>(a->s[SPMVB_S_EXC_VALUES]),
-                             static_cast<const int32_t *>(a->s[SPMVB_S_EXC_COLUMNS]), a->w_exc, x, x_col0, y, e0, e1,
-                             static_cast<const int32_t *>(a->s[SPMVB_S_EXC_ROWS]), st));
+    if (e1 > e0) {
+        cudaStream_t se = forked ? a->exc_stream : st;
+        const int rcw = launch_exception_window(a, x, x_col0, x_len, y, e0, e1, se);  // spmv_exception.cu
+        if (rcw < 0) return SPMVB_ERR_CUDA;
+        if (rcw == 1)
+            SPMVB_TRY(launch_ell(static_cast<const double *>(a->s[SPMVB_S_EXC_VALUES]),
+                                 static_cast<const int32_t *>(a->s[SPMVB_S_EXC_COLUMNS]), a->w_exc, x, x_col0, y, e0, e1,
+                                 static_cast<const int32_t *>(a->s[SPMVB_S_EXC_ROWS]), se));
+        if (forked) {
+            SPMVB_CUDA(cudaEventRecord(a->exc_events[1], se));
+            SPMVB_CUDA(cudaStreamWaitEvent(st, a->exc_events[1], 0));
+        }
     }
     return SPMVB_OK;
 }

@@ -95,7 +95,10 @@ __global__ void __launch_bounds__(ROWS) spmv_ell_kernel(const double *__restrict
     if (r < row_begin || r >= row_end) return;
     const double *v = sv + threadIdx.x * width;
     const int32_t *c = sc + threadIdx.x * width;
-    y[row_map ? row_map[r] : r] = (BULK && width == 27) ? ell_row<27>(v, c, 27, x, x_col0) : ell_row<9>(v, c, width, x, x_col0);
+    // exception block (row_map): its gathers mostly miss L1 (the rows are scattered), so all of a row's operands are requested at
+    // once -- one L2 round trip per row instead of four
+    if (row_map) y[row_map[r]] = (BULK && width <= 32) ? ell_row<32>(v, c, width, x, x_col0) : ell_row<9>(v, c, width, x, x_col0);
+    else y[r] = (BULK && width == 27) ? ell_row<27>(v, c, 27, x, x_col0) : ell_row<9>(v, c, width, x, x_col0);
 }
 
 // Naive thread-per-row form, kept as the A/B baseline ("ell_kernel" = 1).

@@ -225,6 +225,20 @@ def test_hybrid_exception_rows(sp, orc, g):
         finally:
             sp.set_option("pattern_kernel", 0)
         assert np.array_equal(bits(y), bits(ref))
+    # the exception block from shared-memory windows of x (csrc/spmv_exception.cu), whole and over ragged row ranges
+    dx = sp.DeviceVector.from_host(x)
+    for ek in (64, 32):
+        sp.set_option("exception_kernel", ek)
+        try:
+            assert np.array_equal(bits(run(sp, d, x)), bits(ref))
+            n = m.n
+            for b, e in ((0, n // 3 + 1), (n // 3 + 1, n - 5), (n - 5, n), (7, 8)):
+                dy = sp.DeviceVector.from_host(np.full(n, np.nan))
+                sp.spmv_rows(d, dx, dy, b, e)
+                yh = dy.to_host()
+                assert np.array_equal(bits(yh[b:e]), bits(ref[b:e])) and np.all(np.isnan(yh[:b])) and np.all(np.isnan(yh[e:]))
+        finally:
+            sp.set_option("exception_kernel", 0)
     # the uncompressed ELL of the same matrix agrees to 1e-12 per row
     ell = orc.to_ell(m)
     y_ell = run(sp, up_ell(sp, ell), x)
