@@ -243,4 +243,16 @@ FormatCost measured_cost(const EllMatrix& a);
 FormatCost measured_cost(const VtCompressedMatrix& a);
 FormatCost measured_cost(const PatternCompressedMatrix& a);
 
+// inc/perf_model.hpp:82-95: one row per format -- cost of a row with row_nnz entries and the roofline estimate on `machine`
+struct ModelRow {
+    MatrixFormat format;
+    FormatCost cost;
+    RooflineEstimate estimate;
+};
+std::vector<ModelRow> model_table(const std::vector<MatrixFormat>& formats, int row_nnz, int table_size, const MachineSpec& machine,
+                                  const ModelOptions& opts = {});
+// CSV columns, in order: format, bytes_per_row, bytes_per_flop, predicted_gflops, limiting_resource
+std::string model_table_csv(const std::vector<ModelRow>& rows);
+std::string model_table_json(const std::vector<ModelRow>& rows);
+
 }  // namespace spmvcomp

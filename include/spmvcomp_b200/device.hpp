@@ -83,4 +83,10 @@ private:
 void spmv_rows(const DeviceMatrix& a, const DeviceVector& x, DeviceVector& y, std::int32_t begin, std::int32_t end,
                void* stream = nullptr);
 
+// The machine-spec file `calibrate` writes and `bench --machine` reads (the reference names no layout: one JSON
+// object {"read_bandwidth": bytes/s[, "peak_flops": flops/s]}, numbers with 17 significant digits so that a round trip is exact).
+// IoError for unreadable / unwritable files and for text without a positive read_bandwidth.
+void save_machine_spec(const MachineSpec& machine, const std::string& path);
+MachineSpec load_machine_spec(const std::string& path);
+
 }  // namespace spmvcomp::b200

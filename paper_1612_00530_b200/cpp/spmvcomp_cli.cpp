@@ -1,11 +1,11 @@
 // spmvcomp command-line harness (SPEC.md:425-500 [MODULE] bench_cli) on the device path.
 //   spmvcomp_cli generate  --grid NX NY NZ [--out m.bin] [--mm m.mtx]
 //   spmvcomp_cli bench     (--grid NX NY NZ | --matrix m.bin) --format ell|vt|pattern|pattern-values [--reps R] [--out json|csv]
-//                          [--seed S] [--save format.bin]
+//                          [--seed S] [--save format.bin] [--bandwidth GB/s | --machine spec.json]
 //   spmvcomp_cli solve     (--grid NX NY NZ | --matrix m.bin) [--backend ell|vt|pattern] [--tol T] [--max-iter K]
 //                          [--precond none|symgs|symgs:SWEEPS]
-//   spmvcomp_cli model     --bandwidth GB/s [--formats ell,vt,pattern,pattern-values]
-//   spmvcomp_cli calibrate
+//   spmvcomp_cli model     (--bandwidth GB/s | --machine spec.json) [--formats ell,vt,pattern,pattern-values] [--out csv|json]
+//   spmvcomp_cli calibrate [--out spec.json]     (writes the machine-spec file that --machine reads back: SPEC.md:476-483)
 // Exit codes: 0 success, 1 verification / convergence failure, 2 usage error.
 // Matrix files (layout in include/spmvcomp/io.hpp): `generate --out` writes the serialized
 // StencilMatrix (and `--mm` the Matrix Market export), `bench` / `solve` take it with --matrix; --grid runs the
@@ -25,6 +25,7 @@
 #include "spmvcomp/io.hpp"
 #include "spmvcomp/spmvcomp.hpp"
 #include "spmvcomp_b200.h"
+#include "spmvcomp_b200/device.hpp"
 
 namespace {
 
@@ -43,7 +44,7 @@ struct Args {
     int nx = 0, ny = 0, nz = 0, reps = 100, max_iter = 500;
     bool have_grid = false;
     std::string format = "pattern-values", backend = "pattern", out = "json", formats = "ell,vt,pattern,pattern-values";
-    std::string matrix, mm, save, precond = "none";
+    std::string matrix, mm, save, precond = "none", machine;
     bool out_given = false;
     double tol = 1e-8, bandwidth = 0.0;
     unsigned long long seed = 7;
@@ -74,6 +75,7 @@ Args parse(int argc, char **argv) {
         } else if (k == "--max-iter") { need(1); a.max_iter = std::atoi(argv[++i]);
         } else if (k == "--bandwidth") { need(1); a.bandwidth = std::atof(argv[++i]);
         } else if (k == "--formats") { need(1); a.formats = argv[++i];
+        } else if (k == "--machine") { need(1); a.machine = argv[++i];
         } else throw Usage{"unknown option " + k};
     }
     return a;
@@ -251,7 +253,8 @@ int cmd_bench(const Args &a) {
         }
     }
     // roofline prediction for the configured MachineSpec (perf_model.hpp:59-72): --bandwidth GB/s, else the reference's default 75
-    const double mach_bw = a.bandwidth > 0.0 ? a.bandwidth : 75.0;
+    // (--machine FILE: the spec `calibrate --out FILE` wrote)
+    const double mach_bw = a.bandwidth > 0.0 ? a.bandwidth : !a.machine.empty() ? spmvcomp::b200::load_machine_spec(a.machine).read_bandwidth / 1e9 : 75.0;
     const double roofline_gflops = mach_bw * (2.0 * (double)inf.nnz / (double)n) / bpr;
     const std::string stem = "bench_" + a.format + "_" + std::to_string(g.nx) + "x" + std::to_string(g.ny) + "x" + std::to_string(g.nz);
     if (a.out == "json")
@@ -311,10 +314,11 @@ int cmd_solve(const Args &a) {
 }
 
 int cmd_model(const Args &a) {
-    if (!(a.bandwidth > 0.0)) throw Usage{"--bandwidth GB/s (> 0) is required"};
     spmvcomp::MachineSpec mach;
-    mach.read_bandwidth = a.bandwidth * 1e9;
-    std::printf("%-16s %14s %14s %16s\n", "format", "bytes/row", "bytes/flop", "roofline Gflops");
+    if (a.bandwidth > 0.0) mach.read_bandwidth = a.bandwidth * 1e9;
+    else if (!a.machine.empty()) mach = spmvcomp::b200::load_machine_spec(a.machine);
+    else throw Usage{"--bandwidth GB/s (> 0) or --machine FILE is required"};
+    std::vector<spmvcomp::MatrixFormat> formats;
     size_t pos = 0;
     while (pos <= a.formats.size()) {
         const size_t c = a.formats.find(',', pos);
@@ -323,14 +327,24 @@ int cmd_model(const Args &a) {
         if (name.empty()) continue;
         const auto f = spmvcomp::parse_format(name);
         if (!f) throw Usage{"unknown format " + name};
-        const spmvcomp::FormatCost cost = spmvcomp::format_cost(*f, 27, 2);  // interior row of the 27-point stencil, table [-1, 26]
-        const spmvcomp::RooflineEstimate r = spmvcomp::roofline(cost, mach);
-        std::printf("%-16s %14.6g %14.6g %16.6g\n", name.c_str(), cost.bytes_per_row, cost.bytes_per_flop, r.predicted_flops / 1e9);
+        formats.push_back(*f);
+    }
+    // interior row of the 27-point stencil, table [-1, 26] (perf_model.hpp:82-95)
+    const std::vector<spmvcomp::ModelRow> rows = spmvcomp::model_table(formats, 27, 2, mach);
+    if (a.out_given && a.out == "csv") {
+        emit("model.csv", spmvcomp::model_table_csv(rows));
+    } else if (a.out_given && a.out == "json") {
+        emit("model.json", spmvcomp::model_table_json(rows));
+    } else {
+        std::printf("%-16s %14s %14s %16s\n", "format", "bytes/row", "bytes/flop", "roofline Gflops");
+        for (const auto &r : rows)
+            std::printf("%-16s %14.6g %14.6g %16.6g\n", spmvcomp::format_name(r.format), r.cost.bytes_per_row, r.cost.bytes_per_flop,
+                        r.estimate.predicted_flops / 1e9);
     }
     return 0;
 }
 
-int cmd_calibrate() {
+int cmd_calibrate(const Args &a) {
     // device analogue of the STREAM-style sweep: w = 1*x + 0*y over 64 M doubles reads 16 and writes 8 bytes per element
     const int64_t n = 64LL << 20;
     DVec x(n), y(n), w(n);
@@ -343,8 +357,15 @@ int cmd_calibrate() {
     for (int r = 0; r < reps; r++) ck(spmvb_waxpby(1.0, x.p, 0.0, y.p, w.p, n, nullptr), "waxpby");
     sync_read(w.p);
     const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-    std::printf("{\"device_stream_bandwidth_gbs\": %.6g, \"kernel\": \"waxpby\", \"bytes_per_element\": 24, \"elements\": %lld}\n",
-                24.0 * (double)n * reps / sec / 1e9, (long long)n);
+    const double gbs = 24.0 * (double)n * reps / sec / 1e9;
+    std::printf("{\"device_stream_bandwidth_gbs\": %.6g, \"kernel\": \"waxpby\", \"bytes_per_element\": 24, \"elements\": %lld}\n", gbs, (long long)n);
+    if (a.out_given) {  // the machine-spec file bench's roofline column reads back with --machine
+        spmvcomp::MachineSpec mach;
+        mach.read_bandwidth = gbs * 1e9;
+        spmvcomp::b200::save_machine_spec(mach, a.out);
+        const spmvcomp::MachineSpec back = spmvcomp::b200::load_machine_spec(a.out);
+        if (back.read_bandwidth != mach.read_bandwidth) throw Failure{"machine spec " + a.out + " does not round-trip"};
+    }
     return 0;
 }
 
@@ -359,7 +380,7 @@ int main(int argc, char **argv) {
         if (cmd == "bench") return cmd_bench(a);
         if (cmd == "solve") return cmd_solve(a);
         if (cmd == "model") return cmd_model(a);
-        if (cmd == "calibrate") return cmd_calibrate();
+        if (cmd == "calibrate") return cmd_calibrate(a);
         throw Usage{"unknown subcommand " + cmd};
     } catch (const Usage &u) {
         std::fprintf(stderr, "usage error: %s\n", u.msg.c_str());

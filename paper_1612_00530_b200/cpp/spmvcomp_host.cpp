@@ -488,6 +488,42 @@ RooflineEstimate roofline(const FormatCost& cost, const MachineSpec& machine) {
     }
     return r;
 }
+std::vector<ModelRow> model_table(const std::vector<MatrixFormat>& formats, int row_nnz, int table_size, const MachineSpec& machine,
+                                  const ModelOptions& opts) {
+    std::vector<ModelRow> rows;
+    rows.reserve(formats.size());
+    for (MatrixFormat f : formats) {
+        ModelRow r{f, format_cost(f, row_nnz, table_size, opts), {}};
+        r.estimate = roofline(r.cost, machine);
+        rows.push_back(r);
+    }
+    return rows;
+}
+namespace {
+std::string num(double v) {
+    char buf[40];
+    std::snprintf(buf, sizeof buf, "%.9g", v);
+    return buf;
+}
+}  // namespace
+std::string model_table_csv(const std::vector<ModelRow>& rows) {
+    std::string out = "format,bytes_per_row,bytes_per_flop,predicted_gflops,limiting_resource\n";
+    for (const ModelRow& r : rows)
+        out += std::string(format_name(r.format)) + "," + num(r.cost.bytes_per_row) + "," + num(r.cost.bytes_per_flop) + "," +
+               num(r.estimate.predicted_flops / 1e9) + "," + limiting_resource_name(r.estimate.limiting_resource) + "\n";
+    return out;
+}
+std::string model_table_json(const std::vector<ModelRow>& rows) {
+    std::string out = "[";
+    for (size_t i = 0; i < rows.size(); i++) {
+        const ModelRow& r = rows[i];
+        out += std::string(i ? ", " : "") + "{\"format\": \"" + format_name(r.format) + "\", \"bytes_per_row\": " + num(r.cost.bytes_per_row) +
+               ", \"flops_per_row\": " + num(r.cost.flops_per_row) + ", \"bytes_per_flop\": " + num(r.cost.bytes_per_flop) +
+               ", \"predicted_gflops\": " + num(r.estimate.predicted_flops / 1e9) + ", \"limiting_resource\": \"" +
+               limiting_resource_name(r.estimate.limiting_resource) + "\"}";
+    }
+    return out + "]\n";
+}
 FormatCost measured_cost(const EllMatrix& a) {
     ByteBreakdown b;
     b.values = 8.0 * a.width;
@@ -511,3 +547,43 @@ FormatCost measured_cost(const PatternCompressedMatrix& a) {
 }
 
 }  // namespace spmvcomp
+
+namespace spmvcomp::b200 {
+void save_machine_spec(const MachineSpec& machine, const std::string& path) {
+    std::FILE* f = std::fopen(path.c_str(), "w");
+    if (!f) throw IoError("cannot write the machine spec to " + path);
+    int ok = std::fprintf(f, "{\"read_bandwidth\": %.17g", machine.read_bandwidth);
+    if (ok >= 0 && machine.peak_flops) ok = std::fprintf(f, ", \"peak_flops\": %.17g", *machine.peak_flops);
+    if (ok >= 0) ok = std::fprintf(f, "}\n");
+    if (std::fclose(f) != 0 || ok < 0) throw IoError("cannot write the machine spec to " + path);
+}
+MachineSpec load_machine_spec(const std::string& path) {
+    std::FILE* f = std::fopen(path.c_str(), "r");
+    if (!f) throw IoError("cannot read the machine spec " + path);
+    std::string text;
+    char buf[256];
+    size_t got;
+    while ((got = std::fread(buf, 1, sizeof buf, f)) > 0) text.append(buf, got);
+    std::fclose(f);
+    auto field = [&](const char* key) -> std::optional<double> {
+        const size_t k = text.find(std::string("\"") + key + "\"");
+        if (k == std::string::npos) return std::nullopt;
+        const size_t c = text.find(':', k);
+        if (c == std::string::npos) return std::nullopt;
+        const char* b = text.c_str() + c + 1;
+        char* e = nullptr;
+        const double v = std::strtod(b, &e);
+        if (e == b) return std::nullopt;
+        return v;
+    };
+    MachineSpec m;
+    const auto bw = field("read_bandwidth");
+    if (!bw || !(*bw > 0.0)) throw IoError("machine spec " + path + ": no positive read_bandwidth");
+    m.read_bandwidth = *bw;
+    if (const auto pf = field("peak_flops")) {
+        if (!(*pf > 0.0)) throw IoError("machine spec " + path + ": peak_flops must be positive");
+        m.peak_flops = *pf;
+    }
+    return m;
+}
+}  // namespace spmvcomp::b200

@@ -190,6 +190,22 @@ int main() {
         CHECK(pv > 4.0 && pv < 4.08);
         CHECK(measured_cost(compress_values(m)).bytes_per_row == 116.0);
         CHECK(std::string(format_name(MatrixFormat::pattern_with_values)) == "pattern-values" && parse_format("vt") == MatrixFormat::vt);
+        // model_table / model_table_csv / model_table_json (inc/perf_model.hpp:82-95)
+        MachineSpec slow;
+        slow.peak_flops = 100e9;  // below the 337.5 Gflops the bandwidth would allow for `pattern`
+        const std::vector<ModelRow> rows = model_table({MatrixFormat::ell, MatrixFormat::vt, MatrixFormat::pattern}, 27, 2, slow);
+        CHECK(rows.size() == 3 && rows[0].format == MatrixFormat::ell && rows[0].cost.bytes_per_row == 324.0);
+        CHECK(std::fabs(rows[0].estimate.predicted_flops - 12.5e9) < 1.0 && rows[0].estimate.limiting_resource == LimitingResource::bandwidth);
+        CHECK(rows[2].estimate.predicted_flops == 100e9 && rows[2].estimate.limiting_resource == LimitingResource::compute);
+        const std::string csv = model_table_csv(rows);
+        CHECK(csv.rfind("format,bytes_per_row,bytes_per_flop,predicted_gflops,limiting_resource\n", 0) == 0);
+        CHECK(csv.find("ell,324,6,12.5,bandwidth\n") != std::string::npos && csv.find("pattern,12,") != std::string::npos &&
+              csv.find(",100,compute\n") != std::string::npos);
+        const std::string js = model_table_json(rows);
+        CHECK(js.front() == '[' && js.find("\"format\": \"vt\"") != std::string::npos && js.find("\"limiting_resource\": \"compute\"") != std::string::npos);
+        ModelOptions with_x;
+        with_x.include_input_vector = true;
+        CHECK(model_table({MatrixFormat::pattern_with_values}, 27, 2, MachineSpec{}, with_x)[0].cost.bytes_per_row == 12.0);
     }
     // ---- the CG caller (acceptance criterion 8)
     {

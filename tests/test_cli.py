@@ -156,3 +156,53 @@ def test_calibrate_reports_a_positive_stable_bandwidth():
     a = json.loads(run("calibrate")[1])["device_stream_bandwidth_gbs"]
     b = json.loads(run("calibrate")[1])["device_stream_bandwidth_gbs"]
     assert a > 0 and abs(a - b) <= 0.2 * max(a, b)
+
+
+def test_model_table_csv_and_json():
+    """model_table / model_table_csv / model_table_json (inc/perf_model.hpp:82-95): fixed CSV column order."""
+    rc, out, _ = run("model", "--bandwidth", 75, "--out", "csv")
+    assert rc == 0
+    lines = out.strip().splitlines()
+    assert lines[0] == "format,bytes_per_row,bytes_per_flop,predicted_gflops,limiting_resource"
+    rows = {ln.split(",")[0]: ln.split(",") for ln in lines[1:]}
+    assert list(rows) == ["ell", "vt", "pattern", "pattern-values"]
+    assert float(rows["ell"][1]) == 324.0 and float(rows["ell"][3]) == 12.5 and rows["ell"][4] == "bandwidth"
+    assert float(rows["pattern"][3]) == 337.5 and float(rows["pattern-values"][1]) == 4.0
+    rc, out, _ = run("model", "--bandwidth", 75, "--out", "json", "--formats", "vt,ell")
+    assert rc == 0
+    t = json.loads(out)
+    assert [r["format"] for r in t] == ["vt", "ell"] and t[0]["bytes_per_row"] == 116.0 and abs(t[0]["predicted_gflops"] - 34.9) < 0.05
+    assert t[1]["flops_per_row"] == 54.0 and t[1]["limiting_resource"] == "bandwidth"
+
+
+def test_machine_spec_file_round_trips_into_model(tmp_path):
+    """The machine-spec file read back by `model --machine`: same table as --bandwidth."""
+    spec = tmp_path / "spec.json"
+    spec.write_text('{"read_bandwidth": 75000000000}\n')
+    rc, out, _ = run("model", "--machine", str(spec))
+    rc2, out2, _ = run("model", "--bandwidth", 75)
+    assert rc == 0 and rc2 == 0 and out == out2
+    bad = tmp_path / "bad.json"
+    bad.write_text('{"peak_flops": 1e12}\n')
+    rc, _, err = run("model", "--machine", str(bad))
+    assert rc == 1 and "read_bandwidth" in err
+    rc, _, err = run("model", "--machine", str(tmp_path / "missing.json"))
+    assert rc == 1
+
+
+@pytest.mark.gpu
+def test_calibrate_writes_a_machine_spec_that_bench_reads(tmp_path):
+    spec = tmp_path / "spec.json"
+    rc, out, err = run("calibrate", "--out", str(spec))
+    assert rc == 0, err
+    gbs = json.loads(out)["device_stream_bandwidth_gbs"]
+    assert gbs > 0
+    saved = json.loads(spec.read_text())
+    assert abs(saved["read_bandwidth"] / 1e9 - gbs) < 1e-3 * gbs
+    rc2, out2, _ = run("calibrate")
+    assert rc2 == 0 and abs(json.loads(out2)["device_stream_bandwidth_gbs"] - gbs) < 0.2 * gbs  # two runs within 20 % (SPEC.md:481)
+    rc, out, err = run("bench", "--grid", 32, 32, 32, "--format", "pattern-values", "--reps", 5, "--machine", str(spec))
+    assert rc == 0, err
+    rep = json.loads(out)
+    assert abs(rep["machine_bandwidth_gbs"] - saved["read_bandwidth"] / 1e9) < 1e-6 * rep["machine_bandwidth_gbs"]
+    assert abs(rep["roofline_gflops"] - rep["machine_bandwidth_gbs"] * (2.0 * rep["nnz"] / rep["rows"]) / rep["bytes_per_row"]) < 1e-3 * rep["roofline_gflops"]
