@@ -673,7 +673,25 @@ def run_b200(args):
         line["parity"]["rows_differing_from_cpu_oracle"] = int((yo.view(np.uint64) != yg.view(np.uint64)).sum())
         ids_dev = pc.download("row_pattern")
         line["parity"]["pattern_ids_differing_from_cpu_oracle"] = int((ids_dev != r["pc"].row_pattern).sum())
-        del r
+        # The reference-signature convenience call spmv(const PatternCompressedMatrix&, const Vector&) -> Vector as the C++
+        # shim issues it (cpp/spmvcomp_host.cpp:spmv_checked): the struct's arrays uploaded, validated, x in and a fresh y
+        # out through pageable host memory, handle destroyed -- per call.  Callers that keep a device handle get `e2e.value`.
+        o = r["pc"]
+        xs = np.array(r["x"])
+        t_sig = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            d = sp.upload_pattern(o.n, o.table, o.disp_offsets, o.disp_flat, o.ends_flat, o.row_pattern, True)
+            sp.check(sp.lib.spmvb_validate(d.h, o.n, None))
+            ys = np.empty(n)
+            sp.check(sp.lib.spmvb_spmv_host(d.h, xs.ctypes.data, n, ys.ctypes.data))
+            del d
+            t_sig.append((time.perf_counter() - t0) * 1e3)
+        line["e2e"]["ms_per_call_reference_signature"] = min(t_sig)
+        line["e2e"]["reference_signature_note"] = ("spmv(fmt, Vector) -> Vector: upload of the struct's arrays (67 MB of ids), validate, "
+                                                   "pageable x in / fresh pageable y out, handle destroyed; best of 3")
+        line["e2e"]["reference_signature_matches_oracle"] = bool(np.array_equal(ys.view(np.uint64), yo.view(np.uint64)))
+        del r, o
     if world == 1 and not args.no_configs:
         torch.cuda.empty_cache()
         line["configs"] = config_blocks(sp, torch, main, peak, l2_bytes)
