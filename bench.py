@@ -44,8 +44,9 @@ def parse_args():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--grid", type=int, nargs=3, default=[256, 256, 256], help="rows per GPU (nx ny nz_local)")
-    ap.add_argument("--exchange", default=os.environ.get("SPMVB_EXCHANGE", "nccl"), choices=["nccl", "p2p"],
-                    help="N > 1: halo planes by NCCL send/recv, or pulled from CUDA-IPC-mapped neighbour memory")
+    ap.add_argument("--exchange", default=os.environ.get("SPMVB_EXCHANGE", "p2p"), choices=["nccl", "p2p"],
+                    help="N > 1: halo planes pulled from CUDA-IPC-mapped neighbour memory over NVLink (falls back to nccl when "
+                         "a rank cannot map its neighbours), or NCCL send/recv")
     ap.add_argument("--schedule", default=os.environ.get("SPMVB_SCHEDULE", "serial"), choices=["serial", "overlap"],
                     help="N > 1: exchange then one launch, or exchange || interior planes then the two boundary planes")
     ap.add_argument("--no-graph", action="store_true", help="N > 1, nccl: do not capture the step into a CUDA graph")
@@ -492,6 +493,21 @@ def run_b200(args):
 
         slab = sp.DeviceSlabSpmv(sp, L, pc, dist if world > 1 else None, main, comm, torch, exchange=args.exchange,
                                  schedule=args.schedule)
+        if world > 1 and args.exchange == "p2p":  # all ranks map their neighbours, or all fall back to NCCL send/recv
+            try:
+                slab.map_neighbours(x)
+                mapped = 1
+            except Exception as ex:  # noqa: BLE001
+                print(f"rank {rank}: cannot map the neighbours' vectors ({ex}); falling back to --exchange nccl", file=sys.stderr)
+                mapped = 0
+            ok = torch.tensor([mapped], device="cuda")
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if not int(ok.item()):
+                slab.unmap_neighbours()
+                args.exchange = "nccl"
+                slab = sp.DeviceSlabSpmv(sp, L, pc, dist, main, comm, torch, exchange="nccl", schedule=args.schedule)
+            main.synchronize()
+            dist.barrier()  # every rank's x is filled before anyone pulls a plane of it
         whole = kernel_of(pc)
         step = (lambda: whole(x, y, 0, n)) if world == 1 else (lambda: slab.spmv(x, y))
 

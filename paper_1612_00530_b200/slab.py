@@ -192,6 +192,14 @@ class DeviceSlabSpmv(SlabSpmv):
                 self._peers[r] = sp.ipc_open(handles[r])
         self._mapped_for = x_local.data_ptr()
 
+    def fence(self):
+        """"p2p" only: every rank's producers of x_local have completed before anyone pulls a plane of it -- a stream
+        synchronize and a barrier.  A caller whose x changes between SpMVs (CG's search direction) calls it before each
+        spmv(); the all-reduce that follows the SpMV orders the pulls before the next update of x."""
+        if self.exchange_kind == "p2p" and self.dist is not None and self.L.world > 1:
+            self.main_stream.synchronize()
+            self.dist.barrier()
+
     def unmap_neighbours(self):
         for ptr in self._peers.values():
             self.sp.ipc_close(ptr)
@@ -295,6 +303,9 @@ class SlabCg:
         if bnorm == 0.0:
             return 0, True, history
         for it in range(1, max_iterations + 1):
+            fence = getattr(self.spmv, "fence", None)
+            if fence is not None:
+                fence()  # neighbours' memory read in place ("p2p"): their update of p is complete
             self.spmv.spmv(p_ghosted, ap_local)
             alpha = rz / self._sum(ops.dot(p, ap_local))
             ops.waxpby(1.0, x_local, alpha, p, x_local)
