@@ -134,6 +134,9 @@ int spmvb_set_device(int device);
  *                     the marches (the round-1 scheme; 256^3: 72.5 vs 69.7 us)
  *   "host_chunks":    row chunks of the pipelined spmvb_spmv_host (0 = default 8)
  *   "slab_graph":     1 (default) spmvb_slab_spmv replays its copies and launches as a CUDA graph; 0 launches directly
+ *   "symgs_persistent": 1 (default) a symgs sweep is ONE cooperative launch: a CTA per SM walks the hyperplane levels with a
+ *                     grid-wide barrier between them and fetches each row's matrix data ahead of the barrier; 0 a launch
+ *                     per level (recorded into a CUDA graph when "symgs_graph" = 1).  Same bits either way
  *   "symgs_graph":    1 (default) the launches of a symgs sweep are recorded into a CUDA graph and replayed; 0 launches directly
  *   "cg_graph":       1 (default) spmvb_cg_solve records its iteration into a CUDA graph after the first one and replays it (one
  *                     graph launch per iteration); 0 launches the kernels directly.  "last_cg_graph" (read-only) says which ran

@@ -263,6 +263,7 @@ static int *option_slot(const char *key) {
     if (!strcmp(key, "cg_graph")) return &o.cg_graph;
     if (!strcmp(key, "last_cg_graph")) return &o.last_cg_graph;
     if (!strcmp(key, "symgs_graph")) return &o.symgs_graph;
+    if (!strcmp(key, "symgs_persistent")) return &o.symgs_persistent;
     if (!strcmp(key, "slab_graph")) return &o.slab_graph;
     if (!strcmp(key, "last_cg_fused_dot")) return &o.last_cg_fused_dot;
     if (!strcmp(key, "last_pattern_kernel")) return &o.last_pattern_kernel;

@@ -148,6 +148,7 @@ struct Options {
     int ring_pdl = 1;        // tensor ring launched with programmatic stream serialization (its preamble overlaps the previous kernel's tail)
     int ring_leftover = 0;   // tensor ring, left-over column (64 | sy): 0 summed by the last strip's warp from its ring, 1 row by row after the marches
     int slab_graph = 1;         // 1: spmvb_slab_spmv records its exchange copies and launches into a CUDA graph and replays it
+    int symgs_persistent = 1;   // 1: a symgs sweep is one cooperative launch that walks the levels itself (grid-wide barriers); 0: a launch per level
     int symgs_graph = 1;        // 1: a symgs sweep's launches are recorded into a CUDA graph and replayed
     int cg_graph = 1;           // 1: cg_solve records its iteration into a CUDA graph after the first and replays it
     int last_cg_graph = 0;      // read-only: 1 when the last cg_solve replayed a graph

@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "device_utils.cuh"
 #include "spmv_internal.cuh"
 
 namespace spmvb {
@@ -82,6 +83,130 @@ __global__ void symgs_level_kernel(const int64_t *__restrict__ row_start, const 
     x[i] = __ddiv_rn(__dsub_rn(b[i], sum), diag);  // inc/kernels.hpp:46
 }
 
+// ---- the whole sweep in ONE launch ---------------------------------------------------------------------------------
+// A level holds ~10^4 rows (256^3: 16.8 M rows over 1786 levels) -- microseconds of work -- so a sweep of per-level launches
+// is launch latency, 3572 times.  The persistent kernel keeps one CTA per SM resident (cooperative launch) and walks the
+// levels itself, a grid-wide barrier between them.  What a row needs besides x does not depend on the sweep, so it is
+// fetched ahead, into registers: a thread holds the head of the row it will own two levels on (row_start pair, b[row]) and
+// requests the entries of its next row before it arrives at the barrier.  After the barrier only the gathers of x
+// (ld.global.cg: the values were written by other SMs a level ago; one L2 round trip), the ordered sum and the store remain.
+// 256 threads per CTA so that nothing spills (the barrier's acquire invalidates L1, and spill reloads then miss: 384 threads
+// at 168 registers ran 40 % slower; staging the entries in shared memory with cp.async instead: 2.3 x slower).
+// Same per-row expression as the level kernel: bit-identical.
+constexpr int kSymgsThreads = 256;  // one CTA per SM
+constexpr int kSymgsRow = 27;       // entries of a row fetched ahead (longer rows read the rest in place)
+
+__device__ __forceinline__ void symgs_level_rect(int level, int nx, int ny, int nz, int *iz_lo, int *n_iz) {
+    const int rest = level - (nx - 1) - 2 * (ny - 1);
+    const int lo = rest > 0 ? (rest + 3) / 4 : 0;
+    const int hi = min(nz - 1, level / 4);
+    *iz_lo = lo;
+    *n_iz = hi >= lo ? hi - lo + 1 : 0;
+}
+
+__device__ __forceinline__ int symgs_row_of(int t, int level, int nx, int ny, int iz_lo, int n_iz) {
+    if (t >= ny * n_iz) return -1;
+    const int iy = t % ny, iz = iz_lo + t / ny;
+    const int ix = level - 2 * iy - 4 * iz;
+    if (ix < 0 || ix >= nx) return -1;
+    return ix + nx * (iy + ny * iz);
+}
+
+struct SymgsHead {  // what is known of a row before its entries: the row, its first entry, its length, b[row]
+    int i, cnt;
+    int64_t k0;
+    double bi;
+};
+struct SymgsBody {  // the first 27 entries
+    int c[kSymgsRow];
+    double v[kSymgsRow];
+};
+
+__device__ __forceinline__ SymgsHead symgs_head(int i, const int64_t *__restrict__ row_start, const double *__restrict__ b) {
+    SymgsHead h{i, 0, 0, 0.0};
+    if (i >= 0) {
+        h.k0 = __ldg(row_start + i);
+        h.cnt = (int)(__ldg(row_start + i + 1) - h.k0);
+        h.bi = __ldg(b + i);
+    }
+    return h;
+}
+
+__device__ __forceinline__ void symgs_body(SymgsBody &r, const SymgsHead &h, const int32_t *__restrict__ cols, const double *__restrict__ vals) {
+#pragma unroll
+    for (int j = 0; j < kSymgsRow; j++) {
+        const bool in = j < h.cnt;
+        r.c[j] = in ? __ldg(cols + h.k0 + j) : h.i;
+        r.v[j] = in ? __ldg(vals + h.k0 + j) : 0.0;
+    }
+}
+
+// the row's new value from the latest x (entries in ascending column order, inc/kernels.hpp:46)
+__device__ __forceinline__ void symgs_relax(const SymgsHead &h, const SymgsBody &r, const int32_t *__restrict__ cols,
+                                            const double *__restrict__ vals, double *x) {
+    const int i = h.i;
+    double xv[kSymgsRow];
+#pragma unroll
+    for (int j = 0; j < kSymgsRow; j++) xv[j] = (j < h.cnt && r.c[j] != i) ? __ldcg(x + r.c[j]) : 0.0;
+    double sum = 0.0, diag = 0.0;
+#pragma unroll
+    for (int j = 0; j < kSymgsRow; j++) {
+        if (j >= h.cnt) continue;
+        if (r.c[j] == i) diag = r.v[j];
+        else sum = __dadd_rn(sum, __dmul_rn(r.v[j], xv[j]));
+    }
+    for (int j = kSymgsRow; j < h.cnt; j++) {  // longer rows (explicit matrices): the rest entry by entry
+        const int cj = __ldg(cols + h.k0 + j);
+        const double v = __ldg(vals + h.k0 + j);
+        if (cj == i) diag = v;
+        else sum = __dadd_rn(sum, __dmul_rn(v, __ldcg(x + cj)));
+    }
+    __stcg(x + i, __ddiv_rn(__dsub_rn(h.bi, sum), diag));
+}
+
+// grid-wide barrier: one arrival per CTA on a monotonically increasing counter (release / acquire at gpu scope)
+__device__ __forceinline__ void symgs_grid_barrier(unsigned int *counter, unsigned int target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(counter, 1u);
+        unsigned int seen;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(counter) : "memory");
+        } while ((int)(seen - target) < 0);
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kSymgsThreads, 1) symgs_sweep_persistent_kernel(const int64_t *__restrict__ row_start, const int32_t *__restrict__ cols,
+                                                                                  const double *__restrict__ vals, double *x, const double *__restrict__ b,
+                                                                                  int nx, int ny, int nz, int levels, unsigned int *counter,
+                                                                                  unsigned int epoch) {
+    // rows of a level are dealt out across the SMs first (entry t of the level's rectangle -> CTA t % grid): a level holds
+    // fewer rows than the machine has threads, and an SM sustains only so many outstanding gathers
+    const int t0 = blockIdx.x + gridDim.x * threadIdx.x;
+    const int steps = 2 * levels;
+    auto level_of_step = [&](int s) { return s < levels ? s : 2 * levels - 1 - s; };
+    auto head_of_step = [&](int s) {
+        if (s >= steps) return SymgsHead{-1, 0, 0, 0.0};
+        int iz_lo, n_iz;
+        symgs_level_rect(level_of_step(s), nx, ny, nz, &iz_lo, &n_iz);
+        return symgs_head(symgs_row_of(t0, level_of_step(s), nx, ny, iz_lo, n_iz), row_start, b);
+    };
+    SymgsHead cur = head_of_step(0), nxt = head_of_step(1);
+    SymgsBody body;
+    symgs_body(body, cur, cols, vals);
+    for (int s = 0; s < steps; s++) {
+        if (cur.i >= 0) symgs_relax(cur, body, cols, vals, x);
+        if (s + 1 < steps) {
+            cur = nxt;
+            symgs_body(body, cur, cols, vals);  // the next level's entries (its head arrived a level ago) ...
+            nxt = head_of_step(s + 2);          // ... and the head of the level after it: all in flight across the barrier
+            symgs_grid_barrier(counter, epoch + (unsigned int)(s + 1) * gridDim.x);
+        }
+    }
+}
+
 static int check_schedule(const spmvb_matrix *a, const spmvb_grid *g, cudaStream_t st) {
     if (a->symgs_checked[0] == g->nx && a->symgs_checked[1] == g->ny && a->symgs_checked[2] == g->nz) return SPMVB_OK;
     int *flags = nullptr;
@@ -129,7 +254,56 @@ static void launch_levels(const spmvb_matrix *a, const spmvb_grid *g, double *x,
 // A sweep is thousands of tiny dependent launches: they are recorded once into a CUDA graph (kept on the handle, keyed by
 // the vectors and the grid) and replayed, which takes the host's per-launch cost out of every sweep after the first
 // (the preconditioner applies the sweep to the same two vectors in every iteration).  "symgs_graph" = 0 launches directly.
+// one cooperative launch per sweep; 1 = not available here (the caller launches level by level)
+static int sweep_persistent(const spmvb_matrix *a, const spmvb_grid *g, double *x, const double *b, cudaStream_t st) {
+    struct State {
+        int coop = -1, n_sm = 0;
+        unsigned int *counter = nullptr;
+        unsigned int epoch = 0;
+    };
+    static PerDevice<State> state;
+    State &sd = state.get();
+    if (sd.coop < 0) {
+        int dev = 0, coop = 0, per_sm = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&sd.n_sm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, symgs_sweep_persistent_kernel, kSymgsThreads, 0) != cudaSuccess || per_sm < 1 ||
+            cudaMalloc(&sd.counter, sizeof(unsigned int)) != cudaSuccess || cudaMemset(sd.counter, 0, sizeof(unsigned int)) != cudaSuccess)
+            coop = 0;
+        (void)cudaGetLastError();
+        sd.coop = coop ? 1 : 0;
+    }
+    if (!sd.coop) return 1;
+    int nx = g->nx, ny = g->ny, nz = g->nz;
+    {   // a thread owns at most one row per level: the widest level's (iy, iz) rectangle must fit the grid's threads
+        // (256^3: 49 k entries against 37,888 threads -- that sweep stays with the per-level launches)
+        const int64_t span = std::min<int64_t>(nz, ((int64_t)(nx - 1) + 2 * (int64_t)(ny - 1)) / 4 + 2);
+        if ((int64_t)ny * span > (int64_t)sd.n_sm * kSymgsThreads) return 1;
+    }
+    int levels = (nx - 1) + 2 * (ny - 1) + 4 * (nz - 1) + 1;
+    const auto *rs = static_cast<const int64_t *>(a->s[SPMVB_S_CSR_ROW_START]);
+    const auto *cols = static_cast<const int32_t *>(a->s[SPMVB_S_CSR_COLS]);
+    const auto *vals = static_cast<const double *>(a->s[SPMVB_S_CSR_VALS]);
+    // the barrier counter only grows: this sweep's arrivals start at `epoch` (sweeps of one device are ordered by their stream;
+    // two host threads sweeping on two streams of one device at once would share it -- they are serialised by `busy`)
+    const unsigned int arrivals = (unsigned int)(2 * levels - 1) * (unsigned int)sd.n_sm;
+    unsigned int epoch = sd.epoch;
+    sd.epoch += arrivals;
+    unsigned int *counter = sd.counter;
+    void *args[] = {&rs, &cols, &vals, &x, &b, &nx, &ny, &nz, &levels, &counter, &epoch};
+    if (cudaLaunchCooperativeKernel((const void *)symgs_sweep_persistent_kernel, dim3(sd.n_sm), dim3(kSymgsThreads), args, 0, st) != cudaSuccess) {
+        sd.epoch -= arrivals;
+        (void)cudaGetLastError();
+        return 1;
+    }
+    return 0;
+}
+
 static int sweep_device(const spmvb_matrix *a, const spmvb_grid *g, double *x, const double *b, cudaStream_t st) {
+    if (options().symgs_persistent) {
+        const int rc = sweep_persistent(a, g, x, b, st);
+        if (rc == 0) return SPMVB_OK;
+    }
     SymgsGraph &c = a->symgs_graph;
     const bool hit = c.exec && c.x == x && c.b == b && c.nx == g->nx && c.ny == g->ny && c.nz == g->nz;
     if (options().symgs_graph && !hit) {
