@@ -126,6 +126,7 @@ int spmvb_set_device(int device);
  *   "exception_overlap": hybrid handles: 1 (default) the exception block runs on a second stream beside the kernel of the dictionary
  *                     rows (the two write disjoint rows of y; forked and joined by events, so the call still completes in
  *                     stream order); 0 one after the other
+ *   "ring_min_steps": tensor ring: fewest line steps per chunk before the grid shrinks below a full wave of CTAs (0 = default 4)
  *   "ring_pdl":       1 (default) the tensor-ring kernel is launched with programmatic stream serialization: its CTAs take the
  *                     places of the previous kernel's CTAs as those exit and wait (griddepcontrol.wait) for that kernel to
  *                     complete before touching global memory; 0 plain stream order

@@ -255,6 +255,7 @@ static int *option_slot(const char *key) {
     if (!strcmp(key, "box_lines")) return &o.box_lines;
     if (!strcmp(key, "ring_leftover")) return &o.ring_leftover;
     if (!strcmp(key, "ring_pdl")) return &o.ring_pdl;
+    if (!strcmp(key, "ring_min_steps")) return &o.ring_min_steps;
     if (!strcmp(key, "exception_kernel")) return &o.exception_kernel;
     if (!strcmp(key, "exception_overlap")) return &o.exception_overlap;
     if (!strcmp(key, "host_chunks")) return &o.host_chunks;

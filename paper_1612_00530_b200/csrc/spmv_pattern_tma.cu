@@ -184,7 +184,7 @@ template <int Q, int S, int MINB, bool OFF_NEG1, int CENTER_POS, bool IDT, int P
 __global__ void __launch_bounds__(kRingWarps * 32, MINB)
     spmv_pattern_ringp_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm_ids, PatternArgs p, int c_lo,
                               int c_hi, int np_x, int n_strips, int left_lo, int left_in_ring, int id_plane0, int total_steps, int steps_per_warp,
-                              int tile_lines, int rot) {
+                              int steps_rem, int tile_lines, int rot) {
     using L = RingLayout<Q, S, IDT>;
     constexpr int P = L::P;
     const int cpos = CENTER_POS >= 0 ? CENTER_POS : p.center_pos;  // CENTER_POS = -1: the general variant reads it at run time
@@ -231,8 +231,9 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
     const int n_cols = (CTAC ? n_sg : n_strips) * ((c_hi - c_lo + Q) / Q);
     const int n_tiles = tile_lines > 0 ? n_cols * ((pl + tile_lines - 1) / tile_lines) : 0;
     int tile = me;
-    int s_pos = me * steps_per_warp;
-    const int s_end = min(total_steps, s_pos + steps_per_warp);
+    // unit `me` takes steps_per_warp steps, the first steps_rem units one more: every unit of a full wave has work
+    int s_pos = me * steps_per_warp + min(me, steps_rem);
+    const int s_end = min(total_steps, s_pos + steps_per_warp + (me < steps_rem ? 1 : 0));
 #pragma unroll 1
     while (true) {
         int col_idx, b0, nb;
@@ -636,7 +637,7 @@ static int launch_ringp_t(const spmvb_matrix *a, PatternArgs &p_in, int chunk, c
     }
     // one wave of CTAs; every warp gets the same number of line steps (at least `min_steps`, so that small problems
     // do not pay two halo line sets for a handful of steps)
-    const int min_steps = 8;
+    const int min_steps = options().ring_min_steps > 0 ? options().ring_min_steps : 4;  // (128^3: 14.8 us with 8, 13.5 us with 2-4: a full wave, launched with PDL)
 #define LAUNCH_RINGP(NEG, CP)                                                                                                   \
     do {                                                                                                                         \
         static PerDevice<int> per_sm_dev;                                                                                        \
@@ -654,7 +655,10 @@ static int launch_ringp_t(const spmvb_matrix *a, PatternArgs &p_in, int chunk, c
             grid = std::max(1, std::min(grid, (n_tiles + units - 1) / units));                                                   \
         } else                                                                                                                   \
             grid = std::max(1, std::min(grid, (total + min_steps * units - 1) / (min_steps * units)));                          \
-        const int spw = chunk > 0 ? chunk : (total + grid * units - 1) / (grid * units);                                         \
+        /* equal shares: total = (grid * units) * spw + rem, the first rem units take one step more (a forced chunk length:  */ \
+        /* as many units as it needs)                                                                                       */ \
+        int spw = chunk > 0 ? chunk : total / (grid * units), rem = chunk > 0 ? 0 : total - spw * (grid * units);                \
+        if (spw == 0) spw = 1, rem = 0, grid = (total + units - 1) / units;                                                      \
         if (chunk > 0) grid = (total + spw * units - 1) / (spw * units);                                                         \
         const int cols_per_group = CTAC ? n_cols : n_strips;                                                                    \
         const int64_t wgrp = (int64_t)cols_per_group * p.plane_lines, kgrp = (wgrp + spw / 2) / spw;                              \
@@ -674,7 +678,7 @@ static int launch_ringp_t(const spmvb_matrix *a, PatternArgs &p_in, int chunk, c
         cfg.attrs = pdl;                                                                                                         \
         cfg.numAttrs = (options().ring_pdl && grid == n_sm * per_sm) ? 1 : 0; /* only a full wave: early CTAs of a partial grid crowd the SMs that free up first (128^3: 14.2 -> 17.9 us) */                                                                               \
         if (cudaLaunchKernelEx(&cfg, spmv_pattern_ringp_kernel<Q, S, MINB, NEG, CP, IDT, PFD, DBG, CTAC, DOT>, tm, tm_ids, p, c_lo, c_hi, np_x,     \
-                               n_strips, left_lo, left_in_ring, id_plane0, total, spw, tile_lines, rot) != cudaSuccess)          \
+                               n_strips, left_lo, left_in_ring, id_plane0, total, spw, rem, tile_lines, rot) != cudaSuccess)          \
             return check_launch("spmv_pattern_ringp") == SPMVB_OK ? -1 : -1;                                                     \
     } while (0)
     // two instantiations: the HPCG value pattern (off-diagonals -1, centre last) fully specialised, and a general one
