@@ -637,7 +637,9 @@ static int launch_ringp_t(const spmvb_matrix *a, PatternArgs &p_in, int chunk, c
     }
     // one wave of CTAs; every warp gets the same number of line steps (at least `min_steps`, so that small problems
     // do not pay two halo line sets for a handful of steps)
-    const int min_steps = options().ring_min_steps > 0 ? options().ring_min_steps : 4;  // (128^3: 14.8 us with 8, 13.5 us with 2-4: a full wave, launched with PDL)
+    // (128^3: 14.8 us with 8, 13.5 us with 2-4: a full wave, launched with PDL.  Hybrid handles keep 8: their exception block
+    // runs beside this kernel on a second stream and needs room on the SMs -- C4 at 128^3: 41.6 vs 49.8 us)
+    const int min_steps = options().ring_min_steps > 0 ? options().ring_min_steps : (a->n_exc > 0 ? 8 : 4);
 #define LAUNCH_RINGP(NEG, CP)                                                                                                   \
     do {                                                                                                                         \
         static PerDevice<int> per_sm_dev;                                                                                        \

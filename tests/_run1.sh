@@ -1,5 +1,11 @@
-P="python tests/ring_probe.py"
-echo base; SPMVB_LIB=$PWD/paper_1612_00530_b200/libspmvcomp_b200_base.so $P 256 128 96 192 512x512x64
-echo new; $P 256 128 96 192 512x512x64
-for ms in 2 3 4 5 6; do $P 128 96 ring_min_steps=$ms; done
-for ms in 3 4 ; do $P 128 box_march=110 ring_min_steps=$ms; done
+for ms in 6 8 10 12 16 24 32; do echo "min_steps $ms"; python - <<PY
+import sys
+sys.path.insert(0, ".")
+import runpy
+import paper_1612_00530_b200 as sp
+sp.set_option("ring_min_steps", $ms)
+sys.argv=["x"]
+src=open("tests/hybrid_probe.py").read().split('timeit(pc, "hybrid, one kernel')[0]
+exec(src)
+PY
+done
