@@ -276,7 +276,7 @@ static int *option_slot(const char *key) {
 static bool lab_only_value(const char *key, int value) {
     if (kLabBuild) return false;
     if (!strcmp(key, "box_march")) {
-        for (int ok : {0, 3, 90, 101, 107, 108, 109, 110, 111, 112, 113})
+        for (int ok : {0, 3, 90, 101, 107, 108, 109, 110})
             if (value == ok) return false;
         return true;
     }

@@ -767,10 +767,8 @@ int launch_pattern_ring(int which, int lines, const spmvb_matrix *a, PatternArgs
             rc = launch_ringp_t<4, 4, 3, true, 0, 0, true>(a, p, lines, st);
             return rc == 1 ? launch_ringp_t<4, 5, 3, false, 0, 0, true>(a, p, lines, st) : rc;
         // (3 / 5 / 7 / 8 planes per thread, chunk per CTA: 80.6 / 76.2 / 74.0 / 84.1 us at 256^3, r01_probe_planes_per_thread.log)
-        // small (L2-resident) grids: fewer rows per step and a deeper ring, a chunk per warp
-        case 21: rc = launch_ringp_t<2, 8, 2, true>(a, p, lines, st); return rc == 1 ? launch_ringp_t<4, 5, 3, false>(a, p, lines, st) : rc;
-        case 22: rc = launch_ringp_t<4, 6, 2, true>(a, p, lines, st); return rc == 1 ? launch_ringp_t<4, 5, 3, false>(a, p, lines, st) : rc;
-        case 23: rc = launch_ringp_t<2, 6, 3, true>(a, p, lines, st); return rc == 1 ? launch_ringp_t<4, 5, 3, false>(a, p, lines, st) : rc;
+        // (small L2-resident grids, a chunk per warp: 2 planes/thread with 8 or 6 slots, 4 planes/thread with 6 slots -- 15.5 / 15.7 /
+        //  14.8 us at 128^3 against 14.2 us for the default: measured and removed)
         case 19:  // ... a tile per warp
             rc = launch_ringp_t<4, 4, 3, true>(a, p, 0, st, tl);
             return rc == 1 ? launch_ringp_t<4, 5, 3, false>(a, p, 0, st, tl) : rc;
