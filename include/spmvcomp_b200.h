@@ -141,6 +141,11 @@ int spmvb_set_device(int device);
  *   "symgs_graph":    1 (default) the launches of a symgs sweep are recorded into a CUDA graph and replayed; 0 launches directly
  *   "cg_graph":       1 (default) spmvb_cg_solve records its iteration into a CUDA graph after the first one and replays it (one
  *                     graph launch per iteration); 0 launches the kernels directly.  "last_cg_graph" (read-only) says which ran
+ *   "cg_fused_scalars": spmvb_cg_solve's vector kernel (x += alpha p, r -= alpha Ap, r.r): 1 (default) the block that finishes last
+ *                     also forms beta, the stop flag and the iteration's record (4 launches per iteration); 2 every block also
+ *                     forms alpha at its head (3 launches); 0 separate alpha and beta kernels (5 launches).  Same reduction
+ *                     orders, same bits; 281-283 us per iteration at 256^3 in all three (the replayed graph hides the launches)
+ *   "cg_pdl":         1: that kernel and the direction kernel are launched with programmatic stream serialization (default 0: no gain)
  *   "cg_fused_dot":   1 (default) spmvb_cg_solve takes p.Ap from the SpMV kernel when that kernel offers it (pattern format,
  *                     tensor ring, whole square grid): one pass over p and Ap less per iteration; 0 always runs the dot
  *   "last_cg_fused_dot": read-only, 1 when the last spmvb_cg_solve took p.Ap from the SpMV kernel

@@ -262,6 +262,8 @@ static int *option_slot(const char *key) {
     if (!strcmp(key, "cg_keep_workspace")) return &o.cg_keep_workspace;
     if (!strcmp(key, "cg_fused_dot")) return &o.cg_fused_dot;
     if (!strcmp(key, "cg_graph")) return &o.cg_graph;
+    if (!strcmp(key, "cg_pdl")) return &o.cg_pdl;
+    if (!strcmp(key, "cg_fused_scalars")) return &o.cg_fused_scalars;
     if (!strcmp(key, "last_cg_graph")) return &o.last_cg_graph;
     if (!strcmp(key, "symgs_graph")) return &o.symgs_graph;
     if (!strcmp(key, "symgs_persistent")) return &o.symgs_persistent;

@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "device_utils.cuh"
 #include "spmv_internal.cuh"
 
 namespace spmvb {
@@ -44,11 +45,30 @@ __global__ void __launch_bounds__(kDotThreads) dot_partial_kernel(const double *
     }
 }
 
-__global__ void dot_final_kernel(const double *__restrict__ partial, int count, double *__restrict__ out) {
-    // one warp, ascending chunks then a fixed tree: order independent of scheduling
+// Sum of `count` partial sums in the fixed order of dot_final_kernel (lane l: partial[l], partial[l+32], ... ascending, then the
+// shuffle tree), by the first warp of a block whose threads ALL fetch: the values land in shared memory in one round of
+// loads (ld.global.cg: written by other blocks / the previous kernel), then lane l adds its own in order.  A lane-serial loop of
+// dependent global loads took 7 us for 1184 values (the round-1 alpha / beta kernels).  Result valid in thread 0.
+constexpr int kSumChunk = 2048;
+__device__ __forceinline__ double block_ordered_sum(const double *partial, int count, double *buf /* kSumChunk doubles, shared */) {
     double acc = 0.0;
-    for (int i = threadIdx.x; i < count; i += 32) acc = __dadd_rn(acc, partial[i]);
-    for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, o));
+    for (int base = 0; base < count; base += kSumChunk) {
+        const int m = min(kSumChunk, count - base);
+        for (int i = threadIdx.x; i < m; i += blockDim.x) buf[i] = __ldcg(partial + base + i);
+        __syncthreads();
+        if (threadIdx.x < 32)
+            for (int i = threadIdx.x; i < m; i += 32) acc = __dadd_rn(acc, buf[i]);
+        __syncthreads();
+    }
+    if (threadIdx.x < 32)
+        for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, o));
+    return acc;
+}
+
+__global__ void dot_final_kernel(const double *__restrict__ partial, int count, double *__restrict__ out) {
+    // one warp's order -- ascending lane-strided sums, then a fixed tree: independent of scheduling -- fetched by the whole block
+    __shared__ double s_buf[kSumChunk];
+    const double acc = block_ordered_sum(partial, count, s_buf);
     if (threadIdx.x == 0) *out = acc;
 }
 
@@ -65,12 +85,76 @@ __global__ void waxpby_kernel(double alpha, const double *__restrict__ x, double
 //           cg_* kernel is then a no-op, so the host may queue one iteration ahead)  [6] ||b||  [7] tolerance  [8] ||r||/||b||
 __global__ void cg_alpha_kernel(const double *__restrict__ partial, int count, double *__restrict__ scal) {
     if (scal[5] != 0.0) return;
-    double acc = 0.0;
-    for (int i = threadIdx.x; i < count; i += 32) acc = __dadd_rn(acc, partial[i]);
-    for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, o));
+    __shared__ double s_buf[kSumChunk];
+    const double acc = block_ordered_sum(partial, count, s_buf);
     if (threadIdx.x == 0) {
         scal[0] = acc;
         scal[1] = scal[2] / acc;  // alpha = r.z / p.Ap
+    }
+}
+// The iteration's vector kernel ("cg_fused_scalars"): the two updates, r.r, and -- by the block that finishes last (a ticket
+// counter) -- what cg_beta_kernel did: the partial sums of r.r added in that kernel's order, beta, stop flag, iteration count, the
+// record into the host's pinned ring.  alpha comes from cg_alpha_kernel (pap_partial == NULL) or, variant 2, is formed at the head
+// by every block from the partial sums of p.Ap (cg_alpha_kernel's order: the same bits in every block).  At most 32 registers:
+// 1184 blocks of 256 threads are exactly one wave, and one register more makes that two (measured: 119 -> 164 us at 256^3).
+__global__ void __launch_bounds__(kDotThreads, 8) cg_update_fused_kernel(double *__restrict__ scal, const double *__restrict__ p,
+                                                                     const double *__restrict__ ap, double *__restrict__ x,
+                                                                     double *__restrict__ r, int64_t n, const double *pap_partial, int pap_count,
+                                                                     double *partial, unsigned int *ticket, double *host_ring, int ring_slots) {
+    __shared__ double s[kDotThreads / 32];
+    __shared__ double s_alpha;
+    __shared__ int s_last;
+    __shared__ double s_buf[kSumChunk];
+    pdl_launch_dependents();
+    pdl_grid_dependency_wait();
+    if (scal[5] != 0.0) return;
+    // alpha: from cg_alpha_kernel (pap_partial == NULL), or formed here by every block from the partial sums of p.Ap (measured
+    // slower: 1184 blocks reading the same 74 lines of L2 at once cost 45 us at 256^3 -- kept for the record, not used)
+    double pap_sum = 0.0;  // thread 0: p.Ap
+    if (pap_partial) {
+        pap_sum = block_ordered_sum(pap_partial, pap_count, s_buf);
+        if (threadIdx.x == 0) s_alpha = scal[2] / pap_sum;  // alpha = r.z / p.Ap
+    } else if (threadIdx.x == 0) {
+        pap_sum = scal[0];
+        s_alpha = scal[1];
+    }
+    __syncthreads();
+    const double alpha = s_alpha, nalpha = -alpha;
+    double acc = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * kDotThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kDotThreads) {
+        x[i] = __dadd_rn(__dmul_rn(1.0, x[i]), __dmul_rn(alpha, p[i]));
+        const double rn = __dadd_rn(__dmul_rn(1.0, r[i]), __dmul_rn(nalpha, ap[i]));
+        r[i] = rn;
+        acc = __dadd_rn(acc, __dmul_rn(rn, rn));
+    }
+    for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, o));
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        acc = threadIdx.x < kDotThreads / 32 ? s[threadIdx.x] : 0.0;
+        for (int o = 4; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, o));
+        if (threadIdx.x == 0) {
+            partial[blockIdx.x] = acc;
+            __threadfence();  // the partial sum before the ticket
+            s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+        }
+    }
+    __syncthreads();
+    if (!s_last) return;
+    // the last block: every other block has written its partial sum (and has read scal for the last time)
+    __threadfence();
+    const double rr = block_ordered_sum(partial, (int)gridDim.x, s_buf);
+    if (threadIdx.x == 0) {
+        *ticket = 0;
+        const double rz_old = __ldcg(scal + 2), bnorm = __ldcg(scal + 6), tol = __ldcg(scal + 7);
+        const double rel = sqrt(rr) / bnorm;  // ||r||2 / ||b||2
+        const int it = (int)__ldcg(scal + 9) + 1;
+        // [0] p.Ap [1] alpha [2] r.z [3] r.r [4] beta = r.z_new / r.z [5] stop [6] ||b|| [7] tolerance [8] ||r||/||b|| [9] iterations
+        const double v[10] = {pap_sum, alpha, rr, rr, rr / rz_old, (!isfinite(alpha) || !isfinite(rel) || rel <= tol) ? 1.0 : 0.0,
+                              bnorm,   tol,   rel, (double)it};
+        double *rec = host_ring + (size_t)(it % ring_slots) * 16;
+        for (int i = 0; i < 10; i++) scal[i] = v[i], rec[i] = v[i];
+        __threadfence_system();
     }
 }
 // x = 1*x + alpha*p (waxpby 1), r = 1*r + (-alpha)*Ap (waxpby 2), partial sums of r.r (dots 2 and 3) in one pass
@@ -100,9 +184,8 @@ __global__ void __launch_bounds__(kDotThreads) cg_update_kernel(const double *__
 // scal[9] counts the iterations), so that an iteration is kernels only and can be replayed as a CUDA graph
 __global__ void cg_beta_kernel(const double *__restrict__ partial, int count, double *__restrict__ scal, double *host_ring, int ring_slots) {
     if (scal[5] != 0.0) return;
-    double acc = 0.0;
-    for (int i = threadIdx.x; i < count; i += 32) acc = __dadd_rn(acc, partial[i]);
-    for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, o));
+    __shared__ double s_buf[kSumChunk];
+    const double acc = block_ordered_sum(partial, count, s_buf);
     if (threadIdx.x == 0) {
         const double rel = sqrt(acc) / scal[6];  // ||r||2 / ||b||2
         scal[3] = acc;
@@ -119,6 +202,8 @@ __global__ void cg_beta_kernel(const double *__restrict__ partial, int count, do
 }
 // p = 1*r + beta*p (waxpby 3) with beta taken from the device
 __global__ void cg_direction_kernel(const double *__restrict__ scal, const double *__restrict__ r, double *__restrict__ p, int64_t n) {
+    pdl_launch_dependents();  // (no-ops unless launched with programmatic stream serialization)
+    pdl_grid_dependency_wait();
     if (scal[5] != 0.0) return;
     const double beta = scal[4];
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -128,7 +213,11 @@ __global__ void cg_direction_kernel(const double *__restrict__ scal, const doubl
 
 struct DotScratch {
     double *partial = nullptr, *out = nullptr, *scal = nullptr;
+    double *partial2 = nullptr;       // r.r partial sums of the fused vector kernel (p.Ap's are still being read by other blocks)
+    unsigned int *ticket = nullptr;   // its "last block" counter (zero between launches)
     ~DotScratch() {
+        if (partial2) cudaFree(partial2);
+        if (ticket) cudaFree(ticket);
         if (partial) cudaFree(partial);
         if (out) cudaFree(out);
         if (scal) cudaFree(scal);
@@ -137,6 +226,9 @@ struct DotScratch {
         SPMVB_CUDA(cudaMalloc(&partial, kPartialCap * sizeof(double)));
         SPMVB_CUDA(cudaMalloc(&out, sizeof(double)));
         SPMVB_CUDA(cudaMalloc(&scal, 16 * sizeof(double)));
+        SPMVB_CUDA(cudaMalloc(&partial2, kPartialCap * sizeof(double)));
+        SPMVB_CUDA(cudaMalloc(&ticket, sizeof(unsigned int)));
+        SPMVB_CUDA(cudaMemset(ticket, 0, sizeof(unsigned int)));
         return SPMVB_OK;
     }
 };
@@ -144,7 +236,7 @@ struct DotScratch {
 static int dot_device(const double *u, const double *v, int64_t n, DotScratch &sc, double *host, cudaStream_t st) {
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + kDotThreads - 1) / kDotThreads, kDotBlocks));
     dot_partial_kernel<<<blocks, kDotThreads, 0, st>>>(u, v, n, sc.partial);
-    dot_final_kernel<<<1, 32, 0, st>>>(sc.partial, blocks, sc.out);
+    dot_final_kernel<<<1, 256, 0, st>>>(sc.partial, blocks, sc.out);
     SPMVB_CUDA(cudaMemcpyAsync(host, sc.out, sizeof(double), cudaMemcpyDeviceToHost, st));
     SPMVB_CUDA(cudaStreamSynchronize(st));
     return SPMVB_OK;
@@ -310,9 +402,31 @@ int spmvb_cg_solve(const spmvb_matrix *a, const double *b_dev, double *x_dev, in
         if (rc2 != SPMVB_OK) return rc2;
         fused_dot = fused.count != 0;
         if (!fused_dot) dot_partial_kernel<<<blocks, kDotThreads, 0, qs>>>(p, ap, n, sc.partial);
-        cg_alpha_kernel<<<1, 32, 0, qs>>>(sc.partial, fused_dot ? fused.count : blocks, sc.scal);
+        if (options().cg_fused_scalars) {
+            // one vector kernel: alpha at its head, beta / stop flag / record by its last block; it and the direction kernel are
+            // launched with programmatic stream serialization (their blocks take the places of the previous kernel's as those exit)
+            cudaLaunchAttribute pdl[1];
+            pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            pdl[0].val.programmaticStreamSerializationAllowed = 1;
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(blocks), cfg.blockDim = dim3(kDotThreads), cfg.stream = qs, cfg.attrs = pdl, cfg.numAttrs = options().cg_pdl ? 1 : 0;
+            const double *pap = nullptr;
+            int pap_count = 0;
+            if (options().cg_fused_scalars == 2) pap = sc.partial, pap_count = fused_dot ? fused.count : blocks;  // alpha at the head of every block
+            else cg_alpha_kernel<<<1, 256, 0, qs>>>(sc.partial, fused_dot ? fused.count : blocks, sc.scal);
+            if (cudaLaunchKernelEx(&cfg, cg_update_fused_kernel, sc.scal, (const double *)p, (const double *)ap, x_dev, r, n, pap, pap_count,
+                                   sc.partial2, sc.ticket, ring, (int)kRing) != cudaSuccess)
+                return fail(SPMVB_ERR_CUDA, "cg_solve: launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+            if (direction) {
+                cfg.gridDim = dim3(wblocks), cfg.blockDim = dim3(256);
+                if (cudaLaunchKernelEx(&cfg, cg_direction_kernel, (const double *)sc.scal, (const double *)r, p, n) != cudaSuccess)
+                    return fail(SPMVB_ERR_CUDA, "cg_solve: launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+            }
+            return SPMVB_OK;
+        }
+        cg_alpha_kernel<<<1, 256, 0, qs>>>(sc.partial, fused_dot ? fused.count : blocks, sc.scal);
         cg_update_kernel<<<blocks, kDotThreads, 0, qs>>>(sc.scal, p, ap, x_dev, r, n, sc.partial);
-        cg_beta_kernel<<<1, 32, 0, qs>>>(sc.partial, blocks, sc.scal, ring, kRing);
+        cg_beta_kernel<<<1, 256, 0, qs>>>(sc.partial, blocks, sc.scal, ring, kRing);
         if (direction) cg_direction_kernel<<<wblocks, 256, 0, qs>>>(sc.scal, r, p, n);
         return cudaGetLastError() == cudaSuccess ? SPMVB_OK : fail(SPMVB_ERR_CUDA, "cg_solve: launch failed");
     };

@@ -67,6 +67,40 @@ def test_cg_single_unknown_and_errors(sp, orc):
 
 
 @pytest.mark.parametrize("fmt", ["ell", "vt", "pattern", "hybrid"])
+def test_cg_three_launch_iteration_keeps_the_bits(sp, orc, fmt):
+    """"cg_fused_scalars": beta / stop flag / record by the last block of the vector kernel (1), alpha also formed at its head
+    by every block and both kernels launched with programmatic stream serialization (2), against the separate alpha and beta
+    kernels (0): the same reduction orders, so histories and solutions are bit-identical -- with and without the graph
+    replay, converging and capped runs, repeated solves (the ticket counter returns to zero)."""
+    g = (128, 12, 10) if fmt == "pattern" else (40, 9, 11)
+    m = sp.generate_matrix(sp.GridSpec(*g))
+    n = m.n
+    a = {"ell": lambda: sp.to_ell(m), "vt": lambda: sp.compress_values(m), "pattern": lambda: sp.compress_patterns(m, True),
+         "hybrid": lambda: sp.compress_patterns(sp.generate_matrix(sp.GridSpec(*g), perturb=(11, 0.1, 0.1)), True, min_pattern_rows=2)}[fmt]()
+    b = sp.DeviceVector(n)
+    sp.spmv_rows(sp.to_ell(m), sp.DeviceVector.from_host(np.ones(n)), b, 0, n)
+    try:
+        for graph in (1, 0):
+            sp.set_option("cg_graph", graph)
+            for cap, tol in ((300, 1e-10), (7, 1e-30), (1, 1e-30), (2, 1e-30)):
+                got = []
+                for fused in (1, 0, 2, 1):
+                    sp.set_option("cg_fused_scalars", fused)
+                    sp.set_option("cg_pdl", 1 if fused == 2 else 0)
+                    x, rep = sp.cg_solve(a, b, max_iterations=cap, tolerance=tol)
+                    got.append((x.to_host().view(np.uint64), rep))
+                for xb, rep in got[1:]:
+                    assert rep.iterations == got[0][1].iterations and rep.converged == got[0][1].converged
+                    assert rep.residual_history == got[0][1].residual_history and np.array_equal(xb, got[0][0])
+                if fmt != "hybrid" and cap == 300:
+                    assert got[0][1].converged
+    finally:
+        sp.set_option("cg_graph", 1)
+        sp.set_option("cg_fused_scalars", 1)
+        sp.set_option("cg_pdl", 0)
+
+
+@pytest.mark.parametrize("fmt", ["ell", "vt", "pattern", "hybrid"])
 def test_cg_iteration_replayed_as_a_graph(sp, orc, fmt):
     """After the first iteration cg_solve replays its iteration as a CUDA graph ("cg_graph"): the same kernels in the same
     order, so the report and the solution are bit-identical to direct launches, on every backend."""
