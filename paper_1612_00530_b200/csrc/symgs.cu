@@ -104,11 +104,19 @@ __device__ __forceinline__ void symgs_level_rect(int level, int nx, int ny, int 
     *n_iz = hi >= lo ? hi - lo + 1 : 0;
 }
 
+// Entry t of a level's enumeration: plane iz = iz_lo + t / w, and the (t % w)-th node of that plane's part of the level --
+// iy from max(0, ceil((level - 4 iz - (nx-1)) / 2)) upwards while ix = level - 2 iy - 4 iz stays >= 0.  A plane holds at most
+// w = min(ny, nx/2 + 2) nodes of a level, so the enumeration has w * n_iz entries (half of the (iy, iz) rectangle).
+__device__ __forceinline__ int symgs_width(int nx, int ny) { return min(ny, nx / 2 + 2); }
 __device__ __forceinline__ int symgs_row_of(int t, int level, int nx, int ny, int iz_lo, int n_iz) {
-    if (t >= ny * n_iz) return -1;
-    const int iy = t % ny, iz = iz_lo + t / ny;
-    const int ix = level - 2 * iy - 4 * iz;
-    if (ix < 0 || ix >= nx) return -1;
+    const int w = symgs_width(nx, ny);
+    if (t >= w * n_iz) return -1;
+    const int iz = iz_lo + t / w;
+    const int rest = level - 4 * iz;               // = ix + 2 iy
+    const int lo = rest - (nx - 1);                // 2 iy >= lo
+    const int iy = (lo > 0 ? (lo + 1) / 2 : 0) + t % w;
+    const int ix = rest - 2 * iy;
+    if (iy >= ny || ix < 0 || ix >= nx) return -1;
     return ix + nx * (iy + ny * iz);
 }
 
@@ -276,9 +284,10 @@ static int sweep_persistent(const spmvb_matrix *a, const spmvb_grid *g, double *
     if (!sd.coop) return 1;
     int nx = g->nx, ny = g->ny, nz = g->nz;
     {   // a thread owns at most one row per level: the widest level's (iy, iz) rectangle must fit the grid's threads
-        // (256^3: 49 k entries against 37,888 threads -- that sweep stays with the per-level launches)
+        // (256^3: 130 x 193 = 25 k entries against 37,888 threads)
         const int64_t span = std::min<int64_t>(nz, ((int64_t)(nx - 1) + 2 * (int64_t)(ny - 1)) / 4 + 2);
-        if ((int64_t)ny * span > (int64_t)sd.n_sm * kSymgsThreads) return 1;
+        const int64_t width = std::min<int64_t>(ny, nx / 2 + 2);  // symgs_width
+        if (width * span > (int64_t)sd.n_sm * kSymgsThreads) return 1;
     }
     int levels = (nx - 1) + 2 * (ny - 1) + 4 * (nz - 1) + 1;
     const auto *rs = static_cast<const int64_t *>(a->s[SPMVB_S_CSR_ROW_START]);
