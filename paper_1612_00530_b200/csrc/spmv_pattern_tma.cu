@@ -694,8 +694,8 @@ static int launch_ringp_t(const spmvb_matrix *a, PatternArgs &p_in, int chunk, c
 // Second translation unit (spmv_pattern_tma6.cu): the 6-planes-per-thread instantiations, so that the two halves build in parallel.
 // mode 0: chunk per CTA (with the ids-by-loads fallback); 1: per CTA, lab; 2: per warp, lab; 3-5: ablations.
 int launch_ring_q6(int mode, const spmvb_matrix *a, PatternArgs &p, int chunk, cudaStream_t st, int tile_lines) {
+    if (mode == 2) return launch_ringp_t<6, 4, 2, true>(a, p, chunk, st, tile_lines);  // a chunk per warp (strips that do not come in fours)
 #ifdef SPMVB_LAB
-    if (mode == 2) return launch_ringp_t<6, 4, 2, true>(a, p, chunk, st, tile_lines);
     if (mode == 3) return launch_ringp_t<6, 4, 2, true, 0, 6, true>(a, p, chunk, st, tile_lines);  // measurement only: no left-over columns
     if (mode == 4) return launch_ringp_t<6, 4, 2, true, 0, 3, true>(a, p, chunk, st, tile_lines);  // measurement only: fetch + store
     if (mode == 5) return launch_ringp_t<6, 4, 2, true, 0, 4, true>(a, p, chunk, st, tile_lines);  // measurement only: fetch
@@ -799,6 +799,23 @@ int launch_pattern_ring(int which, int lines, const spmvb_matrix *a, PatternArgs
             }
             rc = launch_ring_q4_dot(fours, a, p, chunk, st, tile_lines);  // cg_solve's request for x.y, when there is one
             if (rc != 1) return rc;
+            // 6 planes/thread with a chunk per warp (128^3 13.5 -> 12.8 us, 192^3 33.9 -> 32.4 us) when every warp of its full wave
+            // gets at least 4 steps (96^3 does not: 8.6 -> 10.4 us) and no exception block wants room beside it (C4: 41.9 -> 43.3 us)
+            if (!fours && tile_lines == 0 && a->n_exc == 0) {
+                static PerDevice<int> sm_dev;
+                int &sms = sm_dev.get();
+                if (sms == 0) {
+                    int dev = 0;
+                    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
+                }
+                const int64_t sz = (int64_t)p.sy * p.plane_lines;
+                const int64_t planes = ((int64_t)p.row_end - p.row_begin + sz - 1) / sz;
+                const int64_t steps6 = (int64_t)n_strips * ((planes + 5) / 6) * p.plane_lines;
+                if (steps6 >= 4LL * 2 * sms * kRingWarps) {
+                    rc = launch_ring_q6(2, a, p, chunk, st, 0);
+                    if (rc != 1) return rc;
+                }
+            }
             if (fours) {
                 rc = launch_ringp_t<4, 4, 3, true, 0, 0, true>(a, p, chunk, st, tile_lines);
                 return rc == 1 ? launch_ringp_t<4, 5, 3, false, 0, 0, true>(a, p, chunk, st, tile_lines) : rc;
