@@ -123,6 +123,8 @@ int spmvb_set_device(int device);
  *   "exception_kernel": hybrid handles, the exception-row block: 0 / 1 (default) the ELL kernel with a row map, all gathers of a
  *                     row requested in one batch; 64 / 32: the rows' operands come from three shared-memory windows of x per
  *                     64- / 32-row tile (csrc/spmv_exception.cu; measured slower on BASELINE config 4: 43 vs 34 us)
+ *   "exception_carveout": hybrid handles, the exception-block kernel's preferred shared-memory carve-out in percent of the SM's
+ *                     228 KB (0 = default 60, -1 = the driver's choice): fewer CTAs per SM, more L1 for the scattered gathers
  *   "exception_overlap": hybrid handles: 1 (default) the exception block runs on a second stream beside the kernel of the dictionary
  *                     rows (the two write disjoint rows of y; forked and joined by events, so the call still completes in
  *                     stream order); 0 one after the other

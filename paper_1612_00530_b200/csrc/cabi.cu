@@ -258,6 +258,7 @@ static int *option_slot(const char *key) {
     if (!strcmp(key, "ring_min_steps")) return &o.ring_min_steps;
     if (!strcmp(key, "exception_kernel")) return &o.exception_kernel;
     if (!strcmp(key, "exception_overlap")) return &o.exception_overlap;
+    if (!strcmp(key, "exception_carveout")) return &o.exception_carveout;
     if (!strcmp(key, "host_chunks")) return &o.host_chunks;
     if (!strcmp(key, "cg_keep_workspace")) return &o.cg_keep_workspace;
     if (!strcmp(key, "cg_fused_dot")) return &o.cg_fused_dot;

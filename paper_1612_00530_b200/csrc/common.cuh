@@ -143,6 +143,7 @@ struct Options {
     int box_prefetch_l1 = 0; // L1 prefetch distance in lines (0 = off)
     int debug_nochain = 0;   // measurement only
     int box_lines = 0;       // lines per CTA march of the tensor-ring kernel (0 = default)
+    int exception_carveout = 0; // hybrid format, exception block kernel: preferred shared-memory carve-out in percent (0 = default 60, -1 = the driver's choice): less shared memory = fewer CTAs per SM and more L1 for the scattered gathers
     int exception_overlap = 1; // hybrid format: 1 the exception block on a second stream beside the dictionary rows (fork / join by events), 0 one after the other
     int exception_kernel = 0; // hybrid format, exception rows: 0 / 1 the ELL kernel with a row map (all gathers of a row in one batch), 64 / 32 shared-memory windows of x with that tile height
     int ring_min_steps = 0;  // tensor ring: fewest line steps per chunk before the grid shrinks below a full wave (0 = default 4)

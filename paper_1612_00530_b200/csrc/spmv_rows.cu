@@ -55,7 +55,7 @@ __device__ __forceinline__ double vt_row(const int32_t *c, const int32_t *e, con
 // free for odd widths such as 27).  row_map != nullptr serves the exception block
 // of the hybrid pattern format: tile rows are exception slots, y goes to row_map[e].
 // =============================================================================
-template <int ROWS, bool BULK = false>
+template <int ROWS, bool BULK = false, bool MAP = false>  // MAP: the exception block's own instantiation (row_map != nullptr), so that it can carry its own cache carve-out
 __global__ void __launch_bounds__(ROWS) spmv_ell_kernel(const double *__restrict__ values,
                                                        const int32_t *__restrict__ columns, int width,
                                                        const double *__restrict__ x, int64_t x_col0,
@@ -290,6 +290,21 @@ int launch_ell(const double *values, const int32_t *columns, int width, const do
             else if (rows == 64) spmv_ell_kernel<64, true><<<nt, 64, bytes, st>>>(values, columns, width, x, x_col0, y, row_begin, row_end, t0, row_map, row_end);
             else
 #endif
+            if (row_map) {
+                static PerDevice<int> map_attr;
+                // The block's gathers are scattered (its rows are one grid row in ten), and what they hit in L1 they need not fetch
+                // from L2: with the driver's carve-out 17 CTAs of 12.9 KB leave ~30 KB of L1 per SM; 60 % of the SM's 228 KB for
+                // shared memory keeps 10 CTAs and 90 KB of L1 (block alone 34 -> 25-28 us, C4 overlapped 41.6 -> 38.8 us at 128^3;
+                // 35 % and below starve the kernel of CTAs).  "exception_carveout": percent, 0 = this default, -1 = the driver's.
+                const int opt = options().exception_carveout, carve = opt == 0 ? 60 : opt;
+                if (map_attr.get() != carve + 1) {
+                    SPMVB_CUDA(cudaFuncSetAttribute(spmv_ell_kernel<32, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+                    SPMVB_CUDA(cudaFuncSetAttribute(spmv_ell_kernel<32, true, true>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                                    carve > 0 ? carve : (int)cudaSharedmemCarveoutDefault));
+                    map_attr.get() = carve + 1;
+                }
+                spmv_ell_kernel<32, true, true><<<nt, 32, bytes, st>>>(values, columns, width, x, x_col0, y, row_begin, row_end, t0, row_map, row_end);
+            } else
             spmv_ell_kernel<32, true><<<nt, 32, bytes, st>>>(values, columns, width, x, x_col0, y, row_begin, row_end, t0, row_map, row_end);
             return check_launch("spmv_ell_bulk");
         }
