@@ -136,6 +136,9 @@ int spmvb_set_device(int device);
  *                     the last strip's warp sums it from its own shared-memory ring, 1 row by row from global memory after
  *                     the marches (the round-1 scheme; 256^3: 72.5 vs 69.7 us)
  *   "host_chunks":    row chunks of the pipelined spmvb_spmv_host (0 = default 8)
+ *   "host_stage":     1 (default) spmvb_spmv_host moves PAGEABLE host vectors through process-wide pinned bounce buffers, filled and
+ *                     drained by "host_copy_threads" host threads (0 = default 8) inside the same chunk pipeline; 0 leaves them to
+ *                     the driver's pageable copies.  Pinned (or registered) buffers are used in place either way
  *   "slab_graph":     1 (default) spmvb_slab_spmv replays its copies and launches as a CUDA graph; 0 launches directly
  *   "symgs_persistent": 1 (default) a symgs sweep is ONE cooperative launch: a CTA per SM walks the hyperplane levels with a
  *                     grid-wide barrier between them and fetches each row's matrix data ahead of the barrier; 0 a launch

@@ -61,6 +61,7 @@ void destroy(spmvb_matrix *a) {
     if (a->symgs_graph.capture_stream) cudaStreamDestroy(a->symgs_graph.capture_stream);
     for (auto &st : a->pipe_streams) if (st) cudaStreamDestroy(st);
     for (auto &ev : a->pipe_events) if (ev) cudaEventDestroy(ev);
+    for (auto &ev : a->pipe_out_events) if (ev) cudaEventDestroy(ev);
     if (a->exc_stream) cudaStreamDestroy(a->exc_stream);
     for (auto &ev : a->exc_events) if (ev) cudaEventDestroy(ev);
     if (a->d_masks) cudaFree(a->d_masks);
@@ -260,6 +261,8 @@ static int *option_slot(const char *key) {
     if (!strcmp(key, "exception_overlap")) return &o.exception_overlap;
     if (!strcmp(key, "exception_carveout")) return &o.exception_carveout;
     if (!strcmp(key, "host_chunks")) return &o.host_chunks;
+    if (!strcmp(key, "host_stage")) return &o.host_stage;
+    if (!strcmp(key, "host_copy_threads")) return &o.host_copy_threads;
     if (!strcmp(key, "cg_keep_workspace")) return &o.cg_keep_workspace;
     if (!strcmp(key, "cg_fused_dot")) return &o.cg_fused_dot;
     if (!strcmp(key, "cg_graph")) return &o.cg_graph;

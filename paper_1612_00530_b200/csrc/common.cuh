@@ -119,6 +119,7 @@ struct spmvb_matrix {
     // streams / events of the pipelined host-buffer SpMV (created on first use)
     mutable cudaStream_t pipe_streams[3] = {};
     mutable cudaEvent_t pipe_events[128] = {};
+    mutable cudaEvent_t pipe_out_events[64] = {};  // staged (pageable) y: one per chunk, the drain thread waits on them
     mutable cudaStream_t exc_stream = nullptr;  // hybrid handles: the exception block runs beside the dictionary rows (spmv_pattern.cu)
     mutable cudaEvent_t exc_events[2] = {};
     spmvb::BoxPlan box;
@@ -159,6 +160,8 @@ struct Options {
     int cg_fused_dot = 1;       // 1: cg_solve takes p.Ap from the SpMV kernel where that kernel offers it (pattern format, tensor ring)
     int last_cg_fused_dot = 0;  // read-only: 1 when the last iteration of the last cg_solve took p.Ap from the SpMV kernel
     int cg_keep_workspace = 1;  // 1: spmvb_cg_solve keeps its 3n work doubles on the handle until spmvb_free
+    int host_stage = 1;      // spmv_host: 1 pageable host vectors go through pinned bounce buffers filled / drained by host threads; 0 the driver's pageable copies
+    int host_copy_threads = 0; // ... that many copier threads (0 = default 8, at most the host's hardware threads)
     int host_chunks = 0;     // row chunks of the pipelined host-buffer SpMV (0 = default 8, at most 64)
     int last_pattern_kernel = 0;  // read-only: kernel family of the last pattern launch (1 List 1, 2 box v2, 3 box3, 4 lab, 9 tensor ring)
 };

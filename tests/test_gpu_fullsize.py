@@ -114,3 +114,40 @@ def test_reference_signature_call_with_pageable_vectors(sp, orc):
     with pytest.raises(sp.InvalidArgument):  # length mismatch
         d = sp.upload_pattern(ref.n, ref.table, ref.disp_offsets, ref.disp_flat, ref.ends_flat, ref.row_pattern, True)
         sp.check(sp.lib.spmvb_spmv_host(d.h, x.ctypes.data, ref.n - 1, np.empty(ref.n).ctypes.data))
+
+
+@pytest.mark.parametrize("g", [(128, 128, 64), (64, 64, 64), (128, 128, 65)])
+def test_pageable_host_vectors_are_staged(sp, orc, g):
+    """spmvb_spmv_host with pageable x / y ("host_stage"): pinned bounce buffers filled and drained by host threads inside the
+    chunk pipeline (>= 1 M rows) or around the plain copy-run-copy path -- the same bits as the driver's pageable copies and
+    as pinned buffers, for every format; repeated calls reuse the buffers."""
+    import torch
+    ref = orc.compress_patterns_grid(*g, values_in_pattern=True)
+    n = ref.n
+    x = orc.make_test_vector(n, orc.RANDOM, seed=SEED, lo=-1.0, hi=1.0)
+    y_ref = orc.spmv(ref, x, threads=os.cpu_count() or 1)
+    d = sp.upload_pattern(ref.n, ref.table, ref.disp_offsets, ref.disp_flat, ref.ends_flat, ref.row_pattern, True)
+    xp = torch.from_numpy(x).pin_memory()
+    yp = torch.empty(n, dtype=torch.float64).pin_memory()
+    try:
+        for stage, threads in ((1, 0), (1, 1), (1, 7), (0, 0), (1, 0)):
+            sp.set_option("host_stage", stage)
+            sp.set_option("host_copy_threads", threads)
+            y = np.full(n, np.nan)
+            sp.check(sp.lib.spmvb_spmv_host(d.h, x.ctypes.data, n, y.ctypes.data))            # pageable in, pageable out
+            assert int((bits(y) != bits(y_ref)).sum()) == 0, (stage, threads)
+            y2 = np.full(n, np.nan)
+            sp.check(sp.lib.spmvb_spmv_host(d.h, xp.data_ptr(), n, y2.ctypes.data))            # pinned in, pageable out
+            assert int((bits(y2) != bits(y_ref)).sum()) == 0
+            yp.fill_(float("nan"))
+            sp.check(sp.lib.spmvb_spmv_host(d.h, x.ctypes.data, n, yp.data_ptr()))             # pageable in, pinned out
+            assert int((bits(yp.numpy()) != bits(y_ref)).sum()) == 0
+    finally:
+        sp.set_option("host_stage", 1)
+        sp.set_option("host_copy_threads", 0)
+    ell = orc.to_ell(orc.generate_matrix(*g)) if n <= 300000 else None
+    if ell is not None:  # a format without a known reach: the plain path
+        de = sp.upload_ell(ell.n, ell.width, ell.nnz, ell.values, ell.columns)
+        y = np.full(n, np.nan)
+        sp.check(sp.lib.spmvb_spmv_host(de.h, x.ctypes.data, n, y.ctypes.data))
+        assert int((bits(y) != bits(orc.spmv(ell, x))).sum()) == 0
