@@ -133,8 +133,10 @@ int spmvb_set_device(int device);
  *                     places of the previous kernel's CTAs as those exit and wait (griddepcontrol.wait) for that kernel to
  *                     complete before touching global memory; 0 plain stream order
  *   "ring_leftover":  tensor ring, the one column past the last 64-column strip when 64 divides the line length: 0 (default)
- *                     the last strip's warp sums it from its own shared-memory ring, 1 row by row from global memory after
- *                     the marches (the round-1 scheme; 256^3: 72.5 vs 69.7 us)
+ *                     its operands travel in the last strip's shared-memory ring; in the chunk-per-CTA kernels that warp sets
+ *                     them aside per line and the whole CTA sums the column's rows at the end of a march (256^3: 66.7 -> 65.9 us,
+ *                     512^3: 596 -> 582 us), in the chunk-per-warp kernels the warp sums them step by step; 2 step by step
+ *                     everywhere; 1 row by row from global memory after the marches (the round-1 scheme; 256^3: 73.7 us)
  *   "host_chunks":    row chunks of the pipelined spmvb_spmv_host (0 = default 8)
  *   "host_stage":     1 (default) spmvb_spmv_host moves PAGEABLE host vectors through process-wide pinned bounce buffers, filled and
  *                     drained by "host_copy_threads" host threads (0 = default 8) inside the same chunk pipeline; 0 leaves them to

@@ -39,6 +39,9 @@ constexpr uint32_t kDzHiBits = 0x1FFu << 18;
 constexpr int kStripCols = 64;            // columns per warp
 constexpr int kBoxCols = kStripCols + 4;  // columns 64s-2 .. 64s+65 (the first and last are alignment padding)
 constexpr int kRingWarps = 4;
+#ifndef RING_LEFT_MODE
+#define RING_LEFT_MODE 1  // 1: the left-over column's rows are summed by the whole CTA at the end of a march (chunk-per-CTA kernels); 0: per step
+#endif
 
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap *tm, int c0, int c1, int c2, uint32_t bar) {
     asm volatile(
@@ -61,6 +64,9 @@ __device__ __forceinline__ double lds_f64(uint32_t addr) {
     return v;
 }
 __device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t v) { asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory"); }
+__device__ __forceinline__ void sts_f64x2(uint32_t addr, double2 v) {
+    asm volatile("st.shared.v2.f64 [%0], {%1,%2};" ::"r"(addr), "d"(v.x), "d"(v.y) : "memory");
+}
 
 constexpr int kIdBoxCols = kStripCols + 8;  // id box: columns 64s-4 .. 64s+67 (a 16-byte aligned start for 4-byte ids)
 
@@ -76,7 +82,13 @@ struct RingLayout {
     static constexpr uint32_t kRingBytes = kRingWarps * S * kSlotBytes;
     static constexpr uint32_t kBarBytes = kRingWarps * S * 8;
     static constexpr uint32_t kMaskBytes = ((kDictSmemPat + 1) * 4 + 15u) / 16u * 16u;  // one private copy of the mask table per warp
-    static constexpr uint32_t kTotal = kRingBytes + kBarBytes + kRingWarps * kMaskBytes + 128;  // + alignment slack
+    static constexpr uint32_t kBase = kRingBytes + kBarBytes + kRingWarps * kMaskBytes;
+    // Side buffer of the left-over column (chunk-per-CTA kernels, see the kernel): columns sy-2, sy-1 of the lines b0-1 .. b0+nb of a
+    // march, every plane of the set, 16 bytes each, and the nb x Q pattern ids of column sy-1.  A march is at most kLeftCap lines.
+    static constexpr int kLeftCap = Q >= 6 ? 46 : 16;
+    static constexpr uint32_t kLeftXBytes = (kLeftCap + 2) * P * 16;
+    static constexpr uint32_t kLeftBytes = (kLeftXBytes + kLeftCap * Q * 4 + 15u) / 16u * 16u;
+    static constexpr uint32_t kTotal = kBase + 128;  // + alignment slack
 };
 
 // Rare path of the direct variant, kept out of line so that its registers do not weigh on the main loop: the sums
@@ -198,6 +210,10 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
     const uint32_t ring = sbase + warp * (S * L::kSlotBytes);
     const uint32_t bars = sbase + L::kRingBytes + warp * (S * 8);
     const uint32_t s_masks = sbase + L::kRingBytes + L::kBarBytes + warp * L::kMaskBytes;  // this warp's copy; entry 0 serves id = -1
+    // left_in_ring == 2: the rows of the left-over column are summed by the whole CTA at the end of each march, from a side buffer
+    // that every thread helps to fill (cp.async) when the march begins -- nothing per step, no extra work on the last strip's warp
+    constexpr bool LFLUSH = RING_LEFT_MODE == 1 && IDT && DBG == 0 && CTAC;
+    const uint32_t s_left = sbase + L::kBase;
     // PDL: the next launch of the stream may take this CTA's place as soon as it exits; this launch, in turn, may have been
     // started while the kernel before it was still draining -- no global memory is touched before the wait below.
     pdl_launch_dependents();
@@ -252,11 +268,13 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
             // at the same time, so the halo planes the two groups share are read from DRAM once.
             b0 = (int)((u + (int64_t)(col_idx / (CTAC ? n_sg : n_strips)) * rot) % pl);
             nb = min(min(pl - u, pl - b0), s_end - s_pos);
+            if (LFLUSH && left_in_ring == 2) nb = min(nb, L::kLeftCap);  // what the side buffer holds (the chunk goes on with another march)
             s_pos += nb;
         }
         const int strip = CTAC ? (col_idx % n_sg) * kRingWarps + warp : col_idx % n_strips;
         const int c0 = c_lo + (col_idx / (CTAC ? n_sg : n_strips)) * Q;
-        if (CTAC && strip >= n_strips) continue;  // no such strip in this group
+        const bool cta_left = LFLUSH && left_in_ring == 2 && (col_idx % n_sg) == n_sg - 1;  // this CTA's strips end at column sy-2
+        if (!(CTAC && strip >= n_strips)) {  // (else: no such strip in this group)
         const int a_w = strip * kStripCols - 1;  // first column of the strip (odd; -1 for strip 0)
         const int n_sets = nb + 2;               // line sets b0-1 .. b0+nb
         auto issue = [&](int k) {  // elected lane: line set k of this march -> slot (gs + k) % S
@@ -300,7 +318,7 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
         // The left-over column sy-1 (64 | sy) rides with the last strip: its operands -- columns sy-2, sy-1 of the three lines,
         // box elements 64 and 65; column sy is outside the view -- are in this warp's ring already, and so is its id (element
         // 67 of the id box).  Lane q < Q sums the row of plane c0+q after the strip's own rows, one short chain per step.
-        const bool do_left = IDT && DBG == 0 && left_in_ring && strip == n_strips - 1;
+        const bool do_left = IDT && DBG == 0 && left_in_ring == 1 && strip == n_strips - 1;
         const int ql = min(lane, Q - 1);
         const int rowl0 = (int)((int64_t)(sy - 1) + (int64_t)sy * b0 + (int64_t)sz * (c0 + ql) - p.g0);
         const bool okl = do_left && lane < Q && c0 + ql <= c_hi;
@@ -325,6 +343,23 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
         for (int j = 0; j < nb; j++) {
             const int b = b0 + j;
             wait_set(j + 2);
+            // The last strip's warp keeps what the left-over column needs of each line set in the CTA's side buffer -- columns sy-2,
+            // sy-1 (box elements 64, 65) of every plane and the ids of column sy-1 (element 67 of the id box): loaded here, stored
+            // behind the id / mask look-ups below so that no latency is exposed; the rows are summed by the whole CTA after the march.
+            // (Fetching them from global memory instead -- 2 KB apart -- costs 3 us at 256^3, up front or spread over the steps alike.)
+            const bool lcopy = cta_left && strip == n_strips - 1;
+            double2 lx = make_double2(0.0, 0.0);
+            uint32_t lid = 0;
+            if (lcopy) {
+                if (j == 0) {
+#pragma unroll 1
+                    for (int k = 0; k < 2; k++) {
+                        const uint32_t src = ring + ((gs + k) % S) * L::kSlotBytes;
+                        sts_f64x2(s_left + (k * P + min(lane, P - 1)) * 16, lds_f64x2(src + min(lane, P - 1) * L::kLineBytes + 64 * 8));
+                        if (k == 1) sts_u32(s_left + L::kLeftXBytes + min(lane, Q - 1) * 4, lds_u32(src + L::kXBytes + min(lane, Q - 1) * L::kIdLineBytes + 67 * 4));
+                    }
+                }
+            }
             uint32_t sl[3];
 #pragma unroll
             for (int dy = 0; dy < 3; dy++) sl[dy] = ring + ((gs + j + dy) % S) * L::kSlotBytes + lane_off;
@@ -488,6 +523,12 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
                 y[rowl0 + j * sy] = accl;
                 if (DOT) dsum = __dadd_rn(dsum, __dmul_rn(accl, xcl));
             }
+            if (lcopy) {  // loaded here, stored behind the y stores below: the shared-memory stores then sit at the end of the step, next
+                          // to the fences of the refill, and leave the scheduling of the step's loads alone
+                const uint32_t src = ring + ((gs + j + 2) % S) * L::kSlotBytes;
+                lx = lds_f64x2(src + min(lane, P - 1) * L::kLineBytes + 64 * 8);
+                lid = lds_u32(src + L::kXBytes + min(lane, Q - 1) * L::kIdLineBytes + 67 * 4);
+            }
             // (16-byte stores of the aligned pairs (a+1, a+2) through a lane shuffle were measured slower: 81 vs 78 us)
 #pragma unroll
             for (int q = 0; q < Q; q++)
@@ -499,9 +540,54 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
                         // the row's own x entry is still in the ring (line b, plane q of the box + 1; the refill above took line b-1)
                         if (DOT) dsum = __dadd_rn(dsum, __dmul_rn(acc[q][i], lds_f64(sl[1] + (q + 1) * L::kLineBytes + 8 * (1 + i))));
                     }
+            if (lcopy) {
+                sts_f64x2(s_left + ((j + 2) * P + min(lane, P - 1)) * 16, lx);
+                if (j + 1 < nb) sts_u32(s_left + L::kLeftXBytes + ((j + 1) * Q + min(lane, Q - 1)) * 4, lid);
+            }
         }
         gs += n_sets;
         __syncwarp();
+        }
+        if (cta_left) {
+            // The rows of column sy-1 of this march, dealt out to all threads: same sums, same exactness rule as the strips' rows.
+            if (!masks_staged) {
+                for (int i = lane; i <= p.n_patterns; i += 32) sts_u32(s_masks + 4 * i, i == 0 ? 0u : p.masks[i - 1]);
+                masks_staged = true;
+            }
+            __syncthreads();
+            for (int t = threadIdx.x; t < nb * Q; t += kRingWarps * 32) {
+                const int idl = (int)lds_u32(s_left + L::kLeftXBytes + t * 4);
+                const int ll = t / Q, q = t - ll * Q;
+                const int line = b0 + ll, c = c0 + q;
+                const int rl = (int)((int64_t)(sy - 1) + (int64_t)sy * line + (int64_t)sz * c - p.g0);
+                if (idl < 0 || c > c_hi || (unsigned)(rl - rb) >= n_range) continue;
+                const uint32_t base = s_left + (ll * P + q) * 16;  // (line b0+ll-1, plane c-1): the row's entry dy = dz = -1
+                const double xcl = lds_f64x2(base + (P + 1) * 16).y;
+                double accl = 0.0;
+                if (cpos == 0) accl = __dadd_rn(accl, __dmul_rn(vc, xcl));
+#pragma unroll
+                for (int dz = 0; dz < 3; dz++)
+#pragma unroll
+                    for (int dy = 0; dy < 3; dy++) {
+                        const double2 u = lds_f64x2(base + (dy * P + dz) * 16);
+                        accl = OFF_NEG1 ? __dsub_rn(accl, u.x) : __dadd_rn(accl, __dmul_rn(vo, u.x));
+                        if (dz == 1 && dy == 1) {
+                            if (cpos == 2) accl = __dadd_rn(accl, __dmul_rn(vc, u.y));
+                        } else {
+                            accl = OFF_NEG1 ? __dsub_rn(accl, u.y) : __dadd_rn(accl, __dmul_rn(vo, u.y));
+                        }
+                    }
+                if (cpos == 1) accl = __dadd_rn(accl, __dmul_rn(vc, xcl));
+                const uint32_t exp_l = c >= np_x ? 0u
+                                                 : (kFullBox & ~(kRBits | (c == 0 ? kDzLoBits : 0u) | (c == np_x - 1 ? kDzHiBits : 0u) |
+                                                                 (line == 0 ? kDyLoBits : 0u) | (line == pl - 1 ? kDyHiBits : 0u)));
+                // any other row shape (or entries outside the view): List 1 as written
+                if (lds_u32(s_masks + 4 + 4 * idl) != exp_l) accl = pattern_row_cold(p, idl, (int64_t)rl + p.g0);
+                y[rl] = accl;
+                if (DOT) dsum = __dadd_rn(dsum, __dmul_rn(accl, xcl));
+            }
+            __syncthreads();  // the buffer is free for the next march
+        }
     }
     {  // this warp's share of the left-over columns (after its marches: the warps do not finish in step, so these
        // latency-bound gathers overlap with the marches of the others)
@@ -622,8 +708,12 @@ static int launch_ringp_t(const spmvb_matrix *a, PatternArgs &p_in, int chunk, c
     if (p.sy - (n_strips * kStripCols - 1) > 2) n_strips++;
     int left_lo = std::min(p.sy, n_strips * kStripCols - 1);
     // one left-over column (64 | sy) and ids through the ring: the last strip's warp sums it from its own ring
-    const int left_in_ring = (IDT && DBG == 0 && p.sy - left_lo == 1 && options().ring_leftover != 1) ? 1 : 0;
+    int left_in_ring = (IDT && DBG == 0 && p.sy - left_lo == 1 && options().ring_leftover != 1) ? 1 : 0;
     if (left_in_ring) left_lo = p.sy;
+    // ... or, in the chunk-per-CTA kernels, the whole CTA sums it at the end of each march (2; ring_leftover = 2 keeps the per-step sums)
+    constexpr bool kFlush = RING_LEFT_MODE == 1 && IDT && DBG == 0 && CTAC;
+    if (kFlush && left_in_ring && options().ring_leftover != 2 && tile_lines <= L::kLeftCap) left_in_ring = 2;
+    constexpr uint32_t kSmem = L::kTotal + (kFlush ? L::kLeftBytes : 0u);
     const int n_cols = CTAC ? (n_strips + kRingWarps - 1) / kRingWarps : n_strips;
     const int units = CTAC ? 1 : kRingWarps;  // chunks per CTA
     const int64_t total64 = (int64_t)n_cols * ((c_hi - c_lo + Q) / Q) * p.plane_lines;
@@ -646,9 +736,9 @@ static int launch_ringp_t(const spmvb_matrix *a, PatternArgs &p_in, int chunk, c
         int &per_sm = per_sm_dev.get();                                                                                          \
         if (per_sm == 0) {                                                                                                       \
             if (cudaFuncSetAttribute(spmv_pattern_ringp_kernel<Q, S, MINB, NEG, CP, IDT, PFD, DBG, CTAC, DOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                     (int)L::kTotal) != cudaSuccess ||                                                           \
+                                     (int)kSmem) != cudaSuccess ||                                                               \
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmv_pattern_ringp_kernel<Q, S, MINB, NEG, CP, IDT, PFD, DBG, CTAC, DOT>,      \
-                                                              kRingWarps * 32, L::kTotal) != cudaSuccess || per_sm <= 0)         \
+                                                              kRingWarps * 32, kSmem) != cudaSuccess || per_sm <= 0)             \
                 return -1;                                                                                                       \
         }                                                                                                                        \
         int grid = n_sm * per_sm;                                                                                                \
@@ -672,7 +762,7 @@ static int launch_ringp_t(const spmvb_matrix *a, PatternArgs &p_in, int chunk, c
         cudaLaunchConfig_t cfg = {};                                                                                             \
         cfg.gridDim = dim3(grid);                                                                                                \
         cfg.blockDim = dim3(kRingWarps * 32);                                                                                    \
-        cfg.dynamicSmemBytes = L::kTotal;                                                                                        \
+        cfg.dynamicSmemBytes = kSmem;                                                                                            \
         cfg.stream = st;                                                                                                         \
         cudaLaunchAttribute pdl[1];                                                                                              \
         pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;                                                          \

@@ -43,6 +43,23 @@ def test_ring_march_lengths(sp, orc, lines):
     assert np.array_equal(bits(ring_run(sp, up_pat(sp, pc), x, 90, lines)), bits(orc.spmv(pc, x)))
 
 
+@pytest.mark.parametrize("leftover", [0, 1, 2])
+@pytest.mark.parametrize("march,lines", [(90, 0), (90, 100), (90, 47), (108, 16), (108, 40), (110, 0)])
+def test_ring_leftover_column_schemes(sp, orc, leftover, march, lines):
+    """64 | nx: column nx-1 lies past the last strip.  Chunk-per-CTA kernels gather its operands per line and sum its rows
+    after the march (marches longer than the side buffer are split; tiles longer than it keep the per-step sums); option
+    ring_leftover = 2 forces the per-step sums, 1 the row-by-row tail.  Every scheme is the oracle's List 1 bit for bit."""
+    m = orc.generate_matrix(256, 100, 9)
+    pc = orc.compress_patterns(m, True)
+    x = orc.make_test_vector(m.n, orc.RANDOM, seed=8, lo=-1.0, hi=1.0)
+    sp.set_option("ring_leftover", leftover)
+    try:
+        y = ring_run(sp, up_pat(sp, pc), x, march, lines)
+    finally:
+        sp.set_option("ring_leftover", 0)
+    assert np.array_equal(bits(y), bits(orc.spmv(pc, x)))
+
+
 @pytest.mark.parametrize("march", [90, 108])
 def test_ring_ragged_ranges(sp, orc, march):
     """Partitions at arbitrary (even and odd) rows give the single-call result; other rows stay untouched."""
