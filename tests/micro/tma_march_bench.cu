@@ -52,6 +52,9 @@ __global__ void __launch_bounds__(128, MINB)
     const uint32_t base = (smem_u32(raw) + 127u) & ~127u;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t ring = base + warp * S * SLOT, bars = base + 4 * S * SLOT + warp * S * 8;
+    // do_store == 2: y staged in shared memory (two buffers of Q x 512 B per warp) and written by bulk copies (aligned columns 64s .. 64s+63)
+    const uint32_t stage = base + 4 * S * SLOT + 4 * S * 8 + 128 + warp * (2 * Q * 512);
+    uint32_t n_st = 0;
     if (lane == 0) {
         for (int s = 0; s < S; s++) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bars + 8 * s));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -97,7 +100,25 @@ __global__ void __launch_bounds__(128, MINB)
                 mbar_wait(bars + 8 * ((gs + j + 2) % S), ((gs + j + 2) / S) & 1);
                 double v;
                 asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(ring + ((gs + j + 1) % S) * SLOT + lane * 16 + 8));
-                if (do_store) {
+                if (do_store == 2) {
+                    const uint32_t buf = stage + (n_st & 1) * (Q * 512);
+                    if (n_st >= 2) {
+                        if (lane < Q) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                        __syncwarp();
+                    }
+#pragma unroll
+                    for (int q = 0; q < Q; q++) asm volatile("st.shared.v2.f64 [%0], {%1,%2};" ::"r"(buf + q * 512 + lane * 16), "d"(v), "d"(v) : "memory");
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncwarp();
+                    if (lane < Q) {
+                        const int q = lane;
+                        const int64_t r = MODE == 0 ? (a_w + 1) + (int64_t)sy * (m0 + j) + sz * (blk * Q + q) : (a_w + 1) + (int64_t)sy * (blk * Q + q) + sz * (m0 + j);
+                        const bool lok = MODE == 0 ? blk * Q + q < np : blk * Q + q < pl;
+                        if (lok) asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 512;" ::"l"(y + r), "r"(buf + q * 512) : "memory");
+                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    }
+                    n_st++;
+                } else if (do_store) {
 #pragma unroll
                     for (int q = 0; q < Q; q++) {
                         const int64_t r = MODE == 0 ? a + (int64_t)sy * (m0 + j) + sz * (blk * Q + q) : a + (int64_t)sy * (blk * Q + q) + sz * (m0 + j);
@@ -119,6 +140,7 @@ __global__ void __launch_bounds__(128, MINB)
         pos += nb;
         __syncwarp();
     }
+    if (do_store == 2 && lane < Q) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     if (sink == 1.2345e-300) y[0] = sink;
 }
 
@@ -141,7 +163,7 @@ int main(int argc, char **argv) {
     Enc enc = reinterpret_cast<Enc>(fn);
     int n_sm = 0;
     CK(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0));
-    const size_t smem = 4 * S * SLOT + 4 * S * 8 + 128;
+    const size_t smem = 4 * S * SLOT + 4 * S * 8 + 128 + 128 + 4 * 2 * Q * 512;
     for (int mode = 0; mode < 2; mode++) {
         CUtensorMap tx, ti;
         const cuuint64_t dims[3] = {(cuuint64_t)sy, (cuuint64_t)pl, (cuuint64_t)np};
@@ -163,7 +185,7 @@ int main(int argc, char **argv) {
         const int n_sg = (sy + 255) / 256;
         const int n_units = n_sg * ((mode ? pl : np) + Q - 1) / Q, march_len = mode ? np : pl;
         const int total = n_units * march_len;
-        for (int store = 0; store < 2; store++)
+        for (int store = 0; store < 3; store++)
             for (int sched = 0; sched < 6; sched++) {
                 int persistent = sched == 0, chunk, grid;
                 if (persistent) {
@@ -186,7 +208,7 @@ int main(int argc, char **argv) {
                 float ms;
                 CK(cudaEventElapsedTime(&ms, e0, e1));
                 const double us = ms * 1e3 / reps, bytes = (double)n * (store ? 20 : 12);
-                printf("mode %c %-11s %s  grid %5d chunk %4d: %8.1f us  %7.1f GB/s algorithmic\n", mode ? 'Z' : 'Y', store ? "fetch+store" : "fetch only",
+                printf("mode %c %-11s %s  grid %5d chunk %4d: %8.1f us  %7.1f GB/s algorithmic\n", mode ? 'Z' : 'Y', store == 2 ? "fetch+bulkst" : store ? "fetch+store" : "fetch only",
                        persistent ? "persistent" : "tiles     ", grid, chunk, us, bytes / us / 1e3);
             }
     }
