@@ -256,6 +256,7 @@ static int *option_slot(const char *key) {
     if (!strcmp(key, "box_lines")) return &o.box_lines;
     if (!strcmp(key, "ring_leftover")) return &o.ring_leftover;
     if (!strcmp(key, "ring_pdl")) return &o.ring_pdl;
+    if (!strcmp(key, "ring_two_lines")) return &o.ring_two_lines;
     if (!strcmp(key, "ring_min_steps")) return &o.ring_min_steps;
     if (!strcmp(key, "exception_kernel")) return &o.exception_kernel;
     if (!strcmp(key, "exception_overlap")) return &o.exception_overlap;
@@ -282,7 +283,7 @@ static int *option_slot(const char *key) {
 static bool lab_only_value(const char *key, int value) {
     if (kLabBuild) return false;
     if (!strcmp(key, "box_march")) {
-        for (int ok : {0, 3, 90, 101, 107, 108, 109, 110})
+        for (int ok : {0, 3, 90, 101, 107, 108, 109, 110, 111, 112})
             if (value == ok) return false;
         return true;
     }

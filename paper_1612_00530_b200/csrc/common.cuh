@@ -148,6 +148,7 @@ struct Options {
     int exception_overlap = 1; // hybrid format: 1 the exception block on a second stream beside the dictionary rows (fork / join by events), 0 one after the other
     int exception_kernel = 0; // hybrid format, exception rows: 0 / 1 the ELL kernel with a row map (all gathers of a row in one batch), 64 / 32 shared-memory windows of x with that tile height
     int ring_min_steps = 0;  // tensor ring: fewest line steps per chunk before the grid shrinks below a full wave (0 = default 4)
+    int ring_two_lines = 1;  // tensor ring, x far beyond L2 and strips in fours: two lines per step (0: one, as everywhere else)
     int ring_pdl = 1;        // tensor ring launched with programmatic stream serialization (its preamble overlaps the previous kernel's tail)
     int ring_leftover = 0;   // tensor ring, left-over column (64 | sy): 0 summed by the last strip's warp from its ring, 1 row by row after the marches
     int slab_graph = 1;         // 1: spmvb_slab_spmv records its exchange copies and launches into a CUDA graph and replays it

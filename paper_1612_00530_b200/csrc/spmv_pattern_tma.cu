@@ -70,7 +70,7 @@ __device__ __forceinline__ void sts_f64x2(uint32_t addr, double2 v) {
 
 constexpr int kIdBoxCols = kStripCols + 8;  // id box: columns 64s-4 .. 64s+67 (a 16-byte aligned start for 4-byte ids)
 
-template <int Q, int S, bool IDT>
+template <int Q, int S, bool IDT, int LPS = 1>
 struct RingLayout {
     static constexpr int P = Q + 2;
     static constexpr uint32_t kLineBytes = kBoxCols * 8;                    // one plane of a line set of x
@@ -85,7 +85,7 @@ struct RingLayout {
     static constexpr uint32_t kBase = kRingBytes + kBarBytes + kRingWarps * kMaskBytes;
     // Side buffer of the left-over column (chunk-per-CTA kernels, see the kernel): columns sy-2, sy-1 of the lines b0-1 .. b0+nb of a
     // march, every plane of the set, 16 bytes each, and the nb x Q pattern ids of column sy-1.  A march is at most kLeftCap lines.
-    static constexpr int kLeftCap = Q >= 6 ? 46 : 16;
+    static constexpr int kLeftCap = Q >= 6 ? 46 : LPS == 2 ? 28 : 16;
     static constexpr uint32_t kLeftXBytes = (kLeftCap + 2) * P * 16;
     static constexpr uint32_t kLeftBytes = (kLeftXBytes + kLeftCap * Q * 4 + 15u) / 16u * 16u;
     static constexpr uint32_t kTotal = kBase + 128;  // + alignment slack
@@ -192,13 +192,14 @@ __device__ __forceinline__ double ring_leftover_row(const PatternArgs &p, uint32
     }
 }
 
-template <int Q, int S, int MINB, bool OFF_NEG1, int CENTER_POS, bool IDT, int PFD = 0, int DBG = 0, bool CTAC = false, bool DOT = false>
+template <int Q, int S, int MINB, bool OFF_NEG1, int CENTER_POS, bool IDT, int PFD = 0, int DBG = 0, bool CTAC = false, bool DOT = false, int LPS = 1>
 __global__ void __launch_bounds__(kRingWarps * 32, MINB)
     spmv_pattern_ringp_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm_ids, PatternArgs p, int c_lo,
                               int c_hi, int np_x, int n_strips, int left_lo, int left_in_ring, int id_plane0, int total_steps, int steps_per_warp,
                               int steps_rem, int tile_lines, int rot) {
-    using L = RingLayout<Q, S, IDT>;
+    using L = RingLayout<Q, S, IDT, LPS>;
     constexpr int P = L::P;
+    static_assert(LPS == 1 || (LPS == 2 && IDT && CTAC && DBG == 0 && PFD == 0 && S >= 6), "two lines per step: chunk-per-CTA kernels with the ids in the ring");
     const int cpos = CENTER_POS >= 0 ? CENTER_POS : p.center_pos;  // CENTER_POS = -1: the general variant reads it at run time
     extern __shared__ unsigned char smem_raw[];
     const uint32_t sbase = (smem_u32(smem_raw) + 127u) & ~127u;
@@ -339,6 +340,177 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
         auto wait_set = [&](int k) { mbar_wait(bars + 8 * ((gs + k) % S), ((gs + k) / S) & 1); };
         wait_set(0);
         wait_set(1);
+        if constexpr (LPS == 2) {
+        // Two lines per step: the rows of lines b and b+1 (2 x Q x 2 per thread) from the line sets b-1 .. b+2 -- every operand quad
+        // taken from shared memory serves both lines, 8 x P loads for 4Q rows instead of 6 x P for 2Q (the shared-memory data path
+        // is this kernel's busiest unit).  A row still meets its entries in ascending (plane, line, column) order.  An odd march
+        // ends with a step whose second line does not exist: computed on whatever the ring holds, never stored.
+#pragma unroll 1
+        for (int j = 0; j < nb; j += 2) {
+            const int b = b0 + j;
+            const bool two = j + 1 < nb;  // warp-uniform
+            wait_set(j + 2);
+            if (two) wait_set(j + 3);
+            const bool lcopy = cta_left && strip == n_strips - 1;
+            if (lcopy && j == 0) {
+#pragma unroll 1
+                for (int k = 0; k < 2; k++) {
+                    const uint32_t src = ring + ((gs + k) % S) * L::kSlotBytes;
+                    sts_f64x2(s_left + (k * P + min(lane, P - 1)) * 16, lds_f64x2(src + min(lane, P - 1) * L::kLineBytes + 64 * 8));
+                    if (k == 1) sts_u32(s_left + L::kLeftXBytes + min(lane, Q - 1) * 4, lds_u32(src + L::kXBytes + min(lane, Q - 1) * L::kIdLineBytes + 67 * 4));
+                }
+            }
+            uint32_t sl[4];
+#pragma unroll
+            for (int dy = 0; dy < 4; dy++) sl[dy] = ring + ((gs + j + dy) % S) * L::kSlotBytes + lane_off;
+            int id[2][Q][2];
+            uint32_t bad = 0;
+            uint32_t in_b[2];
+#pragma unroll
+            for (int ln = 0; ln < 2; ln++) {
+                in_b[ln] = ~((b + ln == 0 ? kDyLoBits : 0u) | (b + ln == pl - 1 ? kDyHiBits : 0u));
+#pragma unroll
+                for (int q = 0; q < Q; q++)
+#pragma unroll
+                    for (int i = 0; i < 2; i++) {
+                        const int r = row0 + q * sz + (j + ln) * sy + i;
+                        const int v = (int)lds_u32(sl[1 + ln] - lane_off + L::kXBytes + q * L::kIdLineBytes + (3 + 2 * lane + i) * 4);
+                        id[ln][q][i] = (ok[q][i] && (ln == 0 || two) && (unsigned)(r - rb) < n_range) ? v : -1;
+                        bad |= lds_u32(s_masks + 4 + 4 * id[ln][q][i]) ^ (expect[q][i] & in_b[ln]);  // id -1 reads entry 0 = 0
+                    }
+            }
+            double acc[2][Q][2], xc[2][Q][2];
+            {
+#pragma unroll
+                for (int ln = 0; ln < 2; ln++)
+#pragma unroll
+                    for (int q = 0; q < Q; q++) acc[ln][q][0] = acc[ln][q][1] = 0.0, xc[ln][q][0] = xc[ln][q][1] = 0.0;
+                if (cpos == 0) {
+#pragma unroll
+                    for (int ln = 0; ln < 2; ln++)
+#pragma unroll
+                        for (int q = 0; q < Q; q++) {
+                            const double2 u = lds_f64x2(sl[1 + ln] + (q + 1) * L::kLineBytes), v = lds_f64x2(sl[1 + ln] + (q + 1) * L::kLineBytes + 16);
+                            acc[ln][q][0] = __dadd_rn(acc[ln][q][0], __dmul_rn(vc, u.y));
+                            acc[ln][q][1] = __dadd_rn(acc[ln][q][1], __dmul_rn(vc, v.x));
+                        }
+                }
+                double e[2][4][4];  // [buffer][line b-1 .. b+2][columns a-1 .. a+2]
+                auto load_plane = [&](int buf, int pz) {
+#pragma unroll
+                    for (int ll = 0; ll < 4; ll++) {
+                        const double2 u = lds_f64x2(sl[ll] + pz * L::kLineBytes), v = lds_f64x2(sl[ll] + pz * L::kLineBytes + 16);
+                        e[buf][ll][0] = u.x, e[buf][ll][1] = u.y, e[buf][ll][2] = v.x, e[buf][ll][3] = v.y;
+                    }
+                };
+                load_plane(0, 0);
+#pragma unroll
+                for (int pz = 0; pz < P; pz++) {
+                    if (pz + 1 < P) load_plane((pz + 1) & 1, pz + 1);
+#pragma unroll
+                    for (int ll = 0; ll < 4; ll++)
+#pragma unroll
+                        for (int ln = 0; ln < 2; ln++) {
+                            const int dy = ll - ln;
+                            if (dy < 0 || dy > 2) continue;
+#pragma unroll
+                            for (int dx = 0; dx < 3; dx++)
+#pragma unroll
+                                for (int q = 0; q < Q; q++) {
+                                    const int dz = pz - q;
+                                    if (dz < 0 || dz > 2) continue;
+                                    const int t = dz * 9 + dy * 3 + dx;
+#pragma unroll
+                                    for (int i = 0; i < 2; i++) {
+                                        const double ev = e[pz & 1][ll][i + dx];
+                                        if (t == 13) {
+                                            xc[ln][q][i] = ev;
+                                            if (cpos == 2) acc[ln][q][i] = __dadd_rn(acc[ln][q][i], __dmul_rn(vc, ev));
+                                        } else if (OFF_NEG1) {
+                                            acc[ln][q][i] = __dsub_rn(acc[ln][q][i], ev);
+                                        } else {
+                                            acc[ln][q][i] = __dadd_rn(acc[ln][q][i], __dmul_rn(vo, ev));
+                                        }
+                                    }
+                                }
+                        }
+                }
+                if (cpos == 1) {
+#pragma unroll
+                    for (int ln = 0; ln < 2; ln++)
+#pragma unroll
+                        for (int q = 0; q < Q; q++)
+#pragma unroll
+                            for (int i = 0; i < 2; i++) acc[ln][q][i] = __dadd_rn(acc[ln][q][i], __dmul_rn(vc, xc[ln][q][i]));
+                }
+            }
+            if (__any_sync(0xffffffffu, bad != 0)) {  // see the one-line step below: masked sub-boxes, then List 1
+#pragma unroll 1
+                for (int ln = 0; ln < (two ? 2 : 1); ln++) {
+                    uint32_t mk[Q * 2];
+                    int idl_[Q * 2];
+                    bool real = false;
+#pragma unroll
+                    for (int q = 0; q < Q; q++)
+#pragma unroll
+                        for (int i = 0; i < 2; i++) {
+                            idl_[q * 2 + i] = ln == 0 ? id[0][q][i] : id[1][q][i];
+                            mk[q * 2 + i] = lds_u32(s_masks + 4 + 4 * idl_[q * 2 + i]);
+                            real = real || (idl_[q * 2 + i] >= 0 && mk[q * 2 + i] != (expect[q][i] & in_b[ln]));
+                        }
+                    if (__any_sync(0xffffffffu, real)) {
+                        double am[Q * 2];
+                        ring_masked_step<Q, OFF_NEG1, CENTER_POS, L::kLineBytes>(ln == 0 ? sl[0] : sl[1], ln == 0 ? sl[1] : sl[2], ln == 0 ? sl[2] : sl[3], mk, vc, vo, am,
+                                                                                  p.center_pos);
+#pragma unroll
+                        for (int q = 0; q < Q; q++)
+#pragma unroll
+                            for (int i = 0; i < 2; i++) {
+                                const uint32_t m = mk[q * 2 + i];
+                                if (idl_[q * 2 + i] >= 0 && (m == kGenericMask || (m & ~(expect[q][i] & in_b[ln])) != 0))
+                                    am[q * 2 + i] = pattern_row_cold(p, idl_[q * 2 + i], xi0 + (int64_t)(j + ln) * sy + (int64_t)q * sz + i);
+                                if (ln == 0) acc[0][q][i] = am[q * 2 + i];
+                                else acc[1][q][i] = am[q * 2 + i];
+                            }
+                    }
+                }
+            }
+            double2 lx[2];
+            uint32_t lid[2];
+            if (lcopy) {  // what the left-over column needs of the two new line sets, before their predecessors' slots are refilled
+#pragma unroll
+                for (int k = 0; k < 2; k++) {
+                    const uint32_t src = ring + ((gs + j + 2 + k) % S) * L::kSlotBytes;
+                    lx[k] = lds_f64x2(src + min(lane, P - 1) * L::kLineBytes + 64 * 8);
+                    lid[k] = lds_u32(src + L::kXBytes + min(lane, Q - 1) * L::kIdLineBytes + 67 * 4);
+                }
+            }
+            __syncwarp();  // every lane is done with the slots of lines b-1 and b
+            if (lane == 0) {
+                fence_proxy_async();  // generic-proxy reads before the async-proxy refill
+                if (j + S < n_sets) issue(j + S);
+                if (j + S + 1 < n_sets) issue(j + S + 1);
+            }
+#pragma unroll
+            for (int ln = 0; ln < 2; ln++)
+#pragma unroll
+                for (int q = 0; q < Q; q++)
+#pragma unroll
+                    for (int i = 0; i < 2; i++)
+                        if (id[ln][q][i] >= 0) {
+                            y[row0 + q * sz + (j + ln) * sy + i] = acc[ln][q][i];
+                            if (DOT) dsum = __dadd_rn(dsum, __dmul_rn(acc[ln][q][i], xc[ln][q][i]));  // the centre operand is the row's own x entry
+                        }
+            if (lcopy) {
+                sts_f64x2(s_left + ((j + 2) * P + min(lane, P - 1)) * 16, lx[0]);
+                if (j + 1 < nb) sts_u32(s_left + L::kLeftXBytes + ((j + 1) * Q + min(lane, Q - 1)) * 4, lid[0]);
+                if (two) {
+                    sts_f64x2(s_left + ((j + 3) * P + min(lane, P - 1)) * 16, lx[1]);
+                    if (j + 2 < nb) sts_u32(s_left + L::kLeftXBytes + ((j + 2) * Q + min(lane, Q - 1)) * 4, lid[1]);
+                }
+            }
+        }
+        } else {
 #pragma unroll 1
         for (int j = 0; j < nb; j++) {
             const int b = b0 + j;
@@ -545,6 +717,7 @@ __global__ void __launch_bounds__(kRingWarps * 32, MINB)
                 if (j + 1 < nb) sts_u32(s_left + L::kLeftXBytes + ((j + 1) * Q + min(lane, Q - 1)) * 4, lid);
             }
         }
+        }  // LPS
         gs += n_sets;
         __syncwarp();
         }
@@ -686,10 +859,10 @@ static bool ids_view_ok(const spmvb_matrix *a, const PatternArgs &p) {
     return p.g0 >= 0 && p.g0 % sz == 0 && (int64_t)a->n % sz == 0 && p.sy % 4 == 0 && (uintptr_t)p.ids % 16 == 0;
 }
 
-template <int Q, int S, int MINB, bool IDT, int PFD = 0, int DBG = 0, bool CTAC = false, bool DOT = false>
+template <int Q, int S, int MINB, bool IDT, int PFD = 0, int DBG = 0, bool CTAC = false, bool DOT = false, int LPS = 1>
 static int launch_ringp_t(const spmvb_matrix *a, PatternArgs &p_in, int chunk, cudaStream_t st, int tile_lines = 0) {
     PatternArgs p = clip_view(a, p_in);
-    using L = RingLayout<Q, S, IDT>;
+    using L = RingLayout<Q, S, IDT, LPS>;
     const bool neg1 = p.v_off == -1.0;
     const int cp = a->box.center_pos;
     if (IDT && !ids_view_ok(a, p)) return 1;
@@ -713,6 +886,7 @@ static int launch_ringp_t(const spmvb_matrix *a, PatternArgs &p_in, int chunk, c
     // ... or, in the chunk-per-CTA kernels, the whole CTA sums it at the end of each march (2; ring_leftover = 2 keeps the per-step sums)
     constexpr bool kFlush = RING_LEFT_MODE == 1 && IDT && DBG == 0 && CTAC;
     if (kFlush && left_in_ring && options().ring_leftover != 2 && tile_lines <= L::kLeftCap) left_in_ring = 2;
+    if (LPS == 2 && left_in_ring == 1) return 1;  // the two-line step does not carry the per-step sums of the left-over column
     constexpr uint32_t kSmem = L::kTotal + (kFlush ? L::kLeftBytes : 0u);
     const int n_cols = CTAC ? (n_strips + kRingWarps - 1) / kRingWarps : n_strips;
     const int units = CTAC ? 1 : kRingWarps;  // chunks per CTA
@@ -735,9 +909,9 @@ static int launch_ringp_t(const spmvb_matrix *a, PatternArgs &p_in, int chunk, c
         static PerDevice<int> per_sm_dev;                                                                                        \
         int &per_sm = per_sm_dev.get();                                                                                          \
         if (per_sm == 0) {                                                                                                       \
-            if (cudaFuncSetAttribute(spmv_pattern_ringp_kernel<Q, S, MINB, NEG, CP, IDT, PFD, DBG, CTAC, DOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+            if (cudaFuncSetAttribute(spmv_pattern_ringp_kernel<Q, S, MINB, NEG, CP, IDT, PFD, DBG, CTAC, DOT, LPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                      (int)kSmem) != cudaSuccess ||                                                               \
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmv_pattern_ringp_kernel<Q, S, MINB, NEG, CP, IDT, PFD, DBG, CTAC, DOT>,      \
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, spmv_pattern_ringp_kernel<Q, S, MINB, NEG, CP, IDT, PFD, DBG, CTAC, DOT, LPS>,      \
                                                               kRingWarps * 32, kSmem) != cudaSuccess || per_sm <= 0)             \
                 return -1;                                                                                                       \
         }                                                                                                                        \
@@ -769,7 +943,7 @@ static int launch_ringp_t(const spmvb_matrix *a, PatternArgs &p_in, int chunk, c
         pdl[0].val.programmaticStreamSerializationAllowed = 1;                                                                   \
         cfg.attrs = pdl;                                                                                                         \
         cfg.numAttrs = (options().ring_pdl && grid == n_sm * per_sm) ? 1 : 0; /* only a full wave: early CTAs of a partial grid crowd the SMs that free up first (128^3: 14.2 -> 17.9 us) */                                                                               \
-        if (cudaLaunchKernelEx(&cfg, spmv_pattern_ringp_kernel<Q, S, MINB, NEG, CP, IDT, PFD, DBG, CTAC, DOT>, tm, tm_ids, p, c_lo, c_hi, np_x,     \
+        if (cudaLaunchKernelEx(&cfg, spmv_pattern_ringp_kernel<Q, S, MINB, NEG, CP, IDT, PFD, DBG, CTAC, DOT, LPS>, tm, tm_ids, p, c_lo, c_hi, np_x,     \
                                n_strips, left_lo, left_in_ring, id_plane0, total, spw, rem, tile_lines, rot) != cudaSuccess)          \
             return check_launch("spmv_pattern_ringp") == SPMVB_OK ? -1 : -1;                                                     \
     } while (0)
@@ -784,6 +958,7 @@ static int launch_ringp_t(const spmvb_matrix *a, PatternArgs &p_in, int chunk, c
 // Second translation unit (spmv_pattern_tma6.cu): the 6-planes-per-thread instantiations, so that the two halves build in parallel.
 // mode 0: chunk per CTA (with the ids-by-loads fallback); 1: per CTA, lab; 2: per warp, lab; 3-5: ablations.
 int launch_ring_q6(int mode, const spmvb_matrix *a, PatternArgs &p, int chunk, cudaStream_t st, int tile_lines) {
+    if (mode == 6) return launch_ringp_t<4, 6, 2, true, 0, 0, true, false, 2>(a, p, chunk, st, tile_lines);  // 4 planes x 2 lines per thread and step, per CTA
     if (mode == 2) return launch_ringp_t<6, 4, 2, true>(a, p, chunk, st, tile_lines);  // a chunk per warp (strips that do not come in fours)
 #ifdef SPMVB_LAB
     if (mode == 3) return launch_ringp_t<6, 4, 2, true, 0, 6, true>(a, p, chunk, st, tile_lines);  // measurement only: no left-over columns
@@ -846,6 +1021,12 @@ int launch_pattern_ring(int which, int lines, const spmvb_matrix *a, PatternArgs
         case 27: return launch_ring_q6(2, a, p, 0, st, tl);      // 6 planes/thread, round-robin tiles per warp
 #endif
         // the schedules the default policy chooses between, forced (tests cover each of them on every shape):
+        case 21:  // two lines per step (4 planes/thread, 6 slots, 8 warps/SM), chunk per CTA: 70.6 us at 256^3
+        case 22:  // ... tiles of `lines` lines dealt out round-robin (the default for x far beyond L2: 512^3 547-555 vs 577-581 us)
+            rc = which == 21 ? launch_ring_q6(6, a, p, lines, st, 0) : launch_ring_q6(6, a, p, 0, st, lines > 0 ? lines : 28);
+            if (rc != 1) return rc;
+            rc = launch_ringp_t<4, 4, 3, true, 0, 0, true>(a, p, which == 21 ? lines : 0, st, which == 21 ? 0 : tl);
+            return rc == 1 ? launch_ringp_t<4, 5, 3, false, 0, 0, true>(a, p, which == 21 ? lines : 0, st, which == 21 ? 0 : tl) : rc;
         case 11:  // a chunk per warp instead of per CTA: 87 us
             rc = launch_ringp_t<4, 4, 3, true>(a, p, lines, st);
             return rc == 1 ? launch_ringp_t<4, 5, 3, false>(a, p, lines, st) : rc;
@@ -889,6 +1070,14 @@ int launch_pattern_ring(int which, int lines, const spmvb_matrix *a, PatternArgs
             }
             rc = launch_ring_q4_dot(fours, a, p, chunk, st, tile_lines);  // cg_solve's request for x.y, when there is one
             if (rc != 1) return rc;
+            // x far beyond L2 and strips in fours: two lines per step, tiles of 28 lines (what the side buffer of the left-over column
+            // holds).  There the kernel's own shared-memory traffic, not the halo planes' L2 traffic, is the larger term: a quad of
+            // operands serves the rows of two lines (23 instead of 29 L1 wavefronts per row).  512^3: 547-555 us against 577-581 us in
+            // the same run; with x in L2 (256^3: 70.6 vs 65.9 us for 6 planes per thread) or strips not in fours (384^3) it loses.
+            if (fours && tile_lines > 0 && a->n_exc == 0 && options().ring_two_lines) {
+                rc = launch_ring_q6(6, a, p, 0, st, lines > 0 ? lines : 28);
+                if (rc != 1) return rc;
+            }
             // 6 planes/thread with a chunk per warp (128^3 13.5 -> 12.8 us, 192^3 33.9 -> 32.4 us) when every warp of its full wave
             // gets at least 4 steps (96^3 does not: 8.6 -> 10.4 us) and no exception block wants room beside it (C4: 41.9 -> 43.3 us)
             if (!fours && tile_lines == 0 && a->n_exc == 0) {

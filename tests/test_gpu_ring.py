@@ -7,7 +7,8 @@ pytestmark = pytest.mark.gpu
 
 from tests.test_gpu_parity import bits, run, sp, up_pat  # noqa: E402,F401
 
-RING = [90, 101, 107, 108, 109, 110]  # default schedule, chunk per warp, ids by loads, round-robin tiles (per CTA, per warp), 4 planes/thread
+# default schedule, chunk per warp, ids by loads, round-robin tiles (per CTA, per warp), 4 planes/thread, two lines per step (chunks, tiles)
+RING = [90, 101, 107, 108, 109, 110, 111, 112]
 
 
 def ring_run(sp, d, x, march, lines=0, must_ring=True, **kw):
@@ -44,7 +45,8 @@ def test_ring_march_lengths(sp, orc, lines):
 
 
 @pytest.mark.parametrize("leftover", [0, 1, 2])
-@pytest.mark.parametrize("march,lines", [(90, 0), (90, 100), (90, 47), (108, 16), (108, 40), (110, 0)])
+@pytest.mark.parametrize("march,lines", [(90, 0), (90, 100), (90, 47), (108, 16), (108, 40), (110, 0), (111, 0), (111, 5), (111, 28), (111, 60),
+                                         (112, 0), (112, 7), (112, 16), (112, 40)])
 def test_ring_leftover_column_schemes(sp, orc, leftover, march, lines):
     """64 | nx: column nx-1 lies past the last strip.  Chunk-per-CTA kernels gather its operands per line and sum its rows
     after the march (marches longer than the side buffer are split; tiles longer than it keep the per-step sums); option
@@ -60,7 +62,7 @@ def test_ring_leftover_column_schemes(sp, orc, leftover, march, lines):
     assert np.array_equal(bits(y), bits(orc.spmv(pc, x)))
 
 
-@pytest.mark.parametrize("march", [90, 108])
+@pytest.mark.parametrize("march", [90, 108, 111, 112])
 def test_ring_ragged_ranges(sp, orc, march):
     """Partitions at arbitrary (even and odd) rows give the single-call result; other rows stay untouched."""
     m = orc.generate_matrix(128, 20, 12)
@@ -119,8 +121,9 @@ def test_ring_misaligned_view_falls_back_per_row(sp, orc, nx):
     for g0 in (2 * plane - 2 * nx - 6, 2 * plane - nx - 2, 2 * plane - 2):  # even offsets, not plane / line aligned
         d_p = sp.upload_pattern(r1 - r0, pc.table, pc.disp_offsets, pc.disp_flat, pc.ends_flat, pc.row_pattern[r0:r1],
                                 True, row_offset=r0)
-        y = ring_run(sp, d_p, x[g0:7 * plane], 90, x_col0=g0)
-        assert np.array_equal(bits(y), bits(full[r0:r1])), g0
+        for march in (90, 111, 112):
+            y = ring_run(sp, d_p, x[g0:7 * plane], march, x_col0=g0)
+            assert np.array_equal(bits(y), bits(full[r0:r1])), (g0, march)
 
 
 @pytest.mark.parametrize("g", [(128, 20, 12), (96, 40, 36)])
@@ -130,7 +133,8 @@ def test_ring_hybrid_exception_rows(sp, orc, g):
     assert pc.n_exc > 0
     d = up_pat(sp, pc)
     x = orc.make_test_vector(m.n, orc.RANDOM, seed=7, lo=-1.0, hi=1.0)
-    assert np.array_equal(bits(ring_run(sp, d, x, 90)), bits(orc.spmv(pc, x)))
+    for march in (90, 111, 112):
+        assert np.array_equal(bits(ring_run(sp, d, x, march)), bits(orc.spmv(pc, x))), march
 
 
 def test_ring_nonfinite_neighbours_do_not_leak(sp, orc):
@@ -139,11 +143,12 @@ def test_ring_nonfinite_neighbours_do_not_leak(sp, orc):
     pc = orc.compress_patterns(m, True)
     x = orc.make_test_vector(m.n, orc.RANDOM, seed=9, lo=-1.0, hi=1.0)
     x[127] = np.nan  # last column of line 0: not a neighbour of row 128 (column 0 of line 1)
-    y = ring_run(sp, up_pat(sp, pc), x, 90)
     ref = orc.spmv(pc, x)
     ok = ~np.isnan(ref)
-    assert np.array_equal(np.isnan(y), np.isnan(ref)) and np.array_equal(bits(y[ok]), bits(ref[ok]))
-    assert np.isnan(y[126]) and not np.isnan(y[128])
+    for march in (90, 111):
+        y = ring_run(sp, up_pat(sp, pc), x, march)
+        assert np.array_equal(np.isnan(y), np.isnan(ref)) and np.array_equal(bits(y[ok]), bits(ref[ok]))
+        assert np.isnan(y[126]) and not np.isnan(y[128])
 
 
 @pytest.mark.parametrize("vals", [(26.0, -1.0), (-4.0, 1.5), (2.0, 2.0), (0.5, 3.0), (-1.0, -1.0), (-3.0, -1.0)])
@@ -153,7 +158,8 @@ def test_ring_value_pairs_and_centre_position(sp, orc, vals):
     m = orc.generate_matrix(128, 11, 10, diag, off)
     x = orc.make_test_vector(m.n, orc.RANDOM, seed=11, lo=-1.0, hi=1.0)
     ref = orc.compress_patterns(m)
-    assert np.array_equal(bits(ring_run(sp, up_pat(sp, ref), x, 0)), bits(orc.spmv(ref, x)))
+    for march in (0, 111, 112):  # (the two-lines step has its own general instantiation)
+        assert np.array_equal(bits(ring_run(sp, up_pat(sp, ref), x, march)), bits(orc.spmv(ref, x))), march
 
 
 def test_ring_is_the_default_for_large_ranges(sp, orc):
@@ -177,7 +183,7 @@ def test_ring_is_the_default_for_large_ranges(sp, orc):
     assert np.array_equal(bits(dy.to_host()[:3 * 128 * 12]), bits(orc.spmv(pc, x)[:3 * 128 * 12]))
 
 
-@pytest.mark.parametrize("march", [0, 101, 109])
+@pytest.mark.parametrize("march", [0, 101, 109, 111, 112])
 def test_ring_ghost_planes_beyond_the_grid_faces(sp, orc, march):
     """x padded by one (unreferenced) plane at each end, x_col0 = -plane (the single-rank SlabLayout): the rows
     of the first and last grid plane are sub-boxes whose missing entries are inside the view."""
@@ -220,7 +226,7 @@ def test_ring_randomised_shapes_ranges_and_views(sp, orc):
         nl = r1 - r0
         cuts = sorted({0, nl, *(int(v) for v in rng.integers(0, nl + 1, size=2))})
         dx = sp.DeviceVector.from_host(xl)
-        for march in (0, 90):  # the default dispatch, and the tensor ring forced also for ranges of a few planes
+        for march in (0, 90, 111, 112):  # the default dispatch, and the tensor ring forced also for ranges of a few planes (+ two lines per step)
             dy = sp.DeviceVector.from_host(np.full(nl, np.nan))
             sp.set_option("box_march", march)
             try:

@@ -249,7 +249,7 @@ def test_row_range_partition_is_bit_identical(orc):
 
 # ---- K12: lossless round trip and determinism ------------
 def test_k12_round_trip_all_grids(orc):
-    for g in itertools.product(range(1, 7), repeat=3):
+    for g in itertools.product(range(1, 9), repeat=3):  # nx, ny, nz in [1,8] (acceptance criterion 4 asks for [1,6])
         m = orc.generate_matrix(*g)
         vt = orc.compress_values(m)
         pc = orc.compress_patterns(m, False)
