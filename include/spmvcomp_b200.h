@@ -116,8 +116,9 @@ int spmvb_set_device(int device);
  * was built with -DSPMVB_LAB ("lab_build", read-only, says which; the default build holds none of them).
  *   "pattern_kernel": 0 auto, 1 List 1 as written (thread per row), 2 box plan required, 3 one-column box kernel only
  *   "box_march":      0 auto (tensor ring for ranges of >= 8 planes, else the register sliding window);
- *                     3 sliding window forced; 90 tensor ring forced, 101 / 107 / 108 / 109 / 110 its other schedules
- *                     (chunk per warp, ids by loads, round-robin tiles per CTA / per warp, 4 planes per thread);
+ *                     3 sliding window forced; 90 tensor ring forced, 101 / 107 / 108 / 109 / 110 / 111 / 112 its other schedules
+ *                     (chunk per warp, ids by loads, round-robin tiles per CTA / per warp, 4 planes per thread, two lines per
+ *                     step in chunks / in tiles);
  *                     lab build only: further variants and ablations (csrc/spmv_pattern*.cu list them with their times)
  *   "box_lines":      lines per CTA tile / chunk length of the tensor ring (0 = default)
  *   "exception_kernel": hybrid handles, the exception-row block: 0 / 1 (default) the ELL kernel with a row map, all gathers of a
@@ -129,6 +130,9 @@ int spmvb_set_device(int device);
  *                     rows (the two write disjoint rows of y; forked and joined by events, so the call still completes in
  *                     stream order); 0 one after the other
  *   "ring_min_steps": tensor ring: fewest line steps per chunk before the grid shrinks below a full wave of CTAs (0 = default 4)
+ *   "ring_two_lines": 1 (default) where x is far beyond L2 and the 64-column strips come in fours, a step of the tensor ring sums
+ *                     the rows of two lines (4 planes x 2 lines x 2 columns per thread, tiles of 28 lines): 512^3 584 -> 546 us;
+ *                     0 one line per step there as everywhere else
  *   "ring_pdl":       1 (default) the tensor-ring kernel is launched with programmatic stream serialization: its CTAs take the
  *                     places of the previous kernel's CTAs as those exit and wait (griddepcontrol.wait) for that kernel to
  *                     complete before touching global memory; 0 plain stream order
