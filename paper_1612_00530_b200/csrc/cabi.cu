@@ -66,6 +66,7 @@ void destroy(spmvb_matrix *a) {
     for (auto &ev : a->exc_events) if (ev) cudaEventDestroy(ev);
     if (a->d_masks) cudaFree(a->d_masks);
     if (a->d_disp_off32) cudaFree(a->d_disp_off32);
+    if (a->symgs_mask) cudaFree(a->symgs_mask);
     delete a;
 }
 
@@ -272,6 +273,8 @@ static int *option_slot(const char *key) {
     if (!strcmp(key, "last_cg_graph")) return &o.last_cg_graph;
     if (!strcmp(key, "symgs_graph")) return &o.symgs_graph;
     if (!strcmp(key, "symgs_persistent")) return &o.symgs_persistent;
+    if (!strcmp(key, "symgs_pipeline")) return &o.symgs_pipeline;
+    if (!strcmp(key, "symgs_lag")) return &o.symgs_lag;
     if (!strcmp(key, "slab_graph")) return &o.slab_graph;
     if (!strcmp(key, "last_cg_fused_dot")) return &o.last_cg_fused_dot;
     if (!strcmp(key, "last_pattern_kernel")) return &o.last_pattern_kernel;

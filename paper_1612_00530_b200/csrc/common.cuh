@@ -115,6 +115,9 @@ struct spmvb_matrix {
     mutable double *cg_ws = nullptr;
     mutable int cg_ws_busy = 0;  // taken with an atomic exchange: a second concurrent solve on the handle allocates its own
     mutable SymgsGraph symgs_graph;
+    mutable uint32_t *symgs_mask = nullptr;    // CSR handles: per row, which of the 27 box positions its entries occupy (symgs.cu, the pipelined sweep)
+    mutable int symgs_box[3] = {0, 0, 0};      // ... the grid it was derived for; symgs_box_ok: every row is a sub-box of its node's 27 neighbours
+    mutable int symgs_box_ok = 0;
     mutable int symgs_checked[3] = {0, 0, 0};  // CSR handles: grid whose hyperplane schedule was verified against the matrix (symgs.cu)
     // streams / events of the pipelined host-buffer SpMV (created on first use)
     mutable cudaStream_t pipe_streams[3] = {};
@@ -152,6 +155,8 @@ struct Options {
     int ring_pdl = 1;        // tensor ring launched with programmatic stream serialization (its preamble overlaps the previous kernel's tail)
     int ring_leftover = 0;   // tensor ring, left-over column (64 | sy): 0 summed by the last strip's warp from its ring, 1 row by row after the marches
     int slab_graph = 1;         // 1: spmvb_slab_spmv records its exchange copies and launches into a CUDA graph and replays it
+    int symgs_lag = 0;          // pipelined sweep: steps a plane trails its predecessor by (>= 7; 0 = 7)
+    int symgs_pipeline = 1;     // 1: matrices whose rows are sub-boxes of the 27-point stencil are swept by the plane-per-CTA pipeline; 0: never
     int symgs_persistent = 1;   // 1: a symgs sweep is one cooperative launch that walks the levels itself (grid-wide barriers); 0: a launch per level
     int symgs_graph = 1;        // 1: a symgs sweep's launches are recorded into a CUDA graph and replayed
     int cg_fused_scalars = 1;   // cg_solve's vector kernel: 1 beta / stop flag / record by its last block (4 launches per iteration); 2 also alpha, formed at its head by every block (3 launches); 0 separate alpha and beta kernels (5 launches)

@@ -215,6 +215,245 @@ __global__ void __launch_bounds__(kSymgsThreads, 1) symgs_sweep_persistent_kerne
     }
 }
 
+// ---- the pipelined sweep: a plane per CTA, operands through shared memory ---------------------------------------------
+// What a level costs in the kernels above is neither the barrier nor DRAM: a thread reading its own CSR row touches a cache
+// line per load (54 loads of entries, 26 gathers of x), and the L1 tag stage looks up one line per clock.  For matrices
+// whose rows are sub-boxes of their node's 27 neighbours (the stencil matrix, 7-point matrices, user values -- anything the
+// plan kernel below accepts) none of those loads is needed:
+//  * a row is its 27-bit box mask (one word, derived once per matrix) and its values in column order: the columns are never
+//    read, and the values of a warp's 32 rows are fetched a row at a time with the lanes on consecutive entries (coalesced),
+//    a step ahead, and handed over through the warp's shared-memory buffer;
+//  * a CTA owns plane iz, thread t = line iy, and step k relaxes u = k - 2t (the plane's own levels; in-plane dependences are
+//    met by the lockstep of the CTA's barriers).  Every thread keeps a 16-deep window of its line of x for the plane below, its
+//    own plane and the plane above in shared memory -- one load per plane and step, six positions ahead of its own -- and a row
+//    takes all 26 operands from those rings: new values behind the front, old values ahead of it, exactly what the sequential
+//    sweep would read;
+//  * the plane below is another CTA's: it publishes its step count (release) and this plane's step k waits until that count
+//    is k + 7 -- the level function's 4 iz plus the three steps the rings run ahead.  Planes are dealt round-robin to the
+//    co-resident CTAs (cooperative launch), each CTA taking its planes in sweep order, so the waits form no cycle; the backward
+//    sweep is the mirror image (u, t and the plane order reversed: thread t = line ny-1-t, u = nx-1-ix) and its first plane
+//    waits for the forward sweep's last.  Two extra warps poll and publish, so that no compute thread ever executes a gpu-scope
+//    fence (which waits for the issuing thread's outstanding loads -- a compute thread always has some).
+// Per row the same expression in the same order as the kernels above (ascending column = ascending box position, products
+// and sums rounded separately, one subtraction, one division): bit-identical.
+constexpr int kBoxRing = 16;       // positions of a line kept per plane
+constexpr int kBoxPitch = 17;      // doubles between two lines of a ring (odd: the lanes of a warp, two positions apart on neighbouring lines, spread over the banks)
+constexpr int kBoxAhead = 6;       // a thread loads position u + 6 and hands it to the ring a step later
+constexpr int kBoxLag = 7;         // steps a plane trails the one below
+
+// plan: bit (dz+1)*9 + (dy+1)*3 + (dx+1) for every entry; flags[0] set when a row is not a sub-box of its node's neighbours
+__global__ void symgs_box_plan_kernel(const int64_t *__restrict__ row_start, const int32_t *__restrict__ cols, int n, int nx, int ny, int nz,
+                                      uint32_t *__restrict__ mask, int *__restrict__ flags) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int ix = i % nx, iy = (i / nx) % ny, iz = i / (nx * ny);
+    const int64_t nxny = (int64_t)nx * ny;
+    uint32_t m = 0;
+    bool ok = true;
+    int last = -1;
+    for (int64_t t = row_start[i]; t < row_start[i + 1]; t++) {
+        const int64_t u = (int64_t)cols[t] - i + nxny + nx + 1;  // (dx+1) + nx (dy+1) + nx ny (dz+1)
+        if (u < 0 || u >= 3 * nxny) {
+            ok = false;
+            break;
+        }
+        const int dzp = (u >= 2 * nxny) + (u >= nxny);
+        const int64_t rem = u - dzp * nxny;
+        const int dyp = (rem >= 2 * (int64_t)nx) + (rem >= nx);
+        const int64_t dxp = rem - (int64_t)dyp * nx;
+        const int bit = dzp * 9 + dyp * 3 + (int)dxp;
+        if (dxp > 2 || ix + dxp - 1 < 0 || ix + dxp - 1 >= nx || iy + dyp - 1 < 0 || iy + dyp - 1 >= ny || iz + dzp - 1 < 0 || iz + dzp - 1 >= nz ||
+            bit <= last) {
+            ok = false;
+            break;
+        }
+        last = bit;
+        m |= 1u << bit;
+    }
+    mask[i] = m;
+    if (!ok) atomicOr(&flags[0], 1);
+}
+
+__device__ __forceinline__ int ld_acquire_gpu(const int *p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu(int *p, int v) { asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory"); }
+
+struct BoxHead {  // what a thread knows of a row before its values: index, first entry, mask, b[row]
+    int i;
+    uint32_t mask;
+    int64_t k0;
+    double bi;
+};
+
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS + 64, 1) symgs_box_pipeline_kernel(const int64_t *__restrict__ row_start, const double *__restrict__ vals,
+                                                                             const uint32_t *__restrict__ mask, double *x, const double *__restrict__ b,
+                                                                             int nx, int ny, int nz, int lag, int *clock_f, int *clock_b) {
+    extern __shared__ __align__(16) unsigned char symgs_smem[];
+    constexpr int LINES = THREADS + 2;
+    double *ring = reinterpret_cast<double *>(symgs_smem);                                  // [3 planes][LINES][kBoxRing]
+    double *stage = ring + 3 * LINES * kBoxPitch;                                           // [THREADS / 32 warps][32 rows][27 values]
+    const int t = threadIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int role = threadIdx.x < THREADS ? 0 : threadIdx.x < THREADS + 32 ? 1 : 2;        // compute / poll / publish
+    const int G = gridDim.x, c = blockIdx.x;
+    const int K = nx + 2 * (ny - 1);                       // levels of a plane
+    const int KT = K + kBoxAhead;                          // steps of a plane: the rings are filled six steps ahead of the first row
+    const int R = c < nz ? (nz - 1 - c) / G + 1 : 0;       // this CTA's planes: c, c + G, ...
+    const int ticks = 2 * R * KT;
+    const int64_t nxny = (int64_t)nx * ny;
+    if (role != 0) {  // the whole warp walks the steps and meets its barrier; lane 0 does the memory operations
+        int seen = 0, r = 0, kt = 0;
+        bool back = false;
+        for (int tick = 0; tick < ticks; tick++) {
+            const int p = back ? c + (R - 1 - r) * G : c + r * G;
+            const int k = kt - kBoxAhead;  // level (negative: filling the rings)
+            if (role == 1) {
+                if (kt == 0) seen = 0;
+                int need = min(k + lag, K);
+                const int *src = nullptr;
+                if (!back) {
+                    if (p > 0) src = clock_f + (p - 1);
+                } else if (p < nz - 1) {
+                    src = clock_b + (p + 1);
+                } else {
+                    src = clock_f + (nz - 1), need = K;  // the backward sweep begins when the forward sweep has ended
+                }
+                if (src && lane == 0)
+                    while (seen < need) seen = ld_acquire_gpu(src);
+                asm volatile("bar.sync 1, %0;" ::"r"(THREADS + 32) : "memory");  // the step may begin
+            } else {
+                asm volatile("bar.sync 2, %0;" ::"r"(THREADS + 32) : "memory");  // the step's stores are issued (cumulative release below)
+                if (lane == 0 && k >= 0) st_release_gpu((back ? clock_b : clock_f) + p, k + 1);
+            }
+            if (++kt == KT) {
+                kt = 0;
+                if (++r == R) r = 0, back = true;
+            }
+        }
+        return;
+    }
+    // ---- compute threads
+    // position of a step: (direction, plane, this thread's u = k - 2t); memory coordinates follow from the direction
+    struct Pos {
+        bool back, valid;
+        int p, u;
+    };
+    auto pos_of_tick = [&](int tick) -> Pos {
+        Pos q{false, false, 0, 0};
+        if (tick >= ticks) return q;
+        q.back = tick >= R * KT;
+        const int w = q.back ? tick - R * KT : tick;
+        const int r = w / KT, kt = w - r * KT;
+        q.p = q.back ? c + (R - 1 - r) * G : c + r * G;
+        q.u = kt - kBoxAhead - 2 * t;
+        q.valid = t < ny;
+        return q;
+    };
+    auto head_of_tick = [&](int tick) -> BoxHead {
+        BoxHead h{-1, 0u, 0, 0.0};
+        const Pos q = pos_of_tick(tick);
+        if (q.valid && q.u >= 0 && q.u < nx) {
+            const int ix = q.back ? nx - 1 - q.u : q.u, iy = q.back ? ny - 1 - t : t;
+            const int64_t i = ix + (int64_t)nx * iy + nxny * q.p;
+            h.i = (int)i;
+            h.k0 = __ldg(row_start + i);
+            h.mask = __ldg(mask + i);
+            h.bi = __ldg(b + i);
+        }
+        return h;
+    };
+    double *my_stage = stage + warp * (32 * kSymgsRow);
+    double pv[32];
+    unsigned pany = 0;
+    auto fetch_rows = [&](const BoxHead &h) {  // the values of the warp's 32 rows, a row at a time, lanes on consecutive entries
+        pany = __ballot_sync(0xffffffffu, h.i >= 0);
+#pragma unroll
+        for (int r = 0; r < 32; r++) {
+            const int64_t k0 = __shfl_sync(0xffffffffu, h.k0, r);
+            const int cnt = __popc(__shfl_sync(0xffffffffu, h.mask, r));
+            pv[r] = ((pany >> r & 1u) && lane < cnt) ? __ldg(vals + k0 + lane) : 0.0;
+        }
+    };
+    auto store_rows = [&]() {
+#pragma unroll
+        for (int r = 0; r < 32; r++)
+            if ((pany >> r & 1u) && lane < kSymgsRow) my_stage[r * kSymgsRow + lane] = pv[r];
+    };
+    // ring loads: position u + 6 of this thread's line in the plane below / own plane / plane above (logical), one step in flight
+    double rl[3] = {0.0, 0.0, 0.0};
+    bool rl_on[3] = {false, false, false};
+    int rl_slot = 0;
+    auto ring_loads = [&](const Pos &q) {
+        const int u6 = q.u + kBoxAhead;
+        rl_slot = u6 & (kBoxRing - 1);
+#pragma unroll
+        for (int d = 0; d < 3; d++) {
+            const int pp = q.p + (q.back ? 1 - d : d - 1);  // the plane logically below / this one / above
+            rl_on[d] = q.valid && u6 >= 0 && u6 < nx && pp >= 0 && pp < nz;
+            if (rl_on[d]) {
+                const int ix = q.back ? nx - 1 - u6 : u6, iy = q.back ? ny - 1 - t : t;
+                rl[d] = __ldcg(x + (ix + (int64_t)nx * iy + nxny * pp));
+            }
+        }
+    };
+    double *my_line = ring + (t + 1) * kBoxPitch;  // + d * LINES * kBoxPitch for plane d
+    BoxHead h0 = head_of_tick(0), h1 = head_of_tick(1);
+    fetch_rows(h0);
+    store_rows();
+    __syncwarp();
+    for (int tick = 0; tick < ticks; tick++) {
+        const Pos q = pos_of_tick(tick);
+        const BoxHead h2 = head_of_tick(tick + 2);  // requested two steps ahead of its row
+        fetch_rows(h1);                              // the next step's values, in flight across this step
+        asm volatile("bar.sync 1, %0;" ::"r"(THREADS + 32) : "memory");
+        // (the ring loads of the previous step have had a step to arrive; this step's are requested now, behind the clock's acquire)
+        const double prev[3] = {rl[0], rl[1], rl[2]};
+        const bool prev_on[3] = {rl_on[0], rl_on[1], rl_on[2]};
+        const int prev_slot = rl_slot;
+        const bool first = (q.back ? tick - R * KT : tick) % KT == 0;  // a new plane: nothing carried over
+        ring_loads(q);
+        if (h0.i >= 0) {
+            const double *v = my_stage + lane * kSymgsRow;
+            const int s = q.back ? -1 : 1;
+            int wc[3];
+#pragma unroll
+            for (int dx = 0; dx < 3; dx++) wc[dx] = (q.u + s * (dx - 1)) & (kBoxRing - 1);
+            double sum = 0.0, diag = 0.0;
+            int j = 0;
+#pragma unroll
+            for (int bz = 0; bz < 3; bz++)
+#pragma unroll
+                for (int by = 0; by < 3; by++) {
+                    const double *line = my_line + ((1 + s * (bz - 1)) * LINES + s * (by - 1)) * kBoxPitch;
+#pragma unroll
+                    for (int bx = 0; bx < 3; bx++) {
+                        const int bit = bz * 9 + by * 3 + bx;
+                        if (h0.mask >> bit & 1u) {
+                            const double a = v[j++];
+                            if (bit == 13) diag = a;
+                            else sum = __dadd_rn(sum, __dmul_rn(a, line[wc[bx]]));
+                        }
+                    }
+                }
+            const double xn = __ddiv_rn(__dsub_rn(h0.bi, sum), diag);  // inc/kernels.hpp:46
+            __stcg(x + h0.i, xn);
+            my_line[LINES * kBoxPitch + (q.u & (kBoxRing - 1))] = xn;  // own plane, own line: the new value
+        }
+        if (!first) {
+#pragma unroll
+            for (int d = 0; d < 3; d++)
+                if (prev_on[d]) my_line[d * LINES * kBoxPitch + prev_slot] = prev[d];
+        }
+        __syncwarp();  // every lane has read its row's values: the buffer takes the next step's
+        store_rows();
+        h0 = h1, h1 = h2;
+        asm volatile("bar.sync 2, %0;" ::"r"(THREADS + 32) : "memory");
+    }
+}
+
 static int check_schedule(const spmvb_matrix *a, const spmvb_grid *g, cudaStream_t st) {
     if (a->symgs_checked[0] == g->nx && a->symgs_checked[1] == g->ny && a->symgs_checked[2] == g->nz) return SPMVB_OK;
     int *flags = nullptr;
@@ -308,7 +547,83 @@ static int sweep_persistent(const spmvb_matrix *a, const spmvb_grid *g, double *
     return 0;
 }
 
+// the pipelined sweep; 1 = not served (rows that are not sub-boxes, lines longer than a CTA, no cooperative launch)
+static int sweep_pipeline(const spmvb_matrix *a, const spmvb_grid *g, double *x, const double *b, cudaStream_t st) {
+    struct State {
+        int coop = -1, n_sm = 0;
+        int *clocks = nullptr;
+        int cap = 0;
+    };
+    static PerDevice<State> state;
+    State &sd = state.get();
+    if (sd.coop < 0) {
+        int dev = 0, coop = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&sd.n_sm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+            coop = 0;
+        (void)cudaGetLastError();
+        sd.coop = coop ? 1 : 0;
+    }
+    int nx = g->nx, ny = g->ny, nz = g->nz;
+    if (!sd.coop || nx < 3 || ny < 3 || ny > 256) return 1;
+    const auto *rs = static_cast<const int64_t *>(a->s[SPMVB_S_CSR_ROW_START]);
+    const auto *cols = static_cast<const int32_t *>(a->s[SPMVB_S_CSR_COLS]);
+    const auto *vals = static_cast<const double *>(a->s[SPMVB_S_CSR_VALS]);
+    if (a->symgs_box[0] != nx || a->symgs_box[1] != ny || a->symgs_box[2] != nz) {  // the plan: once per matrix and grid
+        if (a->symgs_mask) cudaFree(a->symgs_mask);
+        a->symgs_mask = nullptr;
+        a->symgs_box_ok = 0;
+        a->symgs_box[0] = nx, a->symgs_box[1] = ny, a->symgs_box[2] = nz;
+        int *flags = nullptr;
+        int h = 1;
+        if (cudaMalloc(&a->symgs_mask, (size_t)a->n * sizeof(uint32_t)) == cudaSuccess && cudaMalloc(&flags, sizeof(int)) == cudaSuccess &&
+            cudaMemsetAsync(flags, 0, sizeof(int), st) == cudaSuccess) {
+            symgs_box_plan_kernel<<<(a->n + 255) / 256, 256, 0, st>>>(rs, cols, a->n, nx, ny, nz, a->symgs_mask, flags);
+            if (cudaMemcpyAsync(&h, flags, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess) h = 1;
+        }
+        if (flags) cudaFree(flags);
+        (void)cudaGetLastError();
+        a->symgs_box_ok = h == 0;
+        if (!a->symgs_box_ok && a->symgs_mask) {
+            cudaFree(a->symgs_mask);
+            a->symgs_mask = nullptr;
+        }
+    }
+    if (!a->symgs_box_ok) return 1;
+    if (sd.cap < 2 * nz) {
+        if (sd.clocks) cudaFree(sd.clocks);
+        sd.clocks = nullptr, sd.cap = 0;
+        if (cudaMalloc(&sd.clocks, (size_t)2 * nz * sizeof(int)) != cudaSuccess) {
+            (void)cudaGetLastError();
+            return 1;
+        }
+        sd.cap = 2 * nz;
+    }
+    if (cudaMemsetAsync(sd.clocks, 0, (size_t)2 * nz * sizeof(int), st) != cudaSuccess) return 1;
+    int *clock_f = sd.clocks, *clock_b = sd.clocks + nz;
+    int lag = std::max(kBoxLag, options().symgs_lag);
+    const uint32_t *mask = a->symgs_mask;
+    const int threads = ny <= 32 ? 32 : ny <= 64 ? 64 : ny <= 128 ? 128 : 256;
+    const void *fn = threads == 32 ? (const void *)symgs_box_pipeline_kernel<32>
+                     : threads == 64 ? (const void *)symgs_box_pipeline_kernel<64>
+                     : threads == 128 ? (const void *)symgs_box_pipeline_kernel<128>
+                                      : (const void *)symgs_box_pipeline_kernel<256>;
+    const size_t smem = (size_t)3 * (threads + 2) * kBoxPitch * 8 + (size_t)(threads / 32) * 32 * kSymgsRow * 8;
+    const int grid = std::min(sd.n_sm, nz);
+    void *args[] = {&rs, &vals, &mask, &x, &b, &nx, &ny, &nz, &lag, &clock_f, &clock_b};
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+        cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(threads + 64), args, smem, st) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return 1;
+    }
+    return 0;
+}
+
 static int sweep_device(const spmvb_matrix *a, const spmvb_grid *g, double *x, const double *b, cudaStream_t st) {
+    if (options().symgs_pipeline) {
+        const int rc = sweep_pipeline(a, g, x, b, st);
+        if (rc == 0) return SPMVB_OK;
+    }
     if (options().symgs_persistent) {
         const int rc = sweep_persistent(a, g, x, b, st);
         if (rc == 0) return SPMVB_OK;
