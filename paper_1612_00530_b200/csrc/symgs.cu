@@ -225,11 +225,11 @@ __global__ void __launch_bounds__(kSymgsThreads, 1) symgs_sweep_persistent_kerne
 //    a step ahead, and handed over through the warp's shared-memory buffer;
 //  * a CTA owns plane iz, thread t = line iy, and step k relaxes u = k - 2t (the plane's own levels; in-plane dependences are
 //    met by the lockstep of the CTA's barriers).  Every thread keeps a 16-deep window of its line of x for the plane below, its
-//    own plane and the plane above in shared memory -- one load per plane and step, six positions ahead of its own -- and a row
+//    own plane and the plane above in shared memory -- one load per plane and step, four to six positions ahead of its own -- and a row
 //    takes all 26 operands from those rings: new values behind the front, old values ahead of it, exactly what the sequential
 //    sweep would read;
 //  * the plane below is another CTA's: it publishes its step count (release) and this plane's step k waits until that count
-//    is k + 7 -- the level function's 4 iz plus the three steps the rings run ahead.  Planes are dealt round-robin to the
+//    is k + 5 -- the level function's 4 iz plus the one step the ring of that plane runs ahead.  Planes are dealt round-robin to the
 //    co-resident CTAs (cooperative launch), each CTA taking its planes in sweep order, so the waits form no cycle; the backward
 //    sweep is the mirror image (u, t and the plane order reversed: thread t = line ny-1-t, u = nx-1-ix) and its first plane
 //    waits for the forward sweep's last.  Two extra warps poll and publish, so that no compute thread ever executes a gpu-scope
@@ -238,8 +238,9 @@ __global__ void __launch_bounds__(kSymgsThreads, 1) symgs_sweep_persistent_kerne
 // and sums rounded separately, one subtraction, one division): bit-identical.
 constexpr int kBoxRing = 16;       // positions of a line kept per plane
 constexpr int kBoxPitch = 17;      // doubles between two lines of a ring (odd: the lanes of a warp, two positions apart on neighbouring lines, spread over the banks)
-constexpr int kBoxAhead = 6;       // a thread loads position u + 6 and hands it to the ring a step later
-constexpr int kBoxLag = 7;         // steps a plane trails the one below
+constexpr int kBoxAhead = 6;       // own plane and the plane above (old values): a thread loads position u + 6 and hands it to the ring a step later
+constexpr int kBoxBelow = 4;       // the plane below (new values): position u + 4, requested behind the step's acquire, in the ring by the step's end
+constexpr int kBoxLag = 5;         // steps a plane trails the one below: the level function's 4 iz and the one step the ring runs ahead
 
 // plan: bit (dz+1)*9 + (dy+1)*3 + (dx+1) for every entry; flags[0] set when a row is not a sub-box of its node's neighbours
 __global__ void symgs_box_plan_kernel(const int64_t *__restrict__ row_start, const int32_t *__restrict__ cols, int n, int nx, int ny, int nz,
@@ -390,8 +391,8 @@ __global__ void __launch_bounds__(THREADS + 64, 1) symgs_box_pipeline_kernel(con
         const int u6 = q.u + kBoxAhead;
         rl_slot = u6 & (kBoxRing - 1);
 #pragma unroll
-        for (int d = 0; d < 3; d++) {
-            const int pp = q.p + (q.back ? 1 - d : d - 1);  // the plane logically below / this one / above
+        for (int d = 1; d < 3; d++) {
+            const int pp = q.p + (q.back ? 1 - d : d - 1);  // this plane / the one logically above
             rl_on[d] = q.valid && u6 >= 0 && u6 < nx && pp >= 0 && pp < nz;
             if (rl_on[d]) {
                 const int ix = q.back ? nx - 1 - u6 : u6, iy = q.back ? ny - 1 - t : t;
@@ -415,6 +416,12 @@ __global__ void __launch_bounds__(THREADS + 64, 1) symgs_box_pipeline_kernel(con
         const int prev_slot = rl_slot;
         const bool first = (q.back ? tick - R * KT : tick) % KT == 0;  // a new plane: nothing carried over
         ring_loads(q);
+        // the plane below: the newest value any neighbour can ask for in the next step, u + 4 (its level there is k + 4: complete, the
+        // clock says so); one L2 round trip, hidden behind this step's sums
+        const int u4 = q.u + kBoxBelow, pb = q.p + (q.back ? 1 : -1);
+        const bool below_on = q.valid && u4 >= 0 && u4 < nx && pb >= 0 && pb < nz;
+        double below = 0.0;
+        if (below_on) below = __ldcg(x + ((q.back ? nx - 1 - u4 : u4) + (int64_t)nx * (q.back ? ny - 1 - t : t) + nxny * pb));
         if (h0.i >= 0) {
             const double *v = my_stage + lane * kSymgsRow;
             const int s = q.back ? -1 : 1;
@@ -444,9 +451,10 @@ __global__ void __launch_bounds__(THREADS + 64, 1) symgs_box_pipeline_kernel(con
         }
         if (!first) {
 #pragma unroll
-            for (int d = 0; d < 3; d++)
+            for (int d = 1; d < 3; d++)
                 if (prev_on[d]) my_line[d * LINES * kBoxPitch + prev_slot] = prev[d];
         }
+        if (below_on) my_line[u4 & (kBoxRing - 1)] = below;
         __syncwarp();  // every lane has read its row's values: the buffer takes the next step's
         store_rows();
         h0 = h1, h1 = h2;
