@@ -146,6 +146,11 @@ int spmvb_set_device(int device);
  *                     drained by "host_copy_threads" host threads (0 = default 8) inside the same chunk pipeline; 0 leaves them to
  *                     the driver's pageable copies.  Pinned (or registered) buffers are used in place either way
  *   "slab_graph":     1 (default) spmvb_slab_spmv replays its copies and launches as a CUDA graph; 0 launches directly
+ *   "symgs_pipeline": 1 (default) a symgs sweep of a matrix whose rows are sub-boxes of the 27-point stencil (lines of at most 256
+ *                     nodes) runs as a pipeline of planes: a CTA per plane, operands through shared-memory rings, release / acquire
+ *                     clocks between neighbouring planes (256^3: 25.3 -> 14.9 ms per sweep); 0 never.  "symgs_lag": steps a plane
+ *                     trails the one below (>= 5; 0 = 5).  "last_symgs_kernel" (read-only): 2 the pipeline, 1 the grid-barrier
+ *                     kernel, 0 a launch per level.  Same bits whichever runs
  *   "symgs_persistent": 1 (default) a symgs sweep is ONE cooperative launch: a CTA per SM walks the hyperplane levels with a
  *                     grid-wide barrier between them and fetches each row's matrix data ahead of the barrier; 0 a launch
  *                     per level (recorded into a CUDA graph when "symgs_graph" = 1).  Same bits either way

@@ -271,6 +271,7 @@ static int *option_slot(const char *key) {
     if (!strcmp(key, "cg_pdl")) return &o.cg_pdl;
     if (!strcmp(key, "cg_fused_scalars")) return &o.cg_fused_scalars;
     if (!strcmp(key, "last_cg_graph")) return &o.last_cg_graph;
+    if (!strcmp(key, "last_symgs_kernel")) return &o.last_symgs_kernel;
     if (!strcmp(key, "symgs_graph")) return &o.symgs_graph;
     if (!strcmp(key, "symgs_persistent")) return &o.symgs_persistent;
     if (!strcmp(key, "symgs_pipeline")) return &o.symgs_pipeline;

@@ -162,6 +162,7 @@ struct Options {
     int cg_fused_scalars = 1;   // cg_solve's vector kernel: 1 beta / stop flag / record by its last block (4 launches per iteration); 2 also alpha, formed at its head by every block (3 launches); 0 separate alpha and beta kernels (5 launches)
     int cg_pdl = 0;             // 1: the fused vector kernel and the direction kernel are launched with programmatic stream serialization (measured: no gain inside the replayed graph)
     int cg_graph = 1;           // 1: cg_solve records its iteration into a CUDA graph after the first and replays it
+    int last_symgs_kernel = 0;  // read-only: what swept last: 0 a launch per level (or their graph), 1 the grid-barrier kernel, 2 the plane pipeline
     int last_cg_graph = 0;      // read-only: 1 when the last cg_solve replayed a graph
     int cg_fused_dot = 1;       // 1: cg_solve takes p.Ap from the SpMV kernel where that kernel offers it (pattern format, tensor ring)
     int last_cg_fused_dot = 0;  // read-only: 1 when the last iteration of the last cg_solve took p.Ap from the SpMV kernel

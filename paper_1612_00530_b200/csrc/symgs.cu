@@ -455,10 +455,9 @@ __global__ void __launch_bounds__(THREADS + 64, 1) symgs_box_pipeline_kernel(con
                 if (prev_on[d]) my_line[d * LINES * kBoxPitch + prev_slot] = prev[d];
         }
         if (below_on) my_line[u4 & (kBoxRing - 1)] = below;
-        __syncwarp();  // every lane has read its row's values: the buffer takes the next step's
-        store_rows();
+        asm volatile("bar.sync 2, %0;" ::"r"(THREADS + 32) : "memory");  // the step's x is on its way: the clock may be published
+        store_rows();  // (every lane has read its row's values: the buffer takes the next step's, behind the barrier and off the clock's path)
         h0 = h1, h1 = h2;
-        asm volatile("bar.sync 2, %0;" ::"r"(THREADS + 32) : "memory");
     }
 }
 
@@ -630,12 +629,19 @@ static int sweep_pipeline(const spmvb_matrix *a, const spmvb_grid *g, double *x,
 static int sweep_device(const spmvb_matrix *a, const spmvb_grid *g, double *x, const double *b, cudaStream_t st) {
     if (options().symgs_pipeline) {
         const int rc = sweep_pipeline(a, g, x, b, st);
-        if (rc == 0) return SPMVB_OK;
+        if (rc == 0) {
+            options().last_symgs_kernel = 2;
+            return SPMVB_OK;
+        }
     }
     if (options().symgs_persistent) {
         const int rc = sweep_persistent(a, g, x, b, st);
-        if (rc == 0) return SPMVB_OK;
+        if (rc == 0) {
+            options().last_symgs_kernel = 1;
+            return SPMVB_OK;
+        }
     }
+    options().last_symgs_kernel = 0;
     SymgsGraph &c = a->symgs_graph;
     const bool hit = c.exec && c.x == x && c.b == b && c.nx == g->nx && c.ny == g->ny && c.nz == g->nz;
     if (options().symgs_graph && !hit) {

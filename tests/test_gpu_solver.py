@@ -216,6 +216,34 @@ def test_symgs_sweep_by_hyperplanes_is_the_sequential_sweep(sp, orc, g):
         assert np.array_equal(dx.to_host().view(np.uint64), x.view(np.uint64))
 
 
+@pytest.mark.parametrize("g,served", [((3, 3, 3), True), ((5, 4, 3), True), ((33, 9, 5), True), ((20, 20, 20), True), ((64, 3, 2), True),
+                                      ((8, 8, 300), True),     # more planes than SMs: a CTA takes several planes, round-robin
+                                      ((9, 200, 150), True),   # ... with lines on seven of the eight warps
+                                      ((40, 257, 3), False),   # lines longer than a CTA: the grid-barrier kernel
+                                      ((2, 5, 4), False), ((7, 2, 6), False)])  # too narrow for the box decode
+def test_symgs_plane_pipeline_and_its_fallbacks(sp, orc, g, served):
+    """The plane-per-CTA pipeline (box masks, operands through shared-memory rings, release / acquire clocks between planes) and the
+    kernels it falls back to are the oracle's sequential sweep bit for bit, whatever the lag between planes."""
+    m = orc.generate_matrix(*g)
+    dm = sp.generate_matrix(sp.GridSpec(*g))
+    x0 = orc.make_test_vector(m.n, orc.RANDOM, seed=13, lo=-1.0, hi=1.0)
+    b = orc.make_test_vector(m.n, orc.RANDOM, seed=14, lo=-1.0, hi=1.0)
+    ref = orc.symgs_sweep(m, orc.symgs_sweep(m, x0, b), b)
+    db = sp.DeviceVector.from_host(b)
+    for pipeline, lag in ((1, 0), (1, 9), (0, 0)):
+        sp.set_option("symgs_pipeline", pipeline)
+        sp.set_option("symgs_lag", lag)
+        try:
+            dx = sp.DeviceVector.from_host(x0)
+            for _ in range(2):
+                sp.symgs_sweep(dm, sp.GridSpec(*g), dx, db)
+            assert sp.get_option("last_symgs_kernel") == (2 if pipeline and served else 1)
+        finally:
+            sp.set_option("symgs_pipeline", 1)
+            sp.set_option("symgs_lag", 0)
+        assert np.array_equal(dx.to_host().view(np.uint64), ref.view(np.uint64)), (pipeline, lag)
+
+
 def test_symgs_examples_and_refusals(sp, orc):
     one = sp.generate_matrix(sp.GridSpec(1, 1, 1))
     dx = sp.DeviceVector.from_host(np.array([0.0]))
@@ -240,6 +268,7 @@ def test_symgs_examples_and_refusals(sp, orc):
     b = np.cos(np.arange(gs.rows()))
     dx, db = sp.DeviceVector.from_host(x), sp.DeviceVector.from_host(b)
     sp.symgs_sweep(d7, gs, dx, db)
+    assert sp.get_option("last_symgs_kernel") == 2  # a sub-box of the 27 neighbours per row: the plane pipeline
     assert np.array_equal(dx.to_host().view(np.uint64), orc.symgs_sweep(m7, x, b).view(np.uint64))
     # refusals leave x untouched: zero diagonal (singularity); a coupling the schedule does not order; wrong grid
     before = dx.to_host().copy()
@@ -254,6 +283,7 @@ def test_symgs_examples_and_refusals(sp, orc):
     far[3] = sorted(far[3] + [(3 + 2 * g[0] - 1, -0.25)])  # node (3,0,0) -> (2,2,0): higher index, higher level
     dfar, xf = sp.DeviceVector.from_host(x), orc.symgs_sweep(orc.stencil_from_rows(gs.rows(), far), x, b)
     sp.symgs_sweep(sp.stencil_from_rows(gs.rows(), far), gs, dfar, db)
+    assert sp.get_option("last_symgs_kernel") == 1  # rows that are no sub-boxes: the general kernel
     assert np.array_equal(dfar.to_host().view(np.uint64), xf.view(np.uint64))
     bad = [list(r) for r in rows]
     bad[5] = sorted(bad[5] + [(6, -0.25)])  # node (5,0,0), level 5 -> node (0,1,0): higher index but level 2
