@@ -123,7 +123,8 @@ int spmvb_set_device(int device);
  *   "box_lines":      lines per CTA tile / chunk length of the tensor ring (0 = default)
  *   "exception_kernel": hybrid handles, the exception-row block: 0 / 1 (default) the ELL kernel with a row map, all gathers of a
  *                     row requested in one batch; 64 / 32: the rows' operands come from three shared-memory windows of x per
- *                     64- / 32-row tile (csrc/spmv_exception.cu; measured slower on BASELINE config 4: 43 vs 34 us)
+ *                     64- / 32-row tile (csrc/spmv_exception.cu; measured slower on BASELINE config 4: 43 vs 34 us; compiled into
+ *                     lab builds only -- the default build runs the ELL kernel whatever the value)
  *   "exception_carveout": hybrid handles, the exception-block kernel's preferred shared-memory carve-out in percent of the SM's
  *                     228 KB (0 = default 60, -1 = the driver's choice): fewer CTAs per SM, more L1 for the scattered gathers
  *   "exception_overlap": hybrid handles: 1 (default) the exception block runs on a second stream beside the kernel of the dictionary
@@ -167,8 +168,9 @@ int spmvb_set_device(int device);
  *   "last_cg_fused_dot": read-only, 1 when the last spmvb_cg_solve took p.Ap from the SpMV kernel
  *   "cg_keep_workspace": 1 (default) spmvb_cg_solve keeps its three work vectors (3n doubles) on the matrix handle
  *                     between solves, released by spmvb_matrix_destroy; 0 allocates and frees them in every solve
- *   "ell_kernel":     0 auto (one bulk-copied tile per CTA: 32 rows for ELL, 128 for vt), 1 naive (ELL), 2 tiles staged with
- *                     vector loads, 3 the persistent two-stage TMA ring; lab build only: 4-7 other tile heights
+ *   "ell_kernel":     0 auto (one bulk-copied tile per CTA: 32 rows for ELL, 128 for vt), 2 tiles staged with vector loads,
+ *                     3 the persistent two-stage TMA ring (ELL); 1 naive (ELL) and 3 for vt exist in lab builds only (the default
+ *                     build runs its default kernel for them); lab build only: 4-7 other tile heights
  *   "box_prefetch", "box_prefetch_l1": L2 / L1 prefetch distance of the sliding-window kernels
  *   "debug_nochain":  lab build only, measurement only (1: sliding-window kernels skip their FP64 chains -- wrong results;
  *                     7: tensor ring without the per-plane-group line rotation -- same results)

@@ -949,7 +949,9 @@ static int launch_ringp_t(const spmvb_matrix *a, PatternArgs &p_in, int chunk, c
     } while (0)
     // two instantiations: the HPCG value pattern (off-diagonals -1, centre last) fully specialised, and a general one
     // (any off-diagonal value -- a product by -1.0 is exact, so it serves that case too -- centre position read at run time)
-    if (neg1 && cp == 1) LAUNCH_RINGP(true, 1); else LAUNCH_RINGP(false, -1);
+    if (neg1 && cp == 1) LAUNCH_RINGP(true, 1);
+    else if constexpr (LPS == 2) return 1;  // the two-lines step is built for the stencil's value pattern only; the caller runs the one-line kernels
+    else LAUNCH_RINGP(false, -1);
 #undef LAUNCH_RINGP
     return check_launch("spmv_pattern_ringp") == SPMVB_OK ? 0 : -1;
 }

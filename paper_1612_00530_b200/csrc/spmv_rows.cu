@@ -101,7 +101,8 @@ __global__ void __launch_bounds__(ROWS) spmv_ell_kernel(const double *__restrict
     else y[r] = (BULK && width == 27) ? ell_row<27>(v, c, 27, x, x_col0) : ell_row<9>(v, c, width, x, x_col0);
 }
 
-// Naive thread-per-row form, kept as the A/B baseline ("ell_kernel" = 1).
+// Naive thread-per-row form, the A/B baseline ("ell_kernel" = 1; lab builds only, the default build runs its default kernel instead).
+#ifdef SPMVB_LAB
 __global__ void spmv_ell_naive_kernel(const double *__restrict__ values, const int32_t *__restrict__ columns,
                                       int width, const double *__restrict__ x, int64_t x_col0,
                                       double *__restrict__ y, int row_begin, int row_end) {
@@ -113,6 +114,7 @@ __global__ void spmv_ell_naive_kernel(const double *__restrict__ values, const i
     for (int k = 0; k < width; k++) acc = __dadd_rn(acc, __dmul_rn(v[k], __ldg(x + ((int64_t)c[k] - x_col0))));
     y[r] = acc;
 }
+#endif
 
 // =============================================================================
 // Value table (inc/compress.hpp:28-44; spmv: inc/kernels.hpp:24,33-34;
@@ -255,12 +257,14 @@ int launch_ell(const double *values, const int32_t *columns, int width, const do
             SPMVB_CUDA(cudaMemsetAsync(y + row_begin, 0, (size_t)(row_end - row_begin) * 8, st));
         return SPMVB_OK;
     }
+#ifdef SPMVB_LAB
     if (options().ell_kernel == 1 && !row_map) {
         const int threads = 128;
         spmv_ell_naive_kernel<<<(row_end - row_begin + threads - 1) / threads, threads, 0, st>>>(
             values, columns, width, x, x_col0, y, row_begin, row_end);
         return check_launch("spmv_ell_naive");
     }
+#endif
     const int tile0 = row_begin / kTileRows;
     const int tiles = (row_end + kTileRows - 1) / kTileRows - tile0;
     const size_t smem = (size_t)kTileRows * width * 12;
@@ -344,7 +348,8 @@ int launch_vt(const spmvb_matrix *a, const double *x, int64_t x_col0, double *y,
     const int tiles = (row_end + kTileRows - 1) / kTileRows - tile0;
     const size_t smem = (size_t)kTileRows * (a->width + a->m) * 4 + (size_t)a->m * 8 + 16;
     if (smem > 200 * 1024) return fail(SPMVB_ERR_INVALID_ARGUMENT, "vt width/table too large for the staged kernel");
-    if (options().ell_kernel == 3) {  // TMA bulk pipeline: measured slower than the staged kernel for vt (545 vs 470 us)
+#ifdef SPMVB_LAB
+    if (options().ell_kernel == 3) {  // TMA bulk pipeline: measured slower than the staged kernel for vt (545 vs 470 us); lab builds only
         constexpr int NS = 2;
         const size_t stage = (size_t)kTileRows * (a->width + a->m) * 4;
         const size_t need = stage * NS;
@@ -362,6 +367,7 @@ int launch_vt(const spmvb_matrix *a, const double *x, int64_t x_col0, double *y,
             return check_launch("spmv_vt_tma");
         }
     }
+#endif
     // bulk-copy staging needs 16-byte multiples per tile part: 128 rows x width (and x m) ints always are
     const bool bulk = options().ell_kernel != 2;
     static PerDevice<bool> attr_set;

@@ -610,11 +610,8 @@ static int sweep_pipeline(const spmvb_matrix *a, const spmvb_grid *g, double *x,
     int *clock_f = sd.clocks, *clock_b = sd.clocks + nz;
     int lag = std::max(kBoxLag, options().symgs_lag);
     const uint32_t *mask = a->symgs_mask;
-    const int threads = ny <= 32 ? 32 : ny <= 64 ? 64 : ny <= 128 ? 128 : 256;
-    const void *fn = threads == 32 ? (const void *)symgs_box_pipeline_kernel<32>
-                     : threads == 64 ? (const void *)symgs_box_pipeline_kernel<64>
-                     : threads == 128 ? (const void *)symgs_box_pipeline_kernel<128>
-                                      : (const void *)symgs_box_pipeline_kernel<256>;
+    const int threads = ny <= 64 ? 64 : 256;
+    const void *fn = threads == 64 ? (const void *)symgs_box_pipeline_kernel<64> : (const void *)symgs_box_pipeline_kernel<256>;
     const size_t smem = (size_t)3 * (threads + 2) * kBoxPitch * 8 + (size_t)(threads / 32) * 32 * kSymgsRow * 8;
     const int grid = std::min(sd.n_sm, nz);
     void *args[] = {&rs, &vals, &mask, &x, &b, &nx, &ny, &nz, &lag, &clock_f, &clock_b};
