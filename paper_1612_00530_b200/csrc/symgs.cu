@@ -13,6 +13,8 @@
 // order says): a matrix that does not fit -- explicit rows with other couplings -- is refused, not swept wrongly.
 // It is launch-bound (256^3: 3570 launches per sweep), far from the SpMV's rate, and far ahead of a sequential sweep.
 #include <cmath>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -505,6 +507,29 @@ static void launch_levels(const spmvb_matrix *a, const spmvb_grid *g, double *x,
         }
 }
 
+// Scratch words for a sweep's synchronisation (barrier counter, plane clocks), one buffer per (device, stream): sweeps on one stream
+// are ordered and share it, sweeps on other streams -- other host threads, other handles -- have their own.
+static int *sweep_scratch(cudaStream_t st, size_t words) {
+    struct Buf {
+        int *p = nullptr;
+        size_t cap = 0;
+    };
+    static PerDevice<std::map<cudaStream_t, Buf>> pools;
+    static std::mutex lock;
+    std::lock_guard<std::mutex> g(lock);
+    Buf &b = pools.get()[st];
+    if (b.cap < words) {
+        if (b.p) cudaFree(b.p);
+        b.p = nullptr, b.cap = 0;
+        if (cudaMalloc(&b.p, words * sizeof(int)) != cudaSuccess) {
+            (void)cudaGetLastError();
+            return nullptr;
+        }
+        b.cap = words;
+    }
+    return b.p;
+}
+
 // A sweep is thousands of tiny dependent launches: they are recorded once into a CUDA graph (kept on the handle, keyed by
 // the vectors and the grid) and replayed, which takes the host's per-launch cost out of every sweep after the first
 // (the preconditioner applies the sweep to the same two vectors in every iteration).  "symgs_graph" = 0 launches directly.
@@ -512,8 +537,6 @@ static void launch_levels(const spmvb_matrix *a, const spmvb_grid *g, double *x,
 static int sweep_persistent(const spmvb_matrix *a, const spmvb_grid *g, double *x, const double *b, cudaStream_t st) {
     struct State {
         int coop = -1, n_sm = 0;
-        unsigned int *counter = nullptr;
-        unsigned int epoch = 0;
     };
     static PerDevice<State> state;
     State &sd = state.get();
@@ -521,8 +544,7 @@ static int sweep_persistent(const spmvb_matrix *a, const spmvb_grid *g, double *
         int dev = 0, coop = 0, per_sm = 0;
         if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev) != cudaSuccess ||
             cudaDeviceGetAttribute(&sd.n_sm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, symgs_sweep_persistent_kernel, kSymgsThreads, 0) != cudaSuccess || per_sm < 1 ||
-            cudaMalloc(&sd.counter, sizeof(unsigned int)) != cudaSuccess || cudaMemset(sd.counter, 0, sizeof(unsigned int)) != cudaSuccess)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, symgs_sweep_persistent_kernel, kSymgsThreads, 0) != cudaSuccess || per_sm < 1)
             coop = 0;
         (void)cudaGetLastError();
         sd.coop = coop ? 1 : 0;
@@ -539,15 +561,13 @@ static int sweep_persistent(const spmvb_matrix *a, const spmvb_grid *g, double *
     const auto *rs = static_cast<const int64_t *>(a->s[SPMVB_S_CSR_ROW_START]);
     const auto *cols = static_cast<const int32_t *>(a->s[SPMVB_S_CSR_COLS]);
     const auto *vals = static_cast<const double *>(a->s[SPMVB_S_CSR_VALS]);
-    // the barrier counter only grows: this sweep's arrivals start at `epoch` (sweeps of one device are ordered by their stream;
-    // two host threads sweeping on two streams of one device at once would share it -- they are serialised by `busy`)
-    const unsigned int arrivals = (unsigned int)(2 * levels - 1) * (unsigned int)sd.n_sm;
-    unsigned int epoch = sd.epoch;
-    sd.epoch += arrivals;
-    unsigned int *counter = sd.counter;
+    // the barrier counter: this stream's scratch word, zeroed in front of the launch
+    unsigned int *counter = reinterpret_cast<unsigned int *>(sweep_scratch(st, 1));
+    unsigned int epoch = 0;
+    if (!counter) return 1;
     void *args[] = {&rs, &cols, &vals, &x, &b, &nx, &ny, &nz, &levels, &counter, &epoch};
-    if (cudaLaunchCooperativeKernel((const void *)symgs_sweep_persistent_kernel, dim3(sd.n_sm), dim3(kSymgsThreads), args, 0, st) != cudaSuccess) {
-        sd.epoch -= arrivals;
+    if (cudaMemsetAsync(counter, 0, sizeof(unsigned int), st) != cudaSuccess ||
+        cudaLaunchCooperativeKernel((const void *)symgs_sweep_persistent_kernel, dim3(sd.n_sm), dim3(kSymgsThreads), args, 0, st) != cudaSuccess) {
         (void)cudaGetLastError();
         return 1;
     }
@@ -558,8 +578,6 @@ static int sweep_persistent(const spmvb_matrix *a, const spmvb_grid *g, double *
 static int sweep_pipeline(const spmvb_matrix *a, const spmvb_grid *g, double *x, const double *b, cudaStream_t st) {
     struct State {
         int coop = -1, n_sm = 0;
-        int *clocks = nullptr;
-        int cap = 0;
     };
     static PerDevice<State> state;
     State &sd = state.get();
@@ -597,17 +615,15 @@ static int sweep_pipeline(const spmvb_matrix *a, const spmvb_grid *g, double *x,
         }
     }
     if (!a->symgs_box_ok) return 1;
-    if (sd.cap < 2 * nz) {
-        if (sd.clocks) cudaFree(sd.clocks);
-        sd.clocks = nullptr, sd.cap = 0;
-        if (cudaMalloc(&sd.clocks, (size_t)2 * nz * sizeof(int)) != cudaSuccess) {
-            (void)cudaGetLastError();
-            return 1;
-        }
-        sd.cap = 2 * nz;
+    // the planes' clocks: this stream's scratch words, zeroed in front of the launch
+    int *clocks = sweep_scratch(st, 1 + (size_t)2 * nz) ;
+    if (!clocks) return 1;
+    clocks += 1;  // (word 0 is the grid-barrier kernel's counter)
+    if (cudaMemsetAsync(clocks, 0, (size_t)2 * nz * sizeof(int), st) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return 1;
     }
-    if (cudaMemsetAsync(sd.clocks, 0, (size_t)2 * nz * sizeof(int), st) != cudaSuccess) return 1;
-    int *clock_f = sd.clocks, *clock_b = sd.clocks + nz;
+    int *clock_f = clocks, *clock_b = clocks + nz;
     int lag = std::max(kBoxLag, options().symgs_lag);
     const uint32_t *mask = a->symgs_mask;
     const int threads = ny <= 64 ? 64 : 256;
@@ -615,8 +631,9 @@ static int sweep_pipeline(const spmvb_matrix *a, const spmvb_grid *g, double *x,
     const size_t smem = (size_t)3 * (threads + 2) * kBoxPitch * 8 + (size_t)(threads / 32) * 32 * kSymgsRow * 8;
     const int grid = std::min(sd.n_sm, nz);
     void *args[] = {&rs, &vals, &mask, &x, &b, &nx, &ny, &nz, &lag, &clock_f, &clock_b};
-    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
-        cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(threads + 64), args, smem, st) != cudaSuccess) {
+    const bool launched = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess &&
+                          cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(threads + 64), args, smem, st) == cudaSuccess;
+    if (!launched) {
         (void)cudaGetLastError();
         return 1;
     }
