@@ -344,20 +344,30 @@ __global__ void __launch_bounds__(THREADS + 64, 1) symgs_box_pipeline_kernel(con
         bool back, valid;
         int p, u;
     };
-    auto pos_of_tick = [&](int tick) -> Pos {
+    // (the step counter is kept as (direction, plane round, step of the plane) and advanced by one: no divisions in the loop)
+    struct Cursor {
+        int tick, r, kt;
+        bool back;
+    };
+    auto advance = [&](Cursor &cu) {
+        cu.tick++;
+        if (++cu.kt == KT) {
+            cu.kt = 0;
+            if (++cu.r == R) cu.r = 0, cu.back = true;
+        }
+    };
+    auto pos_of = [&](const Cursor &cu) -> Pos {
         Pos q{false, false, 0, 0};
-        if (tick >= ticks) return q;
-        q.back = tick >= R * KT;
-        const int w = q.back ? tick - R * KT : tick;
-        const int r = w / KT, kt = w - r * KT;
-        q.p = q.back ? c + (R - 1 - r) * G : c + r * G;
-        q.u = kt - kBoxAhead - 2 * t;
+        if (cu.tick >= ticks) return q;
+        q.back = cu.back;
+        q.p = cu.back ? c + (R - 1 - cu.r) * G : c + cu.r * G;
+        q.u = cu.kt - kBoxAhead - 2 * t;
         q.valid = t < ny;
         return q;
     };
-    auto head_of_tick = [&](int tick) -> BoxHead {
+    auto head_of = [&](const Cursor &cu) -> BoxHead {
         BoxHead h{-1, 0u, 0, 0.0};
-        const Pos q = pos_of_tick(tick);
+        const Pos q = pos_of(cu);
         if (q.valid && q.u >= 0 && q.u < nx) {
             const int ix = q.back ? nx - 1 - q.u : q.u, iy = q.back ? ny - 1 - t : t;
             const int64_t i = ix + (int64_t)nx * iy + nxny * q.p;
@@ -403,20 +413,24 @@ __global__ void __launch_bounds__(THREADS + 64, 1) symgs_box_pipeline_kernel(con
         }
     };
     double *my_line = ring + (t + 1) * kBoxPitch;  // + d * LINES * kBoxPitch for plane d
-    BoxHead h0 = head_of_tick(0), h1 = head_of_tick(1);
+    Cursor now{0, 0, 0, false}, ahead{0, 0, 0, false};  // this step / the step whose row is being requested (two ahead)
+    BoxHead h0 = head_of(ahead);
+    advance(ahead);
+    BoxHead h1 = head_of(ahead);
+    advance(ahead);
     fetch_rows(h0);
     store_rows();
     __syncwarp();
     for (int tick = 0; tick < ticks; tick++) {
-        const Pos q = pos_of_tick(tick);
-        const BoxHead h2 = head_of_tick(tick + 2);  // requested two steps ahead of its row
+        const Pos q = pos_of(now);
+        const BoxHead h2 = head_of(ahead);  // requested two steps ahead of its row
         fetch_rows(h1);                              // the next step's values, in flight across this step
         asm volatile("bar.sync 1, %0;" ::"r"(THREADS + 32) : "memory");
         // (the ring loads of the previous step have had a step to arrive; this step's are requested now, behind the clock's acquire)
         const double prev[3] = {rl[0], rl[1], rl[2]};
         const bool prev_on[3] = {rl_on[0], rl_on[1], rl_on[2]};
         const int prev_slot = rl_slot;
-        const bool first = (q.back ? tick - R * KT : tick) % KT == 0;  // a new plane: nothing carried over
+        const bool first = now.kt == 0;  // a new plane: nothing carried over
         ring_loads(q);
         // the plane below: the newest value any neighbour can ask for in the next step, u + 4 (its level there is k + 4: complete, the
         // clock says so); one L2 round trip, hidden behind this step's sums
@@ -460,6 +474,8 @@ __global__ void __launch_bounds__(THREADS + 64, 1) symgs_box_pipeline_kernel(con
         asm volatile("bar.sync 2, %0;" ::"r"(THREADS + 32) : "memory");  // the step's x is on its way: the clock may be published
         store_rows();  // (every lane has read its row's values: the buffer takes the next step's, behind the barrier and off the clock's path)
         h0 = h1, h1 = h2;
+        advance(now);
+        advance(ahead);
     }
 }
 
