@@ -244,6 +244,44 @@ def test_symgs_plane_pipeline_and_its_fallbacks(sp, orc, g, served):
         assert np.array_equal(dx.to_host().view(np.uint64), ref.view(np.uint64)), (pipeline, lag)
 
 
+def test_symgs_sweeps_on_two_streams_from_two_host_threads(sp, orc):
+    """Sweeps of different handles enqueued from two host threads on two streams of one device: each has its own synchronisation
+    words (per device and stream), so in whatever order the device runs them every one is the oracle's sweep bit for bit."""
+    import threading
+    import torch
+    errors = []
+    cases = []
+    for g in ((20, 20, 20), (33, 9, 5)):
+        m = orc.generate_matrix(*g)
+        x0 = orc.make_test_vector(m.n, orc.RANDOM, seed=21, lo=-1.0, hi=1.0)
+        b = orc.make_test_vector(m.n, orc.RANDOM, seed=22, lo=-1.0, hi=1.0)
+        ref = x0
+        for _ in range(6):
+            ref = orc.symgs_sweep(m, ref, b)
+        cases.append((g, sp.generate_matrix(sp.GridSpec(*g)), x0, sp.DeviceVector.from_host(b), ref, torch.cuda.Stream()))
+
+    def sweeps(g, dm, dx, db, st, pipeline):
+        try:
+            sp.check(sp.lib.spmvb_set_device(0))  # options and the current device are per host thread
+            sp.set_option("symgs_pipeline", pipeline)
+            for _ in range(6):
+                sp.symgs_sweep(dm, sp.GridSpec(*g), dx, db, stream=st)
+            st.synchronize()
+        except Exception as ex:  # noqa: BLE001
+            errors.append(ex)
+
+    for pipeline in (1, 0):
+        xs = [sp.DeviceVector.from_host(c[2]) for c in cases]  # every round starts from the same x
+        threads = [threading.Thread(target=sweeps, args=(c[0], c[1], dx, c[3], c[5], pipeline)) for c, dx in zip(cases, xs)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        assert not errors, errors
+        for c, dx in zip(cases, xs):
+            assert np.array_equal(dx.to_host().view(np.uint64), c[4].view(np.uint64)), (c[0], pipeline)
+
+
 def test_symgs_examples_and_refusals(sp, orc):
     one = sp.generate_matrix(sp.GridSpec(1, 1, 1))
     dx = sp.DeviceVector.from_host(np.array([0.0]))
